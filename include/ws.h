@@ -1,0 +1,155 @@
+/* =====================================================================================
+ *  ws.h — C ABI of the B200-native (sm_100a) hot path of arXiv 2410.08946,
+ *  "Parallel Watershed Partitioning: GPU-Based Hierarchical Image Segmentation".
+ *
+ *  The three calls follow the paper's statement of the problem (BASELINE.json north_star):
+ *    ws_gradient (img, dims, sigma)           -> agreed u8 gradient-magnitude image
+ *    ws_watershed(grad, dims, connectivity)   -> canonical watershed labels
+ *    ws_waterfall(labels, grad, NL)           -> NL nested hierarchical label levels
+ *
+ *  Citation keys: P:n = PAPER.md line n (arXiv 2410.08946 LaTeX source); Cn = reading n in
+ *  DESIGN.md "Readings" (= SURVEY.md §8(c)).
+ *
+ *  Conventions shared by every call
+ *  --------------------------------
+ *  - All array pointers are DEVICE pointers owned by the caller (e.g. torch tensors); the
+ *    library never frees or retains them past the call.  Exception: ws_segment_host takes
+ *    HOST pointers (see there).
+ *  - Layout: row-major, last axis fastest (C1).  Linear voxel index
+ *      p = (z * n1 + y) * n2 + x,   N = n0 * n1 * n2  (must be < 2^31).
+ *  - dims.ndim == 2: n0 independent 2-D images of n1 x n2 (a batch; no adjacency across
+ *    axis 0, C18).  1-D images are 2-D images with n1 == 1.
+ *    dims.ndim == 3: one volume of depth n0.
+ *  - connectivity: 4 or 8 with ndim 2 (von Neumann / Moore), 6 or 26 with ndim 3.
+ *    Neighbourhoods are clipped at the border, the centre excluded (C2).
+ *  - stream: a cudaStream_t passed as void*; NULL = the legacy default stream.  Work is
+ *    enqueued on it.  ws_watershed and ws_waterfall synchronise the stream internally (they
+ *    read convergence flags and sizes back), ws_gradient does not.
+ *  - Errors: every argument is validated before any launch; on error nothing is written to
+ *    any output and a message is available from ws_last_error() (thread-local).  No C++
+ *    exception or abort crosses the ABI.
+ *  - Determinism: outputs are bit-identical across runs ("fully deterministic").
+ * ===================================================================================== */
+#ifndef WS_B200_H
+#define WS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ws_status {
+  WS_OK = 0,
+  WS_ERR_INVALID = 1,  /* bad dims / connectivity / NL / sigma / NULL pointer          */
+  WS_ERR_OOM = 2,      /* workspace allocation failed                                   */
+  WS_ERR_CUDA = 3,     /* a CUDA runtime error (message has the CUDA error string)      */
+  WS_ERR_NCCL = 4,     /* reserved for the sharded path                                 */
+  WS_ERR_INTERNAL = 5, /* an internal consistency check failed                          */
+  WS_ERR_LIMIT = 6     /* a documented size limit was exceeded (message says which)     */
+} ws_status;
+
+typedef struct ws_dims {
+  int32_t ndim;     /* 2 (batch of images) or 3 (volume)                                  */
+  int32_t reserved; /* must be 0                                                          */
+  int64_t n0;       /* ndim 2: number of images (>= 1); ndim 3: depth                     */
+  int64_t n1;       /* height                                                             */
+  int64_t n2;       /* width (fastest axis)                                               */
+} ws_dims;
+
+/* Opaque context: owns the device scratch workspace (grown on demand, freed by destroy)
+ * and the statistics of the last call.  One context per device; not thread-safe. */
+typedef struct ws_ctx ws_ctx;
+
+#define WS_NUM_PHASES 16
+
+typedef struct ws_stats {
+  int64_t n_voxels;
+  int64_t n_regions;          /* R of the last ws_watershed / ws_waterfall               */
+  int64_t n_edges;            /* RAG edge records after tile-local dedup (ws_waterfall)   */
+  int32_t plateau_rounds;     /* step II global relaxation rounds (ws_watershed)          */
+  int32_t waterfall_levels;   /* levels actually iterated (stops early once R == 1)       */
+  int64_t level_counts[16];   /* regions per level (first min(NL,16) levels)              */
+  int64_t kernel_launches;    /* kernels launched by the last call                        */
+  /* per-phase device time of the last call, CUDA events on the call's stream; filled only
+   * when timing is enabled (ws_ctx_set_timing).  Phase names: ws_phase_name(i). */
+  double phase_ms[WS_NUM_PHASES];
+  int32_t phase_launches[WS_NUM_PHASES];
+} ws_stats;
+
+ws_status ws_ctx_create(int32_t device, ws_ctx** out);
+ws_status ws_ctx_destroy(ws_ctx* ctx);
+const char* ws_last_error(void);
+const char* ws_version(void);
+/* Statistics of the most recent call on ctx (copied into *out). */
+ws_status ws_get_stats(const ws_ctx* ctx, ws_stats* out);
+/* Enable (1) / disable (0) per-phase CUDA-event timing in ws_stats.phase_ms. */
+ws_status ws_ctx_set_timing(ws_ctx* ctx, int32_t enable);
+/* Name of phase i (0 <= i < WS_NUM_PHASES), "" if unused. */
+const char* ws_phase_name(int32_t i);
+
+/* ws_gradient — the stencil pre-pass (Fig. 2: "input image smoothing and
+ * use of gradient magnitude image are optional").
+ *   b    = G_sigma * (img / 255): separable sampled Gaussian, radius r = floor(3 sigma + 0.5),
+ *          normalised weights, clamp-to-edge; sigma == 0 is the identity (C8).
+ *          ndim 3 blurs along all three axes, ndim 2 along n1 and n2 of each image.
+ *   g    = || grad b ||_2 with central differences inside and one-sided differences at the
+ *          ends, 0 along an axis of length 1 (C9).
+ *   grad_q[p] = min(255, floor(255 g + 0.5))  (C10, the agreed integer image, C11).
+ * Arguments: img u8[N] (in), grad_q u8[N] (out, required), blur_f32 / grad_f32 f32[N]
+ * (out, optional "verify mode", may be NULL).  Arithmetic is fp32.
+ * Errors: WS_ERR_INVALID for bad dims, sigma < 0 or sigma > 20, NULL img/grad_q. */
+ws_status ws_gradient(ws_ctx* ctx, const uint8_t* img, ws_dims dims, float sigma,
+                      uint8_t* grad_q, float* blur_f32, float* grad_f32, void* stream);
+
+/* ws_watershed — steps I-IV of PRUF (Alg. 1) + canonical relabel.
+ *   Step I   steepest-descent pointer, Eq. 1: among the minimal neighbours
+ *            the one with the largest index (C3).
+ *   Step II  non-minimal plateaux: BFS distance from the plateau's lower voxels, parent =
+ *            max-index equal neighbour one step closer (Sync semantics P:194-203, C5/C6),
+ *            computed by tile-local relaxation (the PRUF_bal mechanism, Alg. 3)
+ *            followed by a pointer-selection pass.
+ *   Step III pointer jumping to the self-loop roots (Alg. 1 l.19-23 / l.28-29).
+ *   Step IV  min-root lock-free union-find over adjacent minimal-plateau voxels.
+ *   Output   labels[p] = smallest linear index in p's catchment basin (C7).
+ * Arguments: grad u8[N] (in), labels i32[N] (out; also used as the working pointer array),
+ * num_regions (HOST i64, optional, may be NULL).
+ * Errors: WS_ERR_INVALID (dims/conn mismatch, NULL), WS_ERR_LIMIT (a non-minimal plateau
+ * deeper than 2^26-2 voxels). */
+ws_status ws_watershed(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity,
+                       int32_t* labels, int64_t* num_regions, void* stream);
+
+/* ws_waterfall — the hierarchical segmentation as the graph waterfall (C13):
+ *   RAG edges {a, b} between adjacent regions with height max(I(p), I(q)), per pair
+ *   the minimum (Alg. 4 l.2-7); strict edge order K = (w asc, max(a,b) desc, min(a,b) desc)
+ *   on level-0 canonical labels (C14).  Level k = 1..NL-1: every component of level k-1
+ *   merges along its min-K outgoing edge (min-root union-find, C16); isolated components
+ *   stay (C17).
+ *   levels[k*N + p] = smallest linear index of p's level-k region; levels[0..N) = labels.
+ * Arguments: labels i32[N] (in; MUST be canonical ws_watershed output for the same grad,
+ * dims and connectivity), grad u8[N] (in), NL >= 1 levels including level 0 (C12),
+ * levels i32[NL*N] (out, level-major), counts (HOST i64[NL], optional).
+ * Errors: WS_ERR_INVALID (dims/conn/NL, NULL), WS_ERR_LIMIT (more than 2^28-1 regions). */
+ws_status ws_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, ws_dims dims,
+                       int32_t connectivity, int32_t NL, int32_t* levels, int64_t* counts,
+                       void* stream);
+
+/* ws_segment_host — the end-to-end user call on HOST buffers: copies grad (host, ideally
+ * pinned) to the device, runs ws_watershed + ws_waterfall, copies levels back to the host
+ * (host i32[NL*N]).  Device buffers come from the context workspace.  Synchronous. */
+ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims,
+                          int32_t connectivity, int32_t NL, int32_t* levels_host,
+                          int64_t* counts, void* stream);
+
+/* ws_plateau_debug — intermediate of step II for per-kernel parity tests (T2):
+ *   dist[p] = 0 for voxels with a lower neighbour, the BFS distance on non-minimal plateaux,
+ *             -1 on minimal plateaux (regional minima, incl. strict single-voxel minima);
+ *   parent[p] = the step-I/II pointer of p (p itself on minimal plateaux).
+ * Arguments: grad u8[N] (in), dist i32[N] (out), parent i32[N] (out). */
+ws_status ws_plateau_debug(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity,
+                           int32_t* dist, int32_t* parent, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WS_B200_H */

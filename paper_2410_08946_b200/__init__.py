@@ -1,0 +1,120 @@
+"""B200-native (sm_100a) hot path of arXiv 2410.08946, "Parallel Watershed Partitioning".
+
+Python API (same names as the C ABI in include/ws.h; argument marshalling only):
+
+    grad_q              = gradient(img, sigma, ndim)             # ws_gradient
+    labels, R           = watershed(grad, conn)                  # ws_watershed
+    levels, counts      = waterfall(labels, grad, conn, NL)      # ws_waterfall
+    levels_h, counts    = segment_host(grad_host, conn, NL)      # ws_segment_host (host buffers)
+
+Tensors live on a CUDA device (PyTorch is used for device memory and streams only); work is
+enqueued on the current torch stream.  ``ndim`` is 2 for (batch, H, W) image stacks (4/8-conn)
+and 3 for (D, H, W) volumes (6/26-conn); it defaults from ``conn``.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _binding as _b
+from ._binding import Context, WsError, default_context  # noqa: F401
+
+__all__ = ["gradient", "watershed", "waterfall", "segment_host", "plateau_debug", "stats", "Context",
+           "WsError", "version"]
+
+
+def version() -> str:
+    return _b.load().ws_version().decode()
+
+
+def _ndim_for(conn, ndim):
+    if ndim is not None:
+        return int(ndim)
+    return 3 if conn in (6, 26) else 2
+
+
+def _req(t, dtype, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("%s must be a CUDA tensor" % name)
+    if t.dtype != dtype:
+        raise TypeError("%s must be %s (got %s)" % (name, dtype, t.dtype))
+    if not t.is_contiguous():
+        raise ValueError("%s must be contiguous" % name)
+
+
+def gradient(img: torch.Tensor, sigma: float = 1.0, ndim: int = None, verify: bool = False,
+             ctx: Context = None, out: torch.Tensor = None):
+    """ws_gradient: u8 image -> agreed u8 gradient image (and fp32 blur/grad if ``verify``)."""
+    _req(img, torch.uint8, "img")
+    ndim = ndim if ndim is not None else (3 if img.dim() == 3 and img.shape[0] > 1 else 2)
+    ctx = ctx or default_context(img.device.index)
+    q = out if out is not None else torch.empty_like(img)
+    blur = torch.empty(img.shape, dtype=torch.float32, device=img.device) if verify else None
+    grad = torch.empty(img.shape, dtype=torch.float32, device=img.device) if verify else None
+    _b.check(_b.load().ws_gradient(ctx.handle, _b.ptr(img), _b.dims_of(img.shape, ndim), float(sigma),
+                                   _b.ptr(q), _b.ptr(blur), _b.ptr(grad), _b.stream_of(img)))
+    return (q, blur, grad) if verify else q
+
+
+def watershed(grad: torch.Tensor, conn: int, ndim: int = None, ctx: Context = None,
+              out: torch.Tensor = None):
+    """ws_watershed: canonical labels (int32, shaped like grad) and the region count R."""
+    _req(grad, torch.uint8, "grad")
+    ndim = _ndim_for(conn, ndim)
+    ctx = ctx or default_context(grad.device.index)
+    labels = out if out is not None else torch.empty(grad.shape, dtype=torch.int32, device=grad.device)
+    R = ctypes.c_int64(0)
+    _b.check(_b.load().ws_watershed(ctx.handle, _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn),
+                                    _b.ptr(labels), ctypes.byref(R), _b.stream_of(grad)))
+    return labels, R.value
+
+
+def waterfall(labels: torch.Tensor, grad: torch.Tensor, conn: int, NL: int, ndim: int = None,
+              ctx: Context = None, out: torch.Tensor = None):
+    """ws_waterfall: levels (int32 [NL, *shape], level 0 = labels) and per-level counts."""
+    _req(labels, torch.int32, "labels")
+    _req(grad, torch.uint8, "grad")
+    if labels.shape != grad.shape:
+        raise ValueError("labels and grad shapes differ")
+    ndim = _ndim_for(conn, ndim)
+    ctx = ctx or default_context(grad.device.index)
+    levels = out if out is not None else torch.empty((max(int(NL), 1),) + tuple(grad.shape), dtype=torch.int32,
+                                                      device=grad.device)
+    counts = (ctypes.c_int64 * max(int(NL), 1))()
+    _b.check(_b.load().ws_waterfall(ctx.handle, _b.ptr(labels), _b.ptr(grad), _b.dims_of(grad.shape, ndim),
+                                    int(conn), int(NL), _b.ptr(levels), counts, _b.stream_of(grad)))
+    return levels, list(counts)
+
+
+def segment_host(grad_host: torch.Tensor, conn: int, NL: int, ndim: int = None, device: int = None,
+                 ctx: Context = None, out: torch.Tensor = None):
+    """ws_segment_host: HOST u8 gradient -> HOST int32 levels [NL, *shape] (copies inside)."""
+    if grad_host.is_cuda or grad_host.dtype != torch.uint8 or not grad_host.is_contiguous():
+        raise TypeError("grad_host must be a contiguous CPU uint8 tensor")
+    ndim = _ndim_for(conn, ndim)
+    ctx = ctx or default_context(device)
+    levels = out if out is not None else torch.empty((int(NL),) + tuple(grad_host.shape), dtype=torch.int32,
+                                                      pin_memory=True)
+    counts = (ctypes.c_int64 * max(int(NL), 1))()
+    st = ctypes.c_void_p(torch.cuda.current_stream(ctx.device).cuda_stream)
+    _b.check(_b.load().ws_segment_host(ctx.handle, _b.ptr(grad_host), _b.dims_of(grad_host.shape, ndim), int(conn),
+                                       int(NL), _b.ptr(levels), counts, st))
+    return levels, list(counts)
+
+
+def plateau_debug(grad: torch.Tensor, conn: int, ndim: int = None, ctx: Context = None):
+    """ws_plateau_debug: (dist, parent) after steps I-II (per-kernel parity, T2)."""
+    _req(grad, torch.uint8, "grad")
+    ndim = _ndim_for(conn, ndim)
+    ctx = ctx or default_context(grad.device.index)
+    dist = torch.empty(grad.shape, dtype=torch.int32, device=grad.device)
+    parent = torch.empty(grad.shape, dtype=torch.int32, device=grad.device)
+    _b.check(_b.load().ws_plateau_debug(ctx.handle, _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn),
+                                        _b.ptr(dist), _b.ptr(parent), _b.stream_of(grad)))
+    return dist, parent
+
+
+def stats(device: int = None) -> dict:
+    """Statistics of the last call on the default context of ``device``."""
+    return default_context(device).stats()

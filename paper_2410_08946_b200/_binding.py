@@ -1,0 +1,154 @@
+"""Thin ctypes binding of libws_b200.so (include/ws.h).  Argument marshalling ONLY: every step
+of the hot path runs in the library's CUDA kernels.  There is no CPU or PyTorch fallback:
+if the shared library is missing or a call fails, this raises."""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libws_b200.so")
+
+WS_OK, WS_ERR_INVALID, WS_ERR_OOM, WS_ERR_CUDA, WS_ERR_NCCL, WS_ERR_INTERNAL, WS_ERR_LIMIT = range(7)
+STATUS_NAMES = {0: "WS_OK", 1: "WS_ERR_INVALID", 2: "WS_ERR_OOM", 3: "WS_ERR_CUDA", 4: "WS_ERR_NCCL",
+                5: "WS_ERR_INTERNAL", 6: "WS_ERR_LIMIT"}
+
+# every symbol include/ws.h declares (checked by tests/test_abi.py)
+EXPORTS = ("ws_ctx_create", "ws_ctx_destroy", "ws_last_error", "ws_version", "ws_get_stats",
+           "ws_ctx_set_timing", "ws_phase_name",
+           "ws_gradient", "ws_watershed", "ws_waterfall", "ws_segment_host", "ws_plateau_debug")
+
+
+class WsDims(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("n0", ctypes.c_int64), ("n1", ctypes.c_int64), ("n2", ctypes.c_int64)]
+
+
+class WsStats(ctypes.Structure):
+    _fields_ = [("n_voxels", ctypes.c_int64), ("n_regions", ctypes.c_int64), ("n_edges", ctypes.c_int64),
+                ("plateau_rounds", ctypes.c_int32), ("waterfall_levels", ctypes.c_int32),
+                ("level_counts", ctypes.c_int64 * 16), ("kernel_launches", ctypes.c_int64),
+                ("phase_ms", ctypes.c_double * 16), ("phase_launches", ctypes.c_int32 * 16)]
+
+    def as_dict(self):
+        lib = load()
+        phases = {}
+        for i in range(16):
+            name = lib.ws_phase_name(i).decode()
+            if name and (self.phase_launches[i] or self.phase_ms[i]):
+                phases[name] = {"ms": self.phase_ms[i], "launches": self.phase_launches[i]}
+        return {"n_voxels": self.n_voxels, "n_regions": self.n_regions, "n_edges": self.n_edges,
+                "plateau_rounds": self.plateau_rounds, "waterfall_levels": self.waterfall_levels,
+                "level_counts": list(self.level_counts), "kernel_launches": self.kernel_launches,
+                "phases": phases}
+
+
+class WsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS_NAMES.get(status, status), msg))
+        self.status = status
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: str = SO_PATH):
+    """Load the CUDA library (raises if it is not built — no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise ImportError("libws_b200.so not built (%s); run __graft_entry__.build()" % path)
+        lib = ctypes.CDLL(path)
+        vp, i32, i64, f32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
+        lib.ws_ctx_create.argtypes = [i32, ctypes.POINTER(vp)]
+        lib.ws_ctx_destroy.argtypes = [vp]
+        lib.ws_last_error.restype = ctypes.c_char_p
+        lib.ws_version.restype = ctypes.c_char_p
+        lib.ws_get_stats.argtypes = [vp, ctypes.POINTER(WsStats)]
+        lib.ws_ctx_set_timing.argtypes = [vp, i32]
+        lib.ws_phase_name.argtypes = [i32]
+        lib.ws_phase_name.restype = ctypes.c_char_p
+        lib.ws_gradient.argtypes = [vp, vp, WsDims, f32, vp, vp, vp, vp]
+        lib.ws_watershed.argtypes = [vp, vp, WsDims, i32, vp, vp, vp]
+        lib.ws_waterfall.argtypes = [vp, vp, vp, WsDims, i32, i32, vp, vp, vp]
+        lib.ws_segment_host.argtypes = [vp, vp, WsDims, i32, i32, vp, vp, vp]
+        lib.ws_plateau_debug.argtypes = [vp, vp, WsDims, i32, vp, vp, vp]
+        for name in EXPORTS:
+            f = getattr(lib, name)
+            if name not in ("ws_last_error", "ws_version", "ws_phase_name"):
+                f.restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def check(status):
+    if status != WS_OK:
+        raise WsError(status, load().ws_last_error().decode(errors="replace"))
+
+
+class Context:
+    """Owns one ws_ctx (device workspace) for one CUDA device."""
+
+    def __init__(self, device: int = None):
+        lib = load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        check(lib.ws_ctx_create(self.device, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            load().ws_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_timing(self, enable: bool = True):
+        check(load().ws_ctx_set_timing(self.handle, 1 if enable else 0))
+
+    def stats(self) -> dict:
+        s = WsStats()
+        check(load().ws_get_stats(self.handle, ctypes.byref(s)))
+        return s.as_dict()
+
+
+_ctxs = {}
+
+
+def default_context(device: int = None) -> Context:
+    if device is None:
+        device = torch.cuda.current_device()
+    if device not in _ctxs:
+        _ctxs[device] = Context(device)
+    return _ctxs[device]
+
+
+def dims_of(shape, ndim: int) -> WsDims:
+    shape = tuple(int(s) for s in shape)
+    if len(shape) == 1:
+        shape = (1, 1) + shape
+    elif len(shape) == 2:
+        shape = (1,) + shape
+    if len(shape) != 3:
+        raise ValueError("expected a 1-, 2- or 3-D tensor, got shape %s" % (shape,))
+    return WsDims(int(ndim), 0, *shape)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def stream_of(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)

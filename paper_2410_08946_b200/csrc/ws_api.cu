@@ -1,0 +1,303 @@
+// ws_api.cu — the C ABI (include/ws.h): validation, context/workspace, error reporting.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "ws_internal.h"
+
+namespace ws {
+
+static thread_local char g_err[512] = "";
+
+void set_error(ws_status st, const char* fmt, ...) {
+  (void)st;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+ws_status cuda_fail(cudaError_t e, const char* where) {
+  set_error(WS_ERR_CUDA, "CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), where);
+  return e == cudaErrorMemoryAllocation ? WS_ERR_OOM : WS_ERR_CUDA;
+}
+
+ws_status Buf::ensure(size_t want, const char* name) {
+  if (want <= bytes) return WS_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  if (want == 0) return WS_OK;
+  cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    p = nullptr;
+    set_error(WS_ERR_OOM, "cannot allocate %zu bytes of device workspace for %s", want, name);
+    return WS_ERR_OOM;
+  }
+  bytes = want;
+  return WS_OK;
+}
+
+void Buf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+// dims + connectivity validation (ws.h "Errors")
+static ws_status check_dims(const ws_dims& d, Geo* g) {
+  if (d.ndim != 2 && d.ndim != 3) {
+    set_error(WS_ERR_INVALID, "dims.ndim must be 2 or 3 (got %d)", d.ndim);
+    return WS_ERR_INVALID;
+  }
+  if (d.reserved != 0) {
+    set_error(WS_ERR_INVALID, "dims.reserved must be 0");
+    return WS_ERR_INVALID;
+  }
+  if (d.n0 < 1 || d.n1 < 1 || d.n2 < 1) {
+    set_error(WS_ERR_INVALID, "dims must be >= 1 (got %lld x %lld x %lld)", (long long)d.n0, (long long)d.n1,
+              (long long)d.n2);
+    return WS_ERR_INVALID;
+  }
+  const double n = (double)d.n0 * (double)d.n1 * (double)d.n2;
+  if (n >= 2147483648.0) {
+    set_error(WS_ERR_INVALID, "N = %.0f voxels: must be < 2^31 (i32 labels)", n);
+    return WS_ERR_INVALID;
+  }
+  g->n0 = (int)d.n0;
+  g->n1 = (int)d.n1;
+  g->n2 = (int)d.n2;
+  g->plane = g->n1 * g->n2;
+  g->N = g->plane * g->n0;
+  return WS_OK;
+}
+
+static ws_status check_conn(const ws_dims& d, int conn) {
+  const bool ok = (d.ndim == 2 && (conn == 4 || conn == 8)) || (d.ndim == 3 && (conn == 6 || conn == 26));
+  if (!ok) {
+    set_error(WS_ERR_INVALID, "connectivity %d does not match ndim %d (2-D: 4|8, 3-D: 6|26)", conn, d.ndim);
+    return WS_ERR_INVALID;
+  }
+  return WS_OK;
+}
+
+static ws_status check_ctx(ws_ctx* ctx) {
+  if (!ctx) {
+    set_error(WS_ERR_INVALID, "ctx is NULL");
+    return WS_ERR_INVALID;
+  }
+  WS_CUDA(cudaSetDevice(ctx->device));
+  return WS_OK;
+}
+
+static ws_status null_arg(const char* name) {
+  set_error(WS_ERR_INVALID, "%s must not be NULL", name);
+  return WS_ERR_INVALID;
+}
+
+static void begin_call(ws_ctx* ctx, const Geo& g) {
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+  ctx->stats.n_voxels = g.N;
+}
+
+void tbegin(ws_ctx* ctx, cudaStream_t st) {
+  ctx->ev_n = 0;
+  if (!ctx->timing) return;
+  cudaEventRecord(ctx->ev[0], st);
+  ctx->ev_phase[0] = -1;
+  ctx->ev_n = 1;
+}
+
+void tmark(ws_ctx* ctx, cudaStream_t st, int phase) {
+  if (!ctx->timing || ctx->ev_n == 0 || ctx->ev_n >= ws_ctx::MAXEV) return;
+  cudaEventRecord(ctx->ev[ctx->ev_n], st);
+  ctx->ev_phase[ctx->ev_n] = phase;
+  ++ctx->ev_n;
+}
+
+void tfinish(ws_ctx* ctx) {
+  if (!ctx->timing || ctx->ev_n < 2) return;
+  cudaEventSynchronize(ctx->ev[ctx->ev_n - 1]);
+  for (int i = 1; i < ctx->ev_n; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev[i - 1], ctx->ev[i]) == cudaSuccess)
+      ctx->stats.phase_ms[ctx->ev_phase[i]] += ms;
+  }
+  (void)cudaGetLastError();
+  ctx->ev_n = 0;
+}
+
+static const char* kPhaseNames[WS_NUM_PHASES] = {
+    "gradient.blur", "gradient.magnitude", "watershed.init", "watershed.relax", "watershed.select",
+    "watershed.jump", "watershed.union", "watershed.find", "watershed.relabel", "waterfall.dense_ids",
+    "waterfall.rag", "waterfall.levels", "waterfall.materialise", "copy", "", ""};
+
+}  // namespace ws
+
+using namespace ws;
+
+extern "C" {
+
+const char* ws_last_error(void) { return g_err; }
+const char* ws_version(void) { return "ws_b200 0.1 (sm_100a)"; }
+
+ws_status ws_ctx_create(int32_t device, ws_ctx** out) {
+  if (!out) return null_arg("out");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || device < 0 || device >= n) {
+    set_error(WS_ERR_CUDA, "no CUDA device %d (%d visible%s%s)", device, n, e != cudaSuccess ? ": " : "",
+              e != cudaSuccess ? cudaGetErrorString(e) : "");
+    (void)cudaGetLastError();
+    return WS_ERR_CUDA;
+  }
+  WS_CUDA(cudaSetDevice(device));
+  ws_ctx* c = new (std::nothrow) ws_ctx();
+  if (!c) {
+    set_error(WS_ERR_OOM, "host allocation failed");
+    return WS_ERR_OOM;
+  }
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  e = cudaMallocHost(&c->pinned, 64 * sizeof(int64_t));
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMallocHost");
+  }
+  *out = c;
+  return WS_OK;
+}
+
+ws_status ws_ctx_destroy(ws_ctx* ctx) {
+  if (!ctx) return WS_OK;
+  cudaSetDevice(ctx->device);
+  ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->blockcnt, &ctx->edges,
+                     &ctx->comp, &ctx->best, &ctx->rep_of, &ctx->levelmap, &ctx->lvcount,
+                     &ctx->h_grad, &ctx->h_labels, &ctx->h_levels};
+  for (auto* b : bufs) b->release();
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (int i = 0; i < ws_ctx::MAXEV; ++i)
+    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  delete ctx;
+  return WS_OK;
+}
+
+const char* ws_phase_name(int32_t i) { return (i >= 0 && i < WS_NUM_PHASES) ? kPhaseNames[i] : ""; }
+
+ws_status ws_ctx_set_timing(ws_ctx* ctx, int32_t enable) {
+  WS_TRY(check_ctx(ctx));
+  if (enable && !ctx->ev[0]) {
+    for (int i = 0; i < ws_ctx::MAXEV; ++i) WS_CUDA(cudaEventCreate(&ctx->ev[i]));
+  }
+  ctx->timing = enable != 0;
+  return WS_OK;
+}
+
+ws_status ws_get_stats(const ws_ctx* ctx, ws_stats* out) {
+  if (!ctx || !out) return null_arg("ctx/out");
+  *out = ctx->stats;
+  return WS_OK;
+}
+
+ws_status ws_gradient(ws_ctx* ctx, const uint8_t* img, ws_dims dims, float sigma, uint8_t* grad_q,
+                      float* blur_f32, float* grad_f32, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  if (!(sigma >= 0.f) || sigma > 20.f) {
+    set_error(WS_ERR_INVALID, "sigma must be in [0, 20] (got %g)", (double)sigma);
+    return WS_ERR_INVALID;
+  }
+  if (!img) return null_arg("img");
+  if (!grad_q) return null_arg("grad_q");
+  begin_call(ctx, g);
+  tbegin(ctx, (cudaStream_t)stream);
+  ws_status s = run_gradient(ctx, img, g, dims.ndim == 3, sigma, grad_q, blur_f32, grad_f32, (cudaStream_t)stream);
+  tfinish(ctx);
+  return s;
+}
+
+ws_status ws_watershed(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity, int32_t* labels,
+                       int64_t* num_regions, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  WS_TRY(check_conn(dims, connectivity));
+  if (!grad) return null_arg("grad");
+  if (!labels) return null_arg("labels");
+  begin_call(ctx, g);
+  tbegin(ctx, (cudaStream_t)stream);
+  ws_status s = run_watershed(ctx, grad, g, connectivity, labels, num_regions, (cudaStream_t)stream);
+  tfinish(ctx);
+  return s;
+}
+
+ws_status ws_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, ws_dims dims, int32_t connectivity,
+                       int32_t NL, int32_t* levels, int64_t* counts, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  WS_TRY(check_conn(dims, connectivity));
+  if (NL < 1) {
+    set_error(WS_ERR_INVALID, "NL must be >= 1 (got %d)", NL);
+    return WS_ERR_INVALID;
+  }
+  if (!labels) return null_arg("labels");
+  if (!grad) return null_arg("grad");
+  if (!levels) return null_arg("levels");
+  begin_call(ctx, g);
+  tbegin(ctx, (cudaStream_t)stream);
+  ws_status s = run_waterfall(ctx, labels, grad, g, connectivity, NL, levels, counts, (cudaStream_t)stream);
+  tfinish(ctx);
+  return s;
+}
+
+ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims, int32_t connectivity, int32_t NL,
+                          int32_t* levels_host, int64_t* counts, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  WS_TRY(check_conn(dims, connectivity));
+  if (NL < 1) {
+    set_error(WS_ERR_INVALID, "NL must be >= 1 (got %d)", NL);
+    return WS_ERR_INVALID;
+  }
+  if (!grad_host) return null_arg("grad_host");
+  if (!levels_host) return null_arg("levels_host");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t N = (size_t)g.N;
+  WS_TRY(ctx->h_grad.ensure(N, "segment grad"));
+  WS_TRY(ctx->h_labels.ensure(N * sizeof(int32_t), "segment labels"));
+  WS_TRY(ctx->h_levels.ensure(N * (size_t)NL * sizeof(int32_t), "segment levels"));
+  begin_call(ctx, g);
+  tbegin(ctx, st);
+  WS_CUDA(cudaMemcpyAsync(ctx->h_grad.p, grad_host, N, cudaMemcpyHostToDevice, st));
+  tmark(ctx, st, PH_COPY);
+  WS_TRY(run_watershed(ctx, ctx->h_grad.as<uint8_t>(), g, connectivity, ctx->h_labels.as<int32_t>(), nullptr, st));
+  WS_TRY(run_waterfall(ctx, ctx->h_labels.as<int32_t>(), ctx->h_grad.as<uint8_t>(), g, connectivity, NL,
+                       ctx->h_levels.as<int32_t>(), counts, st));
+  WS_CUDA(cudaMemcpyAsync(levels_host, ctx->h_levels.p, N * (size_t)NL * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  tmark(ctx, st, PH_COPY);
+  WS_CUDA(cudaStreamSynchronize(st));
+  tfinish(ctx);
+  return WS_OK;
+}
+
+ws_status ws_plateau_debug(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity, int32_t* dist,
+                           int32_t* parent, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  WS_TRY(check_conn(dims, connectivity));
+  if (!grad) return null_arg("grad");
+  if (!dist || !parent) return null_arg("dist/parent");
+  begin_call(ctx, g);
+  ws_status s = run_plateau_debug(ctx, grad, g, connectivity, dist, parent, (cudaStream_t)stream);
+  ctx->ev_n = 0;
+  return s;
+}
+
+}  // extern "C"

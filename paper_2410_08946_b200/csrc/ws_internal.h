@@ -1,0 +1,110 @@
+// ws_internal.h — host-side internals shared by the translation units of libws_b200.so.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/ws.h"
+#include "ws_common.cuh"
+
+namespace ws {
+
+// Status carrier for internal functions (converted to ws_status at the ABI).
+struct Err {
+  ws_status st = WS_OK;
+  bool ok() const { return st == WS_OK; }
+};
+
+void set_error(ws_status st, const char* fmt, ...);
+ws_status cuda_fail(cudaError_t e, const char* where);
+
+#define WS_CUDA(call)                                             \
+  do {                                                            \
+    cudaError_t e__ = (call);                                     \
+    if (e__ != cudaSuccess) return ::ws::cuda_fail(e__, #call);   \
+  } while (0)
+
+#define WS_TRY(call)                       \
+  do {                                     \
+    ws_status s__ = (call);                \
+    if (s__ != WS_OK) return s__;          \
+  } while (0)
+
+// A growable device buffer owned by the context.
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ws_status ensure(size_t want, const char* name);
+  void release();
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace ws
+
+struct ws_ctx {
+  int device = 0;
+  int num_sms = 148;
+  ws::Buf aux;        // i32[N]   union-find canonical minima / dense ids (indexed by label)
+  ws::Buf tmpA, tmpB; // f32[N]   gradient pre-pass intermediates
+  ws::Buf flags;      // small device counters / flags
+  ws::Buf blockcnt;   // per-block counts for the representative scan
+  ws::Buf edges;      // u64[cap] RAG edge keys
+  ws::Buf comp;       // i32[R]   component parent (union-find over dense ids)
+  ws::Buf best;       // u64[R]   per-component min-K edge
+  ws::Buf rep_of;     // i32[R]   dense id -> canonical voxel label
+  ws::Buf levelmap;   // i32[R*(NL-1)]
+  ws::Buf lvcount;    // i64[NL]  device-side region counts
+  ws::Buf h_grad, h_labels, h_levels;  // device copies used by ws_segment_host
+  int64_t* pinned = nullptr;           // small pinned host scratch (flags / counts)
+  ws_stats stats{};
+  // per-phase CUDA-event timing (ws_ctx_set_timing)
+  bool timing = false;
+  static constexpr int MAXEV = 64;
+  cudaEvent_t ev[MAXEV] = {};
+  int ev_phase[MAXEV] = {};
+  int ev_n = 0;
+};
+
+namespace ws {
+
+// phases of ws_stats.phase_ms (names in ws_api.cu)
+enum Phase {
+  PH_GRAD_BLUR = 0, PH_GRAD_MAG, PH_WS_INIT, PH_WS_RELAX, PH_WS_SELECT, PH_WS_JUMP, PH_WS_UNION,
+  PH_WS_FIND, PH_WS_RELABEL, PH_WF_DENSE, PH_WF_RAG, PH_WF_LEVELS, PH_WF_MATERIALISE, PH_COPY
+};
+
+// timing marks: tbegin() at the start of a call; tmark(ph) closes the segment since the
+// previous mark and attributes it to phase ph; tfinish() accumulates the segments.
+void tbegin(ws_ctx* ctx, cudaStream_t st);
+void tmark(ws_ctx* ctx, cudaStream_t st, int phase);
+void tfinish(ws_ctx* ctx);
+inline void launched(ws_ctx* ctx, int phase, int n = 1) {
+  ctx->stats.kernel_launches += n;
+  ctx->stats.phase_launches[phase] += n;
+}
+
+// launch helpers (ws_gradient.cu, ws_watershed.cu, ws_waterfall.cu); each returns WS_OK or a
+// CUDA error status and counts its launches into ctx->stats.kernel_launches.
+ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, float sigma,
+                       uint8_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st);
+ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
+                        int32_t* labels, int64_t* num_regions, cudaStream_t st);
+ws_status run_plateau_debug(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
+                            int32_t* dist, int32_t* parent, cudaStream_t st);
+ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g,
+                        int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
+
+// 3-D launch geometry: block (32, 8, 1), grid over (n2, n1, min(n0, 65535)); kernels loop z.
+struct L3 {
+  dim3 grid, block;
+};
+inline L3 launch3(const Geo& g, int bx = 32, int by = 8) {
+  L3 l;
+  l.block = dim3(bx, by, 1);
+  l.grid = dim3((g.n2 + bx - 1) / bx, (g.n1 + by - 1) / by, g.n0 < 65535 ? g.n0 : 65535);
+  return l;
+}
+
+}  // namespace ws

@@ -1,0 +1,176 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element, on the
+same seeded inputs.  Bars: blur/gradient floats within 1e-5 absolute;
+the u8 gradient equal except on agreed boundary straddles (C11); watershed labels, step II
+intermediates and every waterfall level bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+FTOL = 1e-5  # north_star: blur and gradient floats within 1e-5 absolute
+
+
+def _ws():
+    import paper_2410_08946_b200 as ws
+    return ws
+
+
+def agreed_gradient(raw_np, sigma, ndim, dev="cuda"):
+    """Run ws_gradient and check it against the oracle under C11; return the agreed image
+    (the GPU's bytes, which both sides then share) as (torch cuda u8, numpy u8)."""
+    ws = _ws()
+    img = torch.from_numpy(raw_np).to(dev)
+    q, blur, grad = ws.gradient(img, sigma, ndim=ndim, verify=True)
+    ob, og, oq = oracle.gradient(raw_np, sigma, ndim=ndim)
+    assert np.max(np.abs(blur.cpu().numpy() - ob)) <= FTOL
+    assert np.max(np.abs(grad.cpu().numpy() - og)) <= FTOL
+    qn = q.cpu().numpy()
+    diff = qn != oq
+    if diff.any():  # only boundary straddles may differ (|255 g - (k + 1/2)| <= 255 * tol)
+        t = 255.0 * og[diff]
+        assert np.all(np.abs(t - np.floor(t) - 0.5) <= 255 * FTOL), "gradient quantisation mismatch"
+        assert np.all(np.abs(qn[diff].astype(int) - oq[diff].astype(int)) == 1)
+    return q, qn
+
+
+def check_watershed(q_dev, q_np, conn, ndim):
+    ws = _ws()
+    lab, R = ws.watershed(q_dev, conn, ndim=ndim)
+    ref, dist, ptr, Rref = oracle.watershed(q_np, conn, ndim=ndim, dumps=True)
+    got = lab.cpu().numpy()
+    if not np.array_equal(got, ref):
+        bad = np.flatnonzero(got.ravel() != ref.ravel())
+        pytest.fail("watershed mismatch at %d voxels, first %s: got %s want %s" % (
+            bad.size, bad[:5], got.ravel()[bad[:5]], ref.ravel()[bad[:5]]))
+    assert R == Rref
+    return lab, ref
+
+
+def check_waterfall(lab_dev, q_dev, q_np, ref_lab, conn, ndim, NL):
+    ws = _ws()
+    lv, counts = ws.waterfall(lab_dev, q_dev, conn, NL, ndim=ndim)
+    rlv, rcounts = oracle.waterfall(ref_lab, q_np, conn, NL, ndim=ndim)
+    got = lv.cpu().numpy()
+    for k in range(NL):
+        if not np.array_equal(got[k], rlv[k]):
+            bad = np.flatnonzero(got[k].ravel() != rlv[k].ravel())
+            pytest.fail("level %d mismatch at %d voxels" % (k, bad.size))
+    assert list(counts) == [int(c) for c in rcounts]
+    return lv
+
+
+# ---------------------------------------------------------------- configs, reduced sizes
+CASES = [("C1", None), ("C2", (1, 384, 512)), ("C3", (40, 48, 56)), ("C4", (24, 96, 80)),
+         ("C5", (6, 145, 145))]
+
+
+@pytest.mark.parametrize("name,shape", CASES)
+def test_pipeline_parity_config(name, shape):
+    c = synth.CONFIGS[name]
+    raw = synth.make_config_image(name, shape=shape, device="cuda").cpu().numpy()
+    q, qn = agreed_gradient(raw, c.sigma, c.ndim)
+    lab, ref = check_watershed(q, qn, c.conn, c.ndim)
+    check_waterfall(lab, q, qn, ref, c.conn, c.ndim, c.NL)
+
+
+@pytest.mark.parametrize("conn,ndim,shape", [(4, 2, (3, 37, 61)), (8, 2, (2, 45, 33)), (6, 3, (13, 17, 70)),
+                                             (26, 3, (9, 21, 35)), (4, 2, (1, 1, 300)), (6, 3, (1, 23, 29))])
+@pytest.mark.parametrize("levels", [2, 4, 16])
+def test_random_plateau_images(conn, ndim, shape, levels):
+    """Plateau-forcing inputs: random values in {0..levels-1}; every plateau
+    kind, several tiles and ragged tails in every axis."""
+    g = synth.random_plateau_image(shape, levels, seed=levels * 100 + conn)
+    qn = g.numpy()
+    q = g.cuda()
+    lab, ref = check_watershed(q, qn, conn, ndim)
+    check_waterfall(lab, q, qn, ref, conn, ndim, 6)
+
+
+@pytest.mark.parametrize("conn,ndim,shape", [(4, 2, (2, 33, 47)), (8, 2, (1, 40, 40)), (6, 3, (7, 19, 23)),
+                                             (26, 3, (6, 11, 17))])
+def test_plateau_intermediates(conn, ndim, shape):
+    """T2: step I+II intermediates (BFS distances and parent pointers) exact."""
+    ws = _ws()
+    g = synth.random_plateau_image(shape, 3, seed=conn)
+    dist, parent = ws.plateau_debug(g.cuda(), conn, ndim=ndim)
+    _, rdist, rptr, _ = oracle.watershed(g.numpy(), conn, ndim=ndim, dumps=True)
+    assert np.array_equal(dist.cpu().numpy(), rdist)
+    assert np.array_equal(parent.cpu().numpy().astype(np.int64), rptr)
+
+
+def test_edge_cases():
+    ws = _ws()
+    cases = [
+        (np.zeros((1, 1, 1), np.uint8), 4, 2),                 # single voxel (C4)
+        (np.zeros((1, 1, 1), np.uint8), 26, 3),
+        (np.full((1, 50, 70), 3, np.uint8), 8, 2),             # one giant minimal plateau
+        (np.full((5, 9, 40), 7, np.uint8), 6, 3),
+        (np.arange(4096, dtype=np.int64).reshape(1, 64, 64).astype(np.uint8), 4, 2),  # ramps
+        (np.array([[[75] + [89] * 10 + [81]]], np.uint8), 4, 2),  # P:364 example
+        (np.array([[[75] + [89] * 3000 + [81]]], np.uint8), 4, 2),  # long plateau (deep BFS)
+        (np.tile(np.array([0, 255], np.uint8), 300).reshape(1, 20, 30), 4, 2),  # checkerboard rows
+    ]
+    # serpentine corridor plateau: long BFS depth across many tiles
+    snake = np.full((1, 64, 64), 50, np.uint8)
+    snake[0, 1::4, :-1] = 200
+    snake[0, 3::4, 1:] = 200
+    snake[0, 0, 0] = 1
+    cases.append((snake, 4, 2))
+    for qn, conn, ndim in cases:
+        q = torch.from_numpy(qn).cuda()
+        lab, ref = check_watershed(q, qn, conn, ndim)
+        check_waterfall(lab, q, qn, ref, conn, ndim, 4)
+        check_waterfall(lab, q, qn, ref, conn, ndim, 1)
+
+
+def test_depth1_volume_matches_2d_on_gpu():
+    ws = _ws()
+    g = synth.random_plateau_image((1, 31, 45), 4, seed=9).cuda()
+    a, _ = ws.watershed(g, 6, ndim=3)
+    b, _ = ws.watershed(g, 4, ndim=2)
+    assert torch.equal(a, b)
+
+
+def test_determinism_repeated_runs():
+    ws = _ws()
+    raw = synth.make_config_image("C4", shape=(16, 64, 64), device="cuda")
+    q = ws.gradient(raw, 1.0, ndim=3)
+    a, _ = ws.watershed(q, 6)
+    la, _ = ws.waterfall(a, q, 6, 6)
+    for _ in range(3):
+        b, _ = ws.watershed(q, 6)
+        lb, _ = ws.waterfall(b, q, 6, 6)
+        assert torch.equal(a, b) and torch.equal(la, lb)
+
+
+def test_segment_host_matches_device_path():
+    ws = _ws()
+    raw = synth.make_config_image("C3", shape=(20, 30, 40), device="cuda")
+    q = ws.gradient(raw, 1.0, ndim=3)
+    lab, _ = ws.watershed(q, 6)
+    lv, counts = ws.waterfall(lab, q, 6, 6)
+    lh, ch = ws.segment_host(q.cpu().contiguous(), 6, 6)
+    assert torch.equal(lh, lv.cpu()) and ch == counts
+
+
+def test_abi_errors_on_device():
+    ws = _ws()
+    q = torch.zeros((2, 3, 4), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ws.WsError, match="WS_ERR_INVALID"):
+        ws.watershed(q, 6, ndim=2)      # conn/ndim mismatch
+    with pytest.raises(ws.WsError, match="WS_ERR_INVALID"):
+        ws.watershed(q, 4, ndim=3)
+    lab, _ = ws.watershed(q, 4)
+    with pytest.raises(ws.WsError, match="WS_ERR_INVALID"):
+        ws.waterfall(lab, q, 4, 0)
+    with pytest.raises(ws.WsError, match="WS_ERR_INVALID"):
+        ws.gradient(q, -1.0)
+    # outputs untouched on error
+    out = torch.full((2, 3, 4), -7, dtype=torch.int32, device="cuda")
+    with pytest.raises(ws.WsError):
+        ws.watershed(q, 8, ndim=3, out=out)
+    assert bool((out == -7).all())
