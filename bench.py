@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the hot path (ws_watershed + ws_waterfall NL=6) on B200.
+
+Contract (task statement): ``python bench.py --gpus N --steps K --warmup W`` prints ONE JSON
+line on rank 0.  A step = one ws_watershed + one ws_waterfall(NL) over the workload's u8
+gradient volume, inputs resident in HBM.  Default workload = config C4 (the metric's 805-Mvox
+1024x1024x768 microCT-like volume, 6-conn, NL=6, sigma=1 gradient), see DESIGN.md.
+
+  --impl reference   the oracle (oracle/, plain single-threaded C++) on the host cores, on a
+                     bounded sample of the same workload (rank 0 only; other ranks exit 0).
+N > 1 (torchrun): every rank processes its own full-size volume (seed + rank): independent
+problems, no data-path collective ("scaling": "weak").  Timing: CUDA events on the launching
+stream, barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mvoxel/s watershed+NL=6 waterfall (800 Mvox 3D) at 1/2/4/8 B200; % HBM peak"
+UNIT = "Mvoxel/s"
+PAPER_CONTEXT = ("paper (P:819 Table 3): 4000x4000x50 raw u8 microCT, watershed only, PRUF 6-conn on an "
+                 "RTX 3060 Ti: 1357.75 ms = 589 Mvox/s; no waterfall timings are printed (Figs. 9-10 stripped)")
+
+# algorithmic (compulsory) bytes per voxel of each phase's kernel(s), per launch
+ALG_BYTES = {
+    "watershed.init": 5,        # read I (1) + write L (4)
+    "watershed.relax": 5,       # read I + L per round
+    "watershed.select": 9,      # read I + L, write L
+    "watershed.jump": 8,        # read L, write L
+    "watershed.union": 5,       # read I + L
+    "watershed.find": 8,        # read L, write L
+    "watershed.relabel": 8,     # read L, write L
+    "waterfall.dense_ids": 4,   # read labels
+    "waterfall.rag": 5,         # read labels + I
+    "waterfall.materialise": None,  # read labels + write NL levels: 4 + 4 NL
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--shape", default=None, help="override shape, e.g. 64,128,128 (testing only)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-slices", type=int, default=32)
+    ap.add_argument("--ref-sample-slices", type=int, default=4)
+    return ap.parse_args()
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def workload(args):
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    shape = tuple(int(s) for s in args.shape.split(",")) if args.shape else cfg.shape
+    return cfg, shape
+
+
+def cpu_oracle_rate(grad_np, cfg, slices):
+    """Oracle (single-threaded C++) watershed + waterfall on the first ``slices`` slices of
+    the gradient volume: returns (Mvox/s, seconds, sample description)."""
+    import oracle
+    sub = grad_np[:slices].copy() if cfg.ndim == 3 else grad_np[: max(1, slices)].copy()
+    oracle.build()
+    t0 = time.perf_counter()
+    lab = oracle.watershed(sub, cfg.conn, ndim=cfg.ndim)
+    oracle.waterfall(lab, sub, cfg.conn, cfg.NL, ndim=cfg.ndim)
+    dt = time.perf_counter() - t0
+    return sub.size / dt / 1e6, dt, "first %d slices %s of the same gradient volume (%d voxels)" % (
+        sub.shape[0], "x".join(map(str, sub.shape)), sub.size)
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    import torch
+    import oracle
+    import synth
+    cfg, shape = workload(args)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    sl = max(1, min(args.ref_sample_slices, shape[0]))
+    raw = synth.make_config_image(cfg.name, device=dev, shape=shape)[: sl + 8].cpu().numpy()
+    _, _, q = oracle.gradient(raw, cfg.sigma, ndim=cfg.ndim)   # untimed input preparation
+    grad = np.ascontiguousarray(q[:sl])
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        lab = oracle.watershed(grad, cfg.conn, ndim=cfg.ndim)
+        oracle.waterfall(lab, grad, cfg.conn, cfg.NL, ndim=cfg.ndim)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = grad.size / (ms / 1e3) / 1e6
+    sample = "first %d slices (%s, %d voxels) of the %s workload per step" % (
+        sl, "x".join(map(str, grad.shape)), grad.size, cfg.name)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8/i32", "data": "synthetic",
+            "config": {"workload": cfg.desc, "shape": list(shape), "conn": cfg.conn, "NL": cfg.NL,
+                       "sigma": cfg.sigma, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import synth
+    import paper_2410_08946_b200 as ws
+
+    world, rank, local = dist_setup(args)
+    cfg, shape = workload(args)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    N = int(np.prod(shape))
+    NL, conn = cfg.NL, cfg.conn
+    ctx = ws.Context(dev.index)
+
+    # input generation (untimed): seeded raw volume, one per rank (independent problems)
+    raw = synth.make_config_image(cfg.name, device=dev, shape=shape, seed_offset=1000 * rank)
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- gradient pre-pass (timed separately; not part of the metric step)
+    grad = torch.empty_like(raw)
+    for _ in range(2):
+        ws.gradient(raw, cfg.sigma, ndim=cfg.ndim, ctx=ctx, out=grad)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    GK = 3
+    for _ in range(GK):
+        ws.gradient(raw, cfg.sigma, ndim=cfg.ndim, ctx=ctx, out=grad)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    grad_ms = e0.elapsed_time(e1) / GK
+    del raw
+    torch.cuda.empty_cache()
+
+    labels = torch.empty(shape, dtype=torch.int32, device=dev)
+    levels = torch.empty((NL,) + tuple(shape), dtype=torch.int32, device=dev)
+
+    def step():
+        ws.watershed(grad, conn, ndim=cfg.ndim, ctx=ctx, out=labels)
+        s1 = ctx.stats()
+        ws.waterfall(labels, grad, conn, NL, ndim=cfg.ndim, ctx=ctx, out=levels)
+        s2 = ctx.stats()
+        return s1, s2
+
+    for _ in range(args.warmup):
+        step()
+    ctx.set_timing(True)
+    clocks = Clocks(dev.index)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    phase_ms, phase_launch, launches, stats = {}, {}, 0, []
+    for _ in range(args.steps):
+        s1, s2 = step()
+        stats.append((s1, s2))
+        for s in (s1, s2):
+            launches += s["kernel_launches"]
+            for k, v in s["phases"].items():
+                phase_ms[k] = phase_ms.get(k, 0.0) + v["ms"]
+                phase_launch[k] = phase_launch.get(k, 0) + v["launches"]
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ctx.set_timing(False)
+    ms_local = t_start.elapsed_time(t_end) / args.steps
+    ms = max_over_ranks(ms_local, world)
+    value = N * world / (ms / 1e3) / 1e6
+
+    # ---- roofline of the dominant kernel (phase with the largest share of the step)
+    peak, peak_src = load_peak()
+    traffic = load_traffic()
+    alg = dict(ALG_BYTES)
+    alg["waterfall.materialise"] = 4 + 4 * NL
+    cand = {k: v for k, v in phase_ms.items() if alg.get(k)}
+    dom = max(cand, key=cand.get)
+    per_launch_ms = phase_ms[dom] / max(1, phase_launch[dom])
+    achieved = alg[dom] * N / (per_launch_ms / 1e3) / 1e9
+    tr = traffic.get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": tr.get("bytes_per_launch") if tr else None,
+                "alg_bytes_per_voxel": alg[dom], "avg_launch_ms": per_launch_ms,
+                "share_of_step": phase_ms[dom] / (ms_local * args.steps), "peak_source": peak_src}
+    step_bytes = 38 if NL == 6 else (5 + 9 + 4 * NL)
+    step_roof = {"alg_bytes_per_voxel": step_bytes, "achieved_GBps": step_bytes * N / (ms / 1e3) / 1e9,
+                 "frac": step_bytes * N / (ms / 1e3) / 1e9 / peak}
+
+    # ---- end to end through the public API with HOST buffers (ws_segment_host)
+    e2e = None
+    if not args.no_e2e:
+        gh = torch.empty(shape, dtype=torch.uint8, pin_memory=True)
+        gh.copy_(grad)
+        lh = torch.empty((NL,) + tuple(shape), dtype=torch.int32, pin_memory=True)
+        ws.segment_host(gh, conn, NL, ndim=cfg.ndim, ctx=ctx, out=lh)  # warm
+        barrier(world)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            ws.segment_host(gh, conn, NL, ndim=cfg.ndim, ctx=ctx, out=lh)
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        ems = max_over_ranks(a.elapsed_time(b) / args.e2e_steps, world)
+        e2e = {"value": N * world / (ems / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": N,
+               "d2h_bytes_per_step": NL * N * 4, "ms_per_step": ems, "api": "ws_segment_host"}
+        del gh, lh
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, sample = cpu_oracle_rate(grad.cpu().numpy(), cfg, args.cpu_sample_slices)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, "seconds": dt}
+
+    s1, s2 = stats[-1]
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8/i32", "data": "synthetic",
+            "config": {"workload": cfg.desc, "name": cfg.name, "shape": list(shape), "conn": conn, "NL": NL,
+                       "sigma": cfg.sigma, "global_voxels": N * world,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (grad %.0f MB, labels %.0f MB, levels %.0f MB)" % (
+                           N / 1e6, 4 * N / 1e6, 4 * NL * N / 1e6)},
+            "roofline": roofline, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+            "gradient_prepass": {"ms": grad_ms, "Mvoxel_per_s": N / (grad_ms / 1e3) / 1e6},
+            "phases_ms_per_step": {k: v / args.steps for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
+            "input_stats": {"regions": s1["n_regions"], "edges": s2["n_edges"],
+                            "plateau_rounds": s1["plateau_rounds"], "level_counts": s2["level_counts"][:NL]},
+            "context": PAPER_CONTEXT,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -49,6 +49,7 @@ struct ws_ctx {
   ws::Buf aux;        // i32[N]   union-find canonical minima / dense ids (indexed by label)
   ws::Buf tmpA, tmpB; // f32[N]   gradient pre-pass intermediates
   ws::Buf flags;      // small device counters / flags
+  ws::Buf tiles;      // u8[3 * ntiles] step II active-tile flags
   ws::Buf blockcnt;   // per-block counts for the representative scan
   ws::Buf edges;      // u64[cap] RAG edge keys
   ws::Buf comp;       // i32[R]   component parent (union-find over dense ids)

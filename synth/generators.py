@@ -216,18 +216,20 @@ CONFIGS = {
 }
 
 
-def make_config_image(name: str, device="cpu", shape=None) -> torch.Tensor:
-    """Raw u8 input of config ``name`` (optionally at a reduced ``shape``)."""
+def make_config_image(name: str, device="cpu", shape=None, seed_offset: int = 0) -> torch.Tensor:
+    """Raw u8 input of config ``name`` (optionally at a reduced ``shape``; ``seed_offset``
+    gives independent volumes of the same recipe, e.g. one per rank)."""
     c = CONFIGS[name]
     s = tuple(shape) if shape is not None else c.shape
+    seed = c.seed + seed_offset
     if name == "C1":
-        return cameraman_like(s[1], s[2], c.seed, device)
+        return cameraman_like(s[1], s[2], seed, device)
     if name == "C2":
-        return disc_composite(s[1], s[2], c.seed, device)
+        return disc_composite(s[1], s[2], seed, device)
     if name == "C3":
-        return knee_like(s[0], s[1], s[2], c.seed, device)
+        return knee_like(s[0], s[1], s[2], seed, device)
     if name == "C4":
-        return microct_like(s[0], s[1], s[2], c.seed, device)
+        return microct_like(s[0], s[1], s[2], seed, device)
     if name == "C5":
-        return hsi_batch(s[0], s[1], s[2], c.seed, device)
+        return hsi_batch(s[0], s[1], s[2], seed, device)
     raise KeyError(name)
