@@ -50,6 +50,8 @@ struct ws_ctx {
   ws::Buf tmpA, tmpB; // f32[N]   gradient pre-pass intermediates
   ws::Buf flags;      // small device counters / flags
   ws::Buf tiles;      // u8[3 * ntiles] step II active-tile flags
+  ws::Buf roots;      // i32[cap]  step III roots (self-loops), compact list
+  ws::Buf rootc;      // i32[cap]  canonical label per listed root
   ws::Buf blockcnt;   // per-block counts for the representative scan
   ws::Buf edges;      // u64[cap] RAG edge keys
   ws::Buf comp;       // i32[R]   component parent (union-find over dense ids)

@@ -194,11 +194,15 @@ __global__ void k_edge_min(uint64_t* __restrict__ edges, long long E, const int*
   }
 }
 
+// find with path halving (see ws_watershed.cu uf_find)
 __device__ __forceinline__ int c_find(int* c, int x) {
   while (true) {
     const int y = ld_cg(c + x);
     if (y == x) return x;
-    x = y;
+    const int z = ld_cg(c + y);
+    if (z == y) return y;
+    __stcg(c + x, z);
+    x = z;
   }
 }
 
@@ -217,10 +221,20 @@ __global__ void k_hook(const uint64_t* __restrict__ best, int* comp, int n) {
   }
 }
 
+// read-only find: k_flatten must not path-halve, or a halving store could land after the
+// owner's flattening store and leave a non-root parent behind
+__device__ __forceinline__ int c_find_ro(const int* c, int x) {
+  while (true) {
+    const int y = ld_cg(c + x);
+    if (y == x) return x;
+    x = y;
+  }
+}
+
 __global__ void k_flatten(int* comp, int n, const int* __restrict__ rep_of, int* __restrict__ levelmap,
                           int stride, int col, unsigned long long* nroots) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    const int r = c_find(comp, c);
+    const int r = c_find_ro(comp, c);
     comp[c] = r;
     levelmap[(size_t)c * stride + col] = __ldg(rep_of + r);
     const unsigned act = __activemask();

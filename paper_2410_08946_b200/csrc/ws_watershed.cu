@@ -1,28 +1,37 @@
 // ws_watershed.cu — steps I-IV of PRUF (Alg. 1) + canonical relabel, sm_100a.
 //
 // Tile design: the volume is cut into tiles of 2048 voxels
-// (3-D 32x8x8, 2-D 64x32) staged in shared memory with a halo.
+// (3-D 32x8x8, 2-D 64x32) staged in shared memory with a halo.  Intensities are staged as
+// 16-bit values with an out-of-volume sentinel (0xFFFF: never lower, never equal), so the
+// stencil loops carry no bounds checks.
 //
 //   k_relax_first  step I classification (Alg. 1 l.1-10) fused with the first round of the
 //                  step II distance relaxation (Alg. 3 l.7-8) inside each tile      [all tiles]
 //   k_relax_round  further step II rounds, only on tiles whose halo changed       [active tiles]
 //   k_resolve      step I/II pointers (Eq. 1; C5/C6 selection) + tile-local pointer
-//                  jumping in shared memory (step III inside the tile)  -> P = aux  [all tiles]
-//   k_jump         step III across tiles: chase exits to the self-loop roots (l.19-23/28-29)
-//   k_union        step IV Union over q > p (l.24-27), lock-free min-root CAS
-//   k_find         step IV Find (l.28-29) + warp-aggregated canonical atomicMin (C7)
-//   k_relabel      labels = canonical minimum of the root
+//                  jumping in shared memory (step III inside the tile)  -> P        [all tiles]
+//   k_jump         step III across tiles: chase exits to the self-loop roots (l.19-23/28-29);
+//                  per-root minimum voxel index (warp-aggregated atomicMax on INT_MAX - p);
+//                  compact list of roots
+//   k_union        step IV Union over q > p (l.24-27), lock-free min-root CAS on the roots
+//   k_root_merge / k_root_label / k_root_store   step IV Find (l.28-29) on the root list only:
+//                  canonical label (C7) of every final region, stored into P[root]
+//   k_relabel      labels[p] = canonical label of p's root
 //
 // Arrays: L = the caller's `labels` (i32[N]); during step II it holds the plateau distance
 // code of ws_common.cuh (L >= 0: d = 0; L < 0: -1 - (d << 5)).  P = ctx->aux (i32[N]) holds
-// pointers from k_resolve on.  After k_jump, L[r] of every root r is reused as the canonical
-// minimum of r's region, and finally L[p] = L[P[p]].
+// pointers from k_resolve on.  From k_jump on, L[r] of a root r holds INT_MAX - (smallest
+// voxel index reaching r); all other L entries are dead until k_relabel writes the output.
+#include <climits>
+
 #include "ws_internal.h"
 
 namespace ws {
 
 constexpr int NT = 256;
 constexpr int INF = DUNREACHED;
+using u16 = unsigned short;
+constexpr int OOB = 0xFFFF;  // out-of-volume intensity sentinel in shared memory
 
 template <int CONN> struct Tile {
   static constexpr bool is3d = Conn<CONN>::is3d;
@@ -62,7 +71,7 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int ntx, int nty) {
   return c;
 }
 
-// voxel k of this thread inside the tile
+// voxel k of this thread inside the tile: j = threadIdx.x + k * NT (x fastest)
 template <int CONN>
 __device__ __forceinline__ void my_voxel(int k, int& lx, int& ly, int& lz) {
   using T = Tile<CONN>;
@@ -72,16 +81,23 @@ __device__ __forceinline__ void my_voxel(int k, int& lx, int& ly, int& lz) {
   lz = j / (T::TX * T::TY);
 }
 
+// row-wise staging: one warp per (sz, sy) row, lanes along x
 template <int CONN, int H>
-__device__ __forceinline__ void load_I(const uint8_t* __restrict__ I, const Geo& g, const TileCoord& c, uint8_t* sI) {
+__device__ __forceinline__ void load_I(const uint8_t* __restrict__ I, const Geo& g, const TileCoord& c, u16* sI) {
   using B = Box<CONN, H>;
-  for (int s = threadIdx.x; s < B::S; s += NT) {
-    const int sx = s % B::SX, sy = (s / B::SX) % B::SY, sz = s / (B::SX * B::SY);
-    const int gx = c.bx + sx - H, gy = c.by + sy - H, gz = c.bz + sz - B::HZ;
-    uint8_t v = 0;
-    if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
-      v = __ldg(I + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
-    sI[s] = v;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < B::SY * B::SZ; r += NT / 32) {
+    const int sy = r % B::SY, sz = r / B::SY;
+    const int gy = c.by + sy - H, gz = c.bz + sz - B::HZ;
+    const bool rowok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
+    const uint8_t* row = I + ((size_t)(rowok ? gz : 0) * g.plane + (size_t)(rowok ? gy : 0) * g.n2);
+#pragma unroll
+    for (int sx = lane; sx < B::SX; sx += 32) {
+      const int gx = c.bx + sx - H;
+      int v = OOB;
+      if (rowok && (unsigned)gx < (unsigned)g.n2) v = __ldg(row + gx);
+      sI[r * B::SX + sx] = (u16)v;
+    }
   }
 }
 
@@ -89,13 +105,19 @@ __device__ __forceinline__ void load_I(const uint8_t* __restrict__ I, const Geo&
 template <int CONN>
 __device__ __forceinline__ void load_D(const int* L, const Geo& g, const TileCoord& c, int* sD) {
   using B = Box<CONN, 1>;
-  for (int s = threadIdx.x; s < B::S; s += NT) {
-    const int sx = s % B::SX, sy = (s / B::SX) % B::SY, sz = s / (B::SX * B::SY);
-    const int gx = c.bx + sx - 1, gy = c.by + sy - 1, gz = c.bz + sz - B::HZ;
-    int d = INF;
-    if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
-      d = dec_d(L[(size_t)gz * g.plane + (size_t)gy * g.n2 + gx]);
-    sD[s] = d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < B::SY * B::SZ; r += NT / 32) {
+    const int sy = r % B::SY, sz = r / B::SY;
+    const int gy = c.by + sy - 1, gz = c.bz + sz - B::HZ;
+    const bool rowok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
+    const int* row = L + ((size_t)(rowok ? gz : 0) * g.plane + (size_t)(rowok ? gy : 0) * g.n2);
+#pragma unroll
+    for (int sx = lane; sx < B::SX; sx += 32) {
+      const int gx = c.bx + sx - 1;
+      int d = INF;
+      if (rowok && (unsigned)gx < (unsigned)g.n2) d = dec_d(row[gx]);
+      sD[r * B::SX + sx] = d;
+    }
   }
 }
 
@@ -116,7 +138,7 @@ __device__ __forceinline__ void mark_neighbours(int t, int ntx, int nty, int ntz
   if (i == 0) *any = 1;
 }
 
-// one in-tile relaxation sweep loop until the tile converges (chaotic, in place)
+// in-tile relaxation sweeps until the tile converges (chaotic, in place)
 template <int CONN, int H>
 __device__ __forceinline__ void relax_tile(int* sD, const int* my, const unsigned* eqm, int* limit) {
   using B = Box<CONN, H>;
@@ -128,14 +150,12 @@ __device__ __forceinline__ void relax_tile(int* sD, const int* my, const unsigne
       const unsigned m = eqm[k];
       if (!m) continue;
       const int s = my[k];
-      int best = sD[s];
+      const int cur = sD[s];
+      int best = cur;
 #pragma unroll
       for (int i = 0; i < CONN; ++i)
-        if (m & (1u << i)) {
-          const int dq = sD[s + B::off(i)] + 1;
-          best = dq < best ? dq : best;
-        }
-      if (best < sD[s]) {
+        if (m & (1u << i)) best = min(best, sD[s + B::off(i)] + 1);
+      if (best < cur) {
         sD[s] = best;
         ch = true;
         if (best >= INF - 1) *limit = 1;
@@ -145,6 +165,12 @@ __device__ __forceinline__ void relax_tile(int* sD, const int* my, const unsigne
   }
 }
 
+template <int CONN>
+__device__ __forceinline__ bool on_tile_border(int lx, int ly, int lz) {
+  using T = Tile<CONN>;
+  return lx == 0 || lx == T::TX - 1 || ly == 0 || ly == T::TY - 1 || (T::is3d && (lz == 0 || lz == T::TZ - 1));
+}
+
 // ------------------------------------------- step I + first step II round (all tiles)
 template <int CONN>
 __global__ void __launch_bounds__(NT) k_relax_first(const uint8_t* __restrict__ I, int* __restrict__ L, Geo g,
@@ -152,35 +178,26 @@ __global__ void __launch_bounds__(NT) k_relax_first(const uint8_t* __restrict__ 
                                                      uint8_t* hasplat, int* flags) {
   using T = Tile<CONN>;
   using B2 = Box<CONN, 2>;
-  __shared__ uint8_t sI[B2::S];
+  using B1 = Box<CONN, 1>;
+  __shared__ u16 sI[B2::S];
   __shared__ int sD[B2::S];
   const int t = blockIdx.x;
   const TileCoord c = tile_coord<CONN>(t, ntx, nty);
   load_I<CONN, 2>(I, g, c, sI);
   __syncthreads();
   // classify the tile + 1-voxel halo: lower -> 0, plateau without lower -> INF (Alg. 1 l.3-10)
-  {
-    using B1 = Box<CONN, 1>;
-    for (int s = threadIdx.x; s < B1::S; s += NT) {
-      const int sx = s % B1::SX, sy = (s / B1::SX) % B1::SY, sz = s / (B1::SX * B1::SY);
-      const int lx = sx - 1, ly = sy - 1, lz = sz - B1::HZ;
-      const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
-      const int s2 = B2::at(lz, ly, lx);
-      if (!((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)) {
-        sD[s2] = INF;
-        continue;
-      }
-      const int v = sI[s2];
-      bool lower = false, eq = false;
+  for (int s = threadIdx.x; s < B1::S; s += NT) {
+    const int sx = s % B1::SX, sy = (s / B1::SX) % B1::SY, sz = s / (B1::SX * B1::SY);
+    const int s2 = B2::at(sz - B1::HZ, sy - 1, sx - 1);
+    const int v = sI[s2];
+    bool lower = false, eq = false;
 #pragma unroll
-      for (int i = 0; i < CONN; ++i) {
-        if (!nb_in<CONN>(g, gz, gy, gx, i)) continue;
-        const int nv = sI[s2 + B2::off(i)];
-        lower |= nv < v;
-        eq |= nv == v;
-      }
-      sD[s2] = lower ? 0 : (eq ? INF : 0);
+    for (int i = 0; i < CONN; ++i) {
+      const int nv = sI[s2 + B2::off(i)];
+      lower |= nv < v;
+      eq |= nv == v;
     }
+    sD[s2] = (v == OOB) ? INF : (lower ? 0 : (eq ? INF : 0));
   }
   __syncthreads();
   int my[T::VPT];
@@ -190,18 +207,16 @@ __global__ void __launch_bounds__(NT) k_relax_first(const uint8_t* __restrict__ 
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
     my[k] = B2::at(lz, ly, lx);
-    eqm[k] = 0;
-    if (gx < g.n2 && gy < g.n1 && gz < g.n0 && sD[my[k]] == INF) {
-      const int v = sI[my[k]];
-      unsigned m = 0;
+    const int v = sI[my[k]];
+    unsigned m = 0;
+    if (v != OOB && sD[my[k]] == INF) {
 #pragma unroll
       for (int i = 0; i < CONN; ++i)
-        if (nb_in<CONN>(g, gz, gy, gx, i) && sI[my[k] + B2::off(i)] == v) m |= 1u << i;
-      eqm[k] = m;
+        if (sI[my[k] + B2::off(i)] == v) m |= 1u << i;
       any_plat = true;
     }
+    eqm[k] = m;
   }
   relax_tile<CONN, 2>(sD, my, eqm, flags + 1);
   bool border = false;
@@ -209,13 +224,10 @@ __global__ void __launch_bounds__(NT) k_relax_first(const uint8_t* __restrict__ 
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
-    if (!(gx < g.n2 && gy < g.n1 && gz < g.n0)) continue;
+    if (sI[my[k]] == OOB) continue;
     const int d = sD[my[k]];
-    L[(size_t)gz * g.plane + (size_t)gy * g.n2 + gx] = eqm[k] ? enc(d, DIR_NONE) : 0;
-    if (eqm[k] && d != INF &&
-        (lx == 0 || lx == T::TX - 1 || ly == 0 || ly == T::TY - 1 || (T::is3d && (lz == 0 || lz == T::TZ - 1))))
-      border = true;
+    L[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = eqm[k] ? enc(d, DIR_NONE) : 0;
+    if (eqm[k] && d != INF && on_tile_border<CONN>(lx, ly, lz)) border = true;
   }
   const int hp = __syncthreads_or(any_plat);
   if (threadIdx.x == 0) hasplat[t] = hp ? 1 : 0;
@@ -231,7 +243,7 @@ __global__ void __launch_bounds__(NT) k_relax_round(const uint8_t* __restrict__ 
   using B = Box<CONN, 1>;
   const int t = blockIdx.x;
   if (!cur[t] || !hasplat[t]) return;
-  __shared__ uint8_t sI[B::S];
+  __shared__ u16 sI[B::S];
   __shared__ int sD[B::S];
   const TileCoord c = tile_coord<CONN>(t, ntx, nty);
   load_I<CONN, 1>(I, g, c, sI);
@@ -243,19 +255,16 @@ __global__ void __launch_bounds__(NT) k_relax_round(const uint8_t* __restrict__ 
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
     my[k] = B::at(lz, ly, lx);
-    eqm[k] = 0;
-    d0[k] = 0;
-    if (gx < g.n2 && gy < g.n1 && gz < g.n0 && sD[my[k]] > 0) {  // plateau voxel (d >= 1)
-      d0[k] = sD[my[k]];
-      const int v = sI[my[k]];
-      unsigned m = 0;
+    const int v = sI[my[k]];
+    d0[k] = sD[my[k]];
+    unsigned m = 0;
+    if (v != OOB && d0[k] > 0) {  // plateau voxel (d >= 1)
 #pragma unroll
       for (int i = 0; i < CONN; ++i)
-        if (nb_in<CONN>(g, gz, gy, gx, i) && sI[my[k] + B::off(i)] == v) m |= 1u << i;
-      eqm[k] = m;
+        if (sI[my[k] + B::off(i)] == v) m |= 1u << i;
     }
+    eqm[k] = m;
   }
   relax_tile<CONN, 1>(sD, my, eqm, flags + 1);
   bool border = false;
@@ -267,8 +276,7 @@ __global__ void __launch_bounds__(NT) k_relax_round(const uint8_t* __restrict__ 
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
     L[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = enc(d, DIR_NONE);
-    if (lx == 0 || lx == T::TX - 1 || ly == 0 || ly == T::TY - 1 || (T::is3d && (lz == 0 || lz == T::TZ - 1)))
-      border = true;
+    if (on_tile_border<CONN>(lx, ly, lz)) border = true;
   }
   if (__syncthreads_or(border)) mark_neighbours<CONN>(t, ntx, nty, ntz, next, flags);
 }
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(NT) k_resolve(const uint8_t* __restrict__ I, c
                                                 int ntx, int nty, int* __restrict__ P, int* __restrict__ dist) {
   using T = Tile<CONN>;
   using B = Box<CONN, 1>;
-  __shared__ uint8_t sI[B::S];
+  __shared__ u16 sI[B::S];
   __shared__ int sD[B::S];
   __shared__ short sP[T::V];  // local target, -1 = leaves the tile
   __shared__ int sG[T::V];    // global target when leaving the tile
@@ -294,41 +302,39 @@ __global__ void __launch_bounds__(NT) k_resolve(const uint8_t* __restrict__ I, c
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
     const int j = threadIdx.x + k * NT;
-    const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
-    if (!(gx < g.n2 && gy < g.n1 && gz < g.n0)) {
+    const int s = B::at(lz, ly, lx);
+    const int v = sI[s];
+    if (v == OOB) {
       sP[j] = (short)j;
       continue;
     }
-    const int s = B::at(lz, ly, lx);
-    const int v = sI[s];
-    int m = 256, dm = -1;
+    int m = 0x10000, dm = 0;
     unsigned eqm = 0;
 #pragma unroll
     for (int i = 0; i < CONN; ++i) {
-      if (!nb_in<CONN>(g, gz, gy, gx, i)) continue;
       const int nv = sI[s + B::off(i)];
       if (nv <= m) { m = nv; dm = i; }  // Eq. 1: max index among the minima
       if (nv == v) eqm |= 1u << i;
     }
     int dir = DIR_NONE, dd = 0;
-    if (dm >= 0 && m < v) {
+    bool minimal = (m > v);  // strict single-voxel minimum (or a 1-voxel image, C4)
+    if (m < v) {
       dir = dm;                               // steepest descent (S = 0)
-    } else if (dm >= 0 && m == v) {           // plateau voxel without a lower neighbour
+    } else if (m == v) {                      // plateau voxel without a lower neighbour
       dd = sD[s];
       if (dd != INF) {                        // non-minimal plateau: BFS parent (C5/C6)
 #pragma unroll
         for (int i = 0; i < CONN; ++i)
           if ((eqm & (1u << i)) && sD[s + B::off(i)] == dd - 1) dir = i;
       } else {                                // minimal plateau: state 2 -> q, state 3 -> root
+        minimal = true;
         dir = dm >= Conn<CONN>::nfwd ? dm : DIR_NONE;
       }
     }
-    const int p = (int)((size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
+    const int p = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx);
     if (DEBUG) {
-      const bool term = (dir == DIR_NONE);
-      const bool minimal = (dm < 0 || m > v || (m == v && dd == INF));
       dist[p] = minimal ? -1 : dd;
-      P[p] = (term || minimal) ? p : p + nb_off<CONN>(g, dir);  // oracle: minimal plateaux are terminals
+      P[p] = (dir == DIR_NONE || minimal) ? p : p + nb_off<CONN>(g, dir);  // oracle: minima are terminals
       continue;
     }
     if (dir == DIR_NONE) {
@@ -352,8 +358,7 @@ __global__ void __launch_bounds__(NT) k_resolve(const uint8_t* __restrict__ I, c
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
-    if (!(gx < g.n2 && gy < g.n1 && gz < g.n0)) continue;
+    if (sI[B::at(lz, ly, lx)] == OOB) continue;
     int j = threadIdx.x + k * NT;
     int out;
     while (true) {
@@ -366,34 +371,98 @@ __global__ void __launch_bounds__(NT) k_resolve(const uint8_t* __restrict__ I, c
       }
       j = jn;
     }
-    P[(size_t)gz * g.plane + (size_t)gy * g.n2 + gx] = out;
+    P[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = out;
   }
 }
 
-// ------------------------------------ step III across tiles: chase to the self-loop
-__global__ void k_jump(int* P, int* __restrict__ L, int N) {
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
-    int t = P[p];
-    if (t == p) {
-      L[p] = p;  // root: seed its canonical minimum
-      continue;
+// --------------------------- step III across tiles + per-root minimum + root list
+// After the chase P[p] = r (a self-loop root).  L[r] accumulates INT_MAX - min{p : P[p] = r}
+// with atomicMax: the dead step-II codes left in L are all <= 0 < INT_MAX - p, so no
+// initialisation pass is needed.  Each block owns a contiguous chunk of voxels; within a warp
+// voxels are consecutive, so the first lane of every run of equal roots holds the run's
+// minimum and issues the only atomic for it.  Roots are staged in shared memory and flushed
+// to the global list with one atomicAdd per batch.
+constexpr int RBUF = 2048;
+
+__global__ void __launch_bounds__(NT) k_jump(int* P, int* __restrict__ L, int N, int chunk, int* roots, int cap,
+                                             int* nroots) {
+  __shared__ int sbuf[RBUF];
+  __shared__ int scount, sbase;
+  const int lane = threadIdx.x & 31;
+  const int begin = blockIdx.x * chunk;
+  const int end = min(N, begin + chunk);
+  if (threadIdx.x == 0) scount = 0;
+  __syncthreads();
+  for (int p0 = begin; p0 < end; p0 += NT) {
+    const int p = p0 + threadIdx.x;
+    const bool valid = p < end;
+    int t = -1 - lane;  // unique per lane when invalid (never equals a neighbour's root)
+    if (valid) {
+      t = P[p];
+      if (t != p) {
+        int nt = P[t];
+        if (nt != t) {
+          do {
+            t = nt;
+            nt = P[t];
+          } while (nt != t);
+          P[p] = t;
+        }
+      }
     }
-    int nt = P[t];
-    if (nt == t) continue;
-    while (true) {
-      t = nt;
-      nt = P[t];
-      if (nt == t) break;
+    const int tprev = __shfl_up_sync(0xffffffffu, t, 1);
+    if (valid && (lane == 0 || tprev != t)) atomicMax(L + t, INT_MAX - p);
+    const bool isr = valid && t == p;
+    const unsigned rb = __ballot_sync(0xffffffffu, isr);
+    if (rb) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&scount, __popc(rb));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (isr) sbuf[base + __popc(rb & ((1u << lane) - 1))] = p;
     }
-    P[p] = t;
+    __syncthreads();
+    const int cnt = scount;
+    if (cnt > RBUF - NT || p0 + NT >= end) {  // flush the staged roots
+      if (threadIdx.x == 0) sbase = atomicAdd(nroots, cnt);
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += NT)
+        if (sbase + i < cap) roots[sbase + i] = sbuf[i];
+      __syncthreads();
+      if (threadIdx.x == 0) scount = 0;
+      __syncthreads();
+    }
   }
 }
 
+// rebuild the root list (only if k_jump's list overflowed): roots are P[p] == p
+__global__ void k_collect_roots(const int* __restrict__ P, int N, int* roots, int* nroots) {
+  for (int p0 = blockIdx.x * NT; p0 < N; p0 += gridDim.x * NT) {
+    const int p = p0 + threadIdx.x;
+    if (p >= N) break;
+    const unsigned act = __activemask();
+    const int lane = threadIdx.x & 31;
+    const bool isr = P[p] == p;
+    const unsigned rb = __ballot_sync(act, isr);
+    if (rb) {
+      const int leader = __ffs(act) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(nroots, __popc(rb));
+      base = __shfl_sync(act, base, leader);
+      if (isr) roots[base + __popc(rb & ((1u << lane) - 1))] = p;
+    }
+  }
+}
+
+// find with path halving: x -> y -> z becomes x -> z.  Only non-roots are rewritten, and only
+// to one of their ancestors, so concurrent finds/unions stay correct.
 __device__ __forceinline__ int uf_find(int* P, int x) {
   while (true) {
     const int y = ld_cg(P + x);
     if (y == x) return x;
-    x = y;
+    const int z = ld_cg(P + y);
+    if (z == y) return y;
+    __stcg(P + x, z);
+    x = z;
   }
 }
 
@@ -437,30 +506,36 @@ __global__ void k_union(const uint8_t* __restrict__ I, int* P, Geo g) {
   ZLOOP_END
 }
 
-// ------------------------------- step IV Find (l.28-29) + canonical minimum per root (C7)
-__global__ void k_find(int* P, int* __restrict__ L, int N) {
-  for (int p0 = blockIdx.x * blockDim.x; p0 < N; p0 += gridDim.x * blockDim.x) {
-    const int p = p0 + threadIdx.x;
-    if (p >= N) break;
-    const int r = uf_find(P, ld_cg(P + p));
-    P[p] = r;
-    // warp-aggregated atomicMin: lanes sharing a root elect one leader
+// ------------- step IV Find (l.28-29) on the roots only; canonical labels (C7) per region
+// merge: every root folds its minimum into its final root's (atomicMax on INT_MAX - min)
+__global__ void k_root_merge(int* P, int* L, const int* __restrict__ roots, int n, unsigned long long* nfinal) {
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+    const int r = roots[i];
+    const int f = uf_find(P, r);
+    if (f != r) atomicMax(L + f, L[r]);
     const unsigned act = __activemask();
-    const unsigned grp = __match_any_sync(act, r);
-    const int mn = (int)__reduce_min_sync(grp, (unsigned)p);
-    if (mn < r && (__ffs(grp) - 1) == (int)(threadIdx.x & 31)) atomicMin(L + r, mn);
+    const unsigned b = __ballot_sync(act, f == r);
+    if (b && (threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(nfinal, (unsigned long long)__popc(b));
   }
 }
 
-__global__ void k_relabel(const int* __restrict__ P, int* L, int N, unsigned long long* nroots) {
-  for (int p0 = blockIdx.x * blockDim.x; p0 < N; p0 += gridDim.x * blockDim.x) {
-    const int p = p0 + threadIdx.x;
-    if (p >= N) break;
-    const int c = L[P[p]];  // roots keep L[r] = canonical minimum; other entries are free
-    L[p] = c;
-    const unsigned act = __activemask();
-    const unsigned b = __ballot_sync(act, c == p);
-    if (b && (__ffs(act) - 1) == (int)(threadIdx.x & 31)) atomicAdd(nroots, (unsigned long long)__popc(b));
+// canonical label of every listed root (finds only; no P writes except path halving)
+__global__ void k_root_label(int* P, const int* __restrict__ L, const int* __restrict__ roots, int n,
+                             int* __restrict__ rootc) {
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT)
+    rootc[i] = INT_MAX - L[uf_find(P, roots[i])];
+}
+
+// P[root] = -1 - canonical label (no finds run any more)
+__global__ void k_root_store(int* P, const int* __restrict__ roots, const int* __restrict__ rootc, int n) {
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) P[roots[i]] = -1 - rootc[i];
+}
+
+// labels[p] = canonical label of p's step III root
+__global__ void __launch_bounds__(NT) k_relabel(const int* __restrict__ P, int* __restrict__ L, int N) {
+  for (int p = blockIdx.x * NT + threadIdx.x; p < N; p += gridDim.x * NT) {
+    const int t = P[p];
+    L[p] = -1 - (t < 0 ? t : __ldg(P + t));
   }
 }
 
@@ -480,7 +555,7 @@ static TileGrid tiles_of(const Geo& g) {
   return tg;
 }
 
-static int grid1d(long long n, int sms, int per_sm = 16) {
+static int grid1d(long long n, int sms, int per_sm = 8) {
   long long b = (n + NT - 1) / NT;
   long long cap = (long long)sms * per_sm;
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
@@ -537,24 +612,50 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
   k_resolve<CONN, false><<<tg.n, NT, 0, st>>>(grad, L, g, tg.ntx, tg.nty, P, nullptr);
   launched(ctx, PH_WS_SELECT);
   tmark(ctx, st, PH_WS_SELECT);
+
+  // step III across tiles + root list
+  size_t cap = ctx->roots.bytes / sizeof(int);
+  const size_t want = (size_t)g.N / 16 + 1024;
+  if (cap < want) {
+    WS_TRY(ctx->roots.ensure(want * sizeof(int), "roots"));
+    WS_TRY(ctx->rootc.ensure(want * sizeof(int), "root labels"));
+    cap = want;
+  }
+  int* nr = ctx->flags.as<int>() + 8;
+  unsigned long long* nfinal = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 64);
+  WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
+  WS_CUDA(cudaMemsetAsync(nfinal, 0, sizeof(unsigned long long), st));
   const int gN = grid1d(g.N, ctx->num_sms);
-  k_jump<<<gN, NT, 0, st>>>(P, L, g.N);
+  const int chunk = (int)((((long long)g.N + gN - 1) / gN + NT - 1) / NT * NT);
+  k_jump<<<(g.N + chunk - 1) / chunk, NT, 0, st>>>(P, L, g.N, chunk, ctx->roots.as<int>(), (int)cap, nr);
   launched(ctx, PH_WS_JUMP);
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaStreamSynchronize(st));
+  const int n_roots = (int)reinterpret_cast<const int*>(ctx->pinned)[0];
+  if ((size_t)n_roots > cap) {  // list overflow: grow and rebuild it from P
+    WS_TRY(ctx->roots.ensure((size_t)n_roots * sizeof(int), "roots"));
+    WS_TRY(ctx->rootc.ensure((size_t)n_roots * sizeof(int), "root labels"));
+    WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
+    k_collect_roots<<<gN, NT, 0, st>>>(P, g.N, ctx->roots.as<int>(), nr);
+    launched(ctx, PH_WS_JUMP);
+  }
   tmark(ctx, st, PH_WS_JUMP);
   const L3 l = launch3(g);
   k_union<CONN><<<l.grid, l.block, 0, st>>>(grad, P, g);
   launched(ctx, PH_WS_UNION);
   tmark(ctx, st, PH_WS_UNION);
-  k_find<<<gN, NT, 0, st>>>(P, L, g.N);
-  launched(ctx, PH_WS_FIND);
+  const int gR = grid1d(n_roots, ctx->num_sms);
+  const int* roots = ctx->roots.as<int>();
+  k_root_merge<<<gR, NT, 0, st>>>(P, L, roots, n_roots, nfinal);
+  k_root_label<<<gR, NT, 0, st>>>(P, L, roots, n_roots, ctx->rootc.as<int>());
+  k_root_store<<<gR, NT, 0, st>>>(P, roots, ctx->rootc.as<int>(), n_roots);
+  launched(ctx, PH_WS_FIND, 3);
   tmark(ctx, st, PH_WS_FIND);
-  unsigned long long* nroots = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 64);
-  WS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(unsigned long long), st));
-  k_relabel<<<gN, NT, 0, st>>>(P, L, g.N, nroots);
+  k_relabel<<<gN, NT, 0, st>>>(P, L, g.N);
   launched(ctx, PH_WS_RELABEL);
   tmark(ctx, st, PH_WS_RELABEL);
   WS_CUDA(cudaGetLastError());
-  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nroots, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nfinal, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaStreamSynchronize(st));
   ctx->stats.n_regions = ctx->pinned[0];
   if (num_regions) *num_regions = ctx->pinned[0];
