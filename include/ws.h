@@ -75,6 +75,8 @@ typedef struct ws_stats {
    * when timing is enabled (ws_ctx_set_timing).  Phase names: ws_phase_name(i). */
   double phase_ms[WS_NUM_PHASES];
   int32_t phase_launches[WS_NUM_PHASES];
+  int32_t tma;                /* 1 if the tile kernels staged their boxes with TMA         */
+  int32_t reserved0;
 } ws_stats;
 
 ws_status ws_ctx_create(int32_t device, ws_ctx** out);

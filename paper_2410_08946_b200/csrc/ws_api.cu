@@ -4,6 +4,8 @@
 #include <cstring>
 #include <new>
 
+#include <cuda.h>
+
 #include "ws_internal.h"
 
 namespace ws {
@@ -127,6 +129,41 @@ void tfinish(ws_ctx* ctx) {
   }
   (void)cudaGetLastError();
   ctx->ev_n = 0;
+}
+
+typedef CUresult (*PfnEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PfnEncodeTiled encode_fn() {
+  static PfnEncodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PfnEncodeTiled>(p);
+    (void)cudaGetLastError();
+  }
+  return fn;
+}
+
+bool encode_tmap_3d(void* map, int esize, const void* base, const Geo& g, unsigned bx, unsigned by, unsigned bz) {
+  PfnEncodeTiled fn = encode_fn();
+  if (!fn) return false;
+  const size_t pitch = (size_t)g.n2 * esize, plane = pitch * g.n1;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch & 15) || (plane & 15)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)g.n2, (cuuint64_t)g.n1, (cuuint64_t)g.n0};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)plane};
+  cuuint32_t box[3] = {bx, by, bz};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(map),
+                  esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 static const char* kPhaseNames[WS_NUM_PHASES] = {

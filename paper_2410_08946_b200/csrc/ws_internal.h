@@ -99,6 +99,12 @@ ws_status run_plateau_debug(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int 
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g,
                         int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
 
+// TMA tensor map for a row-major (n0, n1, n2) array of `esize`-byte elements with box
+// {bx, by, bz} (x fastest).  Returns false when the layout cannot be described (global
+// address or row pitch not 16-byte aligned); the caller then uses the fallback loader.
+bool encode_tmap_3d(void* map /* CUtensorMap* */, int esize, const void* base, const Geo& g, unsigned bx,
+                    unsigned by, unsigned bz);
+
 // 3-D launch geometry: block (32, 8, 1), grid over (n2, n1, min(n0, 65535)); kernels loop z.
 struct L3 {
   dim3 grid, block;

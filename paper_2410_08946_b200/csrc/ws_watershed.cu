@@ -23,38 +23,47 @@
 // pointers from k_resolve on.  From k_jump on, L[r] of a root r holds INT_MAX - (smallest
 // voxel index reaching r); all other L entries are dead until k_relabel writes the output.
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 
 #include "ws_internal.h"
+#include "ws_tma.cuh"
 
 namespace ws {
 
 constexpr int NT = 256;
 constexpr int INF = DUNREACHED;
-using u16 = unsigned short;
-constexpr int OOB = 0xFFFF;  // out-of-volume intensity sentinel in shared memory
 
-template <int CONN> struct Tile {
+// Tile layout.  3-D tiles 32x8x8, 2-D tiles 64x32 (2048 voxels, 8 per thread).
+//   I box (u8):  x in [bx-16, bx+TX+16), y in [by-2, by+TY+2), z in [bz-2, bz+TZ+2) (3-D)
+//   L box (i32): x in [bx-4, bx+TX+4),   y in [by-1, by+TY+1), z in [bz-1, bz+TZ+1) (3-D)
+// TMA rules (measured on sm_100a): box widths AND the innermost start coordinate must be
+// multiples of 16 bytes, hence the wide x halos; 2-D tiles have no halo across axis 0.
+template <int CONN> struct TL {
   static constexpr bool is3d = Conn<CONN>::is3d;
   static constexpr int TX = is3d ? 32 : 64;
   static constexpr int TY = is3d ? 8 : 32;
   static constexpr int TZ = is3d ? 8 : 1;
   static constexpr int V = TX * TY * TZ;
   static constexpr int VPT = V / NT;
-  static_assert(V % NT == 0, "tile");
-};
-
-// shared-memory box of the tile plus a halo of H voxels (no halo across axis 0 in 2-D)
-template <int CONN, int H> struct Box {
-  using T = Tile<CONN>;
-  static constexpr int HZ = T::is3d ? H : 0;
-  static constexpr int SX = T::TX + 2 * H, SY = T::TY + 2 * H, SZ = T::TZ + 2 * HZ;
-  static constexpr int S = SX * SY * SZ;
-  __device__ static constexpr int at(int lz, int ly, int lx) { return ((lz + HZ) * SY + (ly + H)) * SX + (lx + H); }
-  __device__ static constexpr int off(int i) {
+  static constexpr int IXO = 16, IYO = 2, IZO = is3d ? 2 : 0;
+  static constexpr int SXI = TX + 32, SYI = TY + 4, SZI = TZ + 2 * IZO, SI = SXI * SYI * SZI;
+  static constexpr int LXO = 4, LYO = 1, LZO = is3d ? 1 : 0;
+  static constexpr int SXL = TX + 8, SYL = TY + 2, SZL = TZ + 2 * LZO, SL = SXL * SYL * SZL;
+  __device__ static constexpr int iI(int lz, int ly, int lx) { return ((lz + IZO) * SYI + ly + IYO) * SXI + lx + IXO; }
+  __device__ static constexpr int iL(int lz, int ly, int lx) { return ((lz + LZO) * SYL + ly + LYO) * SXL + lx + LXO; }
+  __device__ static constexpr int oI(int i) {
     int dz = 0, dy = 0, dx = 0;
     nb_delta(CONN, i, dz, dy, dx);
-    return (dz * SY + dy) * SX + dx;
+    return (dz * SYI + dy) * SXI + dx;
   }
+  __device__ static constexpr int oL(int i) {
+    int dz = 0, dy = 0, dx = 0;
+    nb_delta(CONN, i, dz, dy, dx);
+    return (dz * SYL + dy) * SXL + dx;
+  }
+  static_assert(V % NT == 0, "tile");
+  static_assert((SXI % 16) == 0 && ((SXL * 4) % 16) == 0 && IXO % 16 == 0 && (LXO * 4) % 16 == 0, "TMA");
 };
 
 struct TileCoord {
@@ -63,7 +72,7 @@ struct TileCoord {
 
 template <int CONN>
 __device__ __forceinline__ TileCoord tile_coord(int t, int ntx, int nty) {
-  using T = Tile<CONN>;
+  using T = TL<CONN>;
   TileCoord c;
   c.bx = (t % ntx) * T::TX;
   c.by = ((t / ntx) % nty) * T::TY;
@@ -71,261 +80,359 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int ntx, int nty) {
   return c;
 }
 
+// the tile and its 2-voxel halo lie inside the volume: no neighbour checks needed
+template <int CONN>
+__device__ __forceinline__ bool tile_interior(const TileCoord& c, const Geo& g) {
+  using T = TL<CONN>;
+  return c.bx >= 2 && c.bx + T::TX + 2 <= g.n2 && c.by >= 2 && c.by + T::TY + 2 <= g.n1 &&
+         (!T::is3d || (c.bz >= 2 && c.bz + T::TZ + 2 <= g.n0));
+}
+
 // voxel k of this thread inside the tile: j = threadIdx.x + k * NT (x fastest)
 template <int CONN>
 __device__ __forceinline__ void my_voxel(int k, int& lx, int& ly, int& lz) {
-  using T = Tile<CONN>;
+  using T = TL<CONN>;
   const int j = threadIdx.x + k * NT;
   lx = j % T::TX;
   ly = (j / T::TX) % T::TY;
   lz = j / (T::TX * T::TY);
 }
 
-// row-wise staging: one warp per (sz, sy) row, lanes along x
-template <int CONN, int H>
-__device__ __forceinline__ void load_I(const uint8_t* __restrict__ I, const Geo& g, const TileCoord& c, u16* sI) {
-  using B = Box<CONN, H>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < B::SY * B::SZ; r += NT / 32) {
-    const int sy = r % B::SY, sz = r / B::SY;
-    const int gy = c.by + sy - H, gz = c.bz + sz - B::HZ;
-    const bool rowok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
-    const uint8_t* row = I + ((size_t)(rowok ? gz : 0) * g.plane + (size_t)(rowok ? gy : 0) * g.n2);
-#pragma unroll
-    for (int sx = lane; sx < B::SX; sx += 32) {
-      const int gx = c.bx + sx - H;
-      int v = OOB;
-      if (rowok && (unsigned)gx < (unsigned)g.n2) v = __ldg(row + gx);
-      sI[r * B::SX + sx] = (u16)v;
-    }
-  }
-}
-
-// distances of the tile + 1-voxel halo from the L code (out of the volume: INF, never read)
+// neighbour validity mask (bit i: neighbour i inside the volume) of a voxel at global coords
 template <int CONN>
-__device__ __forceinline__ void load_D(const int* L, const Geo& g, const TileCoord& c, int* sD) {
-  using B = Box<CONN, 1>;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < B::SY * B::SZ; r += NT / 32) {
-    const int sy = r % B::SY, sz = r / B::SY;
-    const int gy = c.by + sy - 1, gz = c.bz + sz - B::HZ;
-    const bool rowok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
-    const int* row = L + ((size_t)(rowok ? gz : 0) * g.plane + (size_t)(rowok ? gy : 0) * g.n2);
+__device__ __forceinline__ unsigned valid_mask(const Geo& g, int gz, int gy, int gx) {
+  unsigned m = 0;
 #pragma unroll
-    for (int sx = lane; sx < B::SX; sx += 32) {
-      const int gx = c.bx + sx - 1;
-      int d = INF;
-      if (rowok && (unsigned)gx < (unsigned)g.n2) d = dec_d(row[gx]);
-      sD[r * B::SX + sx] = d;
-    }
-  }
+  for (int i = 0; i < CONN; ++i)
+    if (nb_in<CONN>(g, gz, gy, gx, i)) m |= 1u << i;
+  return m;
 }
 
-// Mark the (up to 26) neighbouring tiles for the next relaxation round.
+// Stage the I box (and optionally the L box, as raw L values) into shared memory: one
+// cp.async.bulk.tensor per box (TMA zero-fills outside the volume), or a plain loader when
+// the layout has no tensor map.
 template <int CONN>
-__device__ __forceinline__ void mark_neighbours(int t, int ntx, int nty, int ntz, uint8_t* next, int* any) {
-  const int tx = t % ntx, ty = (t / ntx) % nty, tz = t / (ntx * nty);
-  const int i = threadIdx.x;
-  constexpr int ZR = Tile<CONN>::is3d ? 1 : 0;
-  if (i < 27) {
-    const int dz = i / 9 - 1, dy = (i / 3) % 3 - 1, dx = i % 3 - 1;
-    if ((dz == 0 || ZR) && !(dz == 0 && dy == 0 && dx == 0)) {
-      const int x = tx + dx, y = ty + dy, z = tz + dz;
-      if ((unsigned)x < (unsigned)ntx && (unsigned)y < (unsigned)nty && (unsigned)z < (unsigned)ntz)
-        next[(z * nty + y) * ntx + x] = 1;
+__device__ __forceinline__ void stage(const CUtensorMap* mI, const CUtensorMap* mL, bool tma,
+                                      const uint8_t* __restrict__ I, const int* __restrict__ L, const Geo& g,
+                                      const TileCoord& c, uint8_t* sI, int* sL, uint64_t* bar) {
+  using T = TL<CONN>;
+  if (tma) {
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, T::SI + (sL ? T::SL * 4 : 0));
+      tma_load_3d(sI, mI, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, bar);
+      if (sL) tma_load_3d(sL, mL, c.bx - T::LXO, c.by - T::LYO, c.bz - T::LZO, bar);
     }
+    mbar_wait(bar, 0);
+  } else {
+    for (int s = threadIdx.x; s < T::SI; s += NT) {
+      const int sx = s % T::SXI, sy = (s / T::SXI) % T::SYI, sz = s / (T::SXI * T::SYI);
+      const int gx = c.bx + sx - T::IXO, gy = c.by + sy - T::IYO, gz = c.bz + sz - T::IZO;
+      uint8_t v = 0;
+      if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
+        v = __ldg(I + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
+      sI[s] = v;
+    }
+    if (sL) {
+      for (int s = threadIdx.x; s < T::SL; s += NT) {
+        const int sx = s % T::SXL, sy = (s / T::SXL) % T::SYL, sz = s / (T::SXL * T::SYL);
+        const int gx = c.bx + sx - T::LXO, gy = c.by + sy - T::LYO, gz = c.bz + sz - T::LZO;
+        int v = 0;
+        if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
+          v = L[(size_t)gz * g.plane + (size_t)gy * g.n2 + gx];
+        sL[s] = v;
+      }
+    }
+    __syncthreads();
   }
-  if (i == 0) *any = 1;
 }
 
-// in-tile relaxation sweeps until the tile converges (chaotic, in place)
-template <int CONN, int H>
-__device__ __forceinline__ void relax_tile(int* sD, const int* my, const unsigned* eqm, int* limit) {
-  using B = Box<CONN, H>;
-  using T = Tile<CONN>;
+// decode the staged L box in place into plateau distances (L >= 0: 0; else d)
+template <int CONN>
+__device__ __forceinline__ void decode_box(int* sD) {
+  using T = TL<CONN>;
+  for (int s = threadIdx.x; s < T::SL; s += NT) sD[s] = dec_d(sD[s]);
+  __syncthreads();
+}
+
+template <int CONN>
+__device__ __forceinline__ bool on_tile_border(int lx, int ly, int lz) {
+  using T = TL<CONN>;
+  return lx == 0 || lx == T::TX - 1 || ly == 0 || ly == T::TY - 1 || (T::is3d && (lz == 0 || lz == T::TZ - 1));
+}
+
+// Activate a neighbouring tile only where it can gain: a border voxel with distance d whose
+// equal-intensity neighbour h across the tile border still holds sD[h] > d + 1 (the value
+// loaded at kernel start; distances only decrease, so a stale value never hides a gain).
+template <int CONN>
+__device__ __forceinline__ bool mark_gains(const int* sD, int s, int d, unsigned m, int lx, int ly, int lz, int t,
+                                           int ntx, int nty, uint8_t* next) {
+  using T = TL<CONN>;
+  bool any = false;
+#pragma unroll
+  for (int i = 0; i < CONN; ++i) {
+    if (!(m & (1u << i))) continue;
+    int dz, dy, dx;
+    nb_delta(CONN, i, dz, dy, dx);
+    const int ox = (lx + dx < 0) ? -1 : (lx + dx >= T::TX ? 1 : 0);
+    const int oy = (ly + dy < 0) ? -1 : (ly + dy >= T::TY ? 1 : 0);
+    const int oz = (lz + dz < 0) ? -1 : (lz + dz >= T::TZ ? 1 : 0);
+    if ((ox | oy | oz) == 0) continue;
+    if (sD[s + T::oL(i)] > d + 1) {
+      next[t + (oz * nty + oy) * ntx + ox] = 1;
+      any = true;
+    }
+  }
+  return any;
+}
+
+// L-box index of this thread's voxel k: s0 + k * KS (voxel k = threadIdx.x + k * NT)
+template <int CONN> struct Mine {
+  using T = TL<CONN>;
+  static constexpr int KS = (T::is3d ? T::SYL * T::SXL : (NT / T::TX) * T::SXL);
+  __device__ static int s0() {
+    int lx, ly, lz;
+    my_voxel<CONN>(0, lx, ly, lz);
+    return T::iL(lz, ly, lx);
+  }
+};
+
+// in-tile relaxation sweeps until the tile converges (chaotic, in place, on sD); returns a
+// bitmask of this thread's voxels whose distance decreased
+template <int CONN>
+__device__ __forceinline__ unsigned relax_tile(int* sD, int s0, const unsigned* eqm, int* limit) {
+  using T = TL<CONN>;
+  unsigned changed = 0;
   while (true) {
     bool ch = false;
 #pragma unroll
     for (int k = 0; k < T::VPT; ++k) {
       const unsigned m = eqm[k];
       if (!m) continue;
-      const int s = my[k];
+      const int s = s0 + k * Mine<CONN>::KS;
       const int cur = sD[s];
       int best = cur;
 #pragma unroll
       for (int i = 0; i < CONN; ++i)
-        if (m & (1u << i)) best = min(best, sD[s + B::off(i)] + 1);
+        if (m & (1u << i)) best = min(best, sD[s + T::oL(i)] + 1);
       if (best < cur) {
         sD[s] = best;
         ch = true;
+        changed |= 1u << k;
         if (best >= INF - 1) *limit = 1;
       }
     }
     if (!__syncthreads_or(ch)) break;
   }
+  return changed;
 }
 
+// write back the changed voxels of this thread and activate neighbouring tiles that gain
 template <int CONN>
-__device__ __forceinline__ bool on_tile_border(int lx, int ly, int lz) {
-  using T = Tile<CONN>;
-  return lx == 0 || lx == T::TX - 1 || ly == 0 || ly == T::TY - 1 || (T::is3d && (lz == 0 || lz == T::TZ - 1));
+__device__ __forceinline__ bool write_back(const int* sD, int s0, const unsigned* eqm, unsigned todo, int* L,
+                                           const Geo& g, const TileCoord& c, int t, int ntx, int nty,
+                                           uint8_t* next) {
+  bool marked = false;
+#pragma unroll 1
+  for (; todo; todo &= todo - 1) {
+    const int k = __ffs(todo) - 1;
+    int lx, ly, lz;
+    my_voxel<CONN>(k, lx, ly, lz);
+    const int s = s0 + k * Mine<CONN>::KS;
+    const int d = sD[s];
+    L[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = enc(d, DIR_NONE);
+    if (d != INF && on_tile_border<CONN>(lx, ly, lz)) {
+      unsigned m = 0;
+#pragma unroll
+      for (int kk = 0; kk < TL<CONN>::VPT; ++kk)
+        if (kk == k) m = eqm[kk];
+      marked |= mark_gains<CONN>(sD, s, d, m, lx, ly, lz, t, ntx, nty, next);
+    }
+  }
+  return marked;
 }
 
-// ------------------------------------------- step I + first step II round (all tiles)
-template <int CONN>
-__global__ void __launch_bounds__(NT) k_relax_first(const uint8_t* __restrict__ I, int* __restrict__ L, Geo g,
-                                                     int ntx, int nty, int ntz, uint8_t* next,
-                                                     uint8_t* hasplat, int* flags) {
-  using T = Tile<CONN>;
-  using B2 = Box<CONN, 2>;
-  using B1 = Box<CONN, 1>;
-  __shared__ u16 sI[B2::S];
-  __shared__ int sD[B2::S];
-  const int t = blockIdx.x;
-  const TileCoord c = tile_coord<CONN>(t, ntx, nty);
-  load_I<CONN, 2>(I, g, c, sI);
-  __syncthreads();
-  // classify the tile + 1-voxel halo: lower -> 0, plateau without lower -> INF (Alg. 1 l.3-10)
-  for (int s = threadIdx.x; s < B1::S; s += NT) {
-    const int sx = s % B1::SX, sy = (s / B1::SX) % B1::SY, sz = s / (B1::SX * B1::SY);
-    const int s2 = B2::at(sz - B1::HZ, sy - 1, sx - 1);
-    const int v = sI[s2];
+// step I classification of the tile + 1-voxel halo into sD (L layout):
+// lower -> 0, plateau without lower -> INF, strict minimum -> 0 (Alg. 1 l.1-10)
+template <int CONN, bool BORDER>
+__device__ __forceinline__ void classify_box(const uint8_t* sI, int* sD, const Geo& g, const TileCoord& c) {
+  using T = TL<CONN>;
+  for (int s = threadIdx.x; s < T::SL; s += NT) {
+    const int sx = s % T::SXL, sy = (s / T::SXL) % T::SYL, sz = s / (T::SXL * T::SYL);
+    const int lx = sx - T::LXO, ly = sy - T::LYO, lz = sz - T::LZO;
+    if (lx < -1 || lx > T::TX) continue;  // alignment padding of the L box
+    unsigned vm = (1u << CONN) - 1;
+    if (BORDER) {
+      const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
+      if (!((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)) {
+        sD[s] = INF;
+        continue;
+      }
+      vm = valid_mask<CONN>(g, gz, gy, gx);
+    }
+    const int si = T::iI(lz, ly, lx);
+    const int v = sI[si];
     bool lower = false, eq = false;
 #pragma unroll
     for (int i = 0; i < CONN; ++i) {
-      const int nv = sI[s2 + B2::off(i)];
+      if (BORDER && !(vm & (1u << i))) continue;
+      const int nv = sI[si + T::oI(i)];
       lower |= nv < v;
       eq |= nv == v;
     }
-    sD[s2] = (v == OOB) ? INF : (lower ? 0 : (eq ? INF : 0));
+    sD[s] = lower ? 0 : (eq ? INF : 0);
   }
+}
+
+// ------------------------------------------- step I + first step II round (all tiles)
+template <int CONN, bool BORDER>
+__device__ __forceinline__ void relax_first_body(const uint8_t* sI, int* sD, int* __restrict__ L, const Geo& g,
+                                                 const TileCoord& c, int t, int ntx, int nty, uint8_t* next,
+                                                 uint8_t* hasplat, int* flags) {
+  using T = TL<CONN>;
+  classify_box<CONN, BORDER>(sI, sD, g, c);
   __syncthreads();
-  int my[T::VPT];
+  const int s0 = Mine<CONN>::s0();
   unsigned eqm[T::VPT];
-  bool any_plat = false;
+  unsigned plat = 0;
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    my[k] = B2::at(lz, ly, lx);
-    const int v = sI[my[k]];
     unsigned m = 0;
-    if (v != OOB && sD[my[k]] == INF) {
+    const bool inside = !BORDER || (c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0);
+    if (inside && sD[s0 + k * Mine<CONN>::KS] == INF) {
+      const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
+      const int si = T::iI(lz, ly, lx);
+      const int v = sI[si];
 #pragma unroll
       for (int i = 0; i < CONN; ++i)
-        if (sI[my[k] + B2::off(i)] == v) m |= 1u << i;
-      any_plat = true;
+        if ((vm & (1u << i)) && sI[si + T::oI(i)] == v) m |= 1u << i;
+      plat |= 1u << k;
     }
     eqm[k] = m;
   }
-  relax_tile<CONN, 2>(sD, my, eqm, flags + 1);
-  bool border = false;
+  relax_tile<CONN>(sD, s0, eqm, flags + 1);
+  // every voxel is written once: 0 (d = 0) or the plateau code
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
+    if (plat & (1u << k)) continue;
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    if (sI[my[k]] == OOB) continue;
-    const int d = sD[my[k]];
-    L[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = eqm[k] ? enc(d, DIR_NONE) : 0;
-    if (eqm[k] && d != INF && on_tile_border<CONN>(lx, ly, lz)) border = true;
+    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0)) continue;
+    L[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = 0;
   }
-  const int hp = __syncthreads_or(any_plat);
+  const bool marked = write_back<CONN>(sD, s0, eqm, plat, L, g, c, t, ntx, nty, next);
+  const int hp = __syncthreads_or(plat != 0);
   if (threadIdx.x == 0) hasplat[t] = hp ? 1 : 0;
-  if (__syncthreads_or(border)) mark_neighbours<CONN>(t, ntx, nty, ntz, next, flags);
+  if (__syncthreads_or(marked) && threadIdx.x == 0) flags[0] = 1;
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(NT) k_relax_first(const __grid_constant__ CUtensorMap mI, int tma,
+                                                     const uint8_t* __restrict__ I, int* __restrict__ L, Geo g,
+                                                     int ntx, int nty, uint8_t* next, uint8_t* hasplat, int* flags) {
+  using T = TL<CONN>;
+  __shared__ alignas(128) uint8_t sI[T::SI];
+  __shared__ alignas(16) int sD[T::SL];
+  __shared__ uint64_t bar;
+  const int t = blockIdx.x;
+  const TileCoord c = tile_coord<CONN>(t, ntx, nty);
+  stage<CONN>(&mI, nullptr, tma, I, nullptr, g, c, sI, nullptr, &bar);
+  if (tile_interior<CONN>(c, g))
+    relax_first_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, hasplat, flags);
+  else
+    relax_first_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, hasplat, flags);
 }
 
 // ------------------------------------------------ further step II rounds (active tiles)
-template <int CONN>
-__global__ void __launch_bounds__(NT) k_relax_round(const uint8_t* __restrict__ I, int* __restrict__ L, Geo g,
-                                                     int ntx, int nty, int ntz, const uint8_t* cur,
-                                                     uint8_t* next, const uint8_t* hasplat, int* flags) {
-  using T = Tile<CONN>;
-  using B = Box<CONN, 1>;
-  const int t = blockIdx.x;
-  if (!cur[t] || !hasplat[t]) return;
-  __shared__ u16 sI[B::S];
-  __shared__ int sD[B::S];
-  const TileCoord c = tile_coord<CONN>(t, ntx, nty);
-  load_I<CONN, 1>(I, g, c, sI);
-  load_D<CONN>(L, g, c, sD);
-  __syncthreads();
-  int my[T::VPT], d0[T::VPT];
+template <int CONN, bool BORDER>
+__device__ __forceinline__ void relax_round_body(const uint8_t* sI, int* sD, int* __restrict__ L, const Geo& g,
+                                                 const TileCoord& c, int t, int ntx, int nty, uint8_t* next,
+                                                 int* flags) {
+  using T = TL<CONN>;
+  const int s0 = Mine<CONN>::s0();
   unsigned eqm[T::VPT];
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    my[k] = B::at(lz, ly, lx);
-    const int v = sI[my[k]];
-    d0[k] = sD[my[k]];
     unsigned m = 0;
-    if (v != OOB && d0[k] > 0) {  // plateau voxel (d >= 1)
+    const bool inside = !BORDER || (c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0);
+    if (inside && sD[s0 + k * Mine<CONN>::KS] > 0) {  // plateau voxel (d >= 1)
+      const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
+      const int si = T::iI(lz, ly, lx);
+      const int v = sI[si];
 #pragma unroll
       for (int i = 0; i < CONN; ++i)
-        if (sI[my[k] + B::off(i)] == v) m |= 1u << i;
+        if ((vm & (1u << i)) && sI[si + T::oI(i)] == v) m |= 1u << i;
     }
     eqm[k] = m;
   }
-  relax_tile<CONN, 1>(sD, my, eqm, flags + 1);
-  bool border = false;
-#pragma unroll
-  for (int k = 0; k < T::VPT; ++k) {
-    if (!eqm[k]) continue;
-    const int d = sD[my[k]];
-    if (d == d0[k]) continue;
-    int lx, ly, lz;
-    my_voxel<CONN>(k, lx, ly, lz);
-    L[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = enc(d, DIR_NONE);
-    if (on_tile_border<CONN>(lx, ly, lz)) border = true;
-  }
-  if (__syncthreads_or(border)) mark_neighbours<CONN>(t, ntx, nty, ntz, next, flags);
+  const unsigned changed = relax_tile<CONN>(sD, s0, eqm, flags + 1);
+  const bool marked = write_back<CONN>(sD, s0, eqm, changed, L, g, c, t, ntx, nty, next);
+  if (__syncthreads_or(marked) && threadIdx.x == 0) flags[0] = 1;
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUtensorMap mI,
+                                                     const __grid_constant__ CUtensorMap mL, int tma,
+                                                     const uint8_t* __restrict__ I, int* __restrict__ L, Geo g,
+                                                     int ntx, int nty, const uint8_t* cur, uint8_t* next,
+                                                     const uint8_t* hasplat, int* flags) {
+  using T = TL<CONN>;
+  const int t = blockIdx.x;
+  if (!cur[t] || !hasplat[t]) return;
+  __shared__ alignas(128) uint8_t sI[T::SI];
+  __shared__ alignas(128) int sD[T::SL];
+  __shared__ uint64_t bar;
+  const TileCoord c = tile_coord<CONN>(t, ntx, nty);
+  stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);
+  decode_box<CONN>(sD);
+  if (tile_interior<CONN>(c, g))
+    relax_round_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, flags);
+  else
+    relax_round_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, flags);
 }
 
 // ---------------------- pointers (steps I-II) + tile-local pointer jumping (step III)
 // DEBUG: write the un-jumped parent and the distance instead (ws_plateau_debug, T2).
-template <int CONN, bool DEBUG>
-__global__ void __launch_bounds__(NT) k_resolve(const uint8_t* __restrict__ I, const int* __restrict__ L, Geo g,
-                                                int ntx, int nty, int* __restrict__ P, int* __restrict__ dist) {
-  using T = Tile<CONN>;
-  using B = Box<CONN, 1>;
-  __shared__ u16 sI[B::S];
-  __shared__ int sD[B::S];
-  __shared__ short sP[T::V];  // local target, -1 = leaves the tile
-  __shared__ int sG[T::V];    // global target when leaving the tile
-  const int t = blockIdx.x;
-  const TileCoord c = tile_coord<CONN>(t, ntx, nty);
-  load_I<CONN, 1>(I, g, c, sI);
-  load_D<CONN>(L, g, c, sD);
-  __syncthreads();
+template <int CONN, bool DEBUG, bool BORDER>
+__device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, short* sP, int* sG, const Geo& g,
+                                             const TileCoord& c, int* __restrict__ P, int* __restrict__ dist) {
+  using T = TL<CONN>;
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
     const int j = threadIdx.x + k * NT;
-    const int s = B::at(lz, ly, lx);
-    const int v = sI[s];
-    if (v == OOB) {
+    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0)) {
       sP[j] = (short)j;
       continue;
     }
-    int m = 0x10000, dm = 0;
+    const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
+    const int si = T::iI(lz, ly, lx), sl = T::iL(lz, ly, lx);
+    const int v = sI[si];
+    int m = 256, dm = -1;
     unsigned eqm = 0;
 #pragma unroll
     for (int i = 0; i < CONN; ++i) {
-      const int nv = sI[s + B::off(i)];
+      if (BORDER && !(vm & (1u << i))) continue;
+      const int nv = sI[si + T::oI(i)];
       if (nv <= m) { m = nv; dm = i; }  // Eq. 1: max index among the minima
       if (nv == v) eqm |= 1u << i;
     }
     int dir = DIR_NONE, dd = 0;
-    bool minimal = (m > v);  // strict single-voxel minimum (or a 1-voxel image, C4)
-    if (m < v) {
+    bool minimal = (dm < 0 || m > v);  // strict single-voxel minimum (or a 1-voxel image, C4)
+    if (!minimal && m < v) {
       dir = dm;                               // steepest descent (S = 0)
-    } else if (m == v) {                      // plateau voxel without a lower neighbour
-      dd = sD[s];
+    } else if (!minimal) {                    // plateau voxel without a lower neighbour
+      dd = sD[sl];
       if (dd != INF) {                        // non-minimal plateau: BFS parent (C5/C6)
 #pragma unroll
         for (int i = 0; i < CONN; ++i)
-          if ((eqm & (1u << i)) && sD[s + B::off(i)] == dd - 1) dir = i;
+          if ((eqm & (1u << i)) && sD[sl + T::oL(i)] == dd - 1) dir = i;
       } else {                                // minimal plateau: state 2 -> q, state 3 -> root
         minimal = true;
         dir = dm >= Conn<CONN>::nfwd ? dm : DIR_NONE;
@@ -354,48 +461,70 @@ __global__ void __launch_bounds__(NT) k_resolve(const uint8_t* __restrict__ I, c
   if (DEBUG) return;
   __syncthreads();
   // tile-local path reduction: follow in-tile pointers to a root or to the tile exit
+  const int base = (int)((size_t)c.bz * g.plane + (size_t)c.by * g.n2 + c.bx);
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    if (sI[B::at(lz, ly, lx)] == OOB) continue;
+    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0)) continue;
     int j = threadIdx.x + k * NT;
-    int out;
-    while (true) {
-      const int jn = sP[j];
-      if (jn < 0) { out = sG[j]; break; }
-      if (jn == j) {
-        const int rx = j % T::TX, ry = (j / T::TX) % T::TY, rz = j / (T::TX * T::TY);
-        out = (int)((size_t)(c.bz + rz) * g.plane + (size_t)(c.by + ry) * g.n2 + c.bx + rx);
-        break;
-      }
+    int jn = sP[j];
+    while (jn >= 0 && jn != j) {
       j = jn;
+      jn = sP[j];
     }
-    P[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = out;
+    int out;
+    if (jn < 0) {
+      out = sG[j];
+    } else {
+      const int rx = j % T::TX, ry = (j / T::TX) % T::TY, rz = j / (T::TX * T::TY);
+      out = base + rz * g.plane + ry * g.n2 + rx;
+    }
+    P[base + lz * g.plane + ly * g.n2 + lx] = out;
   }
+}
+
+template <int CONN, bool DEBUG>
+__global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensorMap mI,
+                                                const __grid_constant__ CUtensorMap mL, int tma,
+                                                const uint8_t* __restrict__ I, const int* __restrict__ L, Geo g,
+                                                int ntx, int nty, int* __restrict__ P, int* __restrict__ dist) {
+  using T = TL<CONN>;
+  __shared__ alignas(128) uint8_t sI[T::SI];
+  __shared__ alignas(128) int sD[T::SL];
+  __shared__ short sP[T::V];  // local target, -1 = leaves the tile
+  __shared__ int sG[T::V];    // global target when leaving the tile
+  __shared__ uint64_t bar;
+  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty);
+  stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);
+  decode_box<CONN>(sD);
+  if (tile_interior<CONN>(c, g))
+    resolve_body<CONN, DEBUG, false>(sI, sD, sP, sG, g, c, P, dist);
+  else
+    resolve_body<CONN, DEBUG, true>(sI, sD, sP, sG, g, c, P, dist);
 }
 
 // --------------------------- step III across tiles + per-root minimum + root list
 // After the chase P[p] = r (a self-loop root).  L[r] accumulates INT_MAX - min{p : P[p] = r}
 // with atomicMax: the dead step-II codes left in L are all <= 0 < INT_MAX - p, so no
-// initialisation pass is needed.  Each block owns a contiguous chunk of voxels; within a warp
+// initialisation pass is needed.  Grid-stride order keeps every block inside one moving
+// window of the volume (the chase targets of neighbouring tiles stay in L2).  Within a warp
 // voxels are consecutive, so the first lane of every run of equal roots holds the run's
 // minimum and issues the only atomic for it.  Roots are staged in shared memory and flushed
 // to the global list with one atomicAdd per batch.
 constexpr int RBUF = 2048;
 
-__global__ void __launch_bounds__(NT) k_jump(int* P, int* __restrict__ L, int N, int chunk, int* roots, int cap,
+__global__ void __launch_bounds__(NT) k_jump(int* P, int* __restrict__ L, int N, int* roots, int cap,
                                              int* nroots) {
   __shared__ int sbuf[RBUF];
   __shared__ int scount, sbase;
   const int lane = threadIdx.x & 31;
-  const int begin = blockIdx.x * chunk;
-  const int end = min(N, begin + chunk);
   if (threadIdx.x == 0) scount = 0;
   __syncthreads();
-  for (int p0 = begin; p0 < end; p0 += NT) {
+  const int stride = gridDim.x * NT;
+  for (int p0 = blockIdx.x * NT; p0 < N; p0 += stride) {
     const int p = p0 + threadIdx.x;
-    const bool valid = p < end;
+    const bool valid = p < N;
     int t = -1 - lane;  // unique per lane when invalid (never equals a neighbour's root)
     if (valid) {
       t = P[p];
@@ -422,11 +551,13 @@ __global__ void __launch_bounds__(NT) k_jump(int* P, int* __restrict__ L, int N,
     }
     __syncthreads();
     const int cnt = scount;
-    if (cnt > RBUF - NT || p0 + NT >= end) {  // flush the staged roots
-      if (threadIdx.x == 0) sbase = atomicAdd(nroots, cnt);
-      __syncthreads();
-      for (int i = threadIdx.x; i < cnt; i += NT)
-        if (sbase + i < cap) roots[sbase + i] = sbuf[i];
+    if (cnt > RBUF - NT || p0 + stride >= N) {  // flush the staged roots
+      if (cnt > 0) {
+        if (threadIdx.x == 0) sbase = atomicAdd(nroots, cnt);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += NT)
+          if (sbase + i < cap) roots[sbase + i] = sbuf[i];
+      }
       __syncthreads();
       if (threadIdx.x == 0) scount = 0;
       __syncthreads();
@@ -546,7 +677,7 @@ struct TileGrid {
 
 template <int CONN>
 static TileGrid tiles_of(const Geo& g) {
-  using T = Tile<CONN>;
+  using T = TL<CONN>;
   TileGrid tg;
   tg.ntx = (g.n2 + T::TX - 1) / T::TX;
   tg.nty = (g.n1 + T::TY - 1) / T::TY;
@@ -561,9 +692,27 @@ static int grid1d(long long n, int sms, int per_sm = 8) {
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
+// tensor maps of one call (grad u8 box with a 2-voxel halo, L i32 box with a 1-voxel halo);
+// WS_NO_TMA=1 forces the plain loader (tested for parity as well)
+struct Maps {
+  CUtensorMap mI, mL;
+  int tma;
+};
+
+template <int CONN>
+static void make_maps(const uint8_t* grad, const int* L, const Geo& g, Maps& m) {
+  using T = TL<CONN>;
+  const char* env = getenv("WS_NO_TMA");
+  const bool off = env && env[0] == '1';
+  std::memset(&m, 0, sizeof(m));
+  const bool a = !off && encode_tmap_3d(&m.mI, 1, grad, g, T::SXI, T::SYI, T::SZI);
+  const bool b = !off && encode_tmap_3d(&m.mL, 4, L, g, T::SXL, T::SYL, T::SZL);
+  m.tma = (a && b) ? 1 : 0;
+}
+
 template <int CONN>
 static ws_status plateau_phase(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, const TileGrid& tg,
-                               cudaStream_t st) {
+                               const Maps& mp, cudaStream_t st) {
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->tiles.ensure((size_t)tg.n * 3, "tile flags"));
   int* flags = ctx->flags.as<int>();
@@ -572,7 +721,7 @@ static ws_status plateau_phase(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
   uint8_t* hasplat = next + tg.n;
   WS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
-  k_relax_first<CONN><<<tg.n, NT, 0, st>>>(grad, L, g, tg.ntx, tg.nty, tg.ntz, next, hasplat, flags);
+  k_relax_first<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, next, hasplat, flags);
   launched(ctx, PH_WS_INIT);
   tmark(ctx, st, PH_WS_INIT);
   int rounds = 1;
@@ -592,7 +741,8 @@ static ws_status plateau_phase(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
     std::swap(cur, next);
     WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
     WS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
-    k_relax_round<CONN><<<tg.n, NT, 0, st>>>(grad, L, g, tg.ntx, tg.nty, tg.ntz, cur, next, hasplat, flags);
+    k_relax_round<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat,
+                                             flags);
     launched(ctx, PH_WS_RELAX);
     ++rounds;
   }
@@ -606,10 +756,13 @@ template <int CONN>
 static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, int64_t* num_regions,
                              cudaStream_t st) {
   const TileGrid tg = tiles_of<CONN>(g);
-  WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, st));
+  Maps mp;
+  make_maps<CONN>(grad, L, g, mp);
+  ctx->stats.tma = mp.tma;
+  WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, mp, st));
   WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
   int* P = ctx->aux.as<int>();
-  k_resolve<CONN, false><<<tg.n, NT, 0, st>>>(grad, L, g, tg.ntx, tg.nty, P, nullptr);
+  k_resolve<CONN, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr);
   launched(ctx, PH_WS_SELECT);
   tmark(ctx, st, PH_WS_SELECT);
 
@@ -626,8 +779,7 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
   WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(nfinal, 0, sizeof(unsigned long long), st));
   const int gN = grid1d(g.N, ctx->num_sms);
-  const int chunk = (int)((((long long)g.N + gN - 1) / gN + NT - 1) / NT * NT);
-  k_jump<<<(g.N + chunk - 1) / chunk, NT, 0, st>>>(P, L, g.N, chunk, ctx->roots.as<int>(), (int)cap, nr);
+  k_jump<<<gN, NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
   launched(ctx, PH_WS_JUMP);
   WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaStreamSynchronize(st));
@@ -680,8 +832,10 @@ static ws_status debug_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t
   WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
   int* L = ctx->aux.as<int>();
   const TileGrid tg = tiles_of<CONN>(g);
-  WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, st));
-  k_resolve<CONN, true><<<tg.n, NT, 0, st>>>(grad, L, g, tg.ntx, tg.nty, parent, dist);
+  Maps mp;
+  make_maps<CONN>(grad, L, g, mp);
+  WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, mp, st));
+  k_resolve<CONN, true><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, parent, dist);
   launched(ctx, PH_WS_SELECT);
   WS_CUDA(cudaGetLastError());
   return WS_OK;

@@ -174,3 +174,20 @@ def test_abi_errors_on_device():
     with pytest.raises(ws.WsError):
         ws.watershed(q, 8, ndim=3, out=out)
     assert bool((out == -7).all())
+
+
+@pytest.mark.parametrize("conn,ndim,shape", [(6, 3, (20, 48, 64)), (26, 3, (12, 40, 48)), (4, 2, (2, 96, 128)),
+                                             (8, 2, (1, 64, 80))])
+def test_tma_and_fallback_loaders_agree(conn, ndim, shape, monkeypatch):
+    """Aligned shapes (row pitch % 16 == 0) stage tiles with TMA; WS_NO_TMA=1 forces the plain
+    loader.  Both must equal the oracle."""
+    ws = _ws()
+    g = synth.random_plateau_image(shape, 5, seed=conn + 7)
+    qn = g.numpy()
+    q = g.cuda()
+    lab, ref = check_watershed(q, qn, conn, ndim)
+    assert ws.stats()["tma"] == 1
+    monkeypatch.setenv("WS_NO_TMA", "1")
+    lab2, _ = check_watershed(q, qn, conn, ndim)
+    assert ws.stats()["tma"] == 0
+    assert torch.equal(lab, lab2)
