@@ -211,7 +211,7 @@ ws_status ws_ctx_create(int32_t device, ws_ctx** out) {
 ws_status ws_ctx_destroy(ws_ctx* ctx) {
   if (!ctx) return WS_OK;
   cudaSetDevice(ctx->device);
-  ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->tiles, &ctx->roots, &ctx->rootc, &ctx->blockcnt, &ctx->edges,
+  ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->tiles, &ctx->roots, &ctx->rootc, &ctx->blockcnt, &ctx->edges, &ctx->ebufA, &ctx->ebufB, &ctx->rootsA, &ctx->rootsB, &ctx->lvl,
                      &ctx->comp, &ctx->best, &ctx->rep_of, &ctx->levelmap, &ctx->lvcount,
                      &ctx->h_grad, &ctx->h_labels, &ctx->h_levels};
   for (auto* b : bufs) b->release();

@@ -52,8 +52,11 @@ struct ws_ctx {
   ws::Buf tiles;      // u8[3 * ntiles] step II active-tile flags
   ws::Buf roots;      // i32[cap]  step III roots (self-loops), compact list
   ws::Buf rootc;      // i32[cap]  canonical label per listed root
-  ws::Buf blockcnt;   // per-block counts for the representative scan
-  ws::Buf edges;      // u64[cap] RAG edge keys
+  ws::Buf blockcnt;   // per-block look-back status words of the dense-id scan
+  ws::Buf edges;      // u64[cap] RAG edge keys (level 1)
+  ws::Buf ebufA, ebufB;   // compacted live edges (key + current endpoints), ping-pong
+  ws::Buf rootsA, rootsB; // level roots lists, ping-pong
+  ws::Buf lvl;            // u8[R] level at which a component stops being a root
   ws::Buf comp;       // i32[R]   component parent (union-find over dense ids)
   ws::Buf best;       // u64[R]   per-component min-K edge
   ws::Buf rep_of;     // i32[R]   dense id -> canonical voxel label

@@ -1,19 +1,26 @@
 // ws_waterfall.cu — the graph waterfall (C13) over the region adjacency graph, sm_100a.
 //
-//   k_rep_count / k_scan_blocks / k_rep_assign   dense ids: exclusive scan of
-//                                                [labels(p) == p] (prefix-scan compaction)
+//   k_dense      dense ids: single-pass exclusive scan of [labels(p) == p] with decoupled
+//                look-back (prefix-scan compaction); dense_of[label] and rep_of[dense]
 //   k_rag        RAG extraction: forward neighbour pairs with different labels, height
-//                max(I(p), I(q)), deduplicated per tile in a shared-memory hash
-//                with u64 atomicMin on the edge key K (C14) = per-pair minimum (Alg. 4 l.2-7)
-//   per level k: k_best_reset, k_edge_min (per-component min-K edge, u64 atomicMin),
-//                k_hook (min-root CAS union along the picks, C16), k_flatten (+ level map)
+//                max(I(p), I(q)), deduplicated per tile in a shared-memory hash with
+//                u64 atomicMin on the edge key K (C14) = per-pair minimum (Alg. 4 l.2-7);
+//                each unique tile edge also folds into best[] = level-1 min-K edge per region
+//   k_hook       level k: every component merges along its min-K edge (min-root CAS union, C16)
+//   k_flatten    level k: flatten the previous level's roots only; new root list, counts
+//   k_edges      level k >= 2: re-label the live edges to current roots, drop internal ones
+//                (compaction), fold the survivors into best[] (per-component min-K edge)
+//   k_levelmap   per dense id: the chain comp^k(d) = its level-k root -> canonical label rows
 //   k_levels     levels[k][p] = map_k[dense(labels(p))]  (Alg. 5 l.12 output, one pass)
 #include "ws_internal.h"
 
 namespace ws {
 
-constexpr int SCAN_CHUNK = 4096;  // voxels per block in the representative scan
-constexpr int SCAN_THREADS = 256;
+constexpr int NTW = 256;
+
+// ------------------------------------------------------------------ dense ids (scan)
+constexpr int DCHUNK = 4096;  // voxels per block (16 per thread)
+constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_MASK = (1ull << 62) - 1;
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
 #pragma unroll
@@ -24,83 +31,110 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
   return v;
 }
 
-// block-wide exclusive scan of one int per thread (blockDim.x == SCAN_THREADS)
+// block-wide exclusive scan of one int per thread (blockDim.x == NTW)
 __device__ __forceinline__ int block_excl_scan(int v, int* smem, int& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int inc = warp_incl_scan(v);
   if (lane == 31) smem[wid] = inc;
   __syncthreads();
   if (wid == 0) {
-    int s = lane < SCAN_THREADS / 32 ? smem[lane] : 0;
+    int s = lane < NTW / 32 ? smem[lane] : 0;
     s = warp_incl_scan(s);
-    if (lane < SCAN_THREADS / 32) smem[lane] = s;
+    if (lane < NTW / 32) smem[lane] = s;
   }
   __syncthreads();
   const int base = wid ? smem[wid - 1] : 0;
-  total = smem[SCAN_THREADS / 32 - 1];
+  total = smem[NTW / 32 - 1];
   __syncthreads();
   return base + inc - v;
 }
 
-__global__ void k_rep_count(const int* __restrict__ labels, int N, int* __restrict__ blockcnt) {
+// Single pass: block b (in dynamic order) scans its 4096 voxels, publishes its aggregate,
+// looks back over its predecessors' (aggregate | inclusive prefix) words, publishes its
+// inclusive prefix, then writes dense ids.  status[] must be zeroed; *ticket = 0.
+__global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, int N, int aligned,
+                                                unsigned long long* status, int* ticket, int* __restrict__ dense_of,
+                                                int* __restrict__ rep_of, int rep_cap, long long* R) {
   __shared__ int sm[32];
-  const int base = blockIdx.x * SCAN_CHUNK;
-  int c = 0;
-  for (int i = threadIdx.x; i < SCAN_CHUNK; i += SCAN_THREADS) {
-    const int p = base + i;
-    if (p < N && __ldg(labels + p) == p) ++c;
+  __shared__ int sb, sprefix;
+  if (threadIdx.x == 0) sb = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int b = sb;
+  // 16 CONSECUTIVE voxels per thread, so the thread-order block scan is the voxel-order scan
+  // (dense ids must preserve the canonical label order, C14)
+  const int base = b * DCHUNK + threadIdx.x * 16;
+  int f[16];
+  int cnt = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int p = base + j * 4;
+    if (aligned && p + 3 < N) {
+      const int4 v = __ldg(reinterpret_cast<const int4*>(labels + p));
+      f[4 * j + 0] = v.x == p; f[4 * j + 1] = v.y == p + 1; f[4 * j + 2] = v.z == p + 2; f[4 * j + 3] = v.w == p + 3;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) f[4 * j + u] = (p + u < N) ? (__ldg(labels + p + u) == p + u) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cnt += f[4 * j + u];
   }
   int total;
-  block_excl_scan(c, sm, total);
-  if (threadIdx.x == 0) blockcnt[blockIdx.x] = total;
-}
-
-// single block: in-place exclusive scan of blockcnt[0..nb), total -> *R
-__global__ void k_scan_blocks(int* blockcnt, int nb, long long* R) {
-  __shared__ int sm[32];
-  int carry = 0;
-  for (int base = 0; base < nb; base += SCAN_THREADS) {
-    const int i = base + threadIdx.x;
-    const int v = i < nb ? blockcnt[i] : 0;
-    int total;
-    const int ex = block_excl_scan(v, sm, total);
-    if (i < nb) blockcnt[i] = carry + ex;
-    carry += total;
-  }
-  if (threadIdx.x == 0) *R = carry;
-}
-
-__global__ void k_rep_assign(const int* __restrict__ labels, int N, const int* __restrict__ blockoff,
-                             int* __restrict__ dense_of, int* __restrict__ rep_of) {
-  __shared__ int sm[32];
-  const int base = blockIdx.x * SCAN_CHUNK;
-  int off = blockoff[blockIdx.x];
-  for (int i0 = 0; i0 < SCAN_CHUNK; i0 += SCAN_THREADS) {
-    const int p = base + i0 + threadIdx.x;
-    const int f = (p < N && __ldg(labels + p) == p) ? 1 : 0;
-    int total;
-    const int ex = block_excl_scan(f, sm, total);
-    if (f) {
-      dense_of[p] = off + ex;
-      rep_of[off + ex] = p;
+  const int ex = block_excl_scan(cnt, sm, total);
+  if (threadIdx.x == 0) {
+    unsigned long long* my = status + b;
+    long long prefix = 0;
+    if (b == 0) {
+      atomicExch(my, ST_PRE | (unsigned long long)total);
+    } else {
+      atomicExch(my, ST_AGG | (unsigned long long)total);
+      for (int q = b - 1; q >= 0; --q) {
+        unsigned long long s;
+        do {
+          s = atomicAdd(status + q, 0ull);  // L2-coherent read
+        } while ((s >> 62) == 0);
+        prefix += (long long)(s & ST_MASK);
+        if ((s >> 62) == 2) break;
+      }
+      atomicExch(my, ST_PRE | (unsigned long long)(prefix + total));
     }
-    off += total;
+    sprefix = (int)prefix;
+    if ((long long)(b + 1) * DCHUNK >= N) *R = prefix + total;
+  }
+  __syncthreads();
+  int d = sprefix + ex;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (f[4 * j + u]) {
+        const int p = base + j * 4 + u;
+        dense_of[p] = d;
+        if (d < rep_cap) rep_of[d] = p;
+        ++d;
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------------------ RAG extraction
-constexpr int RAG_TZ = 4;           // tile = 32 x 8 x RAG_TZ voxels (3-D), 32 x 8 (2-D)
-constexpr int HCAP = 2048;          // shared hash slots (u64)
+constexpr int RAG_TZ = 4;   // tile = 32 x 8 x RAG_TZ voxels (3-D), 32 x 8 (2-D)
+constexpr int HCAP = 2048;  // shared hash slots (u64)
 constexpr uint64_t PAIRMASK = (1ull << 56) - 1;
 
-__device__ __forceinline__ void emit_global(uint64_t k, uint64_t* edges, unsigned long long* ecount,
-                                            long long cap) {
-  const unsigned long long i = atomicAdd(ecount, 1ull);
-  if ((long long)i < cap) edges[i] = k;
+__device__ __forceinline__ void fold_best(uint64_t* best, uint64_t k) {
+  atomicMin((unsigned long long*)(best + key_lo(k)), (unsigned long long)k);
+  atomicMin((unsigned long long*)(best + key_hi(k)), (unsigned long long)k);
 }
 
-__device__ __forceinline__ void hash_insert(uint64_t* tab, uint64_t k, uint64_t* edges,
-                                            unsigned long long* ecount, long long cap) {
+__device__ __forceinline__ void emit_global(uint64_t k, uint64_t* edges, unsigned long long* ecount, long long cap,
+                                            uint64_t* best) {
+  const unsigned long long i = atomicAdd(ecount, 1ull);
+  if ((long long)i < cap) edges[i] = k;
+  fold_best(best, k);
+}
+
+__device__ __forceinline__ void hash_insert(uint64_t* tab, uint64_t k, uint64_t* edges, unsigned long long* ecount,
+                                            long long cap, uint64_t* best) {
   const uint64_t pair = k & PAIRMASK;
   uint32_t h = (uint32_t)(pair * 0x9E3779B97F4A7C15ull >> 40) & (HCAP - 1);
   for (int probe = 0; probe < 64; ++probe) {
@@ -115,13 +149,13 @@ __device__ __forceinline__ void hash_insert(uint64_t* tab, uint64_t k, uint64_t*
     }
     h = (h + 1) & (HCAP - 1);
   }
-  emit_global(k, edges, ecount, cap);  // table congested: emit undeduplicated (still correct)
+  emit_global(k, edges, ecount, cap, best);  // table congested: emit undeduplicated (still correct)
 }
 
 template <int CONN>
 __global__ void __launch_bounds__(256) k_rag(const int* __restrict__ labels, const uint8_t* __restrict__ I,
                                              const int* __restrict__ dense_of, Geo g, uint64_t* __restrict__ edges,
-                                             unsigned long long* ecount, long long cap) {
+                                             unsigned long long* ecount, long long cap, uint64_t* best) {
   __shared__ uint64_t tab[HCAP];
   __shared__ int nloc;
   __shared__ unsigned long long gbase;
@@ -148,12 +182,13 @@ __global__ void __launch_bounds__(256) k_rag(const int* __restrict__ labels, con
         if (dp < 0) dp = __ldg(dense_of + lp);
         const int dq = __ldg(dense_of + lq);
         const int w = max(vp, (int)__ldg(I + q));
-        hash_insert(tab, make_key((uint32_t)w, (uint32_t)dp, (uint32_t)dq), edges, ecount, cap);
+        hash_insert(tab, make_key((uint32_t)w, (uint32_t)dp, (uint32_t)dq), edges, ecount, cap, best);
       }
     }
   }
   __syncthreads();
-  // flush the tile's unique edges: local slot numbers, one global atomic per block
+  // flush the tile's unique edges (one global atomic per block) and fold them into the
+  // level-1 per-region minima
   int myidx[HCAP / 256];
 #pragma unroll
   for (int j = 0; j < HCAP / 256; ++j) {
@@ -166,63 +201,15 @@ __global__ void __launch_bounds__(256) k_rag(const int* __restrict__ labels, con
 #pragma unroll
   for (int j = 0; j < HCAP / 256; ++j) {
     if (myidx[j] >= 0) {
+      const uint64_t k = tab[tid + j * 256];
       const long long i = (long long)gbase + myidx[j];
-      if (i < cap) edges[i] = tab[tid + j * 256];
+      if (i < cap) edges[i] = k;
+      fold_best(best, k);
     }
   }
 }
 
 // ---------------------------------------------------------------------- level loop
-__global__ void k_iota(int* a, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
-}
-
-__global__ void k_best_reset(uint64_t* best, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) best[i] = KEY_NONE;
-}
-
-// per-component min-K outgoing edge; internal edges are marked dead
-__global__ void k_edge_min(uint64_t* __restrict__ edges, long long E, const int* __restrict__ comp,
-                           uint64_t* __restrict__ best) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < E; e += (long long)gridDim.x * blockDim.x) {
-    const uint64_t k = edges[e];
-    if (k == KEY_NONE) continue;
-    const int ca = __ldg(comp + key_lo(k)), cb = __ldg(comp + key_hi(k));
-    if (ca == cb) { edges[e] = KEY_NONE; continue; }
-    atomicMin((unsigned long long*)(best + ca), (unsigned long long)k);
-    atomicMin((unsigned long long*)(best + cb), (unsigned long long)k);
-  }
-}
-
-// find with path halving (see ws_watershed.cu uf_find)
-__device__ __forceinline__ int c_find(int* c, int x) {
-  while (true) {
-    const int y = ld_cg(c + x);
-    if (y == x) return x;
-    const int z = ld_cg(c + y);
-    if (z == y) return y;
-    __stcg(c + x, z);
-    x = z;
-  }
-}
-
-__global__ void k_hook(const uint64_t* __restrict__ best, int* comp, int n) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    const uint64_t k = best[c];
-    if (k == KEY_NONE) continue;  // non-roots and isolated components (C17)
-    int a = (int)key_lo(k), b = (int)key_hi(k);
-    while (true) {  // min-root union (C16)
-      a = c_find(comp, a);
-      b = c_find(comp, b);
-      if (a == b) break;
-      if (a > b) { const int t = a; a = b; b = t; }
-      if (atomicCAS(comp + b, b, a) == b) break;
-    }
-  }
-}
-
-// read-only find: k_flatten must not path-halve, or a halving store could land after the
-// owner's flattening store and leave a non-root parent behind
 __device__ __forceinline__ int c_find_ro(const int* c, int x) {
   while (true) {
     const int y = ld_cg(c + x);
@@ -231,32 +218,207 @@ __device__ __forceinline__ int c_find_ro(const int* c, int x) {
   }
 }
 
-__global__ void k_flatten(int* comp, int n, const int* __restrict__ rep_of, int* __restrict__ levelmap,
-                          int stride, int col, unsigned long long* nroots) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    const int r = c_find_ro(comp, c);
-    comp[c] = r;
-    levelmap[(size_t)c * stride + col] = __ldg(rep_of + r);
-    const unsigned act = __activemask();
-    const unsigned b = __ballot_sync(act, r == c);
-    if (b && (threadIdx.x & 31) == (unsigned)(__ffs(act) - 1)) atomicAdd(nroots, (unsigned long long)__popc(b));
+__global__ void k_iota(int* a, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+
+// level k: every root c of level k-1 with a min-K edge merges along it (min-root union,
+// C16); best[c] is reset for the next level.  roots == nullptr: all c in [0, n).
+// Finds are read-only: the chains below the previous level's roots (comp^k(d) = level-k
+// root) must survive for k_levelmap, so no path halving here.
+__global__ void k_hook(uint64_t* best, int* comp, const int* __restrict__ roots, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = roots ? roots[i] : i;
+    const uint64_t k = best[c];
+    if (k == KEY_NONE) continue;  // isolated component (C17)
+    best[c] = KEY_NONE;
+    int a = (int)key_lo(k), b = (int)key_hi(k);
+    while (true) {
+      a = c_find_ro(comp, a);
+      b = c_find_ro(comp, b);
+      if (a == b) break;
+      if (a > b) { const int t = a; a = b; b = t; }
+      if (atomicCAS(comp + b, b, a) == b) break;
+    }
   }
 }
 
-__global__ void k_copy_col(int* levelmap, int n, int stride, int from, int to) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
-    levelmap[(size_t)c * stride + to] = levelmap[(size_t)c * stride + from];
+// Flatten the previous level's roots onto their level-k roots (read-only finds, then the
+// stores; non-root entries keep pointing one level up, so comp^k(d) is d's level-k root)
+// and collect the level-k roots (warp-aggregated append, smem-staged per block).
+__global__ void __launch_bounds__(NTW) k_flatten(int* comp, const int* __restrict__ roots, int n,
+                                                  int* __restrict__ out, int* nout, uint8_t* __restrict__ lvl,
+                                                  int level) {
+  __shared__ int sbuf[2 * NTW];
+  __shared__ int scount, sbase;
+  if (threadIdx.x == 0) scount = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int i0 = blockIdx.x * NTW; i0 < n; i0 += gridDim.x * NTW) {
+    const int i = i0 + threadIdx.x;
+    int c = -1, r = -1;
+    if (i < n) {
+      c = roots ? roots[i] : i;
+      r = c_find_ro(comp, c);
+    }
+    const bool isr = (i < n) && r == c;
+    const unsigned rb = __ballot_sync(0xffffffffu, isr);
+    if (rb) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&scount, __popc(rb));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (isr) sbuf[base + __popc(rb & ((1u << lane) - 1))] = c;
+    }
+    __syncthreads();
+    if (i < n && r != c) {
+      comp[c] = r;
+      lvl[c] = (uint8_t)level;  // c stops being a root at this level
+    }
+    const int cnt = scount;
+    if (cnt > NTW || i0 + gridDim.x * NTW >= n) {
+      if (cnt > 0) {
+        if (threadIdx.x == 0) sbase = atomicAdd(nout, cnt);
+        __syncthreads();
+        for (int j = threadIdx.x; j < cnt; j += NTW) out[sbase + j] = sbuf[j];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) scount = 0;
+      __syncthreads();
+    }
+  }
+}
+
+struct Edge {
+  uint64_t k;
+  int a, b;  // current component roots
+};
+
+// level k >= 2: re-label live edges to the level-(k-1) roots, drop edges inside one
+// component, fold survivors into best[] and append them (smem-staged compaction).
+// in_keys != nullptr: the input is the level-1 key list (endpoints decoded from K).
+__global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_keys, const Edge* __restrict__ in,
+                                                long long n, const int* __restrict__ comp, uint64_t* best,
+                                                Edge* __restrict__ out, unsigned long long* nout) {
+  __shared__ Edge sbuf[2 * NTW];
+  __shared__ int scount;
+  __shared__ unsigned long long sbase;
+  if (threadIdx.x == 0) scount = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * NTW;
+  for (long long e0 = (long long)blockIdx.x * NTW; e0 < n; e0 += stride) {
+    const long long e = e0 + threadIdx.x;
+    bool live = false;
+    Edge ed;
+    if (e < n) {
+      if (in_keys) {
+        ed.k = in_keys[e];
+        ed.a = (int)key_lo(ed.k);
+        ed.b = (int)key_hi(ed.k);
+      } else {
+        ed = in[e];
+      }
+      ed.a = __ldg(comp + ed.a);
+      ed.b = __ldg(comp + ed.b);
+      live = ed.a != ed.b;
+      if (live) {
+        atomicMin((unsigned long long*)(best + ed.a), (unsigned long long)ed.k);
+        atomicMin((unsigned long long*)(best + ed.b), (unsigned long long)ed.k);
+      }
+    }
+    const unsigned lb = __ballot_sync(0xffffffffu, live);
+    if (lb) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&scount, __popc(lb));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (live) sbuf[base + __popc(lb & ((1u << lane) - 1))] = ed;
+    }
+    __syncthreads();
+    const int cnt = scount;
+    if (cnt > NTW || e0 + stride >= n) {
+      if (cnt > 0) {
+        if (threadIdx.x == 0) sbase = atomicAdd(nout, (unsigned long long)cnt);
+        __syncthreads();
+        for (int j = threadIdx.x; j < cnt; j += NTW) out[sbase + j] = sbuf[j];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) scount = 0;
+      __syncthreads();
+    }
+  }
+}
+
+// level map rows: row(d)[k-1] = canonical label of d's level-k root, k = 1..NL-1.
+// x stays its own root below lvl[x]; from level lvl[x] on, comp[x] is its root at that level.
+__global__ void k_levelmap(const int* __restrict__ comp, const uint8_t* __restrict__ lvl,
+                           const int* __restrict__ rep_of, int R, int NL, int stride, int* __restrict__ levelmap) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < R; d += gridDim.x * blockDim.x) {
+    int x = d;
+    int* row = levelmap + (size_t)d * stride;
+    for (int k = 1; k < NL; ++k) {
+      while (__ldg(lvl + x) <= k) x = __ldg(comp + x);
+      row[k - 1] = __ldg(rep_of + x);
+    }
+  }
 }
 
 // --------------------------------------------------------------- level materialisation
-__global__ void k_levels(const int* __restrict__ labels, const int* __restrict__ dense_of,
-                         const int* __restrict__ levelmap, int NL, long long N, int* __restrict__ levels) {
+// 4 voxels per thread: one int4 label load, int4 streaming stores per level; the map row of
+// a label is fetched once per run of equal labels.
+template <int STRIDE>
+__device__ __forceinline__ void map_row(const int* levelmap, int d, int* r, int n) {
+  const int* m = levelmap + (size_t)d * STRIDE;
+  if (STRIDE % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < STRIDE; j += 4) {
+      const int4 v = __ldg(reinterpret_cast<const int4*>(m + j));
+      r[j] = v.x; r[j + 1] = v.y; r[j + 2] = v.z; r[j + 3] = v.w;
+    }
+  } else {
+    for (int j = 0; j < n; ++j) r[j] = __ldg(m + j);
+  }
+}
+
+template <int STRIDE>
+__global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ labels, const int* __restrict__ dense_of,
+                                                 const int* __restrict__ levelmap, int NL, long long N,
+                                                 int* __restrict__ levels) {
+  const long long n4 = N / 4;
+  const int nm = NL - 1;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const int4 l = __ldg(reinterpret_cast<const int4*>(labels) + i);
+    __stcs(reinterpret_cast<int4*>(levels) + i, l);
+    if (nm == 0) continue;
+    int r0[STRIDE], r1[STRIDE], r2[STRIDE], r3[STRIDE];
+    map_row<STRIDE>(levelmap, __ldg(dense_of + l.x), r0, nm);
+    if (l.y == l.x) { for (int j = 0; j < STRIDE; ++j) r1[j] = r0[j]; } else map_row<STRIDE>(levelmap, __ldg(dense_of + l.y), r1, nm);
+    if (l.z == l.y) { for (int j = 0; j < STRIDE; ++j) r2[j] = r1[j]; } else map_row<STRIDE>(levelmap, __ldg(dense_of + l.z), r2, nm);
+    if (l.w == l.z) { for (int j = 0; j < STRIDE; ++j) r3[j] = r2[j]; } else map_row<STRIDE>(levelmap, __ldg(dense_of + l.w), r3, nm);
+#pragma unroll
+    for (int k = 1; k <= STRIDE; ++k) {
+      if (k > nm) break;
+      __stcs(reinterpret_cast<int4*>(levels + (size_t)k * N) + i, make_int4(r0[k - 1], r1[k - 1], r2[k - 1], r3[k - 1]));
+    }
+  }
+  // scalar tail (N % 4 voxels)
+  for (long long p = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int l = __ldg(labels + p);
+    levels[p] = l;
+    const int* m = levelmap + (size_t)__ldg(dense_of + l) * STRIDE;
+    for (int k = 1; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k - 1);
+  }
+}
+
+// scalar variant for large NL (stride NL-1 not specialised) or unaligned pointers
+__global__ void k_levels_any(const int* __restrict__ labels, const int* __restrict__ dense_of,
+                             const int* __restrict__ levelmap, int NL, int stride, long long N, int* __restrict__ levels) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
     const int l = __ldg(labels + p);
     levels[p] = l;
     if (NL > 1) {
-      const int* m = levelmap + (size_t)__ldg(dense_of + l) * (NL - 1);
-      for (int k = 1; k < NL; ++k) levels[k * N + p] = __ldg(m + k - 1);
+      const int* m = levelmap + (size_t)__ldg(dense_of + l) * stride;
+      for (int k = 1; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k - 1);
     }
   }
 }
@@ -264,7 +426,7 @@ __global__ void k_levels(const int* __restrict__ labels, const int* __restrict__
 // --------------------------------------------------------------------------- driver
 template <int CONN>
 static ws_status rag_t(const int* labels, const uint8_t* I, const int* dense_of, const Geo& g, uint64_t* edges,
-                       unsigned long long* ecount, long long cap, cudaStream_t st) {
+                       unsigned long long* ecount, long long cap, uint64_t* best, cudaStream_t st) {
   dim3 block(32, 8, 1);
   constexpr int TZ = Conn<CONN>::is3d ? RAG_TZ : 1;
   const int gz = (g.n0 + TZ - 1) / TZ;
@@ -273,126 +435,179 @@ static ws_status rag_t(const int* labels, const uint8_t* I, const int* dense_of,
     return WS_ERR_LIMIT;
   }
   dim3 grid((g.n2 + 31) / 32, (g.n1 + 7) / 8, gz);
-  k_rag<CONN><<<grid, block, 0, st>>>(labels, I, dense_of, g, edges, ecount, cap);
+  k_rag<CONN><<<grid, block, 0, st>>>(labels, I, dense_of, g, edges, ecount, cap, best);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
 
 static ws_status rag(int conn, const int* labels, const uint8_t* I, const int* dense_of, const Geo& g,
-                     uint64_t* edges, unsigned long long* ecount, long long cap, cudaStream_t st) {
+                     uint64_t* edges, unsigned long long* ecount, long long cap, uint64_t* best, cudaStream_t st) {
   switch (conn) {
-    case 4: return rag_t<4>(labels, I, dense_of, g, edges, ecount, cap, st);
-    case 8: return rag_t<8>(labels, I, dense_of, g, edges, ecount, cap, st);
-    case 6: return rag_t<6>(labels, I, dense_of, g, edges, ecount, cap, st);
-    case 26: return rag_t<26>(labels, I, dense_of, g, edges, ecount, cap, st);
+    case 4: return rag_t<4>(labels, I, dense_of, g, edges, ecount, cap, best, st);
+    case 8: return rag_t<8>(labels, I, dense_of, g, edges, ecount, cap, best, st);
+    case 6: return rag_t<6>(labels, I, dense_of, g, edges, ecount, cap, best, st);
+    case 26: return rag_t<26>(labels, I, dense_of, g, edges, ecount, cap, best, st);
   }
   return WS_ERR_INVALID;
 }
 
-static int grid_for(long long n, int sms) {
+static int grid_for(long long n, int sms, int per_sm = 16) {
   long long b = (n + 255) / 256;
-  long long cap = (long long)sms * 16;
+  long long cap = (long long)sms * per_sm;
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+static ws_status read_i64(ws_ctx* ctx, const void* dptr, int64_t* out, cudaStream_t st) {
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, dptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaStreamSynchronize(st));
+  *out = ctx->pinned[0];
+  return WS_OK;
 }
 
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn, int NL,
                         int32_t* levels, int64_t* counts, cudaStream_t st) {
   const int N = g.N;
-  const int nb = (N + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  const int nb = (N + DCHUNK - 1) / DCHUNK;
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->aux.ensure((size_t)N * sizeof(int), "aux"));
-  WS_TRY(ctx->blockcnt.ensure((size_t)nb * sizeof(int), "blockcnt"));
+  WS_TRY(ctx->blockcnt.ensure((size_t)nb * sizeof(unsigned long long), "scan status"));
   int* dense_of = ctx->aux.as<int>();
-  int* blockcnt = ctx->blockcnt.as<int>();
-  long long* dR = reinterpret_cast<long long*>(ctx->flags.as<char>() + 128);
-  unsigned long long* ecount = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 136);
-  unsigned long long* nroots = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 144);
+  char* fl = ctx->flags.as<char>();
+  long long* dR = reinterpret_cast<long long*>(fl + 128);
+  unsigned long long* ecount = reinterpret_cast<unsigned long long*>(fl + 136);
+  int* nroots = reinterpret_cast<int*>(fl + 144);
+  int* ticket = reinterpret_cast<int*>(fl + 148);
+  unsigned long long* nedges = reinterpret_cast<unsigned long long*>(fl + 152);
 
-  // dense ids (prefix-scan compaction of the representatives)
-  k_rep_count<<<nb, SCAN_THREADS, 0, st>>>(labels, N, blockcnt);
-  k_scan_blocks<<<1, SCAN_THREADS, 0, st>>>(blockcnt, nb, dR);
-  launched(ctx, PH_WF_DENSE, 2);
-  WS_CUDA(cudaMemcpyAsync(ctx->pinned, dR, sizeof(long long), cudaMemcpyDeviceToHost, st));
-  WS_CUDA(cudaStreamSynchronize(st));
-  const long long R = ctx->pinned[0];
+  // ---- dense ids (single-pass decoupled look-back scan); rep_of sized by the last call
+  size_t rep_cap = ctx->rep_of.bytes / sizeof(int);
+  if (rep_cap < (size_t)N / 16 + 1024) {
+    WS_TRY(ctx->rep_of.ensure(((size_t)N / 16 + 1024) * sizeof(int), "rep_of"));
+    rep_cap = ctx->rep_of.bytes / sizeof(int);
+  }
+  int64_t R = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    WS_CUDA(cudaMemsetAsync(ctx->blockcnt.p, 0, (size_t)nb * sizeof(unsigned long long), st));
+    WS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+    k_dense<<<nb, NTW, 0, st>>>(labels, N, !(reinterpret_cast<uintptr_t>(labels) & 15),
+                                ctx->blockcnt.as<unsigned long long>(), ticket, dense_of,
+                                ctx->rep_of.as<int>(), (int)rep_cap, dR);
+    launched(ctx, PH_WF_DENSE);
+    WS_TRY(read_i64(ctx, dR, &R, st));
+    if ((size_t)R <= rep_cap) break;
+    WS_TRY(ctx->rep_of.ensure((size_t)R * sizeof(int), "rep_of"));
+    rep_cap = ctx->rep_of.bytes / sizeof(int);
+  }
+  tmark(ctx, st, PH_WF_DENSE);
   if (R > (long long)IDMASK) {
-    set_error(WS_ERR_LIMIT, "ws_waterfall: %lld regions exceed the 2^28-1 edge-key limit", R);
+    set_error(WS_ERR_LIMIT, "ws_waterfall: %lld regions exceed the 2^28-1 edge-key limit", (long long)R);
     return WS_ERR_LIMIT;
   }
   if (R < 1) {
     set_error(WS_ERR_INVALID, "ws_waterfall: labels are not a canonical labelling (no representative)");
     return WS_ERR_INVALID;
   }
-  const int stride = NL > 1 ? NL - 1 : 1;
-  WS_TRY(ctx->rep_of.ensure((size_t)R * sizeof(int), "rep_of"));
+  const int stride = NL <= 5 ? 4 : (NL <= 9 ? 8 : NL - 1);
   WS_TRY(ctx->comp.ensure((size_t)R * sizeof(int), "comp"));
   WS_TRY(ctx->best.ensure((size_t)R * sizeof(uint64_t), "best"));
   WS_TRY(ctx->levelmap.ensure((size_t)R * stride * sizeof(int), "levelmap"));
+  WS_TRY(ctx->rootsA.ensure((size_t)R * sizeof(int), "level roots A"));
+  WS_TRY(ctx->rootsB.ensure((size_t)R * sizeof(int), "level roots B"));
   int* rep_of = ctx->rep_of.as<int>();
   int* comp = ctx->comp.as<int>();
   uint64_t* best = ctx->best.as<uint64_t>();
   int* levelmap = ctx->levelmap.as<int>();
-  k_rep_assign<<<nb, SCAN_THREADS, 0, st>>>(labels, N, blockcnt, dense_of, rep_of);
-  launched(ctx, PH_WF_DENSE);
-  tmark(ctx, st, PH_WF_DENSE);
+  WS_CUDA(cudaMemsetAsync(best, 0xFF, (size_t)R * sizeof(uint64_t), st));
+  WS_TRY(ctx->lvl.ensure((size_t)R, "demotion levels"));
+  uint8_t* lvl = ctx->lvl.as<uint8_t>();
+  WS_CUDA(cudaMemsetAsync(lvl, 0xFF, (size_t)R, st));
 
-  // RAG edges, tile-deduplicated; grow the buffer and redo on overflow
+  // ---- RAG edges, tile-deduplicated, folded into the level-1 minima; grow + redo on overflow
   long long cap = (long long)(ctx->edges.bytes / sizeof(uint64_t));
-  long long want = (long long)N / 4 + 4096;
+  const long long want = (long long)N / 4 + 4096;
   if (cap < want) {
     WS_TRY(ctx->edges.ensure((size_t)want * sizeof(uint64_t), "edges"));
     cap = want;
   }
-  long long E = 0;
+  int64_t E = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ecount, 0, sizeof(unsigned long long), st));
-    WS_TRY(rag(conn, labels, I, dense_of, g, ctx->edges.as<uint64_t>(), ecount, cap, st));
+    WS_TRY(rag(conn, labels, I, dense_of, g, ctx->edges.as<uint64_t>(), ecount, cap, best, st));
     launched(ctx, PH_WF_RAG);
-    WS_CUDA(cudaMemcpyAsync(ctx->pinned, ecount, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    WS_CUDA(cudaStreamSynchronize(st));
-    E = ctx->pinned[0];
+    WS_TRY(read_i64(ctx, ecount, &E, st));
     if (E <= cap) break;
     WS_TRY(ctx->edges.ensure((size_t)E * sizeof(uint64_t), "edges"));
     cap = E;
+    WS_CUDA(cudaMemsetAsync(best, 0xFF, (size_t)R * sizeof(uint64_t), st));
   }
   tmark(ctx, st, PH_WF_RAG);
   ctx->stats.n_edges = E;
   ctx->stats.n_regions = R;
-  uint64_t* edges = ctx->edges.as<uint64_t>();
 
-  const int gR = grid_for(R, ctx->num_sms), gE = grid_for(E, ctx->num_sms);
-  k_iota<<<gR, 256, 0, st>>>(comp, (int)R);
-  launched(ctx, PH_WF_LEVELS);
-  long long prev = R;
-  int lv = 0;
+  // ---- levels
+  WS_TRY(ctx->ebufA.ensure((size_t)(E > 0 ? E : 1) * sizeof(Edge), "edge buffer A"));
+  WS_TRY(ctx->ebufB.ensure((size_t)(E > 0 ? E : 1) * sizeof(Edge), "edge buffer B"));
+  Edge* ein = nullptr;
+  Edge* eout = ctx->ebufA.as<Edge>();
+  Edge* espare = ctx->ebufB.as<Edge>();
+  int* rin = nullptr;  // level-(k-1) roots (nullptr = all R)
+  int* rout = ctx->rootsA.as<int>();
+  int* rspare = ctx->rootsB.as<int>();
+  long long nr_in = R, ne_in = E;
   if (counts) counts[0] = R;
   ctx->stats.level_counts[0] = R;
+  k_iota<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(comp, (int)R);
+  launched(ctx, PH_WF_LEVELS);
+  int lv = 0;
+  long long prev = R;
   for (int k = 1; k < NL; ++k) {
-    if (k >= 2 && (prev == 1 || lv < k - 1)) {  // converged: the hierarchy is constant from here (C17)
-      k_copy_col<<<gR, 256, 0, st>>>(levelmap, (int)R, stride, k - 2, k - 1);
-      launched(ctx, PH_WF_LEVELS);
-      if (counts) counts[k] = prev;
-      if (k < 16) ctx->stats.level_counts[k] = prev;
-      continue;
+    if (prev > 1 && (k == 1 || lv == k - 1)) {
+      if (k >= 2) {  // per-component min-K edges of level k (level 1 came from the RAG)
+        WS_CUDA(cudaMemsetAsync(nedges, 0, sizeof(unsigned long long), st));
+        k_edges<<<grid_for(ne_in, ctx->num_sms, 8), NTW, 0, st>>>(k == 2 ? ctx->edges.as<uint64_t>() : nullptr,
+                                                                   ein, ne_in, comp, best, eout, nedges);
+        launched(ctx, PH_WF_LEVELS);
+      }
+      k_hook<<<grid_for(nr_in, ctx->num_sms), 256, 0, st>>>(best, comp, rin, (int)nr_in);
+      WS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(int), st));
+      k_flatten<<<grid_for(nr_in, ctx->num_sms, 8), NTW, 0, st>>>(comp, rin, (int)nr_in, rout, nroots, lvl, k);
+      launched(ctx, PH_WF_LEVELS, 2);
+      WS_CUDA(cudaMemcpyAsync(ctx->pinned, nroots, sizeof(int), cudaMemcpyDeviceToHost, st));
+      if (k >= 2) WS_CUDA(cudaMemcpyAsync(ctx->pinned + 1, nedges, sizeof(long long), cudaMemcpyDeviceToHost, st));
+      WS_CUDA(cudaStreamSynchronize(st));
+      const long long cnt = reinterpret_cast<const int*>(ctx->pinned)[0];
+      if (k >= 2) {
+        ne_in = ctx->pinned[1];
+        ein = eout;
+        std::swap(eout, espare);
+      } else {
+        ne_in = E;  // level 2 reads the key list
+      }
+      rin = rout;
+      std::swap(rout, rspare);
+      nr_in = cnt;
+      if (cnt < prev) lv = k;
+      prev = cnt;
     }
-    k_best_reset<<<gR, 256, 0, st>>>(best, (int)R);
-    k_edge_min<<<gE, 256, 0, st>>>(edges, E, comp, best);
-    k_hook<<<gR, 256, 0, st>>>(best, comp, (int)R);
-    WS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(unsigned long long), st));
-    k_flatten<<<gR, 256, 0, st>>>(comp, (int)R, rep_of, levelmap, stride, k - 1, nroots);
-    launched(ctx, PH_WF_LEVELS, 4);
-    WS_CUDA(cudaMemcpyAsync(ctx->pinned, nroots, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    WS_CUDA(cudaStreamSynchronize(st));
-    const long long cnt = ctx->pinned[0];
-    if (counts) counts[k] = cnt;
-    if (k < 16) ctx->stats.level_counts[k] = cnt;
-    if (cnt < prev) lv = k;
-    prev = cnt;
+    if (counts) counts[k] = prev;
+    if (k < 16) ctx->stats.level_counts[k] = prev;
   }
   ctx->stats.waterfall_levels = lv;
+  if (NL > 1) {
+    k_levelmap<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(comp, lvl, rep_of, (int)R, NL, stride, levelmap);
+    launched(ctx, PH_WF_LEVELS);
+  }
   tmark(ctx, st, PH_WF_LEVELS);
   const int gN = grid_for(N, ctx->num_sms);
-  k_levels<<<gN, 256, 0, st>>>(labels, dense_of, levelmap, NL, N, levels);
+  const bool vec = (N % 4 == 0) && !(reinterpret_cast<uintptr_t>(labels) & 15) &&
+                   !(reinterpret_cast<uintptr_t>(levels) & 15);
+  if (vec && stride == 4) {
+    k_levels<4><<<gN, NTW, 0, st>>>(labels, dense_of, levelmap, NL, N, levels);
+  } else if (vec && stride == 8) {
+    k_levels<8><<<gN, NTW, 0, st>>>(labels, dense_of, levelmap, NL, N, levels);
+  } else {
+    k_levels_any<<<gN, NTW, 0, st>>>(labels, dense_of, levelmap, NL, stride, N, levels);
+  }
   launched(ctx, PH_WF_MATERIALISE);
   tmark(ctx, st, PH_WF_MATERIALISE);
   WS_CUDA(cudaGetLastError());
