@@ -1,0 +1,147 @@
+// ws_tile.cuh — shared tile layout + TMA staging for the tile kernels (watershed, RAG).
+#pragma once
+#include <cstdlib>
+#include <cstring>
+
+#include "ws_internal.h"
+#include "ws_tma.cuh"
+
+namespace ws {
+
+constexpr int NT = 256;
+
+// Tile layout.  3-D tiles 32x8x8, 2-D tiles 64x32 (2048 voxels, 8 per thread).
+//   I box (u8):  x in [bx-16, bx+TX+16), y in [by-2, by+TY+2), z in [bz-2, bz+TZ+2) (3-D)
+//   L box (i32): x in [bx-4, bx+TX+4),   y in [by-1, by+TY+1), z in [bz-1, bz+TZ+1) (3-D)
+// TMA rules (measured on sm_100a): box widths AND the innermost start coordinate must be
+// multiples of 16 bytes, hence the wide x halos; 2-D tiles have no halo across axis 0.
+template <int CONN> struct TL {
+  static constexpr bool is3d = Conn<CONN>::is3d;
+  static constexpr int TX = is3d ? 32 : 64;
+  static constexpr int TY = is3d ? 8 : 32;
+  static constexpr int TZ = is3d ? 8 : 1;
+  static constexpr int V = TX * TY * TZ;
+  static constexpr int VPT = V / NT;
+  static constexpr int IXO = 16, IYO = 2, IZO = is3d ? 2 : 0;
+  static constexpr int SXI = TX + 32, SYI = TY + 4, SZI = TZ + 2 * IZO, SI = SXI * SYI * SZI;
+  static constexpr int LXO = 4, LYO = 1, LZO = is3d ? 1 : 0;
+  static constexpr int SXL = TX + 8, SYL = TY + 2, SZL = TZ + 2 * LZO, SL = SXL * SYL * SZL;
+  __device__ static constexpr int iI(int lz, int ly, int lx) { return ((lz + IZO) * SYI + ly + IYO) * SXI + lx + IXO; }
+  __device__ static constexpr int iL(int lz, int ly, int lx) { return ((lz + LZO) * SYL + ly + LYO) * SXL + lx + LXO; }
+  __device__ static constexpr int oI(int i) {
+    int dz = 0, dy = 0, dx = 0;
+    nb_delta(CONN, i, dz, dy, dx);
+    return (dz * SYI + dy) * SXI + dx;
+  }
+  __device__ static constexpr int oL(int i) {
+    int dz = 0, dy = 0, dx = 0;
+    nb_delta(CONN, i, dz, dy, dx);
+    return (dz * SYL + dy) * SXL + dx;
+  }
+  static_assert(V % NT == 0, "tile");
+  static_assert((SXI % 16) == 0 && ((SXL * 4) % 16) == 0 && IXO % 16 == 0 && (LXO * 4) % 16 == 0, "TMA");
+};
+
+struct TileCoord {
+  int bx, by, bz;  // global coordinates of the tile origin
+};
+
+template <int CONN>
+__device__ __forceinline__ TileCoord tile_coord(int t, int ntx, int nty) {
+  using T = TL<CONN>;
+  TileCoord c;
+  c.bx = (t % ntx) * T::TX;
+  c.by = ((t / ntx) % nty) * T::TY;
+  c.bz = (t / (ntx * nty)) * T::TZ;
+  return c;
+}
+
+// the tile and its 2-voxel halo lie inside the volume: no neighbour checks needed
+template <int CONN>
+__device__ __forceinline__ bool tile_interior(const TileCoord& c, const Geo& g) {
+  using T = TL<CONN>;
+  return c.bx >= 2 && c.bx + T::TX + 2 <= g.n2 && c.by >= 2 && c.by + T::TY + 2 <= g.n1 &&
+         (!T::is3d || (c.bz >= 2 && c.bz + T::TZ + 2 <= g.n0));
+}
+
+// voxel k of this thread inside the tile: j = threadIdx.x + k * NT (x fastest)
+template <int CONN>
+__device__ __forceinline__ void my_voxel(int k, int& lx, int& ly, int& lz) {
+  using T = TL<CONN>;
+  const int j = threadIdx.x + k * NT;
+  lx = j % T::TX;
+  ly = (j / T::TX) % T::TY;
+  lz = j / (T::TX * T::TY);
+}
+
+// neighbour validity mask (bit i: neighbour i inside the volume) of a voxel at global coords
+template <int CONN>
+__device__ __forceinline__ unsigned valid_mask(const Geo& g, int gz, int gy, int gx) {
+  unsigned m = 0;
+#pragma unroll
+  for (int i = 0; i < CONN; ++i)
+    if (nb_in<CONN>(g, gz, gy, gx, i)) m |= 1u << i;
+  return m;
+}
+
+// Stage the I box (and optionally the L box, as raw L values) into shared memory: one
+// cp.async.bulk.tensor per box (TMA zero-fills outside the volume), or a plain loader when
+// the layout has no tensor map.
+template <int CONN>
+__device__ __forceinline__ void stage(const CUtensorMap* mI, const CUtensorMap* mL, bool tma,
+                                      const uint8_t* __restrict__ I, const int* __restrict__ L, const Geo& g,
+                                      const TileCoord& c, uint8_t* sI, int* sL, uint64_t* bar) {
+  using T = TL<CONN>;
+  if (tma) {
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, T::SI + (sL ? T::SL * 4 : 0));
+      tma_load_3d(sI, mI, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, bar);
+      if (sL) tma_load_3d(sL, mL, c.bx - T::LXO, c.by - T::LYO, c.bz - T::LZO, bar);
+    }
+    mbar_wait(bar, 0);
+  } else {
+    for (int s = threadIdx.x; s < T::SI; s += NT) {
+      const int sx = s % T::SXI, sy = (s / T::SXI) % T::SYI, sz = s / (T::SXI * T::SYI);
+      const int gx = c.bx + sx - T::IXO, gy = c.by + sy - T::IYO, gz = c.bz + sz - T::IZO;
+      uint8_t v = 0;
+      if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
+        v = __ldg(I + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
+      sI[s] = v;
+    }
+    if (sL) {
+      for (int s = threadIdx.x; s < T::SL; s += NT) {
+        const int sx = s % T::SXL, sy = (s / T::SXL) % T::SYL, sz = s / (T::SXL * T::SYL);
+        const int gx = c.bx + sx - T::LXO, gy = c.by + sy - T::LYO, gz = c.bz + sz - T::LZO;
+        int v = 0;
+        if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
+          v = L[(size_t)gz * g.plane + (size_t)gy * g.n2 + gx];
+        sL[s] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+
+// tensor maps of one call (grad u8 box with a 2-voxel halo, L i32 box with a 1-voxel halo);
+// WS_NO_TMA=1 forces the plain loader (tested for parity as well)
+struct Maps {
+  CUtensorMap mI, mL;
+  int tma;
+};
+
+template <int CONN>
+static inline void make_maps(const uint8_t* grad, const int* L, const Geo& g, Maps& m) {
+  using T = TL<CONN>;
+  const char* env = getenv("WS_NO_TMA");
+  const bool off = env && env[0] == '1';
+  std::memset(&m, 0, sizeof(m));
+  const bool a = !off && encode_tmap_3d(&m.mI, 1, grad, g, T::SXI, T::SYI, T::SZI);
+  const bool b = !off && encode_tmap_3d(&m.mL, 4, L, g, T::SXL, T::SYL, T::SZL);
+  m.tma = (a && b) ? 1 : 0;
+}
+
+
+}  // namespace ws

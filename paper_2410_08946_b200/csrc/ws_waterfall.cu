@@ -13,13 +13,16 @@
 //   k_levelmap   per dense id: the chain comp^k(d) = its level-k root -> canonical label rows
 //   k_levels     levels[k][p] = map_k[dense(labels(p))]  (Alg. 5 l.12 output, one pass)
 #include "ws_internal.h"
+#include "ws_tile.cuh"
 
 namespace ws {
 
 constexpr int NTW = 256;
 
 // ------------------------------------------------------------------ dense ids (scan)
-constexpr int DCHUNK = 4096;  // voxels per block (16 per thread)
+constexpr int DROUND = NTW * 16;      // 4096 voxels per round, 16 consecutive per thread
+constexpr int DR = 4;                 // rounds per block
+constexpr int DCHUNK = DROUND * DR;   // 16384 voxels per block
 constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_MASK = (1ull << 62) - 1;
 
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -49,163 +52,236 @@ __device__ __forceinline__ int block_excl_scan(int v, int* smem, int& total) {
   return base + inc - v;
 }
 
-// Single pass: block b (in dynamic order) scans its 4096 voxels, publishes its aggregate,
-// looks back over its predecessors' (aggregate | inclusive prefix) words, publishes its
-// inclusive prefix, then writes dense ids.  status[] must be zeroed; *ticket = 0.
+// Single pass, decoupled look-back: block b (dynamic order) scans its 16384 voxels (thread
+// t owns voxels 16t..16t+15 of each 4096-voxel round, so thread order = voxel order and the
+// dense ids keep the canonical label order, C14), publishes its aggregate, then warp 0 looks
+// back over 32 predecessors at a time until an inclusive prefix is found.
 __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, int N, int aligned,
                                                 unsigned long long* status, int* ticket, int* __restrict__ dense_of,
                                                 int* __restrict__ rep_of, int rep_cap, long long* R) {
   __shared__ int sm[32];
-  __shared__ int sb, sprefix;
+  __shared__ int sb;
+  __shared__ long long sprefix;
   if (threadIdx.x == 0) sb = atomicAdd(ticket, 1);
   __syncthreads();
   const int b = sb;
-  // 16 CONSECUTIVE voxels per thread, so the thread-order block scan is the voxel-order scan
-  // (dense ids must preserve the canonical label order, C14)
-  const int base = b * DCHUNK + threadIdx.x * 16;
-  int f[16];
-  int cnt = 0;
+  const int lane = threadIdx.x & 31;
+  uint64_t fl = 0;
+  int ex[DR];
+  int total = 0;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int p = base + j * 4;
-    if (aligned && p + 3 < N) {
-      const int4 v = __ldg(reinterpret_cast<const int4*>(labels + p));
-      f[4 * j + 0] = v.x == p; f[4 * j + 1] = v.y == p + 1; f[4 * j + 2] = v.z == p + 2; f[4 * j + 3] = v.w == p + 3;
-    } else {
+  for (int r = 0; r < DR; ++r) {
+    const int p0 = b * DCHUNK + r * DROUND + threadIdx.x * 16;
+    int cnt = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) f[4 * j + u] = (p + u < N) ? (__ldg(labels + p + u) == p + u) : 0;
+    for (int j = 0; j < 4; ++j) {
+      const int p = p0 + 4 * j;
+      int f0, f1, f2, f3;
+      if (aligned && p + 3 < N) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(labels + p));
+        f0 = v.x == p; f1 = v.y == p + 1; f2 = v.z == p + 2; f3 = v.w == p + 3;
+      } else {
+        f0 = (p < N) && __ldg(labels + p) == p;
+        f1 = (p + 1 < N) && __ldg(labels + p + 1) == p + 1;
+        f2 = (p + 2 < N) && __ldg(labels + p + 2) == p + 2;
+        f3 = (p + 3 < N) && __ldg(labels + p + 3) == p + 3;
+      }
+      const int sh = r * 16 + 4 * j;
+      fl |= ((uint64_t)f0 << sh) | ((uint64_t)f1 << (sh + 1)) | ((uint64_t)f2 << (sh + 2)) | ((uint64_t)f3 << (sh + 3));
+      cnt += f0 + f1 + f2 + f3;
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) cnt += f[4 * j + u];
+    int tot;
+    ex[r] = block_excl_scan(cnt, sm, tot) + total;
+    total += tot;
   }
-  int total;
-  const int ex = block_excl_scan(cnt, sm, total);
-  if (threadIdx.x == 0) {
-    unsigned long long* my = status + b;
+  if (threadIdx.x < 32) {
     long long prefix = 0;
     if (b == 0) {
-      atomicExch(my, ST_PRE | (unsigned long long)total);
+      if (lane == 0) atomicExch(status, ST_PRE | (unsigned long long)total);
     } else {
-      atomicExch(my, ST_AGG | (unsigned long long)total);
-      for (int q = b - 1; q >= 0; --q) {
-        unsigned long long s;
-        do {
-          s = atomicAdd(status + q, 0ull);  // L2-coherent read
-        } while ((s >> 62) == 0);
-        prefix += (long long)(s & ST_MASK);
-        if ((s >> 62) == 2) break;
+      if (lane == 0) atomicExch(status + b, ST_AGG | (unsigned long long)total);
+      int q = b - 1;
+      while (true) {
+        const int idx = q - lane;
+        unsigned long long s = ST_PRE;  // virtual inclusive prefix 0 before block 0
+        if (idx >= 0) s = *reinterpret_cast<volatile unsigned long long*>(status + idx);
+        const unsigned flag = (unsigned)(s >> 62);
+        if (__any_sync(0xffffffffu, flag == 0)) continue;  // a predecessor has not published yet
+        const unsigned pre = __ballot_sync(0xffffffffu, flag == 2);
+        const int first = pre ? __ffs(pre) - 1 : 31;
+        long long v = (lane <= first) ? (long long)(s & ST_MASK) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (pre) break;
+        q -= 32;
       }
-      atomicExch(my, ST_PRE | (unsigned long long)(prefix + total));
+      if (lane == 0) atomicExch(status + b, ST_PRE | (unsigned long long)(prefix + total));
     }
-    sprefix = (int)prefix;
-    if ((long long)(b + 1) * DCHUNK >= N) *R = prefix + total;
+    if (lane == 0) {
+      sprefix = prefix;
+      if ((long long)(b + 1) * DCHUNK >= N) *R = prefix + total;
+    }
   }
   __syncthreads();
-  int d = sprefix + ex;
+  const int pre = (int)sprefix;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (f[4 * j + u]) {
-        const int p = base + j * 4 + u;
-        dense_of[p] = d;
-        if (d < rep_cap) rep_of[d] = p;
-        ++d;
-      }
+  for (int r = 0; r < DR; ++r) {
+    int d = pre + ex[r];
+    uint32_t m = (uint32_t)((fl >> (r * 16)) & 0xffffu);
+    const int p0 = b * DCHUNK + r * DROUND + threadIdx.x * 16;
+    while (m) {
+      const int u = __ffs(m) - 1;
+      m &= m - 1;
+      dense_of[p0 + u] = d;
+      if (d < rep_cap) rep_of[d] = p0 + u;
+      ++d;
     }
   }
 }
 
 // ------------------------------------------------------------------------ RAG extraction
-constexpr int RAG_TZ = 4;   // tile = 32 x 8 x RAG_TZ voxels (3-D), 32 x 8 (2-D)
-constexpr int HCAP = 2048;  // shared hash slots (u64)
-constexpr uint64_t PAIRMASK = (1ull << 56) - 1;
+// Tiles and TMA staging as in the watershed (ws_tile.cuh): the label box (i32) and the
+// intensity box (u8) of a 2048-voxel tile land in shared memory with one bulk-tensor copy
+// each.  Every thread walks its 8 voxels; per forward direction it run-length-merges equal
+// region pairs in registers (min height), and only run ends touch the shared hash, which is
+// keyed by the LABEL pair (dense ids are looked up once per unique tile edge at the flush).
+constexpr int HC = 1024;                       // shared hash slots per tile
+constexpr uint64_t PKEY_NONE = ~0ull;
+
+__device__ __forceinline__ uint64_t pair_key(int a, int b) {
+  const uint32_t lo = (uint32_t)min(a, b), hi = (uint32_t)max(a, b);
+  return ((uint64_t)lo << 31) | hi;
+}
 
 __device__ __forceinline__ void fold_best(uint64_t* best, uint64_t k) {
   atomicMin((unsigned long long*)(best + key_lo(k)), (unsigned long long)k);
   atomicMin((unsigned long long*)(best + key_hi(k)), (unsigned long long)k);
 }
 
-__device__ __forceinline__ void emit_global(uint64_t k, uint64_t* edges, unsigned long long* ecount, long long cap,
-                                            uint64_t* best) {
+__device__ __noinline__ void emit_global(uint64_t pk, unsigned w, const int* dense_of, uint64_t* edges,
+                                         unsigned long long* ecount, long long cap, uint64_t* best) {
+  const uint64_t k = make_key(w, (uint32_t)__ldg(dense_of + (int)(pk >> 31)),
+                              (uint32_t)__ldg(dense_of + (int)(pk & 0x7fffffffu)));
   const unsigned long long i = atomicAdd(ecount, 1ull);
   if ((long long)i < cap) edges[i] = k;
   fold_best(best, k);
 }
 
-__device__ __forceinline__ void hash_insert(uint64_t* tab, uint64_t k, uint64_t* edges, unsigned long long* ecount,
+__device__ __forceinline__ void pair_insert(unsigned long long* tk, unsigned* tw, uint64_t pk, unsigned w,
+                                            const int* dense_of, uint64_t* edges, unsigned long long* ecount,
                                             long long cap, uint64_t* best) {
-  const uint64_t pair = k & PAIRMASK;
-  uint32_t h = (uint32_t)(pair * 0x9E3779B97F4A7C15ull >> 40) & (HCAP - 1);
-  for (int probe = 0; probe < 64; ++probe) {
-    uint64_t cur = tab[h];
-    if (cur == KEY_NONE) {
-      cur = atomicCAS((unsigned long long*)(tab + h), (unsigned long long)KEY_NONE, (unsigned long long)k);
-      if (cur == KEY_NONE) return;
-    }
-    if ((cur & PAIRMASK) == pair) {  // same region pair: keep the lower pass (min K)
-      atomicMin((unsigned long long*)(tab + h), (unsigned long long)k);
+  uint32_t h = (uint32_t)((pk * 0x9E3779B97F4A7C15ull) >> 54) & (HC - 1);
+#pragma unroll 1
+  for (int probe = 0; probe < 32; ++probe) {
+    unsigned long long cur = tk[h];
+    if (cur == PKEY_NONE) cur = atomicCAS(tk + h, PKEY_NONE, (unsigned long long)pk);
+    if (cur == PKEY_NONE || cur == pk) {  // same region pair: keep the lower pass
+      atomicMin(tw + h, w);
       return;
     }
-    h = (h + 1) & (HCAP - 1);
+    h = (h + 1) & (HC - 1);
   }
-  emit_global(k, edges, ecount, cap, best);  // table congested: emit undeduplicated (still correct)
+  emit_global(pk, w, dense_of, edges, ecount, cap, best);  // congested tile: emit directly
 }
 
-template <int CONN>
-__global__ void __launch_bounds__(256) k_rag(const int* __restrict__ labels, const uint8_t* __restrict__ I,
-                                             const int* __restrict__ dense_of, Geo g, uint64_t* __restrict__ edges,
-                                             unsigned long long* ecount, long long cap, uint64_t* best) {
-  __shared__ uint64_t tab[HCAP];
-  __shared__ int nloc;
-  __shared__ unsigned long long gbase;
-  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
-  for (int i = tid; i < HCAP; i += 256) tab[i] = KEY_NONE;
-  if (tid == 0) nloc = 0;
-  __syncthreads();
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y * blockDim.y + threadIdx.y;
-  constexpr int TZ = Conn<CONN>::is3d ? RAG_TZ : 1;
-  const int z0 = blockIdx.z * TZ;
-  if (x < g.n2 && y < g.n1) {
-    for (int z = z0; z < z0 + TZ && z < g.n0; ++z) {
-      const int p = z * g.plane + y * g.n2 + x;
-      const int lp = __ldg(labels + p);
-      const int vp = __ldg(I + p);
-      int dp = -1;
+template <int CONN, bool BORDER>
+__device__ __forceinline__ void rag_body(const uint8_t* sI, const int* sL, unsigned long long* tk, unsigned* tw,
+                                         const Geo& g, const TileCoord& c, const int* dense_of, uint64_t* edges,
+                                         unsigned long long* ecount, long long cap, uint64_t* best) {
+  using T = TL<CONN>;
+  constexpr int NF = CONN - Conn<CONN>::nfwd;
+  uint64_t lk[NF];
+  unsigned lw[NF];
 #pragma unroll
-      for (int i = Conn<CONN>::nfwd; i < CONN; ++i) {
-        if (!nb_in<CONN>(g, z, y, x, i)) continue;
-        const int q = p + nb_off<CONN>(g, i);
-        const int lq = __ldg(labels + q);
-        if (lq == lp) continue;
-        if (dp < 0) dp = __ldg(dense_of + lp);
-        const int dq = __ldg(dense_of + lq);
-        const int w = max(vp, (int)__ldg(I + q));
-        hash_insert(tab, make_key((uint32_t)w, (uint32_t)dp, (uint32_t)dq), edges, ecount, cap, best);
+  for (int f = 0; f < NF; ++f) { lk[f] = PKEY_NONE; lw[f] = 0xffffffffu; }
+#pragma unroll
+  for (int k = 0; k < T::VPT; ++k) {
+    int lx, ly, lz;
+    my_voxel<CONN>(k, lx, ly, lz);
+    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0)) continue;
+    const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
+    const int sl = T::iL(lz, ly, lx), si = T::iI(lz, ly, lx);
+    const int lp = sL[sl];
+    const unsigned vp = sI[si];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      const int i = Conn<CONN>::nfwd + f;
+      if (BORDER && !(vm & (1u << i))) continue;
+      const int lq = sL[sl + T::oL(i)];
+      if (lq == lp) continue;
+      const unsigned w = max(vp, (unsigned)sI[si + T::oI(i)]);
+      const uint64_t pk = pair_key(lp, lq);
+      if (pk == lk[f]) {
+        lw[f] = min(lw[f], w);
+      } else {
+        if (lk[f] != PKEY_NONE) pair_insert(tk, tw, lk[f], lw[f], dense_of, edges, ecount, cap, best);
+        lk[f] = pk;
+        lw[f] = w;
       }
     }
   }
-  __syncthreads();
-  // flush the tile's unique edges (one global atomic per block) and fold them into the
-  // level-1 per-region minima
-  int myidx[HCAP / 256];
 #pragma unroll
-  for (int j = 0; j < HCAP / 256; ++j) {
-    const uint64_t k = tab[tid + j * 256];
-    myidx[j] = (k != KEY_NONE) ? atomicAdd(&nloc, 1) : -1;
+  for (int f = 0; f < NF; ++f)
+    if (lk[f] != PKEY_NONE) pair_insert(tk, tw, lk[f], lw[f], dense_of, edges, ecount, cap, best);
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mL,
+                                            int tma, const int* __restrict__ labels, const uint8_t* __restrict__ I,
+                                            const int* __restrict__ dense_of, Geo g, int ntx, int nty,
+                                            uint64_t* __restrict__ edges, unsigned long long* ecount, long long cap,
+                                            uint64_t* best) {
+  using T = TL<CONN>;
+  __shared__ alignas(128) uint8_t sI[T::SI];
+  __shared__ alignas(128) int sL[T::SL];
+  __shared__ unsigned long long tk[HC];
+  __shared__ unsigned tw[HC];
+  __shared__ uint64_t bar;
+  __shared__ int nloc;
+  __shared__ unsigned long long gbase;
+  for (int i = threadIdx.x; i < HC; i += NT) {
+    tk[i] = PKEY_NONE;
+    tw[i] = 0xffffffffu;
+  }
+  if (threadIdx.x == 0) nloc = 0;
+  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty);
+  stage<CONN>(&mI, &mL, tma, I, labels, g, c, sI, sL, &bar);
+  __syncthreads();
+  if (tile_interior<CONN>(c, g))
+    rag_body<CONN, false>(sI, sL, tk, tw, g, c, dense_of, edges, ecount, cap, best);
+  else
+    rag_body<CONN, true>(sI, sL, tk, tw, g, c, dense_of, edges, ecount, cap, best);
+  __syncthreads();
+  // flush: dense ids per unique tile edge, K keys, warp-aggregated slot numbers
+  constexpr int M = HC / NT;
+  uint64_t key[M];
+  int idx[M];
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const int slot = threadIdx.x + m * NT;
+    const uint64_t pk = tk[slot];
+    const bool v = pk != PKEY_NONE;
+    key[m] = 0;
+    if (v)
+      key[m] = make_key(tw[slot], (uint32_t)__ldg(dense_of + (int)(pk >> 31)),
+                        (uint32_t)__ldg(dense_of + (int)(pk & 0x7fffffffu)));
+    const unsigned b = __ballot_sync(0xffffffffu, v);
+    int base = 0;
+    if (lane == 0 && b) base = atomicAdd(&nloc, __popc(b));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    idx[m] = v ? base + __popc(b & ((1u << lane) - 1)) : -1;
   }
   __syncthreads();
-  if (tid == 0) gbase = atomicAdd(ecount, (unsigned long long)nloc);
+  if (threadIdx.x == 0) gbase = atomicAdd(ecount, (unsigned long long)nloc);
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < HCAP / 256; ++j) {
-    if (myidx[j] >= 0) {
-      const uint64_t k = tab[tid + j * 256];
-      const long long i = (long long)gbase + myidx[j];
-      if (i < cap) edges[i] = k;
-      fold_best(best, k);
-    }
+  for (int m = 0; m < M; ++m) {
+    if (idx[m] < 0) continue;
+    const long long i = (long long)gbase + idx[m];
+    if (i < cap) edges[i] = key[m];
+    fold_best(best, key[m]);
   }
 }
 
@@ -427,15 +503,12 @@ __global__ void k_levels_any(const int* __restrict__ labels, const int* __restri
 template <int CONN>
 static ws_status rag_t(const int* labels, const uint8_t* I, const int* dense_of, const Geo& g, uint64_t* edges,
                        unsigned long long* ecount, long long cap, uint64_t* best, cudaStream_t st) {
-  dim3 block(32, 8, 1);
-  constexpr int TZ = Conn<CONN>::is3d ? RAG_TZ : 1;
-  const int gz = (g.n0 + TZ - 1) / TZ;
-  if (gz > 65535) {
-    set_error(WS_ERR_LIMIT, "ws_waterfall: axis 0 too long for the RAG launch (%d tiles)", gz);
-    return WS_ERR_LIMIT;
-  }
-  dim3 grid((g.n2 + 31) / 32, (g.n1 + 7) / 8, gz);
-  k_rag<CONN><<<grid, block, 0, st>>>(labels, I, dense_of, g, edges, ecount, cap, best);
+  using T = TL<CONN>;
+  const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY, ntz = (g.n0 + T::TZ - 1) / T::TZ;
+  Maps mp;
+  make_maps<CONN>(I, labels, g, mp);
+  k_rag<CONN><<<ntx * nty * ntz, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, labels, I, dense_of, g, ntx, nty, edges, ecount,
+                                               cap, best);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }

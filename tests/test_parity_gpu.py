@@ -191,3 +191,15 @@ def test_tma_and_fallback_loaders_agree(conn, ndim, shape, monkeypatch):
     lab2, _ = check_watershed(q, qn, conn, ndim)
     assert ws.stats()["tma"] == 0
     assert torch.equal(lab, lab2)
+
+
+@pytest.mark.parametrize("NL", [1, 2, 3, 5, 6, 9, 10, 12])
+@pytest.mark.parametrize("shape", [(1, 64, 96), (1, 37, 61)])
+def test_waterfall_nl_variants(NL, shape):
+    """Every NL (level-map strides 4 / 8 / NL-1, vector and scalar level writes, early
+    termination once one region is left) against the oracle."""
+    g = synth.random_plateau_image(shape, 6, seed=NL)
+    qn = g.numpy()
+    q = g.cuda()
+    lab, ref = check_watershed(q, qn, 8, 2)
+    check_waterfall(lab, q, qn, ref, 8, 2, NL)
