@@ -348,7 +348,8 @@ def run_ours(args):
             "gradient_prepass": {"ms": grad_ms, "Mvoxel_per_s": N / (grad_ms / 1e3) / 1e6},
             "phases_ms_per_step": {k: v / args.steps for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
             "input_stats": {"regions": s1["n_regions"], "edges": s2["n_edges"],
-                            "plateau_rounds": s1["plateau_rounds"], "level_counts": s2["level_counts"][:NL]},
+                            "plateau_rounds": s1["plateau_rounds"], "level_counts": s2["level_counts"][:NL],
+                            "level_edges": s2["level_edges"][1:NL]},
             "context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)

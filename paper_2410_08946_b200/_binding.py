@@ -32,7 +32,7 @@ class WsStats(ctypes.Structure):
                 ("plateau_rounds", ctypes.c_int32), ("waterfall_levels", ctypes.c_int32),
                 ("level_counts", ctypes.c_int64 * 16), ("kernel_launches", ctypes.c_int64),
                 ("phase_ms", ctypes.c_double * 16), ("phase_launches", ctypes.c_int32 * 16),
-                ("tma", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("tma", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("level_edges", ctypes.c_int64 * 16)]
 
     def as_dict(self):
         lib = load()
@@ -44,7 +44,7 @@ class WsStats(ctypes.Structure):
         return {"n_voxels": self.n_voxels, "n_regions": self.n_regions, "n_edges": self.n_edges,
                 "plateau_rounds": self.plateau_rounds, "waterfall_levels": self.waterfall_levels,
                 "level_counts": list(self.level_counts), "kernel_launches": self.kernel_launches,
-                "phases": phases, "tma": self.tma}
+                "phases": phases, "tma": self.tma, "level_edges": list(self.level_edges)}
 
 
 class WsError(RuntimeError):

@@ -143,10 +143,12 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
 // ------------------------------------------------------------------------ RAG extraction
 // Tiles and TMA staging as in the watershed (ws_tile.cuh): the label box (i32) and the
 // intensity box (u8) of a 2048-voxel tile land in shared memory with one bulk-tensor copy
-// each.  Every thread walks its 8 voxels; per forward direction it run-length-merges equal
-// region pairs in registers (min height), and only run ends touch the shared hash, which is
-// keyed by the LABEL pair (dense ids are looked up once per unique tile edge at the flush).
-constexpr int HC = 1024;                       // shared hash slots per tile
+// each.  A boundary pair is keyed by its LABEL pair (62 bits) with the pass height kept
+// separately (atomicMin on a 32-bit slot = per-pair minimum, Alg. 4 l.2-7).  Each thread walks
+// a column of 8 voxels and run-length-merges equal pairs per direction in registers, so only
+// run ends touch the shared hash; dense ids are looked up once per unique tile edge at the
+// flush, where the edge key K = [w:8][~max:28][~min:28] (C14) is formed.
+constexpr int HC = 2048;                      // shared hash slots per tile (load <= ~25%)
 constexpr uint64_t PKEY_NONE = ~0ull;
 
 __device__ __forceinline__ uint64_t pair_key(int a, int b) {
@@ -171,7 +173,7 @@ __device__ __noinline__ void emit_global(uint64_t pk, unsigned w, const int* den
 __device__ __forceinline__ void pair_insert(unsigned long long* tk, unsigned* tw, uint64_t pk, unsigned w,
                                             const int* dense_of, uint64_t* edges, unsigned long long* ecount,
                                             long long cap, uint64_t* best) {
-  uint32_t h = (uint32_t)((pk * 0x9E3779B97F4A7C15ull) >> 54) & (HC - 1);
+  uint32_t h = (((uint32_t)(pk >> 31) * 0x9E3779B1u) ^ ((uint32_t)pk * 0x85EBCA77u)) >> 21;  // 11 bits
 #pragma unroll 1
   for (int probe = 0; probe < 32; ++probe) {
     unsigned long long cur = tk[h];
@@ -191,7 +193,7 @@ __device__ __forceinline__ void rag_body(const uint8_t* sI, const int* sL, unsig
                                          unsigned long long* ecount, long long cap, uint64_t* best) {
   using T = TL<CONN>;
   constexpr int NF = CONN - Conn<CONN>::nfwd;
-  uint64_t lk[NF];
+  uint64_t lk[NF];  // per forward direction: the current run's pair and its min height
   unsigned lw[NF];
 #pragma unroll
   for (int f = 0; f < NF; ++f) { lk[f] = PKEY_NONE; lw[f] = 0xffffffffu; }
@@ -233,10 +235,11 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
                                             uint64_t* __restrict__ edges, unsigned long long* ecount, long long cap,
                                             uint64_t* best) {
   using T = TL<CONN>;
-  __shared__ alignas(128) uint8_t sI[T::SI];
-  __shared__ alignas(128) int sL[T::SL];
-  __shared__ unsigned long long tk[HC];
-  __shared__ unsigned tw[HC];
+  extern __shared__ __align__(128) unsigned char rag_smem[];
+  uint8_t* sI = rag_smem;                                                   // T::SI bytes
+  int* sL = reinterpret_cast<int*>(rag_smem + T::SI);                       // T::SL ints
+  unsigned long long* tk = reinterpret_cast<unsigned long long*>(rag_smem + T::SI + 4 * T::SL);
+  unsigned* tw = reinterpret_cast<unsigned*>(tk + HC);
   __shared__ uint64_t bar;
   __shared__ int nloc;
   __shared__ unsigned long long gbase;
@@ -255,18 +258,11 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
   __syncthreads();
   // flush: dense ids per unique tile edge, K keys, warp-aggregated slot numbers
   constexpr int M = HC / NT;
-  uint64_t key[M];
   int idx[M];
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int m = 0; m < M; ++m) {
-    const int slot = threadIdx.x + m * NT;
-    const uint64_t pk = tk[slot];
-    const bool v = pk != PKEY_NONE;
-    key[m] = 0;
-    if (v)
-      key[m] = make_key(tw[slot], (uint32_t)__ldg(dense_of + (int)(pk >> 31)),
-                        (uint32_t)__ldg(dense_of + (int)(pk & 0x7fffffffu)));
+    const bool v = tk[threadIdx.x + m * NT] != PKEY_NONE;
     const unsigned b = __ballot_sync(0xffffffffu, v);
     int base = 0;
     if (lane == 0 && b) base = atomicAdd(&nloc, __popc(b));
@@ -279,9 +275,13 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     if (idx[m] < 0) continue;
+    const int slot = threadIdx.x + m * NT;
+    const uint64_t pk = tk[slot];
+    const uint64_t k = make_key(tw[slot], (uint32_t)__ldg(dense_of + (int)(pk >> 31)),
+                                (uint32_t)__ldg(dense_of + (int)(pk & 0x7fffffffu)));
     const long long i = (long long)gbase + idx[m];
-    if (i < cap) edges[i] = key[m];
-    fold_best(best, key[m]);
+    if (i < cap) edges[i] = k;
+    fold_best(best, k);
   }
 }
 
@@ -369,58 +369,89 @@ struct Edge {
   int a, b;  // current component roots
 };
 
-// level k >= 2: re-label live edges to the level-(k-1) roots, drop edges inside one
-// component, fold survivors into best[] and append them (smem-staged compaction).
+// level k >= 2: re-label live edges to the level-(k-1) roots, drop edges inside one component,
+// and deduplicate per block chunk by COMPONENT pair in a shared hash (min K per pair: only
+// the lowest edge between two components can ever be picked, C14/C15).  Survivors fold into
+// best[] (per-component min-K edge) and are appended (one global atomic per block).
 // in_keys != nullptr: the input is the level-1 key list (endpoints decoded from K).
+constexpr int ECH = 2048;  // edges per block (8 per thread)
+constexpr int EHC = 4096;  // shared hash slots
+
 __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_keys, const Edge* __restrict__ in,
                                                 long long n, const int* __restrict__ comp, uint64_t* best,
                                                 Edge* __restrict__ out, unsigned long long* nout) {
-  __shared__ Edge sbuf[2 * NTW];
-  __shared__ int scount;
-  __shared__ unsigned long long sbase;
-  if (threadIdx.x == 0) scount = 0;
+  extern __shared__ __align__(16) unsigned long long esm[];
+  unsigned long long* tp = esm;        // component pair (lo << 32 | hi)
+  unsigned long long* tkk = esm + EHC;  // min K of the pair
+  __shared__ int nloc;
+  __shared__ unsigned long long gbase;
+  for (int i = threadIdx.x; i < EHC; i += NTW) {
+    tp[i] = KEY_NONE;
+    tkk[i] = KEY_NONE;
+  }
+  if (threadIdx.x == 0) nloc = 0;
   __syncthreads();
+  const long long e0 = (long long)blockIdx.x * ECH;
+#pragma unroll
+  for (int j = 0; j < ECH / NTW; ++j) {
+    const long long e = e0 + threadIdx.x + j * NTW;
+    if (e >= n) break;
+    uint64_t k;
+    int a, b;
+    if (in_keys) {
+      k = in_keys[e];
+      a = (int)key_lo(k);
+      b = (int)key_hi(k);
+    } else {
+      const Edge ed = in[e];
+      k = ed.k;
+      a = ed.a;
+      b = ed.b;
+    }
+    a = __ldg(comp + a);
+    b = __ldg(comp + b);
+    if (a == b) continue;
+    const uint64_t pk = ((uint64_t)(uint32_t)min(a, b) << 32) | (uint32_t)max(a, b);
+    uint32_t h = (((uint32_t)(pk >> 32) * 0x9E3779B1u) ^ ((uint32_t)pk * 0x85EBCA77u)) >> 20;  // 12 bits
+#pragma unroll 1
+    while (true) {
+      unsigned long long cur = tp[h];
+      if (cur == KEY_NONE) cur = atomicCAS(tp + h, KEY_NONE, (unsigned long long)pk);
+      if (cur == KEY_NONE || cur == pk) {
+        atomicMin(tkk + h, (unsigned long long)k);
+        break;
+      }
+      h = (h + 1) & (EHC - 1);  // at most ECH pairs in EHC slots: always terminates
+    }
+  }
+  __syncthreads();
+  constexpr int M = EHC / NTW;
+  int idx[M];
   const int lane = threadIdx.x & 31;
-  const long long stride = (long long)gridDim.x * NTW;
-  for (long long e0 = (long long)blockIdx.x * NTW; e0 < n; e0 += stride) {
-    const long long e = e0 + threadIdx.x;
-    bool live = false;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const bool v = tp[threadIdx.x + m * NTW] != KEY_NONE;
+    const unsigned bal = __ballot_sync(0xffffffffu, v);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(&nloc, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    idx[m] = v ? base + __popc(bal & ((1u << lane) - 1)) : -1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) gbase = atomicAdd(nout, (unsigned long long)nloc);
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    if (idx[m] < 0) continue;
+    const int slot = threadIdx.x + m * NTW;
+    const unsigned long long pk = tp[slot];
     Edge ed;
-    if (e < n) {
-      if (in_keys) {
-        ed.k = in_keys[e];
-        ed.a = (int)key_lo(ed.k);
-        ed.b = (int)key_hi(ed.k);
-      } else {
-        ed = in[e];
-      }
-      ed.a = __ldg(comp + ed.a);
-      ed.b = __ldg(comp + ed.b);
-      live = ed.a != ed.b;
-      if (live) {
-        atomicMin((unsigned long long*)(best + ed.a), (unsigned long long)ed.k);
-        atomicMin((unsigned long long*)(best + ed.b), (unsigned long long)ed.k);
-      }
-    }
-    const unsigned lb = __ballot_sync(0xffffffffu, live);
-    if (lb) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&scount, __popc(lb));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (live) sbuf[base + __popc(lb & ((1u << lane) - 1))] = ed;
-    }
-    __syncthreads();
-    const int cnt = scount;
-    if (cnt > NTW || e0 + stride >= n) {
-      if (cnt > 0) {
-        if (threadIdx.x == 0) sbase = atomicAdd(nout, (unsigned long long)cnt);
-        __syncthreads();
-        for (int j = threadIdx.x; j < cnt; j += NTW) out[sbase + j] = sbuf[j];
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) scount = 0;
-      __syncthreads();
-    }
+    ed.k = tkk[slot];
+    ed.a = (int)(pk >> 32);
+    ed.b = (int)(pk & 0xffffffffu);
+    atomicMin((unsigned long long*)(best + ed.a), (unsigned long long)ed.k);
+    atomicMin((unsigned long long*)(best + ed.b), (unsigned long long)ed.k);
+    out[gbase + idx[m]] = ed;
   }
 }
 
@@ -507,8 +538,11 @@ static ws_status rag_t(const int* labels, const uint8_t* I, const int* dense_of,
   const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY, ntz = (g.n0 + T::TZ - 1) / T::TZ;
   Maps mp;
   make_maps<CONN>(I, labels, g, mp);
-  k_rag<CONN><<<ntx * nty * ntz, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, labels, I, dense_of, g, ntx, nty, edges, ecount,
-                                               cap, best);
+  const int smem = T::SI + 4 * T::SL + HC * 12;  // I box, L box, hash keys + heights
+  static_assert((T::SI % 16) == 0 && ((T::SI + 4 * T::SL) % 16) == 0, "smem carve-up alignment");
+  WS_CUDA(cudaFuncSetAttribute(k_rag<CONN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_rag<CONN><<<ntx * nty * ntz, NT, smem, st>>>(mp.mI, mp.mL, mp.tma, labels, I, dense_of, g, ntx, nty, edges,
+                                                  ecount, cap, best);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
@@ -634,11 +668,16 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   int lv = 0;
   long long prev = R;
   for (int k = 1; k < NL; ++k) {
+    if (k < 16) ctx->stats.level_edges[k] = ne_in;
     if (prev > 1 && (k == 1 || lv == k - 1)) {
       if (k >= 2) {  // per-component min-K edges of level k (level 1 came from the RAG)
         WS_CUDA(cudaMemsetAsync(nedges, 0, sizeof(unsigned long long), st));
-        k_edges<<<grid_for(ne_in, ctx->num_sms, 8), NTW, 0, st>>>(k == 2 ? ctx->edges.as<uint64_t>() : nullptr,
-                                                                   ein, ne_in, comp, best, eout, nedges);
+        if (ne_in > 0) {
+          const int esmem = EHC * 16;
+          WS_CUDA(cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
+          k_edges<<<(int)((ne_in + ECH - 1) / ECH), NTW, esmem, st>>>(k == 2 ? ctx->edges.as<uint64_t>() : nullptr,
+                                                                     ein, ne_in, comp, best, eout, nedges);
+        }
         launched(ctx, PH_WF_LEVELS);
       }
       k_hook<<<grid_for(nr_in, ctx->num_sms), 256, 0, st>>>(best, comp, rin, (int)nr_in);
