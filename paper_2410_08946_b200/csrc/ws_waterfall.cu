@@ -470,50 +470,54 @@ __global__ void k_levelmap(const int* __restrict__ comp, const uint8_t* __restri
 }
 
 // --------------------------------------------------------------- level materialisation
-// 4 voxels per thread: one int4 label load, int4 streaming stores per level; the map row of
-// a label is fetched once per run of equal labels.
-template <int STRIDE>
-__device__ __forceinline__ void map_row(const int* levelmap, int d, int* r, int n) {
-  const int* m = levelmap + (size_t)d * STRIDE;
-  if (STRIDE % 4 == 0) {
-#pragma unroll
-    for (int j = 0; j < STRIDE; j += 4) {
-      const int4 v = __ldg(reinterpret_cast<const int4*>(m + j));
-      r[j] = v.x; r[j + 1] = v.y; r[j + 2] = v.z; r[j + 3] = v.w;
-    }
-  } else {
-    for (int j = 0; j < n; ++j) r[j] = __ldg(m + j);
-  }
-}
-
-template <int STRIDE>
+// Tiled (the watershed's 2048-voxel tiles): a region's voxels are processed together, so its
+// dense id and level-map row are fetched about once per tile.  Lanes run along x: only the
+// first lane of every run of equal labels gathers (dense_of, then one 16/32-byte map row);
+// the others take the row by shuffle.  Along z each lane also reuses its previous row.
+// Level outputs are streaming stores (evict-first).
+template <int CONN, int STRIDE>
 __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ labels, const int* __restrict__ dense_of,
-                                                 const int* __restrict__ levelmap, int NL, long long N,
+                                                 const int* __restrict__ levelmap, int NL, Geo g, int ntx, int nty,
                                                  int* __restrict__ levels) {
-  const long long n4 = N / 4;
+  using T = TL<CONN>;
+  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty);
+  const int lane = threadIdx.x & 31;
   const int nm = NL - 1;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
-    const int4 l = __ldg(reinterpret_cast<const int4*>(labels) + i);
-    __stcs(reinterpret_cast<int4*>(levels) + i, l);
-    if (nm == 0) continue;
-    int r0[STRIDE], r1[STRIDE], r2[STRIDE], r3[STRIDE];
-    map_row<STRIDE>(levelmap, __ldg(dense_of + l.x), r0, nm);
-    if (l.y == l.x) { for (int j = 0; j < STRIDE; ++j) r1[j] = r0[j]; } else map_row<STRIDE>(levelmap, __ldg(dense_of + l.y), r1, nm);
-    if (l.z == l.y) { for (int j = 0; j < STRIDE; ++j) r2[j] = r1[j]; } else map_row<STRIDE>(levelmap, __ldg(dense_of + l.z), r2, nm);
-    if (l.w == l.z) { for (int j = 0; j < STRIDE; ++j) r3[j] = r2[j]; } else map_row<STRIDE>(levelmap, __ldg(dense_of + l.w), r3, nm);
+  const size_t N = (size_t)g.N;
+  int prev_l = -1;
+  int row[STRIDE];
 #pragma unroll
-    for (int k = 1; k <= STRIDE; ++k) {
-      if (k > nm) break;
-      __stcs(reinterpret_cast<int4*>(levels + (size_t)k * N) + i, make_int4(r0[k - 1], r1[k - 1], r2[k - 1], r3[k - 1]));
+  for (int j = 0; j < STRIDE; ++j) row[j] = 0;
+#pragma unroll 1
+  for (int k = 0; k < T::VPT; ++k) {
+    int lx, ly, lz;
+    my_voxel<CONN>(k, lx, ly, lz);
+    const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
+    const bool valid = gx < g.n2 && gy < g.n1 && gz < g.n0;
+    const size_t p = (size_t)gz * g.plane + (size_t)gy * g.n2 + gx;
+    const int l = valid ? __ldcs(labels + p) : -1 - lane;
+    const int lup = __shfl_up_sync(0xffffffffu, l, 1);
+    const bool head = (lane == 0 || lup != l);
+    const bool fetch = valid && head && l != prev_l;
+    if (fetch) {
+      const int* m = levelmap + (size_t)__ldg(dense_of + l) * STRIDE;
+#pragma unroll
+      for (int j = 0; j < STRIDE; j += 4) {
+        const int4 v = __ldg(reinterpret_cast<const int4*>(m + j));
+        row[j] = v.x; row[j + 1] = v.y; row[j + 2] = v.z; row[j + 3] = v.w;
+      }
     }
-  }
-  // scalar tail (N % 4 voxels)
-  for (long long p = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N;
-       p += (long long)gridDim.x * blockDim.x) {
-    const int l = __ldg(labels + p);
-    levels[p] = l;
-    const int* m = levelmap + (size_t)__ldg(dense_of + l) * STRIDE;
-    for (int k = 1; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k - 1);
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    const int src = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+    for (int j = 0; j < STRIDE; ++j) row[j] = __shfl_sync(0xffffffffu, row[j], src);
+    prev_l = l;
+    if (valid) {
+      __stcs(levels + p, l);
+#pragma unroll
+      for (int j = 0; j < STRIDE; ++j)
+        if (j < nm) __stcs(levels + (size_t)(j + 1) * N + p, row[j]);
+    }
   }
 }
 
@@ -711,12 +715,15 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   }
   tmark(ctx, st, PH_WF_LEVELS);
   const int gN = grid_for(N, ctx->num_sms);
-  const bool vec = (N % 4 == 0) && !(reinterpret_cast<uintptr_t>(labels) & 15) &&
-                   !(reinterpret_cast<uintptr_t>(levels) & 15);
-  if (vec && stride == 4) {
-    k_levels<4><<<gN, NTW, 0, st>>>(labels, dense_of, levelmap, NL, N, levels);
-  } else if (vec && stride == 8) {
-    k_levels<8><<<gN, NTW, 0, st>>>(labels, dense_of, levelmap, NL, N, levels);
+  if (stride == 4 || stride == 8) {
+    const bool is3d = (conn == 6 || conn == 26);
+    const int TX = is3d ? TL<6>::TX : TL<4>::TX, TY = is3d ? TL<6>::TY : TL<4>::TY, TZ = is3d ? TL<6>::TZ : TL<4>::TZ;
+    const int ntx = (g.n2 + TX - 1) / TX, nty = (g.n1 + TY - 1) / TY, ntz = (g.n0 + TZ - 1) / TZ;
+    const int nt = ntx * nty * ntz;
+    if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
+    else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
+    else if (stride == 4) k_levels<4, 4><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
+    else k_levels<4, 8><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
   } else {
     k_levels_any<<<gN, NTW, 0, st>>>(labels, dense_of, levelmap, NL, stride, N, levels);
   }
