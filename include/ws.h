@@ -152,6 +152,54 @@ ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims,
 ws_status ws_plateau_debug(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity,
                            int32_t* dist, int32_t* parent, void* stream);
 
+/* ==================================================================================
+ * z-slab sharding (north_star: "3D volumes are partitioned along z into slabs across the 8
+ * GPUs of one box, with NCCL halo exchange over NVLink and a cross-slab boundary union-find
+ * merge").  Volumes (ndim 3), 6-connectivity.  Rank r of K owns global planes
+ * [z0, z1) and holds an EXTENDED slab [e0, e1) = [max(0, z0-2), min(D, z1+2)) of grad and of
+ * the working array L_ext (i32); every dims argument below is the extended slab
+ * (n0 = e1 - e0, n1, n2).  The caller moves the planes between ranks (NCCL through
+ * torch.distributed, or in-process copies) between the calls; the library computes.
+ * Result: identical labels to ws_watershed on the whole volume (global voxel indices).
+ * ================================================================================== */
+typedef struct ws_slab {
+  int64_t D;        /* global depth                                                        */
+  int64_t z0, z1;   /* owned planes [z0, z1)                                                */
+  int64_t e0, e1;   /* extended planes held by the caller                                   */
+} ws_slab;
+
+/* bytes of one rank's boundary table (ws_shard_local output, ws_shard_merge input) */
+int64_t ws_shard_table_bytes(ws_dims dims_ext);
+
+/* step I + one step II relaxation round on the owned planes (Alg. 1 l.1-18 / Alg. 3).
+ * phase 0: first round (classification + relaxation; halo planes of L_ext need not be set).
+ * phase 1: a further round on the active tiles; act_lo / act_hi re-activate the first / last
+ *          owned tile layer after the halo plane below / above changed.
+ * pending (HOST): 1 if this rank has work for another round.  L_ext halo planes: the plane
+ * just outside the owned range on each side must hold the neighbour's L values (phase 1). */
+ws_status ws_shard_plateau(ws_ctx* ctx, const uint8_t* grad_ext, ws_dims dims_ext, int32_t connectivity,
+                           ws_slab slab, int32_t* L_ext, int32_t phase, int32_t act_lo, int32_t act_hi,
+                           int32_t* pending, void* stream);
+/* copy a neighbour's boundary plane of L (plane_in, i32[n1*n2], device) into the halo plane
+ * below (side 0: z0 - 1) or above (side 1: z1) of L_ext; changed (HOST) = 1 if it differed */
+ws_status ws_shard_halo(ws_ctx* ctx, int32_t* L_ext, ws_dims dims_ext, ws_slab slab, int32_t side,
+                        const int32_t* plane_in, int32_t* changed, void* stream);
+/* pointers (steps I-II), local step III (chains leaving the slab stop at an exit), local
+ * step IV, per-root minima; writes P_ext (i32, owned planes) and this rank's boundary table */
+ws_status ws_shard_local(ws_ctx* ctx, const uint8_t* grad_ext, int32_t* L_ext, ws_dims dims_ext,
+                         int32_t connectivity, ws_slab slab, int32_t* P_ext, void* table, void* stream);
+/* replicated cross-slab merge over the K gathered tables (tables_all: K tables back to back,
+ * device; z0s/z1s: HOST i64[K] owned plane ranges, ascending): chase exits, union minimal
+ * plateaux across every cut plane, canonical minima; writes this rank's root labels into
+ * L_ext and exitcanon (i32[2*n1*n2], device) */
+ws_status ws_shard_merge(ws_ctx* ctx, const void* tables_all, int32_t nranks, const int64_t* z0s,
+                         const int64_t* z1s, ws_dims dims_ext, ws_slab slab, int32_t* L_ext, int32_t* exitcanon,
+                         void* stream);
+/* canonical labels of the owned voxels -> labels_own (i32[(z1-z0)*n1*n2]); nreps (HOST,
+ * optional) = owned voxels that are their region's smallest index (for dense-id offsets) */
+ws_status ws_shard_relabel(ws_ctx* ctx, const int32_t* P_ext, int32_t* L_ext, const int32_t* exitcanon,
+                           ws_dims dims_ext, ws_slab slab, int32_t* labels_own, int64_t* nreps, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

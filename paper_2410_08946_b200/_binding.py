@@ -19,12 +19,19 @@ STATUS_NAMES = {0: "WS_OK", 1: "WS_ERR_INVALID", 2: "WS_ERR_OOM", 3: "WS_ERR_CUD
 # every symbol include/ws.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ws_ctx_create", "ws_ctx_destroy", "ws_last_error", "ws_version", "ws_get_stats",
            "ws_ctx_set_timing", "ws_phase_name",
-           "ws_gradient", "ws_watershed", "ws_waterfall", "ws_segment_host", "ws_plateau_debug")
+           "ws_gradient", "ws_watershed", "ws_waterfall", "ws_segment_host", "ws_plateau_debug",
+           "ws_shard_table_bytes", "ws_shard_plateau", "ws_shard_halo", "ws_shard_local", "ws_shard_merge",
+           "ws_shard_relabel")
 
 
 class WsDims(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("n0", ctypes.c_int64), ("n1", ctypes.c_int64), ("n2", ctypes.c_int64)]
+
+
+class WsSlab(ctypes.Structure):
+    _fields_ = [("D", ctypes.c_int64), ("z0", ctypes.c_int64), ("z1", ctypes.c_int64), ("e0", ctypes.c_int64),
+                ("e1", ctypes.c_int64)]
 
 
 class WsStats(ctypes.Structure):
@@ -80,9 +87,17 @@ def load(path: str = SO_PATH):
         lib.ws_waterfall.argtypes = [vp, vp, vp, WsDims, i32, i32, vp, vp, vp]
         lib.ws_segment_host.argtypes = [vp, vp, WsDims, i32, i32, vp, vp, vp]
         lib.ws_plateau_debug.argtypes = [vp, vp, WsDims, i32, vp, vp, vp]
+        lib.ws_shard_table_bytes.argtypes = [WsDims]
+        lib.ws_shard_table_bytes.restype = ctypes.c_int64
+        pi32 = ctypes.POINTER(ctypes.c_int32)
+        lib.ws_shard_plateau.argtypes = [vp, vp, WsDims, i32, WsSlab, vp, i32, i32, i32, pi32, vp]
+        lib.ws_shard_halo.argtypes = [vp, vp, WsDims, WsSlab, i32, vp, pi32, vp]
+        lib.ws_shard_local.argtypes = [vp, vp, vp, WsDims, i32, WsSlab, vp, vp, vp]
+        lib.ws_shard_merge.argtypes = [vp, vp, i32, vp, vp, WsDims, WsSlab, vp, vp, vp]
+        lib.ws_shard_relabel.argtypes = [vp, vp, vp, vp, WsDims, WsSlab, vp, vp, vp]
         for name in EXPORTS:
             f = getattr(lib, name)
-            if name not in ("ws_last_error", "ws_version", "ws_phase_name"):
+            if name not in ("ws_last_error", "ws_version", "ws_phase_name", "ws_shard_table_bytes"):
                 f.restype = ctypes.c_int
         _lib = lib
         return lib

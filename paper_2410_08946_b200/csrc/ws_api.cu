@@ -73,6 +73,9 @@ static ws_status check_dims(const ws_dims& d, Geo* g) {
   g->n2 = (int)d.n2;
   g->plane = g->n1 * g->n2;
   g->N = g->plane * g->n0;
+  g->zlo = 0;
+  g->zhi = g->n0;
+  g->gofs = 0;
   return WS_OK;
 }
 
@@ -335,6 +338,98 @@ ws_status ws_plateau_debug(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32
   ws_status s = run_plateau_debug(ctx, grad, g, connectivity, dist, parent, (cudaStream_t)stream);
   ctx->ev_n = 0;
   return s;
+}
+
+// ------------------------------------------------------------------ z-slab sharding
+static ws_status check_slab(const ws_dims& d, const ws_slab& sl, int conn, Geo* g) {
+  WS_TRY(check_dims(d, g));
+  if (d.ndim != 3 || conn != 6) {
+    set_error(WS_ERR_INVALID, "the sharded path supports 3-D volumes with 6-connectivity");
+    return WS_ERR_INVALID;
+  }
+  const int64_t plane = d.n1 * d.n2;
+  if (!(0 <= sl.e0 && sl.e0 <= sl.z0 && sl.z0 < sl.z1 && sl.z1 <= sl.e1 && sl.e1 <= sl.D) ||
+      d.n0 != sl.e1 - sl.e0 || (double)sl.D * (double)plane >= 2147483648.0 ||
+      (sl.z0 > 0 && sl.e0 > sl.z0 - 1) || (sl.z1 < sl.D && sl.e1 < sl.z1 + 1)) {
+    set_error(WS_ERR_INVALID, "inconsistent slab (D=%lld z=[%lld,%lld) e=[%lld,%lld) n0=%lld)", (long long)sl.D,
+              (long long)sl.z0, (long long)sl.z1, (long long)sl.e0, (long long)sl.e1, (long long)d.n0);
+    return WS_ERR_INVALID;
+  }
+  g->zlo = (int)(sl.z0 - sl.e0);
+  g->zhi = (int)(sl.z1 - sl.e0);
+  g->gofs = (int)(sl.e0 * plane);
+  return WS_OK;
+}
+
+int64_t ws_shard_table_bytes(ws_dims d) { return (int64_t)d.n1 * d.n2 * 28; }
+
+ws_status ws_shard_plateau(ws_ctx* ctx, const uint8_t* grad_ext, ws_dims dims, int32_t conn, ws_slab slab,
+                           int32_t* L_ext, int32_t phase, int32_t act_lo, int32_t act_hi, int32_t* pending,
+                           void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, conn, &g));
+  if (!grad_ext || !L_ext || !pending) return null_arg("grad_ext/L_ext/pending");
+  begin_call(ctx, g);
+  int pend = 0;
+  ws_status s = phase == 0 ? plateau_first_shard(ctx, grad_ext, g, conn, L_ext, &pend, (cudaStream_t)stream)
+                           : plateau_round_shard(ctx, grad_ext, g, conn, L_ext, act_lo, act_hi, &pend,
+                                                 (cudaStream_t)stream);
+  *pending = pend;
+  return s;
+}
+
+ws_status ws_shard_halo(ws_ctx* ctx, int32_t* L_ext, ws_dims dims, ws_slab slab, int32_t side,
+                        const int32_t* plane_in, int32_t* changed, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, 6, &g));
+  if (!L_ext || !plane_in || !changed) return null_arg("L_ext/plane_in/changed");
+  if ((side == 0 && g.zlo < 1) || (side == 1 && g.zhi >= g.n0) || (side != 0 && side != 1)) {
+    set_error(WS_ERR_INVALID, "no halo plane on side %d", side);
+    return WS_ERR_INVALID;
+  }
+  return shard_halo(ctx, L_ext, g, side, plane_in, changed, (cudaStream_t)stream);
+}
+
+ws_status ws_shard_local(ws_ctx* ctx, const uint8_t* grad_ext, int32_t* L_ext, ws_dims dims, int32_t conn,
+                         ws_slab slab, int32_t* P_ext, void* table, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, conn, &g));
+  if (!grad_ext || !L_ext || !P_ext || !table) return null_arg("grad_ext/L_ext/P_ext/table");
+  begin_call(ctx, g);
+  return shard_local(ctx, grad_ext, g, conn, L_ext, P_ext, table, (cudaStream_t)stream);
+}
+
+ws_status ws_shard_merge(ws_ctx* ctx, const void* tables_all, int32_t nranks, const int64_t* z0s, const int64_t* z1s,
+                         ws_dims dims, ws_slab slab, int32_t* L_ext, int32_t* exitcanon, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, 6, &g));
+  if (!tables_all || !z0s || !z1s || !L_ext || !exitcanon) return null_arg("tables/z0s/z1s/L_ext/exitcanon");
+  int rank = -1;
+  for (int r = 0; r < nranks; ++r) {
+    if (r > 0 && z0s[r] != z1s[r - 1]) {
+      set_error(WS_ERR_INVALID, "slabs must tile [0, D) in order");
+      return WS_ERR_INVALID;
+    }
+    if (z0s[r] == slab.z0 && z1s[r] == slab.z1) rank = r;
+  }
+  if (rank < 0 || nranks < 1 || z0s[0] != 0 || z1s[nranks - 1] != slab.D) {
+    set_error(WS_ERR_INVALID, "slab not among the nranks slabs / slabs do not cover [0, D)");
+    return WS_ERR_INVALID;
+  }
+  return shard_merge(ctx, tables_all, z0s, z1s, nranks, rank, g, L_ext, exitcanon, (cudaStream_t)stream);
+}
+
+ws_status ws_shard_relabel(ws_ctx* ctx, const int32_t* P_ext, int32_t* L_ext, const int32_t* exitcanon, ws_dims dims,
+                           ws_slab slab, int32_t* labels_own, int64_t* nreps, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, 6, &g));
+  if (!P_ext || !L_ext || !exitcanon || !labels_own) return null_arg("P_ext/L_ext/exitcanon/labels_own");
+  return shard_relabel(ctx, P_ext, L_ext, exitcanon, g, labels_own, nreps, (cudaStream_t)stream);
 }
 
 }  // extern "C"

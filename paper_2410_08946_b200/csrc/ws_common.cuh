@@ -10,6 +10,11 @@ struct Geo {
   int n0, n1, n2;   // each < 2^31 and n0*n1*n2 < 2^31
   int plane;        // n1 * n2
   int N;
+  // z-slab sharding (ws_shard_*): planes [zlo, zhi) of this (extended) volume are owned by
+  // the caller, the others are read-only halo; gofs = global linear index of local voxel 0.
+  // Unsharded calls: zlo = 0, zhi = n0, gofs = 0.
+  int zlo, zhi;
+  int gofs;
 };
 
 // ------------------------------------------------------------------------------------

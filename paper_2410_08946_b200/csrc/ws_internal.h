@@ -57,6 +57,12 @@ struct ws_ctx {
   ws::Buf ebufA, ebufB;   // compacted live edges (key + current endpoints), ping-pong
   ws::Buf rootsA, rootsB; // level roots lists, ping-pong
   ws::Buf lvl;            // u8[R] level at which a component stops being a root
+  // z-slab sharding state
+  ws::Buf exitmx;         // i32[2*plane] per-exit minima (INT_MAX - p)
+  ws::Buf mtables, mslabs, mr0, mmap;  // replicated merge: gathered tables, bounds, R0, root map
+  int shard_nroots = 0;
+  int shard_tiles = 0;    // tile count of the current sharded plateau phase
+  int shard_flip = 0;     // which tile-flag buffer holds "next"
   ws::Buf comp;       // i32[R]   component parent (union-find over dense ids)
   ws::Buf best;       // u64[R]   per-component min-K edge
   ws::Buf rep_of;     // i32[R]   dense id -> canonical voxel label
@@ -99,6 +105,20 @@ ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn
                         int32_t* labels, int64_t* num_regions, cudaStream_t st);
 ws_status run_plateau_debug(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
                             int32_t* dist, int32_t* parent, cudaStream_t st);
+// z-slab sharded watershed phases (ws_shard.cu / ws_watershed.cu)
+ws_status plateau_first_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int* pending,
+                              cudaStream_t st);
+ws_status plateau_round_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int act_lo,
+                              int act_hi, int* pending, cudaStream_t st);
+ws_status shard_halo(ws_ctx* ctx, int32_t* L, const Geo& g, int side, const int32_t* plane_in, int32_t* changed,
+                     cudaStream_t st);
+ws_status shard_local(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int32_t* P, void* table,
+                      cudaStream_t st);
+ws_status shard_merge(ws_ctx* ctx, const void* tables, const int64_t* z0s, const int64_t* z1s, int K, int rank,
+                      const Geo& g, int32_t* L, int32_t* exitcanon, cudaStream_t st);
+ws_status shard_relabel(ws_ctx* ctx, const int32_t* P, int32_t* L, const int32_t* exitcanon, const Geo& g,
+                        int32_t* labels_own, int64_t* nreps, cudaStream_t st);
+
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g,
                         int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
 

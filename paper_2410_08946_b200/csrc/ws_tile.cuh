@@ -46,13 +46,14 @@ struct TileCoord {
   int bx, by, bz;  // global coordinates of the tile origin
 };
 
+// tiles cover the owned planes [zlo, zhi) (the whole volume when unsharded)
 template <int CONN>
-__device__ __forceinline__ TileCoord tile_coord(int t, int ntx, int nty) {
+__device__ __forceinline__ TileCoord tile_coord(int t, int ntx, int nty, const Geo& g) {
   using T = TL<CONN>;
   TileCoord c;
   c.bx = (t % ntx) * T::TX;
   c.by = ((t / ntx) % nty) * T::TY;
-  c.bz = (t / (ntx * nty)) * T::TZ;
+  c.bz = g.zlo + (t / (ntx * nty)) * T::TZ;
   return c;
 }
 
@@ -61,7 +62,8 @@ template <int CONN>
 __device__ __forceinline__ bool tile_interior(const TileCoord& c, const Geo& g) {
   using T = TL<CONN>;
   return c.bx >= 2 && c.bx + T::TX + 2 <= g.n2 && c.by >= 2 && c.by + T::TY + 2 <= g.n1 &&
-         (!T::is3d || (c.bz >= 2 && c.bz + T::TZ + 2 <= g.n0));
+         (!T::is3d || (c.bz >= 2 && c.bz + T::TZ + 2 <= g.n0)) &&
+         c.bz + T::TZ + (g.zhi < g.n0 ? 1 : 0) <= g.zhi;  // sharded: the top layer is border
 }
 
 // voxel k of this thread inside the tile: j = threadIdx.x + k * NT (x fastest)

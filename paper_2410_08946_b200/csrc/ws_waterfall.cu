@@ -201,7 +201,7 @@ __device__ __forceinline__ void rag_body(const uint8_t* sI, const int* sL, unsig
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0)) continue;
+    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi)) continue;
     const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
     const int sl = T::iL(lz, ly, lx), si = T::iI(lz, ly, lx);
     const int lp = sL[sl];
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
     tw[i] = 0xffffffffu;
   }
   if (threadIdx.x == 0) nloc = 0;
-  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty);
+  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
   stage<CONN>(&mI, &mL, tma, I, labels, g, c, sI, sL, &bar);
   __syncthreads();
   if (tile_interior<CONN>(c, g))
@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ labels, 
                                                  const int* __restrict__ levelmap, int NL, Geo g, int ntx, int nty,
                                                  int* __restrict__ levels) {
   using T = TL<CONN>;
-  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty);
+  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
   const int lane = threadIdx.x & 31;
   const int nm = NL - 1;
   const size_t N = (size_t)g.N;
@@ -539,7 +539,8 @@ template <int CONN>
 static ws_status rag_t(const int* labels, const uint8_t* I, const int* dense_of, const Geo& g, uint64_t* edges,
                        unsigned long long* ecount, long long cap, uint64_t* best, cudaStream_t st) {
   using T = TL<CONN>;
-  const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY, ntz = (g.n0 + T::TZ - 1) / T::TZ;
+  const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY,
+            ntz = (g.zhi - g.zlo + T::TZ - 1) / T::TZ;
   Maps mp;
   make_maps<CONN>(I, labels, g, mp);
   const int smem = T::SI + 4 * T::SL + HC * 12;  // I box, L box, hash keys + heights
@@ -718,7 +719,7 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   if (stride == 4 || stride == 8) {
     const bool is3d = (conn == 6 || conn == 26);
     const int TX = is3d ? TL<6>::TX : TL<4>::TX, TY = is3d ? TL<6>::TY : TL<4>::TY, TZ = is3d ? TL<6>::TZ : TL<4>::TZ;
-    const int ntx = (g.n2 + TX - 1) / TX, nty = (g.n1 + TY - 1) / TY, ntz = (g.n0 + TZ - 1) / TZ;
+    const int ntx = (g.n2 + TX - 1) / TX, nty = (g.n1 + TY - 1) / TY, ntz = (g.zhi - g.zlo + TZ - 1) / TZ;
     const int nt = ntx * nty * ntz;
     if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
     else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);

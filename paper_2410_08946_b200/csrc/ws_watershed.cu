@@ -52,7 +52,7 @@ __device__ __forceinline__ bool on_tile_border(int lx, int ly, int lz) {
 // loaded at kernel start; distances only decrease, so a stale value never hides a gain).
 template <int CONN>
 __device__ __forceinline__ bool mark_gains(const int* sD, int s, int d, unsigned m, int lx, int ly, int lz, int t,
-                                           int ntx, int nty, uint8_t* next) {
+                                           int ntx, int nty, uint8_t* next, const Geo& g) {
   using T = TL<CONN>;
   bool any = false;
 #pragma unroll
@@ -64,6 +64,8 @@ __device__ __forceinline__ bool mark_gains(const int* sD, int s, int d, unsigned
     const int oy = (ly + dy < 0) ? -1 : (ly + dy >= T::TY ? 1 : 0);
     const int oz = (lz + dz < 0) ? -1 : (lz + dz >= T::TZ ? 1 : 0);
     if ((ox | oy | oz) == 0) continue;
+    const int tz = t / (ntx * nty) + oz;  // no tile beyond the owned planes (slab halo)
+    if (tz < 0 || tz * T::TZ >= g.zhi - g.zlo) continue;
     if (sD[s + T::oL(i)] > d + 1) {
       next[t + (oz * nty + oy) * ntx + ox] = 1;
       any = true;
@@ -132,7 +134,7 @@ __device__ __forceinline__ bool write_back(const int* sD, int s0, const unsigned
 #pragma unroll
       for (int kk = 0; kk < TL<CONN>::VPT; ++kk)
         if (kk == k) m = eqm[kk];
-      marked |= mark_gains<CONN>(sD, s, d, m, lx, ly, lz, t, ntx, nty, next);
+      marked |= mark_gains<CONN>(sD, s, d, m, lx, ly, lz, t, ntx, nty, next, g);
     }
   }
   return marked;
@@ -230,7 +232,7 @@ __device__ __forceinline__ void relax_first_body(const uint8_t* sI, int* sD, int
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
     unsigned m = 0;
-    const bool inside = !BORDER || (c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0);
+    const bool inside = !BORDER || (c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi);
     if (inside && sD[s0 + k * Mine<CONN>::KS] == INF) {
       const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
       const int si = T::iI(lz, ly, lx);
@@ -249,7 +251,7 @@ __device__ __forceinline__ void relax_first_body(const uint8_t* sI, int* sD, int
     if (plat & (1u << k)) continue;
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0)) continue;
+    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi)) continue;
     L[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = 0;
   }
   const bool marked = write_back<CONN>(sD, s0, eqm, plat, L, g, c, t, ntx, nty, next);
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(NT) k_relax_first(const __grid_constant__ CUte
   __shared__ alignas(16) int sD[T::SL];
   __shared__ uint64_t bar;
   const int t = blockIdx.x;
-  const TileCoord c = tile_coord<CONN>(t, ntx, nty);
+  const TileCoord c = tile_coord<CONN>(t, ntx, nty, g);
   stage<CONN>(&mI, nullptr, tma, I, nullptr, g, c, sI, nullptr, &bar);
   if (tile_interior<CONN>(c, g))
     relax_first_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, hasplat, flags);
@@ -288,7 +290,7 @@ __device__ __forceinline__ void relax_round_body(const uint8_t* sI, int* sD, int
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
     unsigned m = 0;
-    const bool inside = !BORDER || (c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0);
+    const bool inside = !BORDER || (c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi);
     if (inside && sD[s0 + k * Mine<CONN>::KS] > 0) {  // plateau voxel (d >= 1)
       const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
       const int si = T::iI(lz, ly, lx);
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUte
   __shared__ alignas(128) uint8_t sI[T::SI];
   __shared__ alignas(128) int sD[T::SL];
   __shared__ uint64_t bar;
-  const TileCoord c = tile_coord<CONN>(t, ntx, nty);
+  const TileCoord c = tile_coord<CONN>(t, ntx, nty, g);
   stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);
   decode_box<CONN>(sD);
   if (tile_interior<CONN>(c, g))
@@ -336,8 +338,10 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
     const int j = threadIdx.x + k * NT;
-    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0)) {
-      sP[j] = (short)j;
+    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi)) {
+      // not owned (halo plane of a z-slab, or outside the volume): a tile exit, never a root
+      sP[j] = -1;
+      sG[j] = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx) + g.gofs;
       continue;
     }
     const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
@@ -365,6 +369,11 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
       } else {                                // minimal plateau: state 2 -> q, state 3 -> root
         minimal = true;
         dir = dm >= Conn<CONN>::nfwd ? dm : DIR_NONE;
+        if (BORDER && dir != DIR_NONE) {  // never let a minimal plateau pointer leave the owned slab:
+          int dz, dy, dx;                 // the cross-slab part is merged by the boundary union-find
+          nb_delta(CONN, dir, dz, dy, dx);
+          if (c.bz + lz + dz >= g.zhi) dir = DIR_NONE;
+        }
       }
     }
     const int p = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx);
@@ -383,7 +392,7 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
         sP[j] = (short)(j + (dz * T::TY + dy) * T::TX + dx);
       } else {
         sP[j] = -1;
-        sG[j] = p + nb_off<CONN>(g, dir);
+        sG[j] = p + nb_off<CONN>(g, dir) + g.gofs;
       }
     }
   }
@@ -395,7 +404,7 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.n0)) continue;
+    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi)) continue;
     int j = threadIdx.x + k * NT;
     int jn = sP[j];
     while (jn >= 0 && jn != j) {
@@ -407,7 +416,7 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
       out = sG[j];
     } else {
       const int rx = j % T::TX, ry = (j / T::TX) % T::TY, rz = j / (T::TX * T::TY);
-      out = base + rz * g.plane + ry * g.n2 + rx;
+      out = base + rz * g.plane + ry * g.n2 + rx + g.gofs;  // global index
     }
     P[base + lz * g.plane + ly * g.n2 + lx] = out;
   }
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensor
   __shared__ short sP[T::V];  // local target, -1 = leaves the tile
   __shared__ int sG[T::V];    // global target when leaving the tile
   __shared__ uint64_t bar;
-  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty);
+  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
   stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);
   decode_box<CONN>(sD);
   if (tile_interior<CONN>(c, g))
@@ -610,7 +619,7 @@ static TileGrid tiles_of(const Geo& g) {
   TileGrid tg;
   tg.ntx = (g.n2 + T::TX - 1) / T::TX;
   tg.nty = (g.n1 + T::TY - 1) / T::TY;
-  tg.ntz = (g.n0 + T::TZ - 1) / T::TZ;
+  tg.ntz = (g.zhi - g.zlo + T::TZ - 1) / T::TZ;
   tg.n = tg.ntx * tg.nty * tg.ntz;
   return tg;
 }
@@ -722,6 +731,103 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
   WS_CUDA(cudaStreamSynchronize(st));
   ctx->stats.n_regions = ctx->pinned[0];
   if (num_regions) *num_regions = ctx->pinned[0];
+  return WS_OK;
+}
+
+// ------------------------------------------------------------- z-slab sharded phases
+__global__ void k_mark_layer(uint8_t* cur, int layer, int per_layer) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per_layer; i += gridDim.x * blockDim.x)
+    cur[layer * per_layer + i] = 1;
+}
+
+template <int CONN>
+static ws_status shard_first_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, int* pending,
+                               cudaStream_t st) {
+  const TileGrid tg = tiles_of<CONN>(g);
+  Maps mp;
+  make_maps<CONN>(grad, L, g, mp);
+  WS_TRY(ctx->flags.ensure(256, "flags"));
+  WS_TRY(ctx->tiles.ensure((size_t)tg.n * 3, "tile flags"));
+  int* flags = ctx->flags.as<int>();
+  uint8_t* a = ctx->tiles.as<uint8_t>();
+  uint8_t* hasplat = a + 2 * tg.n;
+  WS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+  WS_CUDA(cudaMemsetAsync(a, 0, tg.n, st));
+  k_relax_first<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, a, hasplat, flags);
+  launched(ctx, PH_WS_INIT);
+  ctx->shard_tiles = tg.n;
+  ctx->shard_flip = 0;  // "next" = buffer 0
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaStreamSynchronize(st));
+  const int* h = reinterpret_cast<const int*>(ctx->pinned);
+  if (h[1]) {
+    set_error(WS_ERR_LIMIT, "a non-minimal plateau is deeper than 2^26-2 voxels");
+    return WS_ERR_LIMIT;
+  }
+  *pending = h[0];
+  return WS_OK;
+}
+
+template <int CONN>
+static ws_status shard_round_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, int act_lo, int act_hi,
+                               int* pending, cudaStream_t st) {
+  const TileGrid tg = tiles_of<CONN>(g);
+  if (tg.n != ctx->shard_tiles) {
+    set_error(WS_ERR_INVALID, "ws_shard_plateau: round called without a matching first phase");
+    return WS_ERR_INVALID;
+  }
+  Maps mp;
+  make_maps<CONN>(grad, L, g, mp);
+  int* flags = ctx->flags.as<int>();
+  uint8_t* cur = ctx->tiles.as<uint8_t>() + (size_t)ctx->shard_flip * tg.n;
+  uint8_t* next = ctx->tiles.as<uint8_t>() + (size_t)(1 - ctx->shard_flip) * tg.n;
+  uint8_t* hasplat = ctx->tiles.as<uint8_t>() + 2 * (size_t)tg.n;
+  const int per = tg.ntx * tg.nty;
+  if (act_lo) k_mark_layer<<<(per + 255) / 256, 256, 0, st>>>(cur, 0, per);
+  if (act_hi) k_mark_layer<<<(per + 255) / 256, 256, 0, st>>>(cur, tg.ntz - 1, per);
+  WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
+  WS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+  k_relax_round<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat, flags);
+  launched(ctx, PH_WS_RELAX);
+  ctx->shard_flip = 1 - ctx->shard_flip;
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaStreamSynchronize(st));
+  const int* h = reinterpret_cast<const int*>(ctx->pinned);
+  if (h[1]) {
+    set_error(WS_ERR_LIMIT, "a non-minimal plateau is deeper than 2^26-2 voxels");
+    return WS_ERR_LIMIT;
+  }
+  *pending = h[0];
+  return WS_OK;
+}
+
+ws_status plateau_first_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int* pending,
+                              cudaStream_t st) {
+  if (conn == 6) return shard_first_t<6>(ctx, grad, g, L, pending, st);
+  set_error(WS_ERR_INVALID, "the sharded path supports 6-connectivity only");
+  return WS_ERR_INVALID;
+}
+
+ws_status plateau_round_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int act_lo,
+                              int act_hi, int* pending, cudaStream_t st) {
+  if (conn == 6) return shard_round_t<6>(ctx, grad, g, L, act_lo, act_hi, pending, st);
+  set_error(WS_ERR_INVALID, "the sharded path supports 6-connectivity only");
+  return WS_ERR_INVALID;
+}
+
+ws_status resolve_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, const int32_t* L, int32_t* P,
+                        cudaStream_t st) {
+  if (conn != 6) {
+    set_error(WS_ERR_INVALID, "the sharded path supports 6-connectivity only");
+    return WS_ERR_INVALID;
+  }
+  const TileGrid tg = tiles_of<6>(g);
+  Maps mp;
+  make_maps<6>(grad, L, g, mp);
+  k_resolve<6, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr);
+  launched(ctx, PH_WS_SELECT);
+  tmark(ctx, st, PH_WS_SELECT);
+  WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
 

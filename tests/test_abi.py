@@ -19,7 +19,7 @@ def _lib():
 def test_header_declarations_match_exports():
     with open(os.path.join(ROOT, "include", "ws.h")) as f:
         hdr = f.read()
-    declared = set(re.findall(r"^\s*(?:ws_status|const char\*)\s+(ws_\w+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:ws_status|const char\*|int64_t)\s+(ws_\w+)\s*\(", hdr, re.M))
     _, b = _lib()
     assert declared == set(b.EXPORTS)
 
