@@ -200,6 +200,33 @@ ws_status ws_shard_merge(ws_ctx* ctx, const void* tables_all, int32_t nranks, co
 ws_status ws_shard_relabel(ws_ctx* ctx, const int32_t* P_ext, int32_t* L_ext, const int32_t* exitcanon,
                            ws_dims dims_ext, ws_slab slab, int32_t* labels_own, int64_t* nreps, void* stream);
 
+/* z-slab sharded waterfall (same slabs; labels_own = ws_shard_relabel output).
+ * Dense ids follow the rank order: doff = owned representatives (ws_shard_relabel nreps) of
+ * all lower ranks; R = all ranks' total.  dense_of: i32[D*n1*n2] indexed by GLOBAL label
+ * (device, sparse: only labels met by this rank are written).  rep_of: i32[R] (device); this
+ * rank writes its segment [doff, doff + count), the caller reduces (max) it over ranks with
+ * the other entries at -1.  btable: i32[4*n1*n2]: (label, dense id if owned here else -1) of
+ * the first and last owned plane; ws_shard_wf_bfill gives every rank the dense ids of all
+ * labels crossing a cut.  Per-component minima travel as i64 = K ^ 2^63 (all_reduce MIN). */
+ws_status ws_shard_wf_dense(ws_ctx* ctx, const int32_t* labels_own, ws_dims dims_ext, ws_slab slab, int64_t doff,
+                            int32_t* dense_of, int32_t* rep_of, int64_t* count, void* stream);
+ws_status ws_shard_wf_btable(ws_ctx* ctx, const int32_t* labels_own, const int32_t* dense_of, ws_dims dims_ext,
+                             ws_slab slab, int32_t* btable, void* stream);
+ws_status ws_shard_wf_bfill(ws_ctx* ctx, const int32_t* btables_all, int32_t nranks, ws_dims dims_ext,
+                            int32_t* dense_of, void* stream);
+/* RAG of the owned planes plus the cut pairs with the rank above (labels_ext: owned planes and
+ * the plane above, extended layout); best_out: i64[R] this rank's level-1 minima */
+ws_status ws_shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* grad_ext, ws_dims dims_ext,
+                            int32_t connectivity, ws_slab slab, const int32_t* dense_of, int64_t R, int32_t NL,
+                            int64_t* best_out, void* stream);
+/* one level: best_in = all ranks' minima (reduced); count (HOST) = regions after the level;
+ * more (HOST) = 1 if another level follows, then best_out = this rank's minima for it */
+ws_status ws_shard_wf_step(ws_ctx* ctx, const int64_t* best_in, int64_t* best_out, int64_t* count, int32_t* more,
+                           void* stream);
+/* level maps + the NL level arrays of the owned voxels: levels_own i32[NL][(z1-z0)*n1*n2] */
+ws_status ws_shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const int32_t* dense_of, const int32_t* rep_of,
+                          ws_dims dims_ext, int32_t connectivity, ws_slab slab, int32_t* levels_own, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

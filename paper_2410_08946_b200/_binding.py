@@ -21,7 +21,8 @@ EXPORTS = ("ws_ctx_create", "ws_ctx_destroy", "ws_last_error", "ws_version", "ws
            "ws_ctx_set_timing", "ws_phase_name",
            "ws_gradient", "ws_watershed", "ws_waterfall", "ws_segment_host", "ws_plateau_debug",
            "ws_shard_table_bytes", "ws_shard_plateau", "ws_shard_halo", "ws_shard_local", "ws_shard_merge",
-           "ws_shard_relabel")
+           "ws_shard_relabel", "ws_shard_wf_dense", "ws_shard_wf_btable", "ws_shard_wf_bfill", "ws_shard_wf_begin",
+           "ws_shard_wf_step", "ws_shard_wf_end")
 
 
 class WsDims(ctypes.Structure):
@@ -95,6 +96,12 @@ def load(path: str = SO_PATH):
         lib.ws_shard_local.argtypes = [vp, vp, vp, WsDims, i32, WsSlab, vp, vp, vp]
         lib.ws_shard_merge.argtypes = [vp, vp, i32, vp, vp, WsDims, WsSlab, vp, vp, vp]
         lib.ws_shard_relabel.argtypes = [vp, vp, vp, vp, WsDims, WsSlab, vp, vp, vp]
+        lib.ws_shard_wf_dense.argtypes = [vp, vp, WsDims, WsSlab, i64, vp, vp, vp, vp]
+        lib.ws_shard_wf_btable.argtypes = [vp, vp, vp, WsDims, WsSlab, vp, vp]
+        lib.ws_shard_wf_bfill.argtypes = [vp, vp, i32, WsDims, vp, vp]
+        lib.ws_shard_wf_begin.argtypes = [vp, vp, vp, WsDims, i32, WsSlab, vp, i64, i32, vp, vp]
+        lib.ws_shard_wf_step.argtypes = [vp, vp, vp, vp, pi32, vp]
+        lib.ws_shard_wf_end.argtypes = [vp, vp, vp, vp, WsDims, i32, WsSlab, vp, vp]
         for name in EXPORTS:
             f = getattr(lib, name)
             if name not in ("ws_last_error", "ws_version", "ws_phase_name", "ws_shard_table_bytes"):

@@ -432,4 +432,75 @@ ws_status ws_shard_relabel(ws_ctx* ctx, const int32_t* P_ext, int32_t* L_ext, co
   return shard_relabel(ctx, P_ext, L_ext, exitcanon, g, labels_own, nreps, (cudaStream_t)stream);
 }
 
+ws_status ws_shard_wf_dense(ws_ctx* ctx, const int32_t* labels_own, ws_dims dims, ws_slab slab, int64_t doff,
+                            int32_t* dense_of, int32_t* rep_of, int64_t* count, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, 6, &g));
+  if (!labels_own || !dense_of || !rep_of || !count) return null_arg("labels_own/dense_of/rep_of/count");
+  begin_call(ctx, g);
+  const int n = (g.zhi - g.zlo) * g.plane;
+  return shard_wf_dense(ctx, labels_own, n, (int)(slab.z0 * g.plane), (int)doff, dense_of, rep_of, count,
+                        (cudaStream_t)stream);
+}
+
+ws_status ws_shard_wf_btable(ws_ctx* ctx, const int32_t* labels_own, const int32_t* dense_of, ws_dims dims,
+                             ws_slab slab, int32_t* btable, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, 6, &g));
+  if (!labels_own || !dense_of || !btable) return null_arg("labels_own/dense_of/btable");
+  return shard_wf_btable(ctx, labels_own, g.zhi - g.zlo, g.plane, (int)(slab.z0 * g.plane), dense_of, btable,
+                         (cudaStream_t)stream);
+}
+
+ws_status ws_shard_wf_bfill(ws_ctx* ctx, const int32_t* btables_all, int32_t nranks, ws_dims dims, int32_t* dense_of,
+                            void* stream) {
+  WS_TRY(check_ctx(ctx));
+  if (!btables_all || !dense_of || nranks < 1) return null_arg("btables_all/dense_of");
+  return shard_wf_bfill(ctx, btables_all, nranks, (int)(dims.n1 * dims.n2), dense_of, (cudaStream_t)stream);
+}
+
+ws_status ws_shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* grad_ext, ws_dims dims,
+                            int32_t conn, ws_slab slab, const int32_t* dense_of, int64_t R, int32_t NL,
+                            int64_t* best_out, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, conn, &g));
+  if (!labels_ext || !grad_ext || !dense_of || !best_out) return null_arg("labels_ext/grad_ext/dense_of/best_out");
+  if (NL < 1) {
+    set_error(WS_ERR_INVALID, "NL must be >= 1 (got %d)", NL);
+    return WS_ERR_INVALID;
+  }
+  begin_call(ctx, g);
+  return shard_wf_begin(ctx, labels_ext, grad_ext, g, conn, dense_of, R, NL,
+                        reinterpret_cast<uint64_t*>(best_out), (cudaStream_t)stream);
+}
+
+ws_status ws_shard_wf_step(ws_ctx* ctx, const int64_t* best_in, int64_t* best_out, int64_t* count, int32_t* more,
+                           void* stream) {
+  WS_TRY(check_ctx(ctx));
+  if (!best_in || !best_out || !count || !more) return null_arg("best_in/best_out/count/more");
+  int m = 0;
+  ws_status s = shard_wf_step(ctx, reinterpret_cast<const uint64_t*>(best_in), reinterpret_cast<uint64_t*>(best_out),
+                              count, &m, (cudaStream_t)stream);
+  *more = m;
+  return s;
+}
+
+ws_status ws_shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const int32_t* dense_of, const int32_t* rep_of,
+                          ws_dims dims, int32_t conn, ws_slab slab, int32_t* levels_own, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, conn, &g));
+  if (!labels_own || !dense_of || !rep_of || !levels_own) return null_arg("labels_own/dense_of/rep_of/levels_own");
+  Geo go = g;  // the owned planes as their own volume (labels_own / levels_own layout)
+  go.n0 = g.zhi - g.zlo;
+  go.N = go.n0 * go.plane;
+  go.zlo = 0;
+  go.zhi = go.n0;
+  go.gofs = 0;
+  return shard_wf_end(ctx, labels_own, go, conn, dense_of, rep_of, levels_own, (cudaStream_t)stream);
+}
+
 }  // extern "C"

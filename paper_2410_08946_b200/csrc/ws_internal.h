@@ -43,6 +43,12 @@ struct Buf {
 
 }  // namespace ws
 
+// waterfall level-loop state (ws_waterfall.cu); persists across the sharded phase calls
+struct WSState {
+  int64_t R = 0, E = 0, ne_in = 0, nr_in = 0, prev = 0;
+  int NL = 1, stride = 4, lv = 0, k = 1, eflip = 0, rflip = -1;
+};
+
 struct ws_ctx {
   int device = 0;
   int num_sms = 148;
@@ -60,6 +66,7 @@ struct ws_ctx {
   // z-slab sharding state
   ws::Buf exitmx;         // i32[2*plane] per-exit minima (INT_MAX - p)
   ws::Buf mtables, mslabs, mr0, mmap;  // replicated merge: gathered tables, bounds, R0, root map
+  WSState wf;
   int shard_nroots = 0;
   int shard_tiles = 0;    // tile count of the current sharded plateau phase
   int shard_flip = 0;     // which tile-flag buffer holds "next"
@@ -118,6 +125,18 @@ ws_status shard_merge(ws_ctx* ctx, const void* tables, const int64_t* z0s, const
                       const Geo& g, int32_t* L, int32_t* exitcanon, cudaStream_t st);
 ws_status shard_relabel(ws_ctx* ctx, const int32_t* P, int32_t* L, const int32_t* exitcanon, const Geo& g,
                         int32_t* labels_own, int64_t* nreps, cudaStream_t st);
+
+ws_status shard_wf_dense(ws_ctx* ctx, const int32_t* labels_own, int n, int pofs, int doff, int* dense_of,
+                         int* rep_of_global, int64_t* count, cudaStream_t st);
+ws_status shard_wf_btable(ws_ctx* ctx, const int32_t* labels_own, int nplanes, int plane, int pofs, const int* dense_of,
+                          int32_t* out, cudaStream_t st);
+ws_status shard_wf_bfill(ws_ctx* ctx, const int32_t* tabs, int K, int plane, int* dense_of, cudaStream_t st);
+ws_status shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* I_ext, const Geo& g, int conn,
+                         const int* dense_of, int64_t R, int NL, uint64_t* best_out, cudaStream_t st);
+ws_status shard_wf_step(ws_ctx* ctx, const uint64_t* best_in, uint64_t* best_out, int64_t* count, int* more,
+                        cudaStream_t st);
+ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, int conn, const int* dense_of,
+                       const int* rep_of_global, int32_t* levels_own, cudaStream_t st);
 
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g,
                         int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);

@@ -56,9 +56,12 @@ __device__ __forceinline__ int block_excl_scan(int v, int* smem, int& total) {
 // t owns voxels 16t..16t+15 of each 4096-voxel round, so thread order = voxel order and the
 // dense ids keep the canonical label order, C14), publishes its aggregate, then warp 0 looks
 // back over 32 predecessors at a time until an inclusive prefix is found.
+// pofs: label value of a representative at local index 0 (global index of local voxel 0);
+// doff: dense id of this call's first representative (z-slab sharding; 0 / 0 otherwise).
 __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, int N, int aligned,
                                                 unsigned long long* status, int* ticket, int* __restrict__ dense_of,
-                                                int* __restrict__ rep_of, int rep_cap, long long* R) {
+                                                int* __restrict__ rep_of, int rep_cap, long long* R, int pofs,
+                                                int doff) {
   __shared__ int sm[32];
   __shared__ int sb;
   __shared__ long long sprefix;
@@ -77,14 +80,15 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
     for (int j = 0; j < 4; ++j) {
       const int p = p0 + 4 * j;
       int f0, f1, f2, f3;
+      const int q = p + pofs;
       if (aligned && p + 3 < N) {
         const int4 v = __ldg(reinterpret_cast<const int4*>(labels + p));
-        f0 = v.x == p; f1 = v.y == p + 1; f2 = v.z == p + 2; f3 = v.w == p + 3;
+        f0 = v.x == q; f1 = v.y == q + 1; f2 = v.z == q + 2; f3 = v.w == q + 3;
       } else {
-        f0 = (p < N) && __ldg(labels + p) == p;
-        f1 = (p + 1 < N) && __ldg(labels + p + 1) == p + 1;
-        f2 = (p + 2 < N) && __ldg(labels + p + 2) == p + 2;
-        f3 = (p + 3 < N) && __ldg(labels + p + 3) == p + 3;
+        f0 = (p < N) && __ldg(labels + p) == q;
+        f1 = (p + 1 < N) && __ldg(labels + p + 1) == q + 1;
+        f2 = (p + 2 < N) && __ldg(labels + p + 2) == q + 2;
+        f3 = (p + 3 < N) && __ldg(labels + p + 3) == q + 3;
       }
       const int sh = r * 16 + 4 * j;
       fl |= ((uint64_t)f0 << sh) | ((uint64_t)f1 << (sh + 1)) | ((uint64_t)f2 << (sh + 2)) | ((uint64_t)f3 << (sh + 3));
@@ -133,8 +137,8 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
     while (m) {
       const int u = __ffs(m) - 1;
       m &= m - 1;
-      dense_of[p0 + u] = d;
-      if (d < rep_cap) rep_of[d] = p0 + u;
+      dense_of[p0 + u + pofs] = d + doff;
+      if (d < rep_cap) rep_of[d] = p0 + u + pofs;
       ++d;
     }
   }
@@ -576,41 +580,37 @@ static ws_status read_i64(ws_ctx* ctx, const void* dptr, int64_t* out, cudaStrea
   return WS_OK;
 }
 
-ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn, int NL,
-                        int32_t* levels, int64_t* counts, cudaStream_t st) {
-  const int N = g.N;
-  const int nb = (N + DCHUNK - 1) / DCHUNK;
-  WS_TRY(ctx->flags.ensure(256, "flags"));
-  WS_TRY(ctx->aux.ensure((size_t)N * sizeof(int), "aux"));
+// dense ids of the representatives among n labels starting at global index pofs
+static ws_status wf_dense(ws_ctx* ctx, const int32_t* labels, int n, int pofs, int doff, int* dense_of,
+                          int64_t* count, cudaStream_t st) {
+  const int nb = (n + DCHUNK - 1) / DCHUNK;
   WS_TRY(ctx->blockcnt.ensure((size_t)nb * sizeof(unsigned long long), "scan status"));
-  int* dense_of = ctx->aux.as<int>();
   char* fl = ctx->flags.as<char>();
   long long* dR = reinterpret_cast<long long*>(fl + 128);
-  unsigned long long* ecount = reinterpret_cast<unsigned long long*>(fl + 136);
-  int* nroots = reinterpret_cast<int*>(fl + 144);
   int* ticket = reinterpret_cast<int*>(fl + 148);
-  unsigned long long* nedges = reinterpret_cast<unsigned long long*>(fl + 152);
-
-  // ---- dense ids (single-pass decoupled look-back scan); rep_of sized by the last call
   size_t rep_cap = ctx->rep_of.bytes / sizeof(int);
-  if (rep_cap < (size_t)N / 16 + 1024) {
-    WS_TRY(ctx->rep_of.ensure(((size_t)N / 16 + 1024) * sizeof(int), "rep_of"));
+  if (rep_cap < (size_t)n / 16 + 1024) {
+    WS_TRY(ctx->rep_of.ensure(((size_t)n / 16 + 1024) * sizeof(int), "rep_of"));
     rep_cap = ctx->rep_of.bytes / sizeof(int);
   }
-  int64_t R = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ctx->blockcnt.p, 0, (size_t)nb * sizeof(unsigned long long), st));
     WS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
-    k_dense<<<nb, NTW, 0, st>>>(labels, N, !(reinterpret_cast<uintptr_t>(labels) & 15),
-                                ctx->blockcnt.as<unsigned long long>(), ticket, dense_of,
-                                ctx->rep_of.as<int>(), (int)rep_cap, dR);
+    k_dense<<<nb, NTW, 0, st>>>(labels, n, !(reinterpret_cast<uintptr_t>(labels) & 15),
+                                ctx->blockcnt.as<unsigned long long>(), ticket, dense_of, ctx->rep_of.as<int>(),
+                                (int)rep_cap, dR, pofs, doff);
     launched(ctx, PH_WF_DENSE);
-    WS_TRY(read_i64(ctx, dR, &R, st));
-    if ((size_t)R <= rep_cap) break;
-    WS_TRY(ctx->rep_of.ensure((size_t)R * sizeof(int), "rep_of"));
+    WS_TRY(read_i64(ctx, dR, count, st));
+    if ((size_t)*count <= rep_cap) break;
+    WS_TRY(ctx->rep_of.ensure((size_t)*count * sizeof(int), "rep_of"));
     rep_cap = ctx->rep_of.bytes / sizeof(int);
   }
   tmark(ctx, st, PH_WF_DENSE);
+  return WS_OK;
+}
+
+// level-loop buffers for R regions; best[] = KEY_NONE, comp = iota, lvl = 0xFF
+static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
   if (R > (long long)IDMASK) {
     set_error(WS_ERR_LIMIT, "ws_waterfall: %lld regions exceed the 2^28-1 edge-key limit", (long long)R);
     return WS_ERR_LIMIT;
@@ -625,18 +625,24 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   WS_TRY(ctx->levelmap.ensure((size_t)R * stride * sizeof(int), "levelmap"));
   WS_TRY(ctx->rootsA.ensure((size_t)R * sizeof(int), "level roots A"));
   WS_TRY(ctx->rootsB.ensure((size_t)R * sizeof(int), "level roots B"));
-  int* rep_of = ctx->rep_of.as<int>();
-  int* comp = ctx->comp.as<int>();
-  uint64_t* best = ctx->best.as<uint64_t>();
-  int* levelmap = ctx->levelmap.as<int>();
-  WS_CUDA(cudaMemsetAsync(best, 0xFF, (size_t)R * sizeof(uint64_t), st));
   WS_TRY(ctx->lvl.ensure((size_t)R, "demotion levels"));
-  uint8_t* lvl = ctx->lvl.as<uint8_t>();
-  WS_CUDA(cudaMemsetAsync(lvl, 0xFF, (size_t)R, st));
+  WS_CUDA(cudaMemsetAsync(ctx->best.p, 0xFF, (size_t)R * sizeof(uint64_t), st));
+  WS_CUDA(cudaMemsetAsync(ctx->lvl.p, 0xFF, (size_t)R, st));
+  k_iota<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(ctx->comp.as<int>(), (int)R);
+  launched(ctx, PH_WF_LEVELS);
+  ctx->wf.R = R;
+  ctx->wf.NL = NL;
+  ctx->wf.stride = stride;
+  return WS_OK;
+}
 
-  // ---- RAG edges, tile-deduplicated, folded into the level-1 minima; grow + redo on overflow
+// RAG edges of the owned planes, tile-deduplicated, folded into best[] (level-1 minima)
+static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn,
+                        const int* dense_of, cudaStream_t st) {
+  unsigned long long* ecount = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 136);
+  const long long own = (long long)(g.zhi - g.zlo) * g.plane;
   long long cap = (long long)(ctx->edges.bytes / sizeof(uint64_t));
-  const long long want = (long long)N / 4 + 4096;
+  const long long want = own / 4 + 4096;
   if (cap < want) {
     WS_TRY(ctx->edges.ensure((size_t)want * sizeof(uint64_t), "edges"));
     cap = want;
@@ -644,77 +650,97 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   int64_t E = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ecount, 0, sizeof(unsigned long long), st));
-    WS_TRY(rag(conn, labels, I, dense_of, g, ctx->edges.as<uint64_t>(), ecount, cap, best, st));
+    WS_TRY(rag(conn, labels, I, dense_of, g, ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), st));
     launched(ctx, PH_WF_RAG);
     WS_TRY(read_i64(ctx, ecount, &E, st));
     if (E <= cap) break;
     WS_TRY(ctx->edges.ensure((size_t)E * sizeof(uint64_t), "edges"));
     cap = E;
-    WS_CUDA(cudaMemsetAsync(best, 0xFF, (size_t)R * sizeof(uint64_t), st));
+    WS_CUDA(cudaMemsetAsync(ctx->best.p, 0xFF, (size_t)ctx->wf.R * sizeof(uint64_t), st));
   }
   tmark(ctx, st, PH_WF_RAG);
   ctx->stats.n_edges = E;
-  ctx->stats.n_regions = R;
-
-  // ---- levels
+  ctx->stats.n_regions = ctx->wf.R;
   WS_TRY(ctx->ebufA.ensure((size_t)(E > 0 ? E : 1) * sizeof(Edge), "edge buffer A"));
   WS_TRY(ctx->ebufB.ensure((size_t)(E > 0 ? E : 1) * sizeof(Edge), "edge buffer B"));
-  Edge* ein = nullptr;
-  Edge* eout = ctx->ebufA.as<Edge>();
-  Edge* espare = ctx->ebufB.as<Edge>();
-  int* rin = nullptr;  // level-(k-1) roots (nullptr = all R)
-  int* rout = ctx->rootsA.as<int>();
-  int* rspare = ctx->rootsB.as<int>();
-  long long nr_in = R, ne_in = E;
-  if (counts) counts[0] = R;
-  ctx->stats.level_counts[0] = R;
-  k_iota<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(comp, (int)R);
-  launched(ctx, PH_WF_LEVELS);
-  int lv = 0;
-  long long prev = R;
-  for (int k = 1; k < NL; ++k) {
-    if (k < 16) ctx->stats.level_edges[k] = ne_in;
-    if (prev > 1 && (k == 1 || lv == k - 1)) {
-      if (k >= 2) {  // per-component min-K edges of level k (level 1 came from the RAG)
-        WS_CUDA(cudaMemsetAsync(nedges, 0, sizeof(unsigned long long), st));
-        if (ne_in > 0) {
-          const int esmem = EHC * 16;
-          WS_CUDA(cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
-          k_edges<<<(int)((ne_in + ECH - 1) / ECH), NTW, esmem, st>>>(k == 2 ? ctx->edges.as<uint64_t>() : nullptr,
-                                                                     ein, ne_in, comp, best, eout, nedges);
-        }
-        launched(ctx, PH_WF_LEVELS);
-      }
-      k_hook<<<grid_for(nr_in, ctx->num_sms), 256, 0, st>>>(best, comp, rin, (int)nr_in);
-      WS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(int), st));
-      k_flatten<<<grid_for(nr_in, ctx->num_sms, 8), NTW, 0, st>>>(comp, rin, (int)nr_in, rout, nroots, lvl, k);
-      launched(ctx, PH_WF_LEVELS, 2);
-      WS_CUDA(cudaMemcpyAsync(ctx->pinned, nroots, sizeof(int), cudaMemcpyDeviceToHost, st));
-      if (k >= 2) WS_CUDA(cudaMemcpyAsync(ctx->pinned + 1, nedges, sizeof(long long), cudaMemcpyDeviceToHost, st));
-      WS_CUDA(cudaStreamSynchronize(st));
-      const long long cnt = reinterpret_cast<const int*>(ctx->pinned)[0];
-      if (k >= 2) {
-        ne_in = ctx->pinned[1];
-        ein = eout;
-        std::swap(eout, espare);
-      } else {
-        ne_in = E;  // level 2 reads the key list
-      }
-      rin = rout;
-      std::swap(rout, rspare);
-      nr_in = cnt;
-      if (cnt < prev) lv = k;
-      prev = cnt;
-    }
-    if (counts) counts[k] = prev;
-    if (k < 16) ctx->stats.level_counts[k] = prev;
+  ctx->wf.E = E;
+  ctx->wf.ne_in = E;
+  ctx->wf.nr_in = ctx->wf.R;
+  ctx->wf.prev = ctx->wf.R;
+  ctx->wf.lv = 0;
+  ctx->wf.k = 1;
+  ctx->wf.eflip = 0;
+  ctx->wf.rflip = -1;  // level 1 hooks every region
+  return WS_OK;
+}
+
+// Level k = ctx->wf.k: best[] must hold the per-component min-K edges (all ranks' minima when
+// sharded).  Hook + flatten; the new region count goes to *count.  If another level follows,
+// the live edges are re-labelled, compacted and folded into best[] for level k + 1.
+// Returns *more = 0 when the hierarchy is final (one region, or no merge possible).
+static ws_status wf_step(ws_ctx* ctx, int64_t* count, int* more, cudaStream_t st) {
+  WSState& w = ctx->wf;
+  const int k = w.k;
+  char* fl = ctx->flags.as<char>();
+  int* nroots = reinterpret_cast<int*>(fl + 144);
+  unsigned long long* nedges = reinterpret_cast<unsigned long long*>(fl + 152);
+  int* comp = ctx->comp.as<int>();
+  uint64_t* best = ctx->best.as<uint64_t>();
+  int* rA = ctx->rootsA.as<int>();
+  int* rB = ctx->rootsB.as<int>();
+  int* rin = w.rflip < 0 ? nullptr : (w.rflip == 0 ? rA : rB);
+  int* rout = (w.rflip == 0) ? rB : rA;
+  k_hook<<<grid_for(w.nr_in, ctx->num_sms), 256, 0, st>>>(best, comp, rin, (int)w.nr_in);
+  WS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(int), st));
+  k_flatten<<<grid_for(w.nr_in, ctx->num_sms, 8), NTW, 0, st>>>(comp, rin, (int)w.nr_in, rout, nroots,
+                                                                 ctx->lvl.as<uint8_t>(), k);
+  launched(ctx, PH_WF_LEVELS, 2);
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nroots, sizeof(int), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaStreamSynchronize(st));
+  const long long cnt = reinterpret_cast<const int*>(ctx->pinned)[0];
+  w.rflip = (rout == rA) ? 0 : 1;
+  w.nr_in = cnt;
+  if (cnt < w.prev) w.lv = k;
+  const bool merged = cnt < w.prev;
+  w.prev = cnt;
+  *count = cnt;
+  if (k < 16) ctx->stats.level_counts[k] = cnt;
+  *more = (k + 1 < w.NL && cnt > 1 && merged) ? 1 : 0;
+  w.k = k + 1;
+  if (!*more) return WS_OK;
+  // level k + 1 minima from the live edges (level 2 reads the level-1 key list)
+  Edge* ein = (k == 1) ? nullptr : (w.eflip == 0 ? ctx->ebufB.as<Edge>() : ctx->ebufA.as<Edge>());
+  Edge* eout = (w.eflip == 0) ? ctx->ebufA.as<Edge>() : ctx->ebufB.as<Edge>();
+  if (k + 1 < 16) ctx->stats.level_edges[k + 1] = w.ne_in;
+  WS_CUDA(cudaMemsetAsync(nedges, 0, sizeof(unsigned long long), st));
+  if (w.ne_in > 0) {
+    const int esmem = EHC * 16;
+    WS_CUDA(cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
+    k_edges<<<(int)((w.ne_in + ECH - 1) / ECH), NTW, esmem, st>>>(k == 1 ? ctx->edges.as<uint64_t>() : nullptr, ein,
+                                                                  w.ne_in, comp, best, eout, nedges);
+    launched(ctx, PH_WF_LEVELS);
   }
-  ctx->stats.waterfall_levels = lv;
+  int64_t ne = 0;
+  WS_TRY(read_i64(ctx, nedges, &ne, st));
+  w.ne_in = ne;
+  w.eflip = 1 - w.eflip;  // eout becomes the next input
+  return WS_OK;
+}
+
+// level maps (replicated) + level arrays of the voxels of labels (n0 planes of g)
+static ws_status wf_finish(ws_ctx* ctx, const int32_t* labels, const Geo& g, int conn, const int* dense_of,
+                           int32_t* levels, cudaStream_t st) {
+  WSState& w = ctx->wf;
+  const int NL = w.NL, stride = w.stride;
+  ctx->stats.waterfall_levels = w.lv;
+  int* levelmap = ctx->levelmap.as<int>();
   if (NL > 1) {
-    k_levelmap<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(comp, lvl, rep_of, (int)R, NL, stride, levelmap);
+    k_levelmap<<<grid_for(w.R, ctx->num_sms), 256, 0, st>>>(ctx->comp.as<int>(), ctx->lvl.as<uint8_t>(),
+                                                             ctx->rep_of.as<int>(), (int)w.R, NL, stride, levelmap);
     launched(ctx, PH_WF_LEVELS);
   }
   tmark(ctx, st, PH_WF_LEVELS);
+  const int N = g.N;
   const int gN = grid_for(N, ctx->num_sms);
   if (stride == 4 || stride == 8) {
     const bool is3d = (conn == 6 || conn == 26);
@@ -732,6 +758,119 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   tmark(ctx, st, PH_WF_MATERIALISE);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
+}
+
+ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn, int NL,
+                        int32_t* levels, int64_t* counts, cudaStream_t st) {
+  WS_TRY(ctx->flags.ensure(256, "flags"));
+  WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
+  int* dense_of = ctx->aux.as<int>();
+  int64_t R = 0;
+  WS_TRY(wf_dense(ctx, labels, g.N, 0, 0, dense_of, &R, st));
+  WS_TRY(wf_alloc(ctx, R, NL, st));
+  WS_TRY(wf_rag(ctx, labels, I, g, conn, dense_of, st));
+  if (counts) counts[0] = R;
+  ctx->stats.level_counts[0] = R;
+  ctx->stats.level_edges[1] = ctx->wf.E;
+  int more = NL > 1 && R > 1;
+  long long cnt = R;
+  for (int k = 1; k < NL; ++k) {
+    if (more) {
+      int64_t c = 0;
+      WS_TRY(wf_step(ctx, &c, &more, st));
+      cnt = c;
+    }
+    if (counts) counts[k] = cnt;
+    if (k < 16) ctx->stats.level_counts[k] = cnt;
+  }
+  return wf_finish(ctx, labels, g, conn, dense_of, levels, st);
+}
+
+// ------------------------------------------------------------- z-slab sharded waterfall
+// boundary dense table: for the first/last owned plane, (label, dense id if the label's
+// representative is owned here else -1); every region crossing a cut crosses its owner's
+// boundary plane, so the gathered tables give every rank the dense id of every foreign label
+__global__ void k_wf_btable(const int* __restrict__ labels_own, int nplanes, int plane, int pofs_lo, int pofs_hi,
+                            const int* __restrict__ dense_of, int* out) {
+  for (int i = blockIdx.x * NTW + threadIdx.x; i < 2 * plane; i += gridDim.x * NTW) {
+    const int s = i / plane, xy = i % plane;
+    const int z = s == 0 ? 0 : nplanes - 1;
+    const int l = labels_own[(size_t)z * plane + xy];
+    out[i] = l;
+    out[2 * plane + i] = (l >= pofs_lo && l < pofs_hi) ? dense_of[l] : -1;
+  }
+}
+
+__global__ void k_wf_bfill(const int* __restrict__ tabs, int K, int plane, int* dense_of) {
+  const long long n = (long long)K * 2 * plane;
+  for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n; i += (long long)gridDim.x * NTW) {
+    const long long r = i / (2 * plane), j = i % (2 * plane);
+    const int* t = tabs + r * 4 * plane;
+    const int d = t[2 * plane + j];
+    if (d >= 0) dense_of[t[j]] = d;
+  }
+}
+
+ws_status shard_wf_dense(ws_ctx* ctx, const int32_t* labels_own, int n, int pofs, int doff, int* dense_of,
+                         int* rep_of_global, int64_t* count, cudaStream_t st) {
+  WS_TRY(ctx->flags.ensure(256, "flags"));
+  WS_TRY(wf_dense(ctx, labels_own, n, pofs, doff, dense_of, count, st));
+  if (*count > 0)
+    WS_CUDA(cudaMemcpyAsync(rep_of_global + doff, ctx->rep_of.p, (size_t)*count * sizeof(int),
+                            cudaMemcpyDeviceToDevice, st));
+  return WS_OK;
+}
+
+ws_status shard_wf_btable(ws_ctx* ctx, const int32_t* labels_own, int nplanes, int plane, int pofs, const int* dense_of,
+                          int32_t* out, cudaStream_t st) {
+  k_wf_btable<<<grid_for(2LL * plane, ctx->num_sms), NTW, 0, st>>>(labels_own, nplanes, plane, pofs,
+                                                                   pofs + nplanes * plane, dense_of, out);
+  launched(ctx, PH_WF_DENSE);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+ws_status shard_wf_bfill(ws_ctx* ctx, const int32_t* tabs, int K, int plane, int* dense_of, cudaStream_t st) {
+  k_wf_bfill<<<grid_for((long long)K * 2 * plane, ctx->num_sms), NTW, 0, st>>>(tabs, K, plane, dense_of);
+  launched(ctx, PH_WF_DENSE);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+// keys leave / enter the library sign-flipped (K ^ 2^63): the order of K as int64, so the
+// transport's all_reduce(MIN) on int64 is the per-component minimum
+__global__ void k_flip_copy(uint64_t* dst, const uint64_t* __restrict__ src, long long n) {
+  for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n; i += (long long)gridDim.x * NTW)
+    dst[i] = src[i] ^ (1ull << 63);
+}
+
+ws_status shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* I_ext, const Geo& g, int conn,
+                         const int* dense_of, int64_t R, int NL, uint64_t* best_out, cudaStream_t st) {
+  WS_TRY(ctx->flags.ensure(256, "flags"));
+  WS_TRY(wf_alloc(ctx, R, NL, st));
+  WS_TRY(wf_rag(ctx, labels_ext, I_ext, g, conn, dense_of, st));
+  ctx->stats.level_counts[0] = R;
+  ctx->stats.level_edges[1] = ctx->wf.E;
+  k_flip_copy<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(best_out, ctx->best.as<uint64_t>(), R);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+ws_status shard_wf_step(ws_ctx* ctx, const uint64_t* best_in, uint64_t* best_out, int64_t* count, int* more,
+                        cudaStream_t st) {
+  const long long R = ctx->wf.R;
+  k_flip_copy<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(ctx->best.as<uint64_t>(), best_in, R);
+  WS_TRY(wf_step(ctx, count, more, st));
+  k_flip_copy<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(best_out, ctx->best.as<uint64_t>(), R);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, int conn, const int* dense_of,
+                       const int* rep_of_global, int32_t* levels_own, cudaStream_t st) {
+  WS_TRY(ctx->rep_of.ensure((size_t)ctx->wf.R * sizeof(int), "rep_of"));
+  WS_CUDA(cudaMemcpyAsync(ctx->rep_of.p, rep_of_global, (size_t)ctx->wf.R * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  return wf_finish(ctx, labels_own, gown, conn, dense_of, levels_own, st);
 }
 
 }  // namespace ws

@@ -85,6 +85,14 @@ class LocalTransport:
     def any(self, flags):
         return bool(any(flags))
 
+    def allreduce_min(self, xs):
+        m = torch.stack(xs).amin(0)
+        return [m for _ in xs]
+
+    def allreduce_max(self, xs):
+        m = torch.stack(xs).amax(0)
+        return [m for _ in xs]
+
 
 class DistTransport:
     """One rank per process over torch.distributed (NCCL on GPUs; gloo on CPU)."""
@@ -135,6 +143,14 @@ class DistTransport:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return bool(t.item())
 
+    def allreduce_min(self, xs):
+        self.dist.all_reduce(xs[0], op=self.dist.ReduceOp.MIN, group=self.group)
+        return xs
+
+    def allreduce_max(self, xs):
+        self.dist.all_reduce(xs[0], op=self.dist.ReduceOp.MAX, group=self.group)
+        return xs
+
 
 # ------------------------------------------------------------------------ watershed
 def _dims(slab: Slab, n1: int, n2: int):
@@ -166,8 +182,9 @@ def halo_exchange(tr, ctxs, slabs, Ls, n1, n2):
     return ch_lo, ch_hi
 
 
-def sharded_watershed(tr, ctxs, slabs, grads_ext, conn: int = 6):
-    """grads_ext[i]: u8 (e1-e0, n1, n2) of held slab i.  Returns (labels_own list, R)."""
+def sharded_watershed(tr, ctxs, slabs, grads_ext, conn: int = 6, with_nreps: bool = False):
+    """grads_ext[i]: u8 (e1-e0, n1, n2) of held slab i.  Returns (labels_own list, R, rounds
+    [, owned representative counts])."""
     lib = _b.load()
     n1, n2 = grads_ext[0].shape[1], grads_ext[0].shape[2]
     plane = n1 * n2
@@ -211,4 +228,82 @@ def sharded_watershed(tr, ctxs, slabs, grads_ext, conn: int = 6):
         labels.append(out)
         nreps.append(nr.value)
     R = sum(tr.allgather_i64([nreps[0]])[0]) if isinstance(tr, DistTransport) else sum(nreps)
+    if with_nreps:
+        return labels, R, rounds, nreps
     return labels, R, rounds
+
+
+# ------------------------------------------------------------------------ waterfall
+def sharded_waterfall(tr, ctxs, slabs, grads_ext, labels_own, nreps, NL: int, conn: int = 6):
+    """Graph waterfall (C13) on z-slabs: dense ids by rank order, per-rank RAG (own planes + the
+    cut above), per level all_reduce(MIN) of the per-component minima, replicated hook/flatten.
+    Returns (levels_own list [NL, z1-z0, n1, n2], counts)."""
+    lib = _b.load()
+    K = slabs[0].K
+    n1, n2 = grads_ext[0].shape[1], grads_ext[0].shape[2]
+    plane = n1 * n2
+    N = slabs[0].D * plane
+    dev = grads_ext[0].device
+    cnt_all = tr.allgather_i64([nreps[i] for i in range(len(slabs))])
+    R = int(sum(cnt_all[0]))
+    dense_of = [torch.empty(N, dtype=torch.int32, device=dev) for _ in slabs]
+    rep_of = [torch.full((R,), -1, dtype=torch.int32, device=dev) for _ in slabs]
+    for i, s in enumerate(slabs):
+        doff = int(sum(cnt_all[i][:s.rank]))
+        c = ctypes.c_int64(0)
+        _b.check(lib.ws_shard_wf_dense(ctxs[i].handle, _b.ptr(labels_own[i]), _dims(s, n1, n2), s.c(), doff,
+                                       _b.ptr(dense_of[i]), _b.ptr(rep_of[i]), ctypes.byref(c), _stream()))
+    rep_of = tr.allreduce_max(rep_of)
+    bt = [torch.empty(4 * plane, dtype=torch.int32, device=dev) for _ in slabs]
+    for i, s in enumerate(slabs):
+        _b.check(lib.ws_shard_wf_btable(ctxs[i].handle, _b.ptr(labels_own[i]), _b.ptr(dense_of[i]), _dims(s, n1, n2),
+                                        s.c(), _b.ptr(bt[i]), _stream()))
+    allbt = tr.allgather(bt)
+    for i, s in enumerate(slabs):
+        _b.check(lib.ws_shard_wf_bfill(ctxs[i].handle, _b.ptr(allbt[i]), K, _dims(s, n1, n2), _b.ptr(dense_of[i]),
+                                       _stream()))
+    # labels of the owned planes plus the first plane of the rank above (cut pairs)
+    send_lo = [lo[0].contiguous() if s.rank > 0 else None for lo, s in zip(labels_own, slabs)]
+    send_hi = [lo[-1].contiguous() if s.rank < K - 1 else None for lo, s in zip(labels_own, slabs)]
+    below, above = tr.exchange(send_lo, send_hi)
+    labels_ext = []
+    for i, s in enumerate(slabs):
+        le = torch.zeros((s.e1 - s.e0, n1, n2), dtype=torch.int32, device=dev)
+        le[s.zlo:s.zhi] = labels_own[i]
+        if above[i] is not None:
+            le[s.zhi] = above[i].view(n1, n2)
+        labels_ext.append(le)
+    best = [torch.empty(R, dtype=torch.int64, device=dev) for _ in slabs]
+    for i, s in enumerate(slabs):
+        _b.check(lib.ws_shard_wf_begin(ctxs[i].handle, _b.ptr(labels_ext[i]), _b.ptr(grads_ext[i]), _dims(s, n1, n2),
+                                       conn, s.c(), _b.ptr(dense_of[i]), R, NL, _b.ptr(best[i]), _stream()))
+    best = tr.allreduce_min(best)
+    counts = [R]
+    more = 1 if (NL > 1 and R > 1) else 0
+    cnt = R
+    for k in range(1, NL):
+        if more:
+            nxt = [torch.empty(R, dtype=torch.int64, device=dev) for _ in slabs]
+            for i, s in enumerate(slabs):
+                c, m = ctypes.c_int64(0), ctypes.c_int32(0)
+                _b.check(lib.ws_shard_wf_step(ctxs[i].handle, _b.ptr(best[i]), _b.ptr(nxt[i]), ctypes.byref(c),
+                                              ctypes.byref(m), _stream()))
+                cnt, more = c.value, m.value
+            if more:
+                best = tr.allreduce_min(nxt)
+        counts.append(cnt)
+    levels = []
+    for i, s in enumerate(slabs):
+        out = torch.empty((NL, s.z1 - s.z0, n1, n2), dtype=torch.int32, device=dev)
+        _b.check(lib.ws_shard_wf_end(ctxs[i].handle, _b.ptr(labels_own[i]), _b.ptr(dense_of[i]), _b.ptr(rep_of[i]),
+                                     _dims(s, n1, n2), conn, s.c(), _b.ptr(out), _stream()))
+        levels.append(out)
+    return levels, counts
+
+
+def sharded_segment(tr, ctxs, slabs, grads_ext, NL: int, conn: int = 6):
+    """ws_watershed + ws_waterfall(NL) on z-slabs.  Returns (labels_own, levels_own, counts, R,
+    plateau rounds)."""
+    labels, R, rounds, nreps = sharded_watershed(tr, ctxs, slabs, grads_ext, conn, with_nreps=True)
+    levels, counts = sharded_waterfall(tr, ctxs, slabs, grads_ext, labels, nreps, NL, conn)
+    return labels, levels, counts, R, rounds

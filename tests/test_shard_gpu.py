@@ -62,3 +62,35 @@ def test_sharded_constant_and_corridor():
     import paper_2410_08946_b200 as ws
     raw = synth.make_config_image("C3", shape=(30, 40, 48), device="cuda")
     _check(ws.gradient(raw, 1.0, ndim=3), 3)
+
+
+def _check_segment(grad, K, NL=6):
+    import paper_2410_08946_b200 as ws
+    from paper_2410_08946_b200 import shard
+    ref, Rref = ws.watershed(grad, 6)
+    rlv, rcounts = ws.waterfall(ref, grad, 6, NL)
+    slabs = shard.make_slabs(grad.shape[0], K)
+    ctxs = [ws.Context(0) for _ in range(K)]
+    labels, levels, counts, R, rounds = shard.sharded_segment(
+        shard.LocalTransport(K), ctxs, slabs, [grad[s.e0:s.e1].contiguous() for s in slabs], NL)
+    for c in ctxs:
+        c.close()
+    assert torch.equal(torch.cat(labels, 0), ref) and R == Rref
+    got = torch.cat(levels, 1)
+    for k in range(NL):
+        if not torch.equal(got[k], rlv[k]):
+            pytest.fail("K=%d level %d: %d voxels differ" % (K, k, int((got[k] != rlv[k]).sum())))
+    assert counts == list(rcounts)
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_sharded_waterfall_microct(K):
+    import paper_2410_08946_b200 as ws
+    raw = synth.make_config_image("C4", shape=(36, 64, 96), device="cuda")
+    _check_segment(ws.gradient(raw, 1.0, ndim=3), K)
+
+
+@pytest.mark.parametrize("K,shape,levels,NL", [(2, (10, 24, 40), 4, 6), (5, (5, 16, 32), 3, 4), (3, (12, 20, 28), 6, 9)])
+def test_sharded_waterfall_plateaux(K, shape, levels, NL):
+    g = synth.random_plateau_image(shape, levels, seed=K + levels).cuda()
+    _check_segment(g, K, NL)
