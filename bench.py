@@ -8,8 +8,9 @@ gradient volume, inputs resident in HBM.  Default workload = config C4 (the metr
 
   --impl reference   the oracle (oracle/, plain single-threaded C++) on the host cores, on a
                      bounded sample of the same workload (rank 0 only; other ranks exit 0).
-N > 1 (torchrun): every rank processes its own full-size volume (seed + rank): independent
-problems, no data-path collective ("scaling": "weak").  Timing: CUDA events on the launching
+N > 1 (torchrun), 3-D 6-connected workloads (default C4): ONE volume in z-slabs over the ranks
+("scaling": "strong"): NCCL halo exchange + boundary union-find merge + per-level all_reduce
+(paper_2410_08946_b200/shard.py).  Other workloads: one independent volume per rank ("weak").  Timing: CUDA events on the launching
 stream, barrier + synchronize on both sides, max over ranks.
 """
 from __future__ import annotations
@@ -218,6 +219,119 @@ def run_reference(args):
     return 0
 
 
+def run_sharded(args, world, rank, cfg, shape):
+    """N > 1 on a 3-D 6-connected workload: ONE volume split into z-slabs over the ranks (strong
+    scaling), NCCL halo exchange / boundary-table gathers / all_reduce through
+    torch.distributed, every compute step in libws_b200 (paper_2410_08946_b200/shard.py)."""
+    import torch
+    import synth
+    import paper_2410_08946_b200 as ws
+    from paper_2410_08946_b200 import shard
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    D, H, W = shape
+    N = D * H * W
+    NL, conn = cfg.NL, cfg.conn
+    slabs = shard.make_slabs(D, world)
+    s = slabs[rank]
+    ctx = ws.Context(dev.index)
+    stream = torch.cuda.current_stream(dev)
+    # input (untimed): the same seeded volume on every rank; the slab's gradient from raw planes
+    # [e0-4, e1+4) (blur radius 3 + 1 for the derivative) is exactly the global gradient
+    raw = synth.make_config_image(cfg.name, device=dev, shape=shape)
+    r0, r1 = max(0, s.e0 - 4), min(D, s.e1 + 4)
+    raw_ext = raw[r0:r1].contiguous()
+    del raw
+    torch.cuda.empty_cache()
+    gfull = torch.empty_like(raw_ext)
+    ws.gradient(raw_ext, cfg.sigma, ndim=3, ctx=ctx, out=gfull)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(3):
+        ws.gradient(raw_ext, cfg.sigma, ndim=3, ctx=ctx, out=gfull)
+    b.record(stream)
+    torch.cuda.synchronize()
+    grad_ms = max_over_ranks(a.elapsed_time(b) / 3, world)
+    grad_ext = gfull[s.e0 - r0:s.e1 - r0].contiguous()
+    del gfull, raw_ext
+    torch.cuda.empty_cache()
+    tr = shard.DistTransport()
+
+    def step():
+        return shard.sharded_segment(tr, [ctx], [s], [grad_ext], NL, conn)
+
+    for _ in range(args.warmup):
+        out = step()
+    l0 = ctx.stats()["total_launches"]
+    clocks = Clocks(dev.index)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    launches = ctx.stats()["total_launches"] - l0
+    ms = max_over_ranks(t0.elapsed_time(t1) / args.steps, world)
+    value = N / (ms / 1e3) / 1e6
+    labels, levels, counts, R, rounds = out
+    peak, peak_src = load_peak()
+    own = (s.z1 - s.z0) * H * W
+    step_bytes = 38 if NL == 6 else (5 + 9 + 4 * NL)
+    achieved = step_bytes * own / (ms / 1e3) / 1e9  # per GPU (the slowest rank bounds the step)
+    roofline = {"bound": "hbm", "kernel": "whole sharded step (per GPU slab)", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None, "alg_bytes_per_voxel": step_bytes,
+                "peak_source": peak_src}
+    e2e = None
+    if not args.no_e2e:
+        gh = torch.empty(grad_ext.shape, dtype=torch.uint8, pin_memory=True)
+        gh.copy_(grad_ext)
+        lh = torch.empty((NL, s.z1 - s.z0, H, W), dtype=torch.int32, pin_memory=True)
+        gdev = torch.empty_like(grad_ext)
+
+        def e2e_step():
+            gdev.copy_(gh, non_blocking=True)
+            o = shard.sharded_segment(tr, [ctx], [s], [gdev], NL, conn)
+            lh.copy_(o[1][0], non_blocking=True)
+
+        e2e_step()
+        barrier(world)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        ems = max_over_ranks(a.elapsed_time(b) / args.e2e_steps, world)
+        e2e = {"value": N / (ems / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": grad_ext.numel() * world,
+               "d2h_bytes_per_step": NL * N * 4, "ms_per_step": ems, "api": "shard.sharded_segment (host buffers)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8/i32", "data": "synthetic",
+            "config": {"workload": cfg.desc, "name": cfg.name, "shape": list(shape), "conn": conn, "NL": NL,
+                       "sigma": cfg.sigma, "global_voxels": N, "parallelism": "z-slab x%d (NCCL halo + boundary "
+                       "union-find + per-level all_reduce)" % world,
+                       "l2": "inputs larger than L2 (slab grad %.0f MB, levels %.0f MB per GPU)" % (
+                           grad_ext.numel() / 1e6, 4 * NL * own / 1e6)},
+            "roofline": roofline, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "gradient_prepass": {"ms": grad_ms, "Mvoxel_per_s": N / (grad_ms / 1e3) / 1e6},
+            "input_stats": {"regions": R, "plateau_rounds": rounds, "level_counts": counts},
+            "context": PAPER_CONTEXT,
+        }
+        print(json.dumps(line), flush=True)
+    import torch.distributed as dist
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -226,6 +340,8 @@ def run_ours(args):
 
     world, rank, local = dist_setup(args)
     cfg, shape = workload(args)
+    if world > 1 and cfg.ndim == 3 and cfg.conn == 6:
+        return run_sharded(args, world, rank, cfg, shape)
     dev = torch.device("cuda", torch.cuda.current_device())
     N = int(np.prod(shape))
     NL, conn = cfg.NL, cfg.conn

@@ -78,6 +78,7 @@ typedef struct ws_stats {
   int32_t tma;                /* 1 if the tile kernels staged their boxes with TMA         */
   int32_t reserved0;
   int64_t level_edges[16];    /* live RAG edge records entering each waterfall level       */
+  int64_t total_launches;     /* kernels launched by this context since its creation       */
 } ws_stats;
 
 ws_status ws_ctx_create(int32_t device, ws_ctx** out);

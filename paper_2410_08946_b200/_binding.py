@@ -40,7 +40,8 @@ class WsStats(ctypes.Structure):
                 ("plateau_rounds", ctypes.c_int32), ("waterfall_levels", ctypes.c_int32),
                 ("level_counts", ctypes.c_int64 * 16), ("kernel_launches", ctypes.c_int64),
                 ("phase_ms", ctypes.c_double * 16), ("phase_launches", ctypes.c_int32 * 16),
-                ("tma", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("level_edges", ctypes.c_int64 * 16)]
+                ("tma", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("level_edges", ctypes.c_int64 * 16),
+                ("total_launches", ctypes.c_int64)]
 
     def as_dict(self):
         lib = load()
@@ -52,7 +53,8 @@ class WsStats(ctypes.Structure):
         return {"n_voxels": self.n_voxels, "n_regions": self.n_regions, "n_edges": self.n_edges,
                 "plateau_rounds": self.plateau_rounds, "waterfall_levels": self.waterfall_levels,
                 "level_counts": list(self.level_counts), "kernel_launches": self.kernel_launches,
-                "phases": phases, "tma": self.tma, "level_edges": list(self.level_edges)}
+                "phases": phases, "tma": self.tma, "level_edges": list(self.level_edges),
+                "total_launches": self.total_launches}
 
 
 class WsError(RuntimeError):

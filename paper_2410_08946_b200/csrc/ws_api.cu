@@ -239,6 +239,7 @@ ws_status ws_ctx_set_timing(ws_ctx* ctx, int32_t enable) {
 ws_status ws_get_stats(const ws_ctx* ctx, ws_stats* out) {
   if (!ctx || !out) return null_arg("ctx/out");
   *out = ctx->stats;
+  out->total_launches = ctx->total_launches;
   return WS_OK;
 }
 

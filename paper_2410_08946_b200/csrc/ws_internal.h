@@ -67,6 +67,7 @@ struct ws_ctx {
   ws::Buf exitmx;         // i32[2*plane] per-exit minima (INT_MAX - p)
   ws::Buf mtables, mslabs, mr0, mmap;  // replicated merge: gathered tables, bounds, R0, root map
   WSState wf;
+  int64_t total_launches = 0;
   int shard_nroots = 0;
   int shard_tiles = 0;    // tile count of the current sharded plateau phase
   int shard_flip = 0;     // which tile-flag buffer holds "next"
@@ -100,6 +101,7 @@ void tbegin(ws_ctx* ctx, cudaStream_t st);
 void tmark(ws_ctx* ctx, cudaStream_t st, int phase);
 void tfinish(ws_ctx* ctx);
 inline void launched(ws_ctx* ctx, int phase, int n = 1) {
+  ctx->total_launches += n;
   ctx->stats.kernel_launches += n;
   ctx->stats.phase_launches[phase] += n;
 }
