@@ -3,12 +3,17 @@
 //
 // v1 design: one separable pass per blurred axis (fp32, clamp-to-edge) through fp32 scratch,
 // then one fused gradient + quantise pass.  HBM-bound; see DESIGN.md §Kernels.
+#include <cstdlib>
+#include <cstring>
+
 #include "ws_internal.h"
+#include "ws_tma.cuh"
 
 namespace ws {
 
 constexpr int RMAX = 60;  // sigma <= 20  ->  r = floor(3 sigma + 0.5) <= 60
 __constant__ float c_w[2 * RMAX + 1];
+__constant__ float c_w255[2 * RMAX + 1];  // w / 255: the x pass reads raw u8
 
 template <class Tin>
 __device__ __forceinline__ float load_norm(const Tin* in, size_t i);
@@ -75,9 +80,187 @@ __global__ void k_gradmag(const Tin* __restrict__ b, Geo g, int is3d, uint8_t* _
   }
 }
 
+// ------------------------------------------------------------ fused tile kernel (r <= 4)
+// One CTA = one output tile (3-D 32x8x8, 2-D 64x32).  The raw u8 box (tile + H = r+1 halo,
+// x widened to 16-byte TMA alignment) is staged with ONE cp.async.bulk.tensor (interior
+// tiles) or by clamped loads (border tiles: clamp-to-edge = replicated edge values, C8); the
+// separable blur runs in shared memory (x, then y, then z, fp32 on x/255), then central /
+// one-sided differences, |grad|, quantisation (C9, C10).  HBM traffic: 1 B in + 1 B out per
+// voxel (+ halo re-reads from L2).
+template <bool IS3D> struct GT {
+  static constexpr int TX = IS3D ? 32 : 64, TY = IS3D ? 8 : 32, TZ = IS3D ? 8 : 1;
+  static constexpr int XO = 16, SXB = TX + 32;  // box x: [bx - 16, bx + TX + 16)
+};
+
+template <bool IS3D, int R>
+__global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUtensorMap mImg, int tma,
+                                                    const uint8_t* __restrict__ img, Geo g, int ntx, int nty,
+                                                    uint8_t* __restrict__ q, float* __restrict__ blur_out,
+                                                    float* __restrict__ grad_out) {
+  using T = GT<IS3D>;
+  constexpr int H = R + 1;
+  constexpr int SYB = T::TY + 2 * H, SZB = IS3D ? T::TZ + 2 * H : 1;
+  constexpr int AX = T::TX + 2;                                 // blurred x range [-1, TX]
+  constexpr int BY = T::TY + 2, CZ = IS3D ? T::TZ + 2 : 1;
+  extern __shared__ __align__(128) unsigned char gsm[];
+  uint8_t* sIn = gsm;                                           // [SZB][SYB][SXB] u8
+  float* A = reinterpret_cast<float*>(gsm + ((SZB * SYB * T::SXB + 127) / 128) * 128);  // [SZB][SYB][AX]
+  float* B = A + SZB * SYB * AX;                                // [SZB][BY][AX]
+  float* C = IS3D ? A : B;                                      // [CZ][BY][AX] (reuses A in 3-D)
+  __shared__ uint64_t bar;
+  const int t = blockIdx.x;
+  const int bx = (t % ntx) * T::TX, by = ((t / ntx) % nty) * T::TY, bz = (t / (ntx * nty)) * T::TZ;
+  const bool interior = bx >= T::XO && bx + T::TX + T::XO <= g.n2 && by >= H && by + T::TY + H <= g.n1 &&
+                        (!IS3D || (bz >= H && bz + T::TZ + H <= g.n0));
+  if (tma && interior) {
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bar, SZB * SYB * T::SXB);
+      tma_load_3d(sIn, &mImg, bx - T::XO, by - H, IS3D ? bz - H : bz, &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
+    for (int s = threadIdx.x; s < SZB * SYB * T::SXB; s += 256) {
+      const int sx = s % T::SXB, sy = (s / T::SXB) % SYB, sz = s / (T::SXB * SYB);
+      const int gx = min(max(bx + sx - T::XO, 0), g.n2 - 1);
+      const int gy = min(max(by + sy - H, 0), g.n1 - 1);
+      const int gz = IS3D ? min(max(bz + sz - H, 0), g.n0 - 1) : bz;
+      sIn[s] = __ldg(img + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
+    }
+    __syncthreads();
+  }
+  // x pass: A[z][y][x'] for x' in [-1, TX]; a thread computes 4 consecutive outputs from one
+  // window of 4 + 2R converted inputs (AXP = AX rounded up to 4)
+  constexpr int AXP = (AX + 3) / 4 * 4;
+  for (int job = threadIdx.x; job < SZB * SYB * (AXP / 4); job += 256) {
+    const int grp = job % (AXP / 4), row = job / (AXP / 4);
+    const uint8_t* src = sIn + row * T::SXB + T::XO - 1 + 4 * grp - R;
+    float v[4 + 2 * R];
+#pragma unroll
+    for (int j = 0; j < 4 + 2 * R; ++j) v[j] = (float)src[j];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int x = 4 * grp + o;
+      if (x >= AX) break;
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i <= 2 * R; ++i) acc = fmaf(c_w255[i], v[o + i], acc);  // w / 255 folded in
+      A[row * AX + x] = acc;
+    }
+  }
+  __syncthreads();
+  // y pass: a thread owns one (z, x) column and computes its BY outputs from SYB inputs
+  for (int job = threadIdx.x; job < SZB * AX; job += 256) {
+    const int x = job % AX, z = job / AX;
+    float v[SYB];
+#pragma unroll
+    for (int j = 0; j < SYB; ++j) v[j] = A[(z * SYB + j) * AX + x];
+#pragma unroll
+    for (int y = 0; y < BY; ++y) {
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i <= 2 * R; ++i) acc = fmaf(c_w[i], v[H - 1 + y - R + i], acc);
+      B[(z * BY + y) * AX + x] = acc;
+    }
+  }
+  __syncthreads();
+  if (IS3D) {  // z pass: a thread owns one (y, x) column
+    for (int job = threadIdx.x; job < BY * AX; job += 256) {
+      const int x = job % AX, y = job / AX;
+      float v[SZB];
+#pragma unroll
+      for (int j = 0; j < SZB; ++j) v[j] = B[(j * BY + y) * AX + x];
+#pragma unroll
+      for (int z = 0; z < CZ; ++z) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i <= 2 * R; ++i) acc = fmaf(c_w[i], v[H - 1 + z - R + i], acc);
+        C[(z * BY + y) * AX + x] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  // gradient + quantisation of the tile voxels
+  for (int s = threadIdx.x; s < T::TX * T::TY * T::TZ; s += 256) {
+    const int lx = s % T::TX, ly = (s / T::TX) % T::TY, lz = s / (T::TX * T::TY);
+    const int gx = bx + lx, gy = by + ly, gz = bz + lz;
+    if (gx >= g.n2 || gy >= g.n1 || gz >= g.n0) continue;
+    const int c = ((IS3D ? lz + 1 : 0) * BY + ly + 1) * AX + lx + 1;
+    const float v = C[c];
+    float ss = 0.f;
+    {  // x
+      float d = 0.f;
+      if (g.n2 >= 2) d = gx == 0 ? C[c + 1] - v : (gx == g.n2 - 1 ? v - C[c - 1] : 0.5f * (C[c + 1] - C[c - 1]));
+      ss = fmaf(d, d, ss);
+    }
+    {  // y
+      float d = 0.f;
+      if (g.n1 >= 2) d = gy == 0 ? C[c + AX] - v : (gy == g.n1 - 1 ? v - C[c - AX] : 0.5f * (C[c + AX] - C[c - AX]));
+      ss = fmaf(d, d, ss);
+    }
+    if (IS3D) {  // z
+      const int zs = BY * AX;
+      float d = 0.f;
+      if (g.n0 >= 2) d = gz == 0 ? C[c + zs] - v : (gz == g.n0 - 1 ? v - C[c - zs] : 0.5f * (C[c + zs] - C[c - zs]));
+      ss = fmaf(d, d, ss);
+    }
+    const float gm = sqrtf(ss);
+    const float qq = floorf(fmaf(255.0f, gm, 0.5f));
+    const size_t p = (size_t)gz * g.plane + (size_t)gy * g.n2 + gx;
+    q[p] = (uint8_t)(qq > 255.f ? 255.f : qq);
+    if (blur_out) blur_out[p] = v;
+    if (grad_out) grad_out[p] = gm;
+  }
+}
+
+template <bool IS3D, int R>
+static ws_status grad_fused_t(ws_ctx* ctx, const uint8_t* img, const Geo& g, uint8_t* q, float* blur, float* grad,
+                              cudaStream_t st) {
+  using T = GT<IS3D>;
+  constexpr int H = R + 1;
+  constexpr int SYB = T::TY + 2 * H, SZB = IS3D ? T::TZ + 2 * H : 1;
+  constexpr int AX = T::TX + 2, BY = T::TY + 2;
+  const int smem = ((SZB * SYB * T::SXB + 127) / 128) * 128 + 4 * (SZB * SYB * AX + SZB * BY * AX);
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  const char* env = getenv("WS_NO_TMA");
+  const int tma = !(env && env[0] == '1') && encode_tmap_3d(&m, 1, img, g, T::SXB, SYB, SZB);
+  const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY, ntz = (g.n0 + T::TZ - 1) / T::TZ;
+  WS_CUDA(cudaFuncSetAttribute(k_grad_fused<IS3D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_grad_fused<IS3D, R><<<ntx * nty * ntz, 256, smem, st>>>(m, tma, img, g, ntx, nty, q, blur, grad);
+  launched(ctx, PH_GRAD_MAG);
+  tmark(ctx, st, PH_GRAD_MAG);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
 ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, float sigma,
                        uint8_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st) {
   L3 l = launch3(g);
+  const int rr = sigma > 0.f ? (int)floor(3.0 * (double)sigma + 0.5) : 0;
+  if (rr >= 1 && rr <= 4) {  // fused tile kernel
+    float w[2 * RMAX + 1];
+    double wsum = 0, wd[2 * RMAX + 1];
+    for (int i = -rr; i <= rr; ++i) { wd[i + rr] = exp(-(double)i * i / (2.0 * sigma * (double)sigma)); wsum += wd[i + rr]; }
+    float w255[2 * RMAX + 1];
+    for (int i = 0; i <= 2 * rr; ++i) {
+      w[i] = (float)(wd[i] / wsum);
+      w255[i] = (float)(wd[i] / wsum / 255.0);
+    }
+    WS_CUDA(cudaMemcpyToSymbolAsync(c_w, w, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
+    WS_CUDA(cudaMemcpyToSymbolAsync(c_w255, w255, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
+    switch (rr + (is3d ? 10 : 0)) {
+      case 1: return grad_fused_t<false, 1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 2: return grad_fused_t<false, 2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 3: return grad_fused_t<false, 3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 4: return grad_fused_t<false, 4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 11: return grad_fused_t<true, 1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 12: return grad_fused_t<true, 2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 13: return grad_fused_t<true, 3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      default: return grad_fused_t<true, 4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+    }
+  }
   if (sigma == 0.f) {
     k_gradmag<uint8_t><<<l.grid, l.block, 0, st>>>(img, g, is3d, grad_q, blur_f32, grad_f32);
     launched(ctx, PH_GRAD_MAG);

@@ -203,3 +203,14 @@ def test_waterfall_nl_variants(NL, shape):
     q = g.cuda()
     lab, ref = check_watershed(q, qn, 8, 2)
     check_waterfall(lab, q, qn, ref, 8, 2, NL)
+
+
+@pytest.mark.parametrize("sigma", [0.0, 0.4, 0.7, 1.0, 1.3, 2.0])
+@pytest.mark.parametrize("shape,ndim", [((20, 40, 96), 3), ((3, 70, 130), 2), ((9, 30, 17), 3)])
+def test_gradient_sigmas_and_loaders(sigma, shape, ndim, monkeypatch):
+    """Fused tile kernel (radius 1..4, TMA or clamped loads) and the separable fallback
+    (radius > 4, sigma = 0) against the oracle under C11."""
+    raw = synth.random_plateau_image(shape, 256, seed=int(sigma * 10) + ndim).numpy()
+    agreed_gradient(raw, sigma, ndim)
+    monkeypatch.setenv("WS_NO_TMA", "1")
+    agreed_gradient(raw, sigma, ndim)
