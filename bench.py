@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-paper-protocol", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=32)
     ap.add_argument("--ref-sample-slices", type=int, default=4)
     return ap.parse_args()
@@ -364,6 +365,28 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize()
     grad_ms = e0.elapsed_time(e1) / GK
+
+    # the paper's own protocol for context ("all images are raw", Table 3): the
+    # watershed alone on the RAW volume, 6- and 26-connectivity (3-D configs only)
+    paper_protocol = None
+    if cfg.ndim == 3 and not args.no_paper_protocol:
+        lab_raw = torch.empty(shape, dtype=torch.int32, device=dev)
+        paper_protocol = {"workload": "raw u8 volume of the same config, watershed only (ws_watershed)",
+                          "paper": {"volume": "4000x4000x50 raw microCT (800 Mvox)", "gpu": "RTX 3060 Ti",
+                                    "ms": {"6": 1357.75, "26": 2258.02}, "Mvoxel_per_s": {"6": 589.2, "26": 354.3},
+                                    "cite": "P:819, P:823 (Table 3, PRUF)"}}
+        for c3 in (6, 26):
+            for _ in range(2):
+                _, Rraw = ws.watershed(raw, c3, ndim=3, ctx=ctx, out=lab_raw)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(3):
+                _, Rraw = ws.watershed(raw, c3, ndim=3, ctx=ctx, out=lab_raw)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            pms = e0.elapsed_time(e1) / 3
+            paper_protocol[str(c3)] = {"ms": pms, "Mvoxel_per_s": N / (pms / 1e3) / 1e6, "regions": Rraw}
+        del lab_raw
     del raw
     torch.cuda.empty_cache()
 
@@ -462,6 +485,7 @@ def run_ours(args):
             "roofline": roofline, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
             "gradient_prepass": {"ms": grad_ms, "Mvoxel_per_s": N / (grad_ms / 1e3) / 1e6},
+            "paper_protocol_watershed_raw": paper_protocol,
             "phases_ms_per_step": {k: v / args.steps for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
             "input_stats": {"regions": s1["n_regions"], "edges": s2["n_edges"],
                             "plateau_rounds": s1["plateau_rounds"], "level_counts": s2["level_counts"][:NL],

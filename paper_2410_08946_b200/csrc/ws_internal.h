@@ -57,6 +57,7 @@ struct ws_ctx {
   ws::Buf flags;      // small device counters / flags
   ws::Buf tiles;      // u8[3 * ntiles] step II active-tile flags
   ws::Buf roots;      // i32[cap]  step III roots (self-loops), compact list
+  ws::Buf upairs;     // int2[cap] step IV pairs crossing a tile face (k_resolve -> k_union_pairs)
   ws::Buf rootc;      // i32[cap]  canonical label per listed root
   ws::Buf blockcnt;   // per-block look-back status words of the dense-id scan
   ws::Buf edges;      // u64[cap] RAG edge keys (level 1)

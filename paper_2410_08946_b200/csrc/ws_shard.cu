@@ -141,7 +141,21 @@ __device__ __forceinline__ int sfind_ro(const int* P, const Geo& g, int x) {
   }
 }
 
-// step IV inside the slab: pairs of owned voxels (q > p) on one minimal plateau.  A voxel
+// step IV inside the slab on the cross-tile pairs k_resolve listed (global indices)
+__global__ void k_union_pairs_shard(int* P, const int2* __restrict__ pairs, int n, Geo g) {
+  for (int i = blockIdx.x * NTS + threadIdx.x; i < n; i += gridDim.x * NTS) {
+    int a = pairs[i].x, b = pairs[i].y;
+    while (true) {
+      a = sfind(P, g, a);
+      b = sfind(P, g, b);
+      if (a == b) break;
+      if (a > b) { const int t = a; a = b; b = t; }
+      if (atomicCAS(P + b - g.gofs, b, a) == b) break;
+    }
+  }
+}
+
+// step IV inside the slab (fallback when the pair list overflowed): pairs of owned voxels (q > p) on one minimal plateau.  A voxel
 // whose terminal is an exit descends out of the slab and is never on a minimal plateau
 // (minimal-plateau pointers are kept inside the slab by k_resolve).
 template <int CONN>
@@ -410,23 +424,27 @@ ws_status shard_local(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, 
   const int gN = grid_s((long long)own, ctx->num_sms);
   k_jump_shard<<<gN, NTS, 0, st>>>(P, L, g, ctx->exitmx.as<int>(), ctx->roots.as<int>(), (int)cap, nr);
   launched(ctx, PH_WS_JUMP);
-  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));  // nr, -, npairs
   WS_CUDA(cudaStreamSynchronize(st));
   int n_roots = reinterpret_cast<const int*>(ctx->pinned)[0];
+  const int n_pairs = reinterpret_cast<const int*>(ctx->pinned)[2];
+  const int pcap = (int)(ctx->upairs.bytes / sizeof(int2));
   if ((size_t)n_roots > cap) {
     set_error(WS_ERR_LIMIT, "ws_shard_local: more than %zu step III roots in one slab", cap);
     return WS_ERR_LIMIT;
   }
   tmark(ctx, st, PH_WS_JUMP);
-  L3 l = launch3(g);
-  l.grid.z = (g.zhi - g.zlo) < 65535 ? (g.zhi - g.zlo) : 65535;
-  switch (conn) {
-    case 6: k_union_shard<6><<<l.grid, l.block, 0, st>>>(grad, P, g); break;
-    default:
-      set_error(WS_ERR_INVALID, "the sharded path supports 6-connectivity only");
-      return WS_ERR_INVALID;
+  if (n_pairs <= pcap) {
+    if (n_pairs > 0) {
+      k_union_pairs_shard<<<grid_s(n_pairs, ctx->num_sms), NTS, 0, st>>>(P, ctx->upairs.as<int2>(), n_pairs, g);
+      launched(ctx, PH_WS_UNION);
+    }
+  } else {
+    L3 l = launch3(g);
+    l.grid.z = (g.zhi - g.zlo) < 65535 ? (g.zhi - g.zlo) : 65535;
+    k_union_shard<6><<<l.grid, l.block, 0, st>>>(grad, P, g);  // resolve_shard checked conn == 6
+    launched(ctx, PH_WS_UNION);
   }
-  launched(ctx, PH_WS_UNION);
   tmark(ctx, st, PH_WS_UNION);
   const int gR = grid_s(n_roots, ctx->num_sms);
   k_root_fold<<<gR, NTS, 0, st>>>(P, L, ctx->roots.as<int>(), n_roots, g);

@@ -329,10 +329,47 @@ __global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUte
 
 // ---------------------- pointers (steps I-II) + tile-local pointer jumping (step III)
 // DEBUG: write the un-jumped parent and the distance instead (ws_plateau_debug, T2).
+//
+// Minimal plateaus (step IV, Alg. 1 l.24-27) are merged inside the tile here: the tile's
+// minimal voxels form a shared-memory union-find (min-root, in sG, unused by them otherwise)
+// over their in-tile q > p equal pairs, and every minimal voxel points at its in-tile root.
+// The q > p pairs that cross the tile face go to a global list for k_union_pairs (about
+// 0.1% of the voxels on the paper-like inputs), so step IV never rescans the volume.
+constexpr int QCAP = 128;  // per-tile staging of the cross-tile pairs
+
+struct PairOut {
+  int2* pairs;   // cross-tile union pairs (global indices)
+  int* npairs;   // counter (may exceed cap: the host then runs the full k_union scan)
+  int cap;
+};
+
+__device__ __forceinline__ int s_find(volatile int* U, int x) {
+  while (true) {
+    const int y = U[x];
+    if (y == x) return x;
+    const int z = U[y];
+    if (z == y) return y;
+    U[x] = z;  // path halving (z is an ancestor of x: benign race)
+    x = z;
+  }
+}
+
+__device__ __forceinline__ void s_unite(int* U, int a, int b) {
+  while (true) {
+    a = s_find(U, a);
+    b = s_find(U, b);
+    if (a == b) return;
+    if (a > b) { const int t = a; a = b; b = t; }
+    if (atomicCAS(U + b, b, a) == b) return;
+  }
+}
+
 template <int CONN, bool DEBUG, bool BORDER>
-__device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, short* sP, int* sG, const Geo& g,
-                                             const TileCoord& c, int* __restrict__ P, int* __restrict__ dist) {
+__device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, short* sP, int* sG, int2* sQ,
+                                             int* sQn, int* sQb, const Geo& g, const TileCoord& c,
+                                             int* __restrict__ P, int* __restrict__ dist, const PairOut& po) {
   using T = TL<CONN>;
+  uint32_t minmask = 0;  // bit k: voxel k of this thread is on a minimal plateau (or a strict minimum)
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
@@ -366,14 +403,8 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
 #pragma unroll
         for (int i = 0; i < CONN; ++i)
           if ((eqm & (1u << i)) && sD[sl + T::oL(i)] == dd - 1) dir = i;
-      } else {                                // minimal plateau: state 2 -> q, state 3 -> root
+      } else {                                // minimal plateau: merged below
         minimal = true;
-        dir = dm >= Conn<CONN>::nfwd ? dm : DIR_NONE;
-        if (BORDER && dir != DIR_NONE) {  // never let a minimal plateau pointer leave the owned slab:
-          int dz, dy, dx;                 // the cross-slab part is merged by the boundary union-find
-          nb_delta(CONN, dir, dz, dy, dx);
-          if (c.bz + lz + dz >= g.zhi) dir = DIR_NONE;
-        }
       }
     }
     const int p = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx);
@@ -382,8 +413,10 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
       P[p] = (dir == DIR_NONE || minimal) ? p : p + nb_off<CONN>(g, dir);  // oracle: minima are terminals
       continue;
     }
-    if (dir == DIR_NONE) {
+    if (minimal) {
+      minmask |= 1u << k;
       sP[j] = (short)j;
+      sG[j] = j;  // union-find parent (local index)
     } else {
       int dz, dy, dx;
       nb_delta(CONN, dir, dz, dy, dx);
@@ -397,7 +430,55 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     }
   }
   if (DEBUG) return;
-  __syncthreads();
+  // step IV inside the tile + the cross-tile pairs (q > p: the forward half).  Only
+  // the (few) minimal voxels loop; cross-tile pairs are staged in shared memory (sQ) and
+  // flushed with one global atomic per tile.
+  const bool anymin = __syncthreads_or(minmask != 0);
+  if (anymin) {
+    for (uint32_t mm = minmask; mm; mm &= mm - 1) {
+      const int k = __ffs(mm) - 1;
+      const int j = threadIdx.x + k * NT;
+      const int lx = j % T::TX, ly = (j / T::TX) % T::TY, lz = j / (T::TX * T::TY);
+      const int si = T::iI(lz, ly, lx);
+      const int v = sI[si];
+      const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
+#pragma unroll
+      for (int i = Conn<CONN>::nfwd; i < CONN; ++i) {
+        if (sI[si + T::oI(i)] != v) continue;
+        int dz, dy, dx;
+        nb_delta(CONN, i, dz, dy, dx);
+        const int nx = lx + dx, ny = ly + dy, nz = lz + dz;
+        if (BORDER && (!(vm & (1u << i)) || c.bz + nz >= g.zhi)) continue;  // cut plane: ws_shard_merge
+        if ((unsigned)nx < (unsigned)T::TX && (unsigned)ny < (unsigned)T::TY && (unsigned)nz < (unsigned)T::TZ) {
+          s_unite(sG, j, j + (dz * T::TY + dy) * T::TX + dx);
+        } else {
+          const int p = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx) + g.gofs;
+          const int2 e = make_int2(p, p + nb_off<CONN>(g, i));
+          const int s = atomicAdd(sQn, 1);
+          if (s < QCAP) {
+            sQ[s] = e;
+          } else {
+            const int gi = atomicAdd(po.npairs, 1);
+            if (gi < po.cap) po.pairs[gi] = e;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int nq = *sQn < QCAP ? *sQn : QCAP;
+    if (threadIdx.x == 0 && nq > 0) *sQb = atomicAdd(po.npairs, nq);
+#pragma unroll
+    for (int k = 0; k < T::VPT; ++k)
+      if ((minmask >> k) & 1) {
+        const int j = threadIdx.x + k * NT;
+        sP[j] = (short)s_find(sG, j);
+      }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nq; i += NT)
+      if (*sQb + i < po.cap) po.pairs[*sQb + i] = sQ[i];
+  } else {
+    __syncthreads();
+  }
   // tile-local path reduction: follow in-tile pointers to a root or to the tile exit
   const int base = (int)((size_t)c.bz * g.plane + (size_t)c.by * g.n2 + c.bx);
 #pragma unroll
@@ -426,20 +507,24 @@ template <int CONN, bool DEBUG>
 __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensorMap mI,
                                                 const __grid_constant__ CUtensorMap mL, int tma,
                                                 const uint8_t* __restrict__ I, const int* __restrict__ L, Geo g,
-                                                int ntx, int nty, int* __restrict__ P, int* __restrict__ dist) {
+                                                int ntx, int nty, int* __restrict__ P, int* __restrict__ dist,
+                                                PairOut po) {
   using T = TL<CONN>;
   __shared__ alignas(128) uint8_t sI[T::SI];
   __shared__ alignas(128) int sD[T::SL];
   __shared__ short sP[T::V];  // local target, -1 = leaves the tile
-  __shared__ int sG[T::V];    // global target when leaving the tile
+  __shared__ int sG[T::V];    // global target when leaving the tile / union-find of minimal voxels
+  __shared__ int2 sQ[QCAP];   // cross-tile step IV pairs
+  __shared__ int sQn, sQb;
   __shared__ uint64_t bar;
   const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
+  if (threadIdx.x == 0) sQn = 0;
   stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);
   decode_box<CONN>(sD);
   if (tile_interior<CONN>(c, g))
-    resolve_body<CONN, DEBUG, false>(sI, sD, sP, sG, g, c, P, dist);
+    resolve_body<CONN, DEBUG, false>(sI, sD, sP, sG, sQ, &sQn, &sQb, g, c, P, dist, po);
   else
-    resolve_body<CONN, DEBUG, true>(sI, sD, sP, sG, g, c, P, dist);
+    resolve_body<CONN, DEBUG, true>(sI, sD, sP, sG, sQ, &sQn, &sQb, g, c, P, dist, po);
 }
 
 // --------------------------- step III across tiles + per-root minimum + root list
@@ -575,6 +660,14 @@ __global__ void k_union(const uint8_t* __restrict__ I, int* P, Geo g) {
   ZLOOP_END
 }
 
+// step IV Union on the cross-tile pairs k_resolve listed (the in-tile ones are merged there)
+__global__ void k_union_pairs(int* P, const int2* __restrict__ pairs, int n) {
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+    const int2 e = pairs[i];
+    if (ld_cg(P + e.x) != ld_cg(P + e.y)) uf_unite(P, e.x, e.y);
+  }
+}
+
 // ------------- step IV Find (l.28-29) on the roots only; canonical labels (C7) per region
 // merge: every root folds its minimum into its final root's (atomicMax on INT_MAX - min)
 __global__ void k_root_merge(int* P, int* L, const int* __restrict__ roots, int n, unsigned long long* nfinal) {
@@ -672,6 +765,19 @@ static ws_status plateau_phase(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
   return WS_OK;
 }
 
+// cross-tile step IV pair list of k_resolve: ctx->upairs, counter at flags int 10
+static ws_status pair_out(ws_ctx* ctx, const Geo& g, PairOut& po, cudaStream_t st) {
+  const size_t own = (size_t)(g.zhi - g.zlo) * g.plane;
+  const size_t want = own / 64 + 65536;
+  if (ctx->upairs.bytes / sizeof(int2) < want) WS_TRY(ctx->upairs.ensure(want * sizeof(int2), "union pairs"));
+  WS_TRY(ctx->flags.ensure(256, "flags"));
+  po.pairs = ctx->upairs.as<int2>();
+  po.npairs = ctx->flags.as<int>() + 10;
+  po.cap = (int)(ctx->upairs.bytes / sizeof(int2));
+  WS_CUDA(cudaMemsetAsync(po.npairs, 0, sizeof(int), st));
+  return WS_OK;
+}
+
 template <int CONN>
 static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, int64_t* num_regions,
                              cudaStream_t st) {
@@ -682,7 +788,9 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
   WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, mp, st));
   WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
   int* P = ctx->aux.as<int>();
-  k_resolve<CONN, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr);
+  PairOut po;
+  WS_TRY(pair_out(ctx, g, po, st));
+  k_resolve<CONN, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr, po);
   launched(ctx, PH_WS_SELECT);
   tmark(ctx, st, PH_WS_SELECT);
 
@@ -701,9 +809,10 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
   const int gN = grid1d(g.N, ctx->num_sms);
   k_jump<<<gN, NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
   launched(ctx, PH_WS_JUMP);
-  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));  // nr, -, npairs
   WS_CUDA(cudaStreamSynchronize(st));
   const int n_roots = (int)reinterpret_cast<const int*>(ctx->pinned)[0];
+  const int n_pairs = (int)reinterpret_cast<const int*>(ctx->pinned)[2];
   if ((size_t)n_roots > cap) {  // list overflow: grow and rebuild it from P
     WS_TRY(ctx->roots.ensure((size_t)n_roots * sizeof(int), "roots"));
     WS_TRY(ctx->rootc.ensure((size_t)n_roots * sizeof(int), "root labels"));
@@ -712,9 +821,16 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
     launched(ctx, PH_WS_JUMP);
   }
   tmark(ctx, st, PH_WS_JUMP);
-  const L3 l = launch3(g);
-  k_union<CONN><<<l.grid, l.block, 0, st>>>(grad, P, g);
-  launched(ctx, PH_WS_UNION);
+  if (n_pairs <= po.cap) {
+    if (n_pairs > 0) {
+      k_union_pairs<<<grid1d(n_pairs, ctx->num_sms), NT, 0, st>>>(P, po.pairs, n_pairs);
+      launched(ctx, PH_WS_UNION);
+    }
+  } else {  // pair list overflow (near-flat inputs): the full q > p scan
+    const L3 l = launch3(g);
+    k_union<CONN><<<l.grid, l.block, 0, st>>>(grad, P, g);
+    launched(ctx, PH_WS_UNION);
+  }
   tmark(ctx, st, PH_WS_UNION);
   const int gR = grid1d(n_roots, ctx->num_sms);
   const int* roots = ctx->roots.as<int>();
@@ -824,7 +940,9 @@ ws_status resolve_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn
   const TileGrid tg = tiles_of<6>(g);
   Maps mp;
   make_maps<6>(grad, L, g, mp);
-  k_resolve<6, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr);
+  PairOut po;
+  WS_TRY(pair_out(ctx, g, po, st));
+  k_resolve<6, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr, po);
   launched(ctx, PH_WS_SELECT);
   tmark(ctx, st, PH_WS_SELECT);
   WS_CUDA(cudaGetLastError());
@@ -852,7 +970,8 @@ static ws_status debug_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t
   Maps mp;
   make_maps<CONN>(grad, L, g, mp);
   WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, mp, st));
-  k_resolve<CONN, true><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, parent, dist);
+  k_resolve<CONN, true><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, parent, dist,
+                                             PairOut{nullptr, nullptr, 0});
   launched(ctx, PH_WS_SELECT);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
