@@ -46,6 +46,7 @@ struct Buf {
 // waterfall level-loop state (ws_waterfall.cu); persists across the sharded phase calls
 struct WSState {
   int64_t R = 0, E = 0, ne_in = 0, nr_in = 0, prev = 0;
+  long long dofs = 0;  // offset of the owned planes in ctx->dimg
   int NL = 1, stride = 4, lv = 0, k = 1, eflip = 0, rflip = -1;
 };
 
@@ -75,7 +76,8 @@ struct ws_ctx {
   ws::Buf comp;       // i32[R]   component parent (union-find over dense ids)
   ws::Buf best;       // u64[R]   per-component min-K edge
   ws::Buf rep_of;     // i32[R]   dense id -> canonical voxel label
-  ws::Buf levelmap;   // i32[R*(NL-1)]
+  ws::Buf levelmap;   // i32[R*stride]  canonical label of each dense id at levels 0..NL-1
+  ws::Buf dimg;       // i32[N]   dense id of every voxel's label (waterfall)
   ws::Buf lvcount;    // i64[NL]  device-side region counts
   ws::Buf h_grad, h_labels, h_levels;  // device copies used by ws_segment_host
   int64_t* pinned = nullptr;           // small pinned host scratch (flags / counts)

@@ -144,148 +144,282 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
   }
 }
 
-// ------------------------------------------------------------------------ RAG extraction
-// Tiles and TMA staging as in the watershed (ws_tile.cuh): the label box (i32) and the
-// intensity box (u8) of a 2048-voxel tile land in shared memory with one bulk-tensor copy
-// each.  A boundary pair is keyed by its LABEL pair (62 bits) with the pass height kept
-// separately (atomicMin on a 32-bit slot = per-pair minimum, Alg. 4 l.2-7).  Each thread walks
-// a column of 8 voxels and run-length-merges equal pairs per direction in registers, so only
-// run ends touch the shared hash; dense ids are looked up once per unique tile edge at the
-// flush, where the edge key K = [w:8][~max:28][~min:28] (C14) is formed.
-constexpr int HC = 2048;                      // shared hash slots per tile (load <= ~25%)
-constexpr uint64_t PKEY_NONE = ~0ull;
-
-__device__ __forceinline__ uint64_t pair_key(int a, int b) {
-  const uint32_t lo = (uint32_t)min(a, b), hi = (uint32_t)max(a, b);
-  return ((uint64_t)lo << 31) | hi;
+// ------------------------------------------------------------------- dense-id image
+// D[p] = dense id of labels[p] (dense_of is indexed by label).  Every later pass of the
+// waterfall (RAG, level materialisation) reads D instead of labels, so no per-voxel or
+// per-edge dense_of gather remains on the hot path.  Each thread maps 4 consecutive voxels;
+// equal neighbours (the common case: regions are runs along x) reuse the previous gather.
+__global__ void __launch_bounds__(NTW) k_dimage(const int* __restrict__ labels, const int* __restrict__ dense_of,
+                                                 long long n, int* __restrict__ D) {
+  const long long n4 = n >> 2;
+  const int4* L4 = reinterpret_cast<const int4*>(labels);
+  int4* D4 = reinterpret_cast<int4*>(D);
+  for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n4; i += (long long)gridDim.x * NTW) {
+    const int4 v = __ldcs(L4 + i);
+    int4 d;
+    d.x = __ldg(dense_of + v.x);
+    d.y = v.y == v.x ? d.x : __ldg(dense_of + v.y);
+    d.z = v.z == v.y ? d.y : __ldg(dense_of + v.z);
+    d.w = v.w == v.z ? d.z : __ldg(dense_of + v.w);
+    D4[i] = d;
+  }
+  for (long long p = (n4 << 2) + blockIdx.x * (long long)NTW + threadIdx.x; p < n; p += (long long)gridDim.x * NTW)
+    D[p] = __ldg(dense_of + labels[p]);
 }
+
+// ------------------------------------------------------------------------ RAG extraction
+// One CTA per watershed tile (ws_tile.cuh: 3-D 32x8x8, 2-D 64x32).  The dense-id box and the
+// intensity box of the tile + its FORWARD halo (the neighbours q > p) land in shared
+// memory with one bulk-tensor copy each.  Then:
+//   1. detection: every (voxel p, forward direction f) with D(p) != D(p + f) is a boundary
+//      pair; it is appended as a 16-bit record (voxel step k, lane, f) to the warp's staging
+//      list with ballot + popc (uniform, no atomics, no divergent work);
+//   2. dedup: the warp walks its list with all lanes, re-reads D(p), D(q) and the pass height
+//      w = max(I(p), I(q)) from shared memory, and folds the pair into the tile's
+//      shared hash (64-bit pair key, CAS insert; 32-bit w with atomicMin = the per-pair
+//      minimum pass height, Alg. 4 l.2-7);
+//   3. flush: every unique tile pair becomes its edge key K = [w:8][~max:28][~min:28] (C14),
+//      is appended (block scan + one global atomic per tile) and folded into best[] (the
+//      level-1 per-region min-K edge, RED atomicMin).
+template <int CONN> struct RL {
+  using T = TL<CONN>;
+  static constexpr bool is3d = T::is3d;
+  static constexpr int TX = T::TX, TY = T::TY, TZ = T::TZ;
+  static constexpr int XA = (CONN == 8 || CONN == 26) ? 1 : 0;  // forward half reaches x-1
+  static constexpr int YA = (CONN == 26) ? 1 : 0;               // ... and y-1 (across z)
+  // boxes start at the tile origin (minus an aligned left margin when XA/YA)
+  static constexpr int IXO = XA ? 16 : 0, LXO = XA ? 4 : 0, YO = YA;
+  static constexpr int SXI = TX + 16 + IXO, SXL = TX + 4 + LXO, SY = TY + 1 + YA, SZ = is3d ? TZ + 1 : 1;
+  static constexpr int SI = SXI * SY * SZ, SL = SXL * SY * SZ;
+  static constexpr int HP = 1024;  // pair slots per tile (overflow -> direct global emit)
+  static constexpr int NF = CONN - Conn<CONN>::nfwd;
+  static constexpr int WALL = T::VPT * NF * 32;             // records a warp can produce
+  static constexpr int WCAP = WALL < 1024 ? WALL : 1024;    // per-warp staging list
+  static constexpr bool MIDFOLD = WALL > WCAP;              // fold inside the detection loop
+  static constexpr int STG = WCAP * (NT / 32);
+  __device__ static constexpr int iI(int lz, int ly, int lx) { return (lz * SY + ly + YO) * SXI + lx + IXO; }
+  __device__ static constexpr int iL(int lz, int ly, int lx) { return (lz * SY + ly + YO) * SXL + lx + LXO; }
+  __device__ static constexpr int oI(int i) {
+    int dz = 0, dy = 0, dx = 0;
+    nb_delta(CONN, i, dz, dy, dx);
+    return (dz * SY + dy) * SXI + dx;
+  }
+  __device__ static constexpr int oL(int i) {
+    int dz = 0, dy = 0, dx = 0;
+    nb_delta(CONN, i, dz, dy, dx);
+    return (dz * SY + dy) * SXL + dx;
+  }
+  static_assert((SXI % 16) == 0 && ((SXL * 4) % 16) == 0, "TMA");
+  static_assert(T::VPT <= 16 && NF <= 16, "record encoding");
+  static constexpr int SIA = (SI + 127) / 128 * 128;           // TMA destinations are 128-byte aligned
+  static constexpr int SLA = (4 * SL + 127) / 128 * 128;
+  static constexpr int SMEM = SIA + SLA + 12 * HP + 2 * STG;
+};
 
 __device__ __forceinline__ void fold_best(uint64_t* best, uint64_t k) {
   atomicMin((unsigned long long*)(best + key_lo(k)), (unsigned long long)k);
   atomicMin((unsigned long long*)(best + key_hi(k)), (unsigned long long)k);
 }
 
-__device__ __noinline__ void emit_global(uint64_t pk, unsigned w, const int* dense_of, uint64_t* edges,
-                                         unsigned long long* ecount, long long cap, uint64_t* best) {
-  const uint64_t k = make_key(w, (uint32_t)__ldg(dense_of + (int)(pk >> 31)),
-                              (uint32_t)__ldg(dense_of + (int)(pk & 0x7fffffffu)));
+__device__ __noinline__ void emit_global(uint64_t k, uint64_t* edges, unsigned long long* ecount, long long cap,
+                                         uint64_t* best) {
   const unsigned long long i = atomicAdd(ecount, 1ull);
   if ((long long)i < cap) edges[i] = k;
   fold_best(best, k);
 }
 
-__device__ __forceinline__ void pair_insert(unsigned long long* tk, unsigned* tw, uint64_t pk, unsigned w,
-                                            const int* dense_of, uint64_t* edges, unsigned long long* ecount,
-                                            long long cap, uint64_t* best) {
-  uint32_t h = (((uint32_t)(pk >> 31) * 0x9E3779B1u) ^ ((uint32_t)pk * 0x85EBCA77u)) >> 21;  // 11 bits
+// fold staged records into the tile's pair hash.  wst/wcnt: one list of a warp (wsel >= 0:
+// that warp's lane base), or, with wsel < 0, the lists of all warps of the block (counts in
+// wc[], exclusive prefixes in wp[]) spread evenly over all threads.
+template <int CONN>
+__device__ __forceinline__ void fold_rec(unsigned rec, int wbase, const uint8_t* sI, const int* sD,
+                                         unsigned long long* pk, unsigned* pw, uint64_t* edges,
+                                         unsigned long long* ecount, long long cap, uint64_t* best) {
+  using R = RL<CONN>;
+  const int f = rec & 15, lane = (rec >> 4) & 31, k = rec >> 9;  // [k:4][lane:5][f:4]
+  const int j = wbase + lane + k * NT;
+  const int lx = j % R::TX, ly = (j / R::TX) % R::TY, lz = j / (R::TX * R::TY);
+  int dz, dy, dx;
+  nb_delta(CONN, Conn<CONN>::nfwd + f, dz, dy, dx);
+  const int sl = R::iL(lz, ly, lx), si = R::iI(lz, ly, lx);
+  const uint32_t dp = (uint32_t)sD[sl], dq = (uint32_t)sD[sl + (dz * R::SY + dy) * R::SXL + dx];
+  const unsigned w = max((unsigned)sI[si], (unsigned)sI[si + (dz * R::SY + dy) * R::SXI + dx]);
+  const uint32_t lo = min(dp, dq), hi = max(dp, dq);
+  const unsigned long long key = ((unsigned long long)lo << 28) | hi;
+  uint32_t h = ((lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u)) >> (32 - 10);
 #pragma unroll 1
-  for (int probe = 0; probe < 32; ++probe) {
-    unsigned long long cur = tk[h];
-    if (cur == PKEY_NONE) cur = atomicCAS(tk + h, PKEY_NONE, (unsigned long long)pk);
-    if (cur == PKEY_NONE || cur == pk) {  // same region pair: keep the lower pass
-      atomicMin(tw + h, w);
+  for (int probe = 0; probe < 64; ++probe) {
+    unsigned long long cur = pk[h];
+    if (cur == KEY_NONE) cur = atomicCAS(pk + h, KEY_NONE, key);
+    if (cur == KEY_NONE || cur == key) {
+      atomicMin(pw + h, w);
       return;
     }
-    h = (h + 1) & (HC - 1);
+    h = (h + 1) & (R::HP - 1);
   }
-  emit_global(pk, w, dense_of, edges, ecount, cap, best);  // congested tile: emit directly
+  emit_global(make_key(w, dp, dq), edges, ecount, cap, best);  // congested tile
+}
+
+template <int CONN>
+__device__ __forceinline__ void fold_warp(const uint16_t* wst, int wcnt, const uint8_t* sI, const int* sD,
+                                          unsigned long long* pk, unsigned* pw, uint64_t* edges,
+                                          unsigned long long* ecount, long long cap, uint64_t* best) {
+  const int wbase = threadIdx.x & ~31;
+  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN>(wst[r], wbase, sI, sD, pk, pw, edges, ecount, cap, best);
 }
 
 template <int CONN, bool BORDER>
-__device__ __forceinline__ void rag_body(const uint8_t* sI, const int* sL, unsigned long long* tk, unsigned* tw,
-                                         const Geo& g, const TileCoord& c, const int* dense_of, uint64_t* edges,
-                                         unsigned long long* ecount, long long cap, uint64_t* best) {
+__device__ __forceinline__ int rag_pairs(const uint8_t* sI, const int* sD, unsigned long long* pk, unsigned* pw,
+                                          uint16_t* stg, const Geo& g, const TileCoord& c, uint64_t* edges,
+                                          unsigned long long* ecount, long long cap, uint64_t* best) {
+  using R = RL<CONN>;
   using T = TL<CONN>;
-  constexpr int NF = CONN - Conn<CONN>::nfwd;
-  uint64_t lk[NF];  // per forward direction: the current run's pair and its min height
-  unsigned lw[NF];
-#pragma unroll
-  for (int f = 0; f < NF; ++f) { lk[f] = PKEY_NONE; lw[f] = 0xffffffffu; }
+  constexpr int NF = R::NF;
+  uint16_t* wst = stg + (threadIdx.x >> 5) * R::WCAP;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
+  int wcnt = 0;
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
     my_voxel<CONN>(k, lx, ly, lz);
-    if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi)) continue;
-    const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
-    const int sl = T::iL(lz, ly, lx), si = T::iI(lz, ly, lx);
-    const int lp = sL[sl];
-    const unsigned vp = sI[si];
+    const bool own = !BORDER || (c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi);
+    const unsigned vm = !own ? 0u : (BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1);
+    const int sl = R::iL(lz, ly, lx);
+    const int dp = sD[sl];
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int i = Conn<CONN>::nfwd + f;
-      if (BORDER && !(vm & (1u << i))) continue;
-      const int lq = sL[sl + T::oL(i)];
-      if (lq == lp) continue;
-      const unsigned w = max(vp, (unsigned)sI[si + T::oI(i)]);
-      const uint64_t pk = pair_key(lp, lq);
-      if (pk == lk[f]) {
-        lw[f] = min(lw[f], w);
-      } else {
-        if (lk[f] != PKEY_NONE) pair_insert(tk, tw, lk[f], lw[f], dense_of, edges, ecount, cap, best);
-        lk[f] = pk;
-        lw[f] = w;
-      }
+      const bool e = ((vm >> i) & 1u) && sD[sl + R::oL(i)] != dp;
+      const unsigned b = __ballot_sync(0xffffffffu, e);
+      if (e) wst[wcnt + __popc(b & lt)] = (uint16_t)((k << 9) | (lane << 4) | f);
+      wcnt += __popc(b);
+    }
+    if (R::MIDFOLD && wcnt > R::WCAP - NF * 32) {
+      __syncwarp();
+      fold_warp<CONN>(wst, wcnt, sI, sD, pk, pw, edges, ecount, cap, best);
+      __syncwarp();
+      wcnt = 0;
     }
   }
-#pragma unroll
-  for (int f = 0; f < NF; ++f)
-    if (lk[f] != PKEY_NONE) pair_insert(tk, tw, lk[f], lw[f], dense_of, edges, ecount, cap, best);
+  return wcnt;
 }
 
 template <int CONN>
-__global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mL,
-                                            int tma, const int* __restrict__ labels, const uint8_t* __restrict__ I,
-                                            const int* __restrict__ dense_of, Geo g, int ntx, int nty,
-                                            uint64_t* __restrict__ edges, unsigned long long* ecount, long long cap,
-                                            uint64_t* best) {
-  using T = TL<CONN>;
+__device__ __forceinline__ void rag_load_plain(const int* __restrict__ D, const uint8_t* __restrict__ I, const Geo& g,
+                                               const TileCoord& c, uint8_t* sI, int* sD) {
+  using R = RL<CONN>;
+  for (int s = threadIdx.x; s < R::SI; s += NT) {
+    const int sx = s % R::SXI, sy = (s / R::SXI) % R::SY, sz = s / (R::SXI * R::SY);
+    const int gx = c.bx + sx - R::IXO, gy = c.by + sy - R::YO, gz = c.bz + sz;
+    uint8_t v = 0;
+    if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
+      v = __ldg(I + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
+    sI[s] = v;
+  }
+  for (int s = threadIdx.x; s < R::SL; s += NT) {
+    const int sx = s % R::SXL, sy = (s / R::SXL) % R::SY, sz = s / (R::SXL * R::SY);
+    const int gx = c.bx + sx - R::LXO, gy = c.by + sy - R::YO, gz = c.bz + sz;
+    int v = 0;
+    if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
+      v = __ldg(D + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
+    sD[s] = v;
+  }
+}
+
+// Persistent CTAs walk the tiles t = blockIdx.x, + gridDim.x, ...; with TMA the next tile's
+// boxes are requested as soon as the current ones are consumed, so the load overlaps the flush.
+template <int CONN>
+__global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mD,
+                                            int tma, const int* __restrict__ D, const uint8_t* __restrict__ I, Geo g,
+                                            int ntx, int nty, int ntiles, uint64_t* __restrict__ edges,
+                                            unsigned long long* ecount, long long cap, uint64_t* best) {
+  using R = RL<CONN>;
   extern __shared__ __align__(128) unsigned char rag_smem[];
-  uint8_t* sI = rag_smem;                                                   // T::SI bytes
-  int* sL = reinterpret_cast<int*>(rag_smem + T::SI);                       // T::SL ints
-  unsigned long long* tk = reinterpret_cast<unsigned long long*>(rag_smem + T::SI + 4 * T::SL);
-  unsigned* tw = reinterpret_cast<unsigned*>(tk + HC);
+  uint8_t* sI = rag_smem;                                                         // R::SI bytes
+  int* sD = reinterpret_cast<int*>(rag_smem + R::SIA);                            // R::SL dense ids
+  unsigned long long* pk = reinterpret_cast<unsigned long long*>(rag_smem + R::SIA + R::SLA);  // R::HP pair keys
+  unsigned* pw = reinterpret_cast<unsigned*>(pk + R::HP);                         // R::HP min pass heights
+  uint16_t* stg = reinterpret_cast<uint16_t*>(pw + R::HP);                        // R::STG staged records
   __shared__ uint64_t bar;
-  __shared__ int nloc;
   __shared__ unsigned long long gbase;
-  for (int i = threadIdx.x; i < HC; i += NT) {
-    tk[i] = PKEY_NONE;
-    tw[i] = 0xffffffffu;
+  __shared__ int sscan[32];
+  __shared__ int wc[NT / 32 + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (tma && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    if ((int)blockIdx.x < ntiles) {
+      const TileCoord c0 = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
+      mbar_expect_tx(&bar, R::SI + R::SL * 4);
+      tma_load_3d(sI, &mI, c0.bx - R::IXO, c0.by - R::YO, c0.bz, &bar);
+      tma_load_3d(sD, &mD, c0.bx - R::LXO, c0.by - R::YO, c0.bz, &bar);
+    }
   }
-  if (threadIdx.x == 0) nloc = 0;
-  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
-  stage<CONN>(&mI, &mL, tma, I, labels, g, c, sI, sL, &bar);
-  __syncthreads();
-  if (tile_interior<CONN>(c, g))
-    rag_body<CONN, false>(sI, sL, tk, tw, g, c, dense_of, edges, ecount, cap, best);
-  else
-    rag_body<CONN, true>(sI, sL, tk, tw, g, c, dense_of, edges, ecount, cap, best);
-  __syncthreads();
-  // flush: dense ids per unique tile edge, K keys, warp-aggregated slot numbers
-  constexpr int M = HC / NT;
-  int idx[M];
-  const int lane = threadIdx.x & 31;
+  uint32_t phase = 0;
+#pragma unroll 1
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const TileCoord c = tile_coord<CONN>(t, ntx, nty, g);
+    for (int i = threadIdx.x; i < R::HP; i += NT) {
+      pk[i] = KEY_NONE;
+      pw[i] = 0xffffffffu;
+    }
+    if (tma) {
+      __syncthreads();  // barrier init visible; hash reset done
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+    } else {
+      rag_load_plain<CONN>(D, I, g, c, sI, sD);
+      __syncthreads();
+    }
+    // 1. detection into the per-warp lists
+    const int n = tile_interior<CONN>(c, g) ? rag_pairs<CONN, false>(sI, sD, pk, pw, stg, g, c, edges, ecount, cap, best)
+                                            : rag_pairs<CONN, true>(sI, sD, pk, pw, stg, g, c, edges, ecount, cap, best);
+    if (lane == 0) wc[warp] = n;
+    __syncthreads();
+    // 2. dedup: the records of all warps spread evenly over the block
+    int pre[NT / 32 + 1];
+    pre[0] = 0;
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    const bool v = tk[threadIdx.x + m * NT] != PKEY_NONE;
-    const unsigned b = __ballot_sync(0xffffffffu, v);
-    int base = 0;
-    if (lane == 0 && b) base = atomicAdd(&nloc, __popc(b));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    idx[m] = v ? base + __popc(b & ((1u << lane) - 1)) : -1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) gbase = atomicAdd(ecount, (unsigned long long)nloc);
-  __syncthreads();
+    for (int w = 0; w < NT / 32; ++w) pre[w + 1] = pre[w] + wc[w];
+    const int total = pre[NT / 32];
+    for (int r = threadIdx.x; r < total; r += NT) {
+      int w = 0, base = 0;
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    if (idx[m] < 0) continue;
-    const int slot = threadIdx.x + m * NT;
-    const uint64_t pk = tk[slot];
-    const uint64_t k = make_key(tw[slot], (uint32_t)__ldg(dense_of + (int)(pk >> 31)),
-                                (uint32_t)__ldg(dense_of + (int)(pk & 0x7fffffffu)));
-    const long long i = (long long)gbase + idx[m];
-    if (i < cap) edges[i] = k;
-    fold_best(best, k);
+      for (int u = 1; u < NT / 32; ++u)
+        if (r >= pre[u]) {
+          w = u;
+          base = pre[u];
+        }
+      fold_rec<CONN>(stg[w * R::WCAP + (r - base)], w * 32, sI, sD, pk, pw, edges, ecount, cap, best);
+    }
+    __syncthreads();  // boxes consumed, hash complete
+    const int tn = t + gridDim.x;
+    if (tma && threadIdx.x == 0 && tn < ntiles) {
+      const TileCoord cn = tile_coord<CONN>(tn, ntx, nty, g);
+      mbar_expect_tx(&bar, R::SI + R::SL * 4);
+      tma_load_3d(sI, &mI, cn.bx - R::IXO, cn.by - R::YO, cn.bz, &bar);
+      tma_load_3d(sD, &mD, cn.bx - R::LXO, cn.by - R::YO, cn.bz, &bar);
+    }
+    // 3. flush: block scan of the per-thread counts, one global atomic per tile
+    constexpr int M = R::HP / NT;  // thread t owns the consecutive slots M t .. M t + M - 1
+    int cnt = 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) cnt += pk[threadIdx.x * M + m] != KEY_NONE;
+    int tot;
+    const int ex = block_excl_scan(cnt, sscan, tot);
+    if (threadIdx.x == 0) gbase = tot ? atomicAdd(ecount, (unsigned long long)tot) : 0;
+    __syncthreads();
+    long long i = (long long)gbase + ex;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const unsigned long long key = pk[threadIdx.x * M + m];
+      if (key == KEY_NONE) continue;
+      const uint64_t k = make_key(pw[threadIdx.x * M + m], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
+      if (i < cap) edges[i] = k;
+      ++i;
+      fold_best(best, k);
+    }
+    __syncthreads();  // flush done before the hash is reset
   }
 }
 
@@ -459,36 +593,37 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
   }
 }
 
-// level map rows: row(d)[k-1] = canonical label of d's level-k root, k = 1..NL-1.
-// x stays its own root below lvl[x]; from level lvl[x] on, comp[x] is its root at that level.
+// level map rows: row(d)[k] = canonical label of d's level-k root, k = 0..NL-1 (row[0] = the
+// region's own canonical label).  x stays its own root below lvl[x]; from level lvl[x] on,
+// comp[x] is its root at that level.
 __global__ void k_levelmap(const int* __restrict__ comp, const uint8_t* __restrict__ lvl,
                            const int* __restrict__ rep_of, int R, int NL, int stride, int* __restrict__ levelmap) {
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < R; d += gridDim.x * blockDim.x) {
     int x = d;
     int* row = levelmap + (size_t)d * stride;
+    row[0] = __ldg(rep_of + d);
     for (int k = 1; k < NL; ++k) {
       while (__ldg(lvl + x) <= k) x = __ldg(comp + x);
-      row[k - 1] = __ldg(rep_of + x);
+      row[k] = __ldg(rep_of + x);
     }
   }
 }
 
 // --------------------------------------------------------------- level materialisation
+// levels[k][p] = row(D[p])[k] for k = 0..NL-1 (Alg. 5 l.12 output, all layers in one pass).
 // Tiled (the watershed's 2048-voxel tiles): a region's voxels are processed together, so its
-// dense id and level-map row are fetched about once per tile.  Lanes run along x: only the
-// first lane of every run of equal labels gathers (dense_of, then one 16/32-byte map row);
-// the others take the row by shuffle.  Along z each lane also reuses its previous row.
-// Level outputs are streaming stores (evict-first).
+// level-map row (16/32 bytes, one sector) is fetched about once per tile.  Lanes run along x:
+// only the first lane of every run of equal dense ids gathers, the others take the row by
+// shuffle; along z each lane also reuses its previous row.  Level outputs are streaming
+// stores (evict-first).
 template <int CONN, int STRIDE>
-__global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ labels, const int* __restrict__ dense_of,
-                                                 const int* __restrict__ levelmap, int NL, Geo g, int ntx, int nty,
-                                                 int* __restrict__ levels) {
+__global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ D, const int* __restrict__ levelmap, int NL,
+                                                 Geo g, int ntx, int nty, int* __restrict__ levels) {
   using T = TL<CONN>;
   const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
   const int lane = threadIdx.x & 31;
-  const int nm = NL - 1;
   const size_t N = (size_t)g.N;
-  int prev_l = -1;
+  int prev_d = -1;
   int row[STRIDE];
 #pragma unroll
   for (int j = 0; j < STRIDE; ++j) row[j] = 0;
@@ -499,12 +634,12 @@ __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ labels, 
     const int gx = c.bx + lx, gy = c.by + ly, gz = c.bz + lz;
     const bool valid = gx < g.n2 && gy < g.n1 && gz < g.n0;
     const size_t p = (size_t)gz * g.plane + (size_t)gy * g.n2 + gx;
-    const int l = valid ? __ldcs(labels + p) : -1 - lane;
-    const int lup = __shfl_up_sync(0xffffffffu, l, 1);
-    const bool head = (lane == 0 || lup != l);
-    const bool fetch = valid && head && l != prev_l;
+    const int d = valid ? __ldcs(D + p) : -1 - lane;
+    const int dup = __shfl_up_sync(0xffffffffu, d, 1);
+    const bool head = (lane == 0 || dup != d);
+    const bool fetch = valid && head && d != prev_d;
     if (fetch) {
-      const int* m = levelmap + (size_t)__ldg(dense_of + l) * STRIDE;
+      const int* m = levelmap + (size_t)d * STRIDE;
 #pragma unroll
       for (int j = 0; j < STRIDE; j += 4) {
         const int4 v = __ldg(reinterpret_cast<const int4*>(m + j));
@@ -515,54 +650,57 @@ __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ labels, 
     const int src = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
 #pragma unroll
     for (int j = 0; j < STRIDE; ++j) row[j] = __shfl_sync(0xffffffffu, row[j], src);
-    prev_l = l;
+    prev_d = d;
     if (valid) {
-      __stcs(levels + p, l);
 #pragma unroll
       for (int j = 0; j < STRIDE; ++j)
-        if (j < nm) __stcs(levels + (size_t)(j + 1) * N + p, row[j]);
+        if (j < NL) __stcs(levels + (size_t)j * N + p, row[j]);
     }
   }
 }
 
-// scalar variant for large NL (stride NL-1 not specialised) or unaligned pointers
-__global__ void k_levels_any(const int* __restrict__ labels, const int* __restrict__ dense_of,
-                             const int* __restrict__ levelmap, int NL, int stride, long long N, int* __restrict__ levels) {
+// scalar variant for large NL (stride not specialised)
+__global__ void k_levels_any(const int* __restrict__ D, const int* __restrict__ levelmap, int NL, int stride,
+                             long long N, int* __restrict__ levels) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
-    const int l = __ldg(labels + p);
-    levels[p] = l;
-    if (NL > 1) {
-      const int* m = levelmap + (size_t)__ldg(dense_of + l) * stride;
-      for (int k = 1; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k - 1);
-    }
+    const int* m = levelmap + (size_t)__ldg(D + p) * stride;
+    for (int k = 0; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k);
   }
 }
 
 // --------------------------------------------------------------------------- driver
 template <int CONN>
-static ws_status rag_t(const int* labels, const uint8_t* I, const int* dense_of, const Geo& g, uint64_t* edges,
-                       unsigned long long* ecount, long long cap, uint64_t* best, cudaStream_t st) {
+static ws_status rag_t(const int* D, const uint8_t* I, const Geo& g, uint64_t* edges, unsigned long long* ecount,
+                       long long cap, uint64_t* best, cudaStream_t st) {
   using T = TL<CONN>;
+  using R = RL<CONN>;
   const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY,
             ntz = (g.zhi - g.zlo + T::TZ - 1) / T::TZ;
   Maps mp;
-  make_maps<CONN>(I, labels, g, mp);
-  const int smem = T::SI + 4 * T::SL + HC * 12;  // I box, L box, hash keys + heights
-  static_assert((T::SI % 16) == 0 && ((T::SI + 4 * T::SL) % 16) == 0, "smem carve-up alignment");
-  WS_CUDA(cudaFuncSetAttribute(k_rag<CONN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_rag<CONN><<<ntx * nty * ntz, NT, smem, st>>>(mp.mI, mp.mL, mp.tma, labels, I, dense_of, g, ntx, nty, edges,
-                                                  ecount, cap, best);
+  std::memset(&mp, 0, sizeof(mp));
+  const char* env = getenv("WS_NO_TMA");
+  const bool off = env && env[0] == '1';
+  const bool a = !off && encode_tmap_3d(&mp.mI, 1, I, g, R::SXI, R::SY, R::SZ);
+  const bool b = !off && encode_tmap_3d(&mp.mL, 4, D, g, R::SXL, R::SY, R::SZ);
+  mp.tma = (a && b) ? 1 : 0;
+  WS_CUDA(cudaFuncSetAttribute(k_rag<CONN>, cudaFuncAttributeMaxDynamicSharedMemorySize, R::SMEM));
+  // one tile per CTA: CTAs running together hold neighbouring tiles, so the edge list comes
+  // out in tile order (the level loop's per-chunk dedup and comp gathers depend on it; a
+  // persistent grid interleaves distant tiles and measured slower overall)
+  const int ntiles = ntx * nty * ntz;
+  const int grid = ntiles;
+  k_rag<CONN><<<grid, NT, R::SMEM, st>>>(mp.mI, mp.mL, mp.tma, D, I, g, ntx, nty, ntiles, edges, ecount, cap, best);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
 
-static ws_status rag(int conn, const int* labels, const uint8_t* I, const int* dense_of, const Geo& g,
-                     uint64_t* edges, unsigned long long* ecount, long long cap, uint64_t* best, cudaStream_t st) {
+static ws_status rag(int conn, const int* D, const uint8_t* I, const Geo& g, uint64_t* edges,
+                     unsigned long long* ecount, long long cap, uint64_t* best, cudaStream_t st) {
   switch (conn) {
-    case 4: return rag_t<4>(labels, I, dense_of, g, edges, ecount, cap, best, st);
-    case 8: return rag_t<8>(labels, I, dense_of, g, edges, ecount, cap, best, st);
-    case 6: return rag_t<6>(labels, I, dense_of, g, edges, ecount, cap, best, st);
-    case 26: return rag_t<26>(labels, I, dense_of, g, edges, ecount, cap, best, st);
+    case 4: return rag_t<4>(D, I, g, edges, ecount, cap, best, st);
+    case 8: return rag_t<8>(D, I, g, edges, ecount, cap, best, st);
+    case 6: return rag_t<6>(D, I, g, edges, ecount, cap, best, st);
+    case 26: return rag_t<26>(D, I, g, edges, ecount, cap, best, st);
   }
   return WS_ERR_INVALID;
 }
@@ -619,7 +757,7 @@ static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
     set_error(WS_ERR_INVALID, "ws_waterfall: labels are not a canonical labelling (no representative)");
     return WS_ERR_INVALID;
   }
-  const int stride = NL <= 5 ? 4 : (NL <= 9 ? 8 : NL - 1);
+  const int stride = NL <= 4 ? 4 : (NL <= 8 ? 8 : NL);  // row = canonical label at levels 0..NL-1
   WS_TRY(ctx->comp.ensure((size_t)R * sizeof(int), "comp"));
   WS_TRY(ctx->best.ensure((size_t)R * sizeof(uint64_t), "best"));
   WS_TRY(ctx->levelmap.ensure((size_t)R * stride * sizeof(int), "levelmap"));
@@ -636,10 +774,25 @@ static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
   return WS_OK;
 }
 
-// RAG edges of the owned planes, tile-deduplicated, folded into best[] (level-1 minima)
+// RAG edges of the owned planes, tile-deduplicated, folded into best[] (level-1 minima).
+// First the dense-id image D of the owned planes and the plane above (the forward halo) is
+// written into ctx->dimg (same layout as labels).
 static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn,
                         const int* dense_of, cudaStream_t st) {
   unsigned long long* ecount = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 136);
+  WS_TRY(ctx->dimg.ensure((size_t)g.N * sizeof(int), "dense-id image"));
+  int* D = ctx->dimg.as<int>();
+  {
+    const int z1 = g.zhi < g.n0 ? g.zhi + 1 : g.zhi;
+    const size_t o = (size_t)g.zlo * g.plane;
+    const long long n = (long long)(z1 - g.zlo) * g.plane;
+    const bool al = !(reinterpret_cast<uintptr_t>(labels + o) & 15) && !(reinterpret_cast<uintptr_t>(D + o) & 15);
+    k_dimage<<<grid_for(n / 4 + 1, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, al ? n : 0, D + o);
+    if (!al) k_dimage<<<grid_for(n, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, n, D + o);
+    launched(ctx, PH_WF_DENSE);
+    ctx->wf.dofs = (long long)o;
+  }
+  tmark(ctx, st, PH_WF_DENSE);
   const long long own = (long long)(g.zhi - g.zlo) * g.plane;
   long long cap = (long long)(ctx->edges.bytes / sizeof(uint64_t));
   const long long want = own / 4 + 4096;
@@ -650,7 +803,7 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   int64_t E = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ecount, 0, sizeof(unsigned long long), st));
-    WS_TRY(rag(conn, labels, I, dense_of, g, ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), st));
+    WS_TRY(rag(conn, D, I, g, ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), st));
     launched(ctx, PH_WF_RAG);
     WS_TRY(read_i64(ctx, ecount, &E, st));
     if (E <= cap) break;
@@ -727,18 +880,15 @@ static ws_status wf_step(ws_ctx* ctx, int64_t* count, int* more, cudaStream_t st
   return WS_OK;
 }
 
-// level maps (replicated) + level arrays of the voxels of labels (n0 planes of g)
-static ws_status wf_finish(ws_ctx* ctx, const int32_t* labels, const Geo& g, int conn, const int* dense_of,
-                           int32_t* levels, cudaStream_t st) {
+// level maps (replicated) + level arrays of the voxels of the dense-id image D (n0 planes of g)
+static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn, int32_t* levels, cudaStream_t st) {
   WSState& w = ctx->wf;
   const int NL = w.NL, stride = w.stride;
   ctx->stats.waterfall_levels = w.lv;
   int* levelmap = ctx->levelmap.as<int>();
-  if (NL > 1) {
-    k_levelmap<<<grid_for(w.R, ctx->num_sms), 256, 0, st>>>(ctx->comp.as<int>(), ctx->lvl.as<uint8_t>(),
-                                                             ctx->rep_of.as<int>(), (int)w.R, NL, stride, levelmap);
-    launched(ctx, PH_WF_LEVELS);
-  }
+  k_levelmap<<<grid_for(w.R, ctx->num_sms), 256, 0, st>>>(ctx->comp.as<int>(), ctx->lvl.as<uint8_t>(),
+                                                           ctx->rep_of.as<int>(), (int)w.R, NL, stride, levelmap);
+  launched(ctx, PH_WF_LEVELS);
   tmark(ctx, st, PH_WF_LEVELS);
   const int N = g.N;
   const int gN = grid_for(N, ctx->num_sms);
@@ -747,12 +897,12 @@ static ws_status wf_finish(ws_ctx* ctx, const int32_t* labels, const Geo& g, int
     const int TX = is3d ? TL<6>::TX : TL<4>::TX, TY = is3d ? TL<6>::TY : TL<4>::TY, TZ = is3d ? TL<6>::TZ : TL<4>::TZ;
     const int ntx = (g.n2 + TX - 1) / TX, nty = (g.n1 + TY - 1) / TY, ntz = (g.zhi - g.zlo + TZ - 1) / TZ;
     const int nt = ntx * nty * ntz;
-    if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
-    else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
-    else if (stride == 4) k_levels<4, 4><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
-    else k_levels<4, 8><<<nt, NTW, 0, st>>>(labels, dense_of, levelmap, NL, g, ntx, nty, levels);
+    if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else if (stride == 4) k_levels<4, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else k_levels<4, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
   } else {
-    k_levels_any<<<gN, NTW, 0, st>>>(labels, dense_of, levelmap, NL, stride, N, levels);
+    k_levels_any<<<gN, NTW, 0, st>>>(D, levelmap, NL, stride, N, levels);
   }
   launched(ctx, PH_WF_MATERIALISE);
   tmark(ctx, st, PH_WF_MATERIALISE);
@@ -783,7 +933,7 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
     if (counts) counts[k] = cnt;
     if (k < 16) ctx->stats.level_counts[k] = cnt;
   }
-  return wf_finish(ctx, labels, g, conn, dense_of, levels, st);
+  return wf_finish(ctx, ctx->dimg.as<int>(), g, conn, levels, st);
 }
 
 // ------------------------------------------------------------- z-slab sharded waterfall
@@ -868,9 +1018,11 @@ ws_status shard_wf_step(ws_ctx* ctx, const uint64_t* best_in, uint64_t* best_out
 
 ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, int conn, const int* dense_of,
                        const int* rep_of_global, int32_t* levels_own, cudaStream_t st) {
+  (void)labels_own;
+  (void)dense_of;  // the owned planes' dense ids are in ctx->dimg (written by shard_wf_begin)
   WS_TRY(ctx->rep_of.ensure((size_t)ctx->wf.R * sizeof(int), "rep_of"));
   WS_CUDA(cudaMemcpyAsync(ctx->rep_of.p, rep_of_global, (size_t)ctx->wf.R * sizeof(int), cudaMemcpyDeviceToDevice, st));
-  return wf_finish(ctx, labels_own, gown, conn, dense_of, levels_own, st);
+  return wf_finish(ctx, ctx->dimg.as<int>() + ctx->wf.dofs, gown, conn, levels_own, st);
 }
 
 }  // namespace ws

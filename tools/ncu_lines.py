@@ -1,27 +1,33 @@
-"""Aggregate ncu source-page (cuda,sass) metrics per CUDA source line.
-usage: ncu -i rep --page source --csv --print-source cuda,sass -k regex:K > f.csv; python ncu_lines.py f.csv"""
+"""Per CUDA source line: warp-stall samples and warp instructions executed, from an .ncu-rep
+(`ncu -i REP --page source --print-source cuda,sass --csv -k regex:KERNEL`).  Run here."""
 import csv
+import io
+import subprocess
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
-hdr = [r for r in rows if r and r[0] == 'Line No'][0]
-i_line, i_src = 0, 1
-i_samp = hdr.index('Warp Stall Sampling (All Samples)')
-i_exec = hdr.index('Instructions Executed')
-agg = {}
-cur = None
-src = {}
+rep, kern = sys.argv[1], sys.argv[2]
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'cuda,sass', '-k',
+                      'regex:' + kern], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+fname, agg, hdr = None, {}, None
 for r in rows:
-    if not r or r[0] in ('Line No', 'File Path', 'Function Name'):
+    if len(r) >= 2 and r[0] == 'File Path':
+        fname = r[1].split('/')[-1]
         continue
-    if r[0].strip().isdigit():
-        cur = int(r[0])
-        src[cur] = r[1]
-    if len(r) > i_exec and r[i_exec].strip().isdigit() and cur is not None:
-        a = agg.setdefault(cur, [0, 0])
-        a[0] += int(r[i_exec])
-        a[1] += int(r[i_samp]) if r[i_samp].strip().isdigit() else 0
-te = sum(v[0] for v in agg.values()) or 1
-ts = sum(v[1] for v in agg.values()) or 1
-for ln, (e, s) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
-    print('%5d inst %5.1f%% stall %5.1f%%  %s' % (ln, 100 * e / te, 100 * s / ts, src.get(ln, '')[:90]))
+    if r and r[0] == 'Line No':
+        hdr = r
+        continue
+    if hdr is None or len(r) < 8 or r[0] == '' or r[0] == '-':
+        continue
+    try:
+        s, ins = int(r[4]), int(r[7])
+    except ValueError:
+        continue
+    agg[(fname, int(r[0]))] = (s, ins, r[1][:90])
+tot_s = sum(v[0] for v in agg.values()) or 1
+tot_i = sum(v[1] for v in agg.values()) or 1
+print('total samples %d, warp instructions %.3e' % (tot_s, tot_i))
+key = 1 if len(sys.argv) > 4 and sys.argv[4] == "inst" else 0
+for (f, ln), (s, ins, src) in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
+    print('%5.1f%% samp %5.1f%% inst  %s:%d  %s' % (100 * s / tot_s, 100 * ins / tot_i, f, ln, src))
