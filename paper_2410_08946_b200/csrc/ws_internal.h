@@ -57,6 +57,7 @@ struct ws_ctx {
   ws::Buf tmpA, tmpB; // f32[N]   gradient pre-pass intermediates
   ws::Buf flags;      // small device counters / flags
   ws::Buf tiles;      // u8[3 * ntiles] step II active-tile flags
+  ws::Buf tlist;      // i32[ntiles]  compacted active tiles of the next step II round
   ws::Buf roots;      // i32[cap]  step III roots (self-loops), compact list
   ws::Buf upairs;     // int2[cap] step IV pairs crossing a tile face (k_resolve -> k_union_pairs)
   ws::Buf rootc;      // i32[cap]  canonical label per listed root

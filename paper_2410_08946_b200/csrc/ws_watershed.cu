@@ -22,6 +22,7 @@
 // code of ws_common.cuh (L >= 0: d = 0; L < 0: -1 - (d << 5)).  P = ctx->aux (i32[N]) holds
 // pointers from k_resolve on.  From k_jump on, L[r] of a root r holds INT_MAX - (smallest
 // voxel index reaching r); all other L entries are dead until k_relabel writes the output.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -311,10 +312,10 @@ __global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUte
                                                      const __grid_constant__ CUtensorMap mL, int tma,
                                                      const uint8_t* __restrict__ I, int* __restrict__ L, Geo g,
                                                      int ntx, int nty, const uint8_t* cur, uint8_t* next,
-                                                     const uint8_t* hasplat, int* flags) {
+                                                     const uint8_t* hasplat, int* flags, const int* list) {
   using T = TL<CONN>;
-  const int t = blockIdx.x;
-  if (!cur[t] || !hasplat[t]) return;
+  const int t = list ? list[blockIdx.x] : blockIdx.x;  // list: the compacted active tiles
+  if (!list && (!cur[t] || !hasplat[t])) return;
   __shared__ alignas(128) uint8_t sI[T::SI];
   __shared__ alignas(128) int sD[T::SL];
   __shared__ uint64_t bar;
@@ -325,6 +326,22 @@ __global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUte
     relax_round_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, flags);
   else
     relax_round_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, flags);
+}
+
+// compact list of the tiles of the next round: marked by a neighbour and holding plateau voxels
+__global__ void k_tile_list(const uint8_t* __restrict__ next, const uint8_t* __restrict__ hasplat, int n,
+                            int* __restrict__ list, int* count) {
+  for (int t0 = blockIdx.x * NT; t0 < n; t0 += gridDim.x * NT) {
+    const int t = t0 + threadIdx.x;
+    const bool a = t < n && next[t] && hasplat[t];
+    const unsigned b = __ballot_sync(0xffffffffu, a);
+    if (!b) continue;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(count, __popc(b));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (a) list[base + __popc(b & ((1u << lane) - 1))] = t;
+  }
 }
 
 // ---------------------- pointers (steps I-II) + tile-local pointer jumping (step III)
@@ -732,31 +749,37 @@ static ws_status plateau_phase(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
   uint8_t* cur = ctx->tiles.as<uint8_t>();
   uint8_t* next = cur + tg.n;
   uint8_t* hasplat = next + tg.n;
-  WS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
+  WS_TRY(ctx->tlist.ensure((size_t)tg.n * sizeof(int), "active tile list"));
+  int* list = ctx->tlist.as<int>();
+  const int gl = std::max(1, std::min((tg.n + NT - 1) / NT, ctx->num_sms * 8));
+  WS_CUDA(cudaMemsetAsync(flags, 0, 5 * sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
   k_relax_first<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, next, hasplat, flags);
-  launched(ctx, PH_WS_INIT);
+  k_tile_list<<<gl, NT, 0, st>>>(next, hasplat, tg.n, list, flags + 4);
+  launched(ctx, PH_WS_INIT, 2);
   tmark(ctx, st, PH_WS_INIT);
   int rounds = 1;
   while (true) {
-    WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 5 * sizeof(int), cudaMemcpyDeviceToHost, st));
     WS_CUDA(cudaStreamSynchronize(st));
     const int* h = reinterpret_cast<const int*>(ctx->pinned);
     if (h[1]) {
       set_error(WS_ERR_LIMIT, "a non-minimal plateau is deeper than 2^26-2 voxels");
       return WS_ERR_LIMIT;
     }
-    if (!h[0]) break;
+    const int nact = h[4];
+    if (!h[0] || nact == 0) break;
     if (rounds > g.N + 2) {
       set_error(WS_ERR_INTERNAL, "step II did not converge");
       return WS_ERR_INTERNAL;
     }
     std::swap(cur, next);
     WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
-    WS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int), st));
-    k_relax_round<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat,
-                                             flags);
-    launched(ctx, PH_WS_RELAX);
+    WS_CUDA(cudaMemsetAsync(flags, 0, 5 * sizeof(int), st));
+    k_relax_round<CONN><<<nact, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat,
+                                             flags, list);
+    k_tile_list<<<gl, NT, 0, st>>>(next, hasplat, tg.n, list, flags + 4);
+    launched(ctx, PH_WS_RELAX, 2);
     ++rounds;
   }
   ctx->stats.plateau_rounds = rounds;
@@ -903,7 +926,8 @@ static ws_status shard_round_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
   if (act_hi) k_mark_layer<<<(per + 255) / 256, 256, 0, st>>>(cur, tg.ntz - 1, per);
   WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
   WS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
-  k_relax_round<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat, flags);
+  k_relax_round<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat, flags,
+                                           nullptr);
   launched(ctx, PH_WS_RELAX);
   ctx->shard_flip = 1 - ctx->shard_flip;
   WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
