@@ -25,13 +25,21 @@ ws_status cuda_fail(cudaError_t e, const char* where) {
   return e == cudaErrorMemoryAllocation ? WS_ERR_OOM : WS_ERR_CUDA;
 }
 
+// Grows with 1/8 headroom: sizes that vary slightly from call to call (edge counts) must not
+// re-allocate (cudaFree synchronises the device) on every call.
 ws_status Buf::ensure(size_t want, const char* name) {
   if (want <= bytes) return WS_OK;
   if (p) cudaFree(p);
   p = nullptr;
   bytes = 0;
   if (want == 0) return WS_OK;
-  cudaError_t e = cudaMalloc(&p, want);
+  const size_t grow = want + want / 8;
+  cudaError_t e = cudaMalloc(&p, grow);
+  if (e == cudaSuccess) want = grow;
+  else {
+    (void)cudaGetLastError();
+    e = cudaMalloc(&p, want);
+  }
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     p = nullptr;
@@ -202,7 +210,7 @@ ws_status ws_ctx_create(int32_t device, ws_ctx** out) {
   }
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-  e = cudaMallocHost(&c->pinned, 64 * sizeof(int64_t));
+  e = cudaMallocHost(&c->pinned, 256 * sizeof(int64_t));
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(e, "cudaMallocHost");

@@ -440,7 +440,9 @@ __global__ void k_iota(int* a, int n) {
 // C16); best[c] is reset for the next level.  roots == nullptr: all c in [0, n).
 // Finds are read-only: the chains below the previous level's roots (comp^k(d) = level-k
 // root) must survive for k_levelmap, so no path halving here.
-__global__ void k_hook(uint64_t* best, int* comp, const int* __restrict__ roots, int n) {
+__global__ void k_hook(uint64_t* best, int* comp, const int* __restrict__ roots, int n,
+                       const unsigned long long* nptr) {
+  if (nptr) n = (int)*nptr;  // device-resident count of the previous level's roots
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int c = roots ? roots[i] : i;
     const uint64_t k = best[c];
@@ -461,10 +463,12 @@ __global__ void k_hook(uint64_t* best, int* comp, const int* __restrict__ roots,
 // stores; non-root entries keep pointing one level up, so comp^k(d) is d's level-k root)
 // and collect the level-k roots (warp-aggregated append, smem-staged per block).
 __global__ void __launch_bounds__(NTW) k_flatten(int* comp, const int* __restrict__ roots, int n,
-                                                  int* __restrict__ out, int* nout, uint8_t* __restrict__ lvl,
-                                                  int level) {
+                                                  const unsigned long long* nptr, int* __restrict__ out,
+                                                  unsigned long long* nout, uint8_t* __restrict__ lvl, int level) {
   __shared__ int sbuf[2 * NTW];
-  __shared__ int scount, sbase;
+  __shared__ int scount;
+  __shared__ unsigned long long sbase;
+  if (nptr) n = (int)*nptr;
   if (threadIdx.x == 0) scount = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(NTW) k_flatten(int* comp, const int* __restric
     const int cnt = scount;
     if (cnt > NTW || i0 + gridDim.x * NTW >= n) {
       if (cnt > 0) {
-        if (threadIdx.x == 0) sbase = atomicAdd(nout, cnt);
+        if (threadIdx.x == 0) sbase = atomicAdd(nout, (unsigned long long)cnt);
         __syncthreads();
         for (int j = threadIdx.x; j < cnt; j += NTW) out[sbase + j] = sbuf[j];
       }
@@ -516,80 +520,78 @@ constexpr int ECH = 2048;  // edges per block (8 per thread)
 constexpr int EHC = 4096;  // shared hash slots
 
 __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_keys, const Edge* __restrict__ in,
-                                                long long n, const int* __restrict__ comp, uint64_t* best,
-                                                Edge* __restrict__ out, unsigned long long* nout) {
+                                                long long n, const unsigned long long* nptr,
+                                                const int* __restrict__ comp, uint64_t* best, Edge* __restrict__ out,
+                                                unsigned long long* nout) {
   extern __shared__ __align__(16) unsigned long long esm[];
   unsigned long long* tp = esm;        // component pair (lo << 32 | hi)
   unsigned long long* tkk = esm + EHC;  // min K of the pair
-  __shared__ int nloc;
+  __shared__ int sscan[32];
   __shared__ unsigned long long gbase;
-  for (int i = threadIdx.x; i < EHC; i += NTW) {
-    tp[i] = KEY_NONE;
-    tkk[i] = KEY_NONE;
-  }
-  if (threadIdx.x == 0) nloc = 0;
-  __syncthreads();
-  const long long e0 = (long long)blockIdx.x * ECH;
-#pragma unroll
-  for (int j = 0; j < ECH / NTW; ++j) {
-    const long long e = e0 + threadIdx.x + j * NTW;
-    if (e >= n) break;
-    uint64_t k;
-    int a, b;
-    if (in_keys) {
-      k = in_keys[e];
-      a = (int)key_lo(k);
-      b = (int)key_hi(k);
-    } else {
-      const Edge ed = in[e];
-      k = ed.k;
-      a = ed.a;
-      b = ed.b;
-    }
-    a = __ldg(comp + a);
-    b = __ldg(comp + b);
-    if (a == b) continue;
-    const uint64_t pk = ((uint64_t)(uint32_t)min(a, b) << 32) | (uint32_t)max(a, b);
-    uint32_t h = (((uint32_t)(pk >> 32) * 0x9E3779B1u) ^ ((uint32_t)pk * 0x85EBCA77u)) >> 20;  // 12 bits
+  if (nptr) n = (long long)*nptr;  // device-resident count of the previous level's live edges
+  constexpr int M = EHC / NTW;     // thread t owns the consecutive slots M t .. M t + M - 1
 #pragma unroll 1
-    while (true) {
-      unsigned long long cur = tp[h];
-      if (cur == KEY_NONE) cur = atomicCAS(tp + h, KEY_NONE, (unsigned long long)pk);
-      if (cur == KEY_NONE || cur == pk) {
-        atomicMin(tkk + h, (unsigned long long)k);
-        break;
-      }
-      h = (h + 1) & (EHC - 1);  // at most ECH pairs in EHC slots: always terminates
+  for (long long e0 = (long long)blockIdx.x * ECH; e0 < n; e0 += (long long)gridDim.x * ECH) {
+    for (int i = threadIdx.x; i < EHC; i += NTW) {
+      tp[i] = KEY_NONE;
+      tkk[i] = KEY_NONE;
     }
-  }
-  __syncthreads();
-  constexpr int M = EHC / NTW;
-  int idx[M];
-  const int lane = threadIdx.x & 31;
+    __syncthreads();
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    const bool v = tp[threadIdx.x + m * NTW] != KEY_NONE;
-    const unsigned bal = __ballot_sync(0xffffffffu, v);
-    int base = 0;
-    if (lane == 0 && bal) base = atomicAdd(&nloc, __popc(bal));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    idx[m] = v ? base + __popc(bal & ((1u << lane) - 1)) : -1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) gbase = atomicAdd(nout, (unsigned long long)nloc);
-  __syncthreads();
+    for (int j = 0; j < ECH / NTW; ++j) {
+      const long long e = e0 + threadIdx.x + j * NTW;
+      if (e >= n) break;
+      uint64_t k;
+      int a, b;
+      if (in_keys) {
+        k = in_keys[e];
+        a = (int)key_lo(k);
+        b = (int)key_hi(k);
+      } else {
+        const Edge ed = in[e];
+        k = ed.k;
+        a = ed.a;
+        b = ed.b;
+      }
+      a = __ldg(comp + a);
+      b = __ldg(comp + b);
+      if (a == b) continue;
+      const uint64_t pk = ((uint64_t)(uint32_t)min(a, b) << 32) | (uint32_t)max(a, b);
+      uint32_t h = (((uint32_t)(pk >> 32) * 0x9E3779B1u) ^ ((uint32_t)pk * 0x85EBCA77u)) >> 20;  // 12 bits
+#pragma unroll 1
+      while (true) {
+        unsigned long long cur = tp[h];
+        if (cur == KEY_NONE) cur = atomicCAS(tp + h, KEY_NONE, (unsigned long long)pk);
+        if (cur == KEY_NONE || cur == pk) {
+          if (k < tkk[h]) atomicMin(tkk + h, (unsigned long long)k);
+          break;
+        }
+        h = (h + 1) & (EHC - 1);  // at most ECH pairs in EHC slots: always terminates
+      }
+    }
+    __syncthreads();
+    int cnt = 0;
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    if (idx[m] < 0) continue;
-    const int slot = threadIdx.x + m * NTW;
-    const unsigned long long pk = tp[slot];
-    Edge ed;
-    ed.k = tkk[slot];
-    ed.a = (int)(pk >> 32);
-    ed.b = (int)(pk & 0xffffffffu);
-    atomicMin((unsigned long long*)(best + ed.a), (unsigned long long)ed.k);
-    atomicMin((unsigned long long*)(best + ed.b), (unsigned long long)ed.k);
-    out[gbase + idx[m]] = ed;
+    for (int m = 0; m < M; ++m) cnt += tp[threadIdx.x * M + m] != KEY_NONE;
+    int tot;
+    const int ex = block_excl_scan(cnt, sscan, tot);
+    if (threadIdx.x == 0) gbase = tot ? atomicAdd(nout, (unsigned long long)tot) : 0;
+    __syncthreads();
+    unsigned long long o = gbase + ex;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int slot = threadIdx.x * M + m;
+      const unsigned long long pk = tp[slot];
+      if (pk == KEY_NONE) continue;
+      Edge ed;
+      ed.k = tkk[slot];
+      ed.a = (int)(pk >> 32);
+      ed.b = (int)(pk & 0xffffffffu);
+      atomicMin((unsigned long long*)(best + ed.a), (unsigned long long)ed.k);
+      atomicMin((unsigned long long*)(best + ed.b), (unsigned long long)ed.k);
+      out[o++] = ed;
+    }
+    __syncthreads();  // the chunk's hash is consumed before the next chunk resets it
   }
 }
 
@@ -747,6 +749,10 @@ static ws_status wf_dense(ws_ctx* ctx, const int32_t* labels, int n, int pofs, i
   return WS_OK;
 }
 
+// device-resident level counters (ctx->lvcount): [k] = roots after level k, [LVC + k] = live
+// edges entering level k (k < LVC); the level loop runs without host round trips
+constexpr int LVC = 64;
+
 // level-loop buffers for R regions; best[] = KEY_NONE, comp = iota, lvl = 0xFF
 static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
   if (R > (long long)IDMASK) {
@@ -764,6 +770,8 @@ static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
   WS_TRY(ctx->rootsA.ensure((size_t)R * sizeof(int), "level roots A"));
   WS_TRY(ctx->rootsB.ensure((size_t)R * sizeof(int), "level roots B"));
   WS_TRY(ctx->lvl.ensure((size_t)R, "demotion levels"));
+  WS_TRY(ctx->lvcount.ensure(2 * LVC * sizeof(unsigned long long), "level counters"));
+  WS_CUDA(cudaMemsetAsync(ctx->lvcount.p, 0, 2 * LVC * sizeof(unsigned long long), st));
   WS_CUDA(cudaMemsetAsync(ctx->best.p, 0xFF, (size_t)R * sizeof(uint64_t), st));
   WS_CUDA(cudaMemsetAsync(ctx->lvl.p, 0xFF, (size_t)R, st));
   k_iota<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(ctx->comp.as<int>(), (int)R);
@@ -827,56 +835,82 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   return WS_OK;
 }
 
-// Level k = ctx->wf.k: best[] must hold the per-component min-K edges (all ranks' minima when
-// sharded).  Hook + flatten; the new region count goes to *count.  If another level follows,
-// the live edges are re-labelled, compacted and folded into best[] for level k + 1.
-// Returns *more = 0 when the hierarchy is final (one region, or no merge possible).
-static ws_status wf_step(ws_ctx* ctx, int64_t* count, int* more, cudaStream_t st) {
+// Level k = ctx->wf.k: hook + flatten (+ the live edges of level k + 1 when `edges_next`).
+// Counts stay on the device; nothing here synchronises.
+static ws_status wf_level(ws_ctx* ctx, bool edges_next, cudaStream_t st) {
   WSState& w = ctx->wf;
   const int k = w.k;
-  char* fl = ctx->flags.as<char>();
-  int* nroots = reinterpret_cast<int*>(fl + 144);
-  unsigned long long* nedges = reinterpret_cast<unsigned long long*>(fl + 152);
+  unsigned long long* cnt = ctx->lvcount.as<unsigned long long>();
   int* comp = ctx->comp.as<int>();
   uint64_t* best = ctx->best.as<uint64_t>();
   int* rA = ctx->rootsA.as<int>();
   int* rB = ctx->rootsB.as<int>();
   int* rin = w.rflip < 0 ? nullptr : (w.rflip == 0 ? rA : rB);
   int* rout = (w.rflip == 0) ? rB : rA;
-  k_hook<<<grid_for(w.nr_in, ctx->num_sms), 256, 0, st>>>(best, comp, rin, (int)w.nr_in);
-  WS_CUDA(cudaMemsetAsync(nroots, 0, sizeof(int), st));
-  k_flatten<<<grid_for(w.nr_in, ctx->num_sms, 8), NTW, 0, st>>>(comp, rin, (int)w.nr_in, rout, nroots,
-                                                                 ctx->lvl.as<uint8_t>(), k);
+  const unsigned long long* nin = rin ? cnt + (k - 1) : nullptr;  // level 1: all R regions
+  k_hook<<<grid_for(w.R, ctx->num_sms), 256, 0, st>>>(best, comp, rin, (int)w.R, nin);
+  k_flatten<<<grid_for(w.R, ctx->num_sms, 8), NTW, 0, st>>>(comp, rin, (int)w.R, nin, rout, cnt + k,
+                                                             ctx->lvl.as<uint8_t>(), k);
   launched(ctx, PH_WF_LEVELS, 2);
-  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nroots, sizeof(int), cudaMemcpyDeviceToHost, st));
-  WS_CUDA(cudaStreamSynchronize(st));
-  const long long cnt = reinterpret_cast<const int*>(ctx->pinned)[0];
   w.rflip = (rout == rA) ? 0 : 1;
-  w.nr_in = cnt;
-  if (cnt < w.prev) w.lv = k;
-  const bool merged = cnt < w.prev;
-  w.prev = cnt;
-  *count = cnt;
-  if (k < 16) ctx->stats.level_counts[k] = cnt;
-  *more = (k + 1 < w.NL && cnt > 1 && merged) ? 1 : 0;
   w.k = k + 1;
-  if (!*more) return WS_OK;
+  if (!edges_next || k + 1 >= LVC) return WS_OK;
   // level k + 1 minima from the live edges (level 2 reads the level-1 key list)
   Edge* ein = (k == 1) ? nullptr : (w.eflip == 0 ? ctx->ebufB.as<Edge>() : ctx->ebufA.as<Edge>());
   Edge* eout = (w.eflip == 0) ? ctx->ebufA.as<Edge>() : ctx->ebufB.as<Edge>();
-  if (k + 1 < 16) ctx->stats.level_edges[k + 1] = w.ne_in;
-  WS_CUDA(cudaMemsetAsync(nedges, 0, sizeof(unsigned long long), st));
-  if (w.ne_in > 0) {
+  if (w.E > 0) {
     const int esmem = EHC * 16;
     WS_CUDA(cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
-    k_edges<<<(int)((w.ne_in + ECH - 1) / ECH), NTW, esmem, st>>>(k == 1 ? ctx->edges.as<uint64_t>() : nullptr, ein,
-                                                                  w.ne_in, comp, best, eout, nedges);
+    // one wave of resident CTAs walking the chunks (no partial last wave)
+    static int occ = 0;
+    if (!occ) WS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_edges, NTW, esmem));
+    const long long chunks = (w.E + ECH - 1) / ECH;
+    const int grid = (int)std::min<long long>(chunks, (long long)ctx->num_sms * std::max(1, occ));
+    k_edges<<<grid, NTW, esmem, st>>>(k == 1 ? ctx->edges.as<uint64_t>() : nullptr, ein, w.E,
+                                      k == 1 ? nullptr : cnt + LVC + k, comp, best, eout, cnt + LVC + k + 1);
     launched(ctx, PH_WF_LEVELS);
   }
-  int64_t ne = 0;
-  WS_TRY(read_i64(ctx, nedges, &ne, st));
-  w.ne_in = ne;
   w.eflip = 1 - w.eflip;  // eout becomes the next input
+  return WS_OK;
+}
+
+// host copy of the device level counters of levels 1..k_last; region counts, the last level
+// that merged, per-level edge counts
+static ws_status wf_read_counts(ws_ctx* ctx, int k_last, int64_t* counts, cudaStream_t st) {
+  WSState& w = ctx->wf;
+  static_assert(2 * LVC <= 256, "pinned scratch");
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, ctx->lvcount.p, 2 * LVC * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          st));
+  WS_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long* h = reinterpret_cast<const unsigned long long*>(ctx->pinned);
+  long long prev = w.R;
+  for (int k = 1; k <= k_last && k < LVC; ++k) {
+    const long long c = (long long)h[k];
+    if (c < prev) w.lv = k;
+    prev = c;
+    if (counts) counts[k] = c;
+    if (k < 16) ctx->stats.level_counts[k] = c;
+    if (k >= 2 && k < 16) ctx->stats.level_edges[k] = (long long)h[LVC + k];
+  }
+  w.prev = prev;
+  return WS_OK;
+}
+
+// sharded level step (ws_shard_wf_step): best[] holds all ranks' minima; the count of the
+// level is read back (the host decides whether another level follows)
+static ws_status wf_step(ws_ctx* ctx, int64_t* count, int* more, cudaStream_t st) {
+  WSState& w = ctx->wf;
+  const int k = w.k;
+  if (k >= LVC) {
+    set_error(WS_ERR_LIMIT, "ws_waterfall: more than %d levels", LVC - 1);
+    return WS_ERR_LIMIT;
+  }
+  const long long prev = k == 1 ? w.R : w.prev;
+  WS_TRY(wf_level(ctx, k + 1 < w.NL, st));
+  int64_t c[LVC] = {};
+  WS_TRY(wf_read_counts(ctx, k, c, st));
+  *count = c[k];
+  *more = (k + 1 < w.NL && c[k] > 1 && c[k] < prev) ? 1 : 0;
   return WS_OK;
 }
 
@@ -912,6 +946,10 @@ static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn
 
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn, int NL,
                         int32_t* levels, int64_t* counts, cudaStream_t st) {
+  if (NL > LVC) {
+    set_error(WS_ERR_LIMIT, "ws_waterfall: NL must be <= %d", LVC);
+    return WS_ERR_LIMIT;
+  }
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
   int* dense_of = ctx->aux.as<int>();
@@ -922,18 +960,13 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   if (counts) counts[0] = R;
   ctx->stats.level_counts[0] = R;
   ctx->stats.level_edges[1] = ctx->wf.E;
-  int more = NL > 1 && R > 1;
-  long long cnt = R;
-  for (int k = 1; k < NL; ++k) {
-    if (more) {
-      int64_t c = 0;
-      WS_TRY(wf_step(ctx, &c, &more, st));
-      cnt = c;
-    }
-    if (counts) counts[k] = cnt;
-    if (k < 16) ctx->stats.level_counts[k] = cnt;
-  }
-  return wf_finish(ctx, ctx->dimg.as<int>(), g, conn, levels, st);
+  // all levels are enqueued back to back (a level without merges leaves everything as is);
+  // the counts are read once, after the level arrays are enqueued
+  for (int k = 1; k < NL; ++k) WS_TRY(wf_level(ctx, k + 1 < NL, st));
+  WS_TRY(wf_finish(ctx, ctx->dimg.as<int>(), g, conn, levels, st));
+  if (NL > 1) WS_TRY(wf_read_counts(ctx, NL - 1, counts, st));
+  ctx->stats.waterfall_levels = ctx->wf.lv;
+  return WS_OK;
 }
 
 // ------------------------------------------------------------- z-slab sharded waterfall
