@@ -79,6 +79,7 @@ struct ws_ctx {
   ws::Buf rep_of;     // i32[R]   dense id -> canonical voxel label
   ws::Buf levelmap;   // i32[R*stride]  canonical label of each dense id at levels 0..NL-1
   ws::Buf dimg;       // i32[N]   dense id of every voxel's label (waterfall)
+  ws::Buf rank;       // uint2[N/32+1] dense-id rank structure (k_dense, unsharded)
   ws::Buf lvcount;    // i64[NL]  device-side region counts
   ws::Buf h_grad, h_labels, h_levels;  // device copies used by ws_segment_host
   int64_t* pinned = nullptr;           // small pinned host scratch (flags / counts)

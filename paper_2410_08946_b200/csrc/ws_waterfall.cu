@@ -58,10 +58,14 @@ __device__ __forceinline__ int block_excl_scan(int v, int* smem, int& total) {
 // back over 32 predecessors at a time until an inclusive prefix is found.
 // pofs: label value of a representative at local index 0 (global index of local voxel 0);
 // doff: dense id of this call's first representative (z-slab sharding; 0 / 0 otherwise).
+// rk != nullptr (unsharded): instead of dense_of, the rank structure rk[w] = (dense id of the
+// first representative at or after voxel 32 w, bit mask of the representatives among voxels
+// 32 w .. 32 w + 31) is written: dense(l) = rk[l/32].x + popc(rk[l/32].y & ((1 << l%32) - 1)).
+// It holds 8 bytes per 32 voxels, so the lookups of k_dimage stay in L2.
 __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, int N, int aligned,
                                                 unsigned long long* status, int* ticket, int* __restrict__ dense_of,
                                                 int* __restrict__ rep_of, int rep_cap, long long* R, int pofs,
-                                                int doff) {
+                                                int doff, uint2* __restrict__ rk) {
   __shared__ int sm[32];
   __shared__ int sb;
   __shared__ long long sprefix;
@@ -134,10 +138,14 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
     int d = pre + ex[r];
     uint32_t m = (uint32_t)((fl >> (r * 16)) & 0xffffu);
     const int p0 = b * DCHUNK + r * DROUND + threadIdx.x * 16;
+    if (rk) {  // even thread: voxels 32 w .. 32 w + 15, odd thread: the next 16
+      const uint32_t mo = __shfl_down_sync(0xffffffffu, m, 1);
+      if (!(threadIdx.x & 1) && p0 < N) rk[p0 >> 5] = make_uint2((unsigned)d, m | (mo << 16));
+    }
     while (m) {
       const int u = __ffs(m) - 1;
       m &= m - 1;
-      dense_of[p0 + u + pofs] = d + doff;
+      if (!rk) dense_of[p0 + u + pofs] = d + doff;
       if (d < rep_cap) rep_of[d] = p0 + u + pofs;
       ++d;
     }
@@ -165,6 +173,30 @@ __global__ void __launch_bounds__(NTW) k_dimage(const int* __restrict__ labels, 
   }
   for (long long p = (n4 << 2) + blockIdx.x * (long long)NTW + threadIdx.x; p < n; p += (long long)gridDim.x * NTW)
     D[p] = __ldg(dense_of + labels[p]);
+}
+
+// the same from the rank structure of k_dense (unsharded calls)
+__device__ __forceinline__ int rank_of(const uint2* __restrict__ rk, int l) {
+  const uint2 e = __ldg(rk + (l >> 5));
+  return (int)e.x + __popc(e.y & ((1u << (l & 31)) - 1u));
+}
+
+__global__ void __launch_bounds__(NTW) k_dimage_rk(const int* __restrict__ labels, const uint2* __restrict__ rk,
+                                                    long long n, int* __restrict__ D) {
+  const long long n4 = n >> 2;
+  const int4* L4 = reinterpret_cast<const int4*>(labels);
+  int4* D4 = reinterpret_cast<int4*>(D);
+  for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n4; i += (long long)gridDim.x * NTW) {
+    const int4 v = __ldcs(L4 + i);
+    int4 d;
+    d.x = rank_of(rk, v.x);
+    d.y = v.y == v.x ? d.x : rank_of(rk, v.y);
+    d.z = v.z == v.y ? d.y : rank_of(rk, v.z);
+    d.w = v.w == v.z ? d.z : rank_of(rk, v.w);
+    D4[i] = d;
+  }
+  for (long long p = (n4 << 2) + blockIdx.x * (long long)NTW + threadIdx.x; p < n; p += (long long)gridDim.x * NTW)
+    D[p] = rank_of(rk, labels[p]);
 }
 
 // ------------------------------------------------------------------------ RAG extraction
@@ -537,25 +569,39 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
       tkk[i] = KEY_NONE;
     }
     __syncthreads();
+    // all loads of the chunk first (keys, then the component gathers), then the hash: the
+    // loads of a thread are independent and overlap instead of one round trip per edge
+    constexpr int J = ECH / NTW;
+    uint64_t kk[J];
+    int ca[J], cb[J];
 #pragma unroll
-    for (int j = 0; j < ECH / NTW; ++j) {
+    for (int j = 0; j < J; ++j) {
       const long long e = e0 + threadIdx.x + j * NTW;
-      if (e >= n) break;
-      uint64_t k;
-      int a, b;
-      if (in_keys) {
-        k = in_keys[e];
-        a = (int)key_lo(k);
-        b = (int)key_hi(k);
-      } else {
-        const Edge ed = in[e];
-        k = ed.k;
-        a = ed.a;
-        b = ed.b;
+      kk[j] = KEY_NONE;
+      ca[j] = cb[j] = 0;
+      if (e < n) {
+        if (in_keys) {
+          kk[j] = in_keys[e];
+          ca[j] = (int)key_lo(kk[j]);
+          cb[j] = (int)key_hi(kk[j]);
+        } else {
+          const Edge ed = in[e];
+          kk[j] = ed.k;
+          ca[j] = ed.a;
+          cb[j] = ed.b;
+        }
       }
-      a = __ldg(comp + a);
-      b = __ldg(comp + b);
-      if (a == b) continue;
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      ca[j] = __ldg(comp + ca[j]);
+      cb[j] = __ldg(comp + cb[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int a = ca[j], b = cb[j];
+      const uint64_t k = kk[j];
+      if (k == KEY_NONE || a == b) continue;
       const uint64_t pk = ((uint64_t)(uint32_t)min(a, b) << 32) | (uint32_t)max(a, b);
       uint32_t h = (((uint32_t)(pk >> 32) * 0x9E3779B1u) ^ ((uint32_t)pk * 0x85EBCA77u)) >> 20;  // 12 bits
 #pragma unroll 1
@@ -722,7 +768,7 @@ static ws_status read_i64(ws_ctx* ctx, const void* dptr, int64_t* out, cudaStrea
 
 // dense ids of the representatives among n labels starting at global index pofs
 static ws_status wf_dense(ws_ctx* ctx, const int32_t* labels, int n, int pofs, int doff, int* dense_of,
-                          int64_t* count, cudaStream_t st) {
+                          int64_t* count, cudaStream_t st, uint2* rk = nullptr) {
   const int nb = (n + DCHUNK - 1) / DCHUNK;
   WS_TRY(ctx->blockcnt.ensure((size_t)nb * sizeof(unsigned long long), "scan status"));
   char* fl = ctx->flags.as<char>();
@@ -738,7 +784,7 @@ static ws_status wf_dense(ws_ctx* ctx, const int32_t* labels, int n, int pofs, i
     WS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     k_dense<<<nb, NTW, 0, st>>>(labels, n, !(reinterpret_cast<uintptr_t>(labels) & 15),
                                 ctx->blockcnt.as<unsigned long long>(), ticket, dense_of, ctx->rep_of.as<int>(),
-                                (int)rep_cap, dR, pofs, doff);
+                                (int)rep_cap, dR, pofs, doff, rk);
     launched(ctx, PH_WF_DENSE);
     WS_TRY(read_i64(ctx, dR, count, st));
     if ((size_t)*count <= rep_cap) break;
@@ -786,7 +832,7 @@ static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
 // First the dense-id image D of the owned planes and the plane above (the forward halo) is
 // written into ctx->dimg (same layout as labels).
 static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn,
-                        const int* dense_of, cudaStream_t st) {
+                        const int* dense_of, cudaStream_t st, const uint2* rk = nullptr) {
   unsigned long long* ecount = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 136);
   WS_TRY(ctx->dimg.ensure((size_t)g.N * sizeof(int), "dense-id image"));
   int* D = ctx->dimg.as<int>();
@@ -795,8 +841,13 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
     const size_t o = (size_t)g.zlo * g.plane;
     const long long n = (long long)(z1 - g.zlo) * g.plane;
     const bool al = !(reinterpret_cast<uintptr_t>(labels + o) & 15) && !(reinterpret_cast<uintptr_t>(D + o) & 15);
-    k_dimage<<<grid_for(n / 4 + 1, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, al ? n : 0, D + o);
-    if (!al) k_dimage<<<grid_for(n, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, n, D + o);
+    if (rk) {  // unsharded: the rank structure of k_dense
+      k_dimage_rk<<<grid_for(n / 4 + 1, ctx->num_sms), NTW, 0, st>>>(labels + o, rk, al ? n : 0, D + o);
+      if (!al) k_dimage_rk<<<grid_for(n, ctx->num_sms), NTW, 0, st>>>(labels + o, rk, n, D + o);
+    } else {
+      k_dimage<<<grid_for(n / 4 + 1, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, al ? n : 0, D + o);
+      if (!al) k_dimage<<<grid_for(n, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, n, D + o);
+    }
     launched(ctx, PH_WF_DENSE);
     ctx->wf.dofs = (long long)o;
   }
@@ -954,9 +1005,11 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
   int* dense_of = ctx->aux.as<int>();
   int64_t R = 0;
-  WS_TRY(wf_dense(ctx, labels, g.N, 0, 0, dense_of, &R, st));
+  WS_TRY(ctx->rank.ensure(((size_t)g.N / 32 + 1) * sizeof(uint2), "dense rank structure"));
+  uint2* rk = ctx->rank.as<uint2>();
+  WS_TRY(wf_dense(ctx, labels, g.N, 0, 0, dense_of, &R, st, rk));
   WS_TRY(wf_alloc(ctx, R, NL, st));
-  WS_TRY(wf_rag(ctx, labels, I, g, conn, dense_of, st));
+  WS_TRY(wf_rag(ctx, labels, I, g, conn, dense_of, st, rk));
   if (counts) counts[0] = R;
   ctx->stats.level_counts[0] = R;
   ctx->stats.level_edges[1] = ctx->wf.E;
