@@ -415,11 +415,15 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     if (!minimal && m < v) {
       dir = dm;                               // steepest descent (S = 0)
     } else if (!minimal) {                    // plateau voxel without a lower neighbour
-      dd = sD[sl];
-      if (dd != INF) {                        // non-minimal plateau: BFS parent (C5/C6)
+      // sD holds the raw step II codes: 0 for d = 0, enc(d, DIR_NONE) = -32 d - 32 for a
+      // plateau voxel (INT_MIN = not reached), so the parent test needs no decoding
+      const int Lp = sD[sl];
+      if (Lp != enc(INF, DIR_NONE)) {         // non-minimal plateau: BFS parent (C5/C6)
+        const int want = Lp == enc(1, DIR_NONE) ? 0 : Lp + 32;  // the code of distance d - 1
 #pragma unroll
         for (int i = 0; i < CONN; ++i)
-          if ((eqm & (1u << i)) && sD[sl + T::oL(i)] == dd - 1) dir = i;
+          if ((eqm & (1u << i)) && sD[sl + T::oL(i)] == want) dir = i;
+        if (DEBUG) dd = dec_d(Lp);
       } else {                                // minimal plateau: merged below
         minimal = true;
       }
@@ -496,7 +500,8 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
   } else {
     __syncthreads();
   }
-  // tile-local path reduction: follow in-tile pointers to a root or to the tile exit
+  // tile-local path reduction: follow in-tile pointers to a root or to the tile exit (a
+  // serial walk per voxel measured faster than pointer doubling with block-wide rounds)
   const int base = (int)((size_t)c.bz * g.plane + (size_t)c.by * g.n2 + c.bx);
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
@@ -536,8 +541,7 @@ __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensor
   __shared__ uint64_t bar;
   const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
   if (threadIdx.x == 0) sQn = 0;
-  stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);
-  decode_box<CONN>(sD);
+  stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);  // raw step II codes (no decoding)
   if (tile_interior<CONN>(c, g))
     resolve_body<CONN, DEBUG, false>(sI, sD, sP, sG, sQ, &sQn, &sQb, g, c, P, dist, po);
   else
