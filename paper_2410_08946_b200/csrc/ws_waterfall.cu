@@ -556,22 +556,24 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
                                                 const int* __restrict__ comp, uint64_t* best, Edge* __restrict__ out,
                                                 unsigned long long* nout) {
   extern __shared__ __align__(16) unsigned long long esm[];
-  unsigned long long* tp = esm;        // component pair (lo << 32 | hi)
-  unsigned long long* tkk = esm + EHC;  // min K of the pair
+  unsigned long long* tp = esm;                         // component pair (lo << 32 | hi)
+  unsigned* khi = reinterpret_cast<unsigned*>(esm + EHC);  // min K of the pair: high word,
+  unsigned* klo = khi + EHC;                               // then low word (two 32-bit passes)
   __shared__ int sscan[32];
   __shared__ unsigned long long gbase;
   if (nptr) n = (long long)*nptr;  // device-resident count of the previous level's live edges
   constexpr int M = EHC / NTW;     // thread t owns the consecutive slots M t .. M t + M - 1
+  constexpr int J = ECH / NTW;
 #pragma unroll 1
   for (long long e0 = (long long)blockIdx.x * ECH; e0 < n; e0 += (long long)gridDim.x * ECH) {
     for (int i = threadIdx.x; i < EHC; i += NTW) {
       tp[i] = KEY_NONE;
-      tkk[i] = KEY_NONE;
+      khi[i] = 0xffffffffu;
+      klo[i] = 0xffffffffu;
     }
     __syncthreads();
     // all loads of the chunk first (keys, then the component gathers), then the hash: the
     // loads of a thread are independent and overlap instead of one round trip per edge
-    constexpr int J = ECH / NTW;
     uint64_t kk[J];
     int ca[J], cb[J];
 #pragma unroll
@@ -597,24 +599,32 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
       ca[j] = __ldg(comp + ca[j]);
       cb[j] = __ldg(comp + cb[j]);
     }
+    // pass 1: insert the component pair, fold the high word of K (native 32-bit atomics;
+    // a 64-bit shared atomicMin would be a CAS loop)
+    int slot[J];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const int a = ca[j], b = cb[j];
-      const uint64_t k = kk[j];
-      if (k == KEY_NONE || a == b) continue;
+      slot[j] = -1;
+      if (kk[j] == KEY_NONE || a == b) continue;
       const uint64_t pk = ((uint64_t)(uint32_t)min(a, b) << 32) | (uint32_t)max(a, b);
       uint32_t h = (((uint32_t)(pk >> 32) * 0x9E3779B1u) ^ ((uint32_t)pk * 0x85EBCA77u)) >> 20;  // 12 bits
 #pragma unroll 1
       while (true) {
         unsigned long long cur = tp[h];
         if (cur == KEY_NONE) cur = atomicCAS(tp + h, KEY_NONE, (unsigned long long)pk);
-        if (cur == KEY_NONE || cur == pk) {
-          if (k < tkk[h]) atomicMin(tkk + h, (unsigned long long)k);
-          break;
-        }
+        if (cur == KEY_NONE || cur == pk) break;
         h = (h + 1) & (EHC - 1);  // at most ECH pairs in EHC slots: always terminates
       }
+      slot[j] = (int)h;
+      const unsigned hi = (unsigned)(kk[j] >> 32);
+      if (hi < khi[h]) atomicMin(khi + h, hi);
     }
+    __syncthreads();
+    // pass 2: among the edges with the pair's minimum high word, the minimum low word
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (slot[j] >= 0 && (unsigned)(kk[j] >> 32) == khi[slot[j]]) atomicMin(klo + slot[j], (unsigned)kk[j]);
     __syncthreads();
     int cnt = 0;
 #pragma unroll
@@ -626,11 +636,11 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
     unsigned long long o = gbase + ex;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const int slot = threadIdx.x * M + m;
-      const unsigned long long pk = tp[slot];
+      const int sl = threadIdx.x * M + m;
+      const unsigned long long pk = tp[sl];
       if (pk == KEY_NONE) continue;
       Edge ed;
-      ed.k = tkk[slot];
+      ed.k = ((uint64_t)khi[sl] << 32) | klo[sl];
       ed.a = (int)(pk >> 32);
       ed.b = (int)(pk & 0xffffffffu);
       atomicMin((unsigned long long*)(best + ed.a), (unsigned long long)ed.k);
