@@ -242,7 +242,7 @@ template <int CONN> struct RL {
     return (dz * SY + dy) * SXL + dx;
   }
   static_assert((SXI % 16) == 0 && ((SXL * 4) % 16) == 0, "TMA");
-  static_assert(T::VPT <= 16 && NF <= 16, "record encoding");
+  static_assert(SL <= 4096 && NF <= 16, "record encoding [sl:12][f:4]");
   static constexpr int SIA = (SI + 127) / 128 * 128;           // TMA destinations are 128-byte aligned
   static constexpr int SLA = (4 * SL + 127) / 128 * 128;
   static constexpr int SMEM = SIA + SLA + 12 * HP + 2 * STG;
@@ -264,18 +264,14 @@ __device__ __noinline__ void emit_global(uint64_t k, uint64_t* edges, unsigned l
 // that warp's lane base), or, with wsel < 0, the lists of all warps of the block (counts in
 // wc[], exclusive prefixes in wp[]) spread evenly over all threads.
 template <int CONN>
-__device__ __forceinline__ void fold_rec(unsigned rec, int wbase, const uint8_t* sI, const int* sD,
+__device__ __forceinline__ void fold_rec(unsigned rec, const short* offs, const uint8_t* sI, const int* sD,
                                          unsigned long long* pk, unsigned* pw, uint64_t* edges,
                                          unsigned long long* ecount, long long cap, uint64_t* best) {
   using R = RL<CONN>;
-  const int f = rec & 15, lane = (rec >> 4) & 31, k = rec >> 9;  // [k:4][lane:5][f:4]
-  const int j = wbase + lane + k * NT;
-  const int lx = j % R::TX, ly = (j / R::TX) % R::TY, lz = j / (R::TX * R::TY);
-  int dz, dy, dx;
-  nb_delta(CONN, Conn<CONN>::nfwd + f, dz, dy, dx);
-  const int sl = R::iL(lz, ly, lx), si = R::iI(lz, ly, lx);
-  const uint32_t dp = (uint32_t)sD[sl], dq = (uint32_t)sD[sl + (dz * R::SY + dy) * R::SXL + dx];
-  const unsigned w = max((unsigned)sI[si], (unsigned)sI[si + (dz * R::SY + dy) * R::SXI + dx]);
+  const int sl = rec >> 4, f = rec & 15;  // [sl:12][f:4]: D-box index of p, forward direction
+  const int si = sl + (sl / R::SXL) * (R::SXI - R::SXL) + (R::IXO - R::LXO);  // same voxel in the I box
+  const uint32_t dp = (uint32_t)sD[sl], dq = (uint32_t)sD[sl + offs[f]];
+  const unsigned w = max((unsigned)sI[si], (unsigned)sI[si + offs[16 + f]]);
   const uint32_t lo = min(dp, dq), hi = max(dp, dq);
   const unsigned long long key = ((unsigned long long)lo << 28) | hi;
   uint32_t h = ((lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u)) >> (32 - 10);
@@ -293,16 +289,15 @@ __device__ __forceinline__ void fold_rec(unsigned rec, int wbase, const uint8_t*
 }
 
 template <int CONN>
-__device__ __forceinline__ void fold_warp(const uint16_t* wst, int wcnt, const uint8_t* sI, const int* sD,
-                                          unsigned long long* pk, unsigned* pw, uint64_t* edges,
+__device__ __forceinline__ void fold_warp(const uint16_t* wst, int wcnt, const short* offs, const uint8_t* sI,
+                                          const int* sD, unsigned long long* pk, unsigned* pw, uint64_t* edges,
                                           unsigned long long* ecount, long long cap, uint64_t* best) {
-  const int wbase = threadIdx.x & ~31;
-  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN>(wst[r], wbase, sI, sD, pk, pw, edges, ecount, cap, best);
+  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN>(wst[r], offs, sI, sD, pk, pw, edges, ecount, cap, best);
 }
 
 template <int CONN, bool BORDER>
 __device__ __forceinline__ int rag_pairs(const uint8_t* sI, const int* sD, unsigned long long* pk, unsigned* pw,
-                                          uint16_t* stg, const Geo& g, const TileCoord& c, uint64_t* edges,
+                                          uint16_t* stg, const short* offs, const Geo& g, const TileCoord& c, uint64_t* edges,
                                           unsigned long long* ecount, long long cap, uint64_t* best) {
   using R = RL<CONN>;
   using T = TL<CONN>;
@@ -324,12 +319,12 @@ __device__ __forceinline__ int rag_pairs(const uint8_t* sI, const int* sD, unsig
       const int i = Conn<CONN>::nfwd + f;
       const bool e = ((vm >> i) & 1u) && sD[sl + R::oL(i)] != dp;
       const unsigned b = __ballot_sync(0xffffffffu, e);
-      if (e) wst[wcnt + __popc(b & lt)] = (uint16_t)((k << 9) | (lane << 4) | f);
+      if (e) wst[wcnt + __popc(b & lt)] = (uint16_t)((sl << 4) | f);
       wcnt += __popc(b);
     }
     if (R::MIDFOLD && wcnt > R::WCAP - NF * 32) {
       __syncwarp();
-      fold_warp<CONN>(wst, wcnt, sI, sD, pk, pw, edges, ecount, cap, best);
+      fold_warp<CONN>(wst, wcnt, offs, sI, sD, pk, pw, edges, ecount, cap, best);
       __syncwarp();
       wcnt = 0;
     }
@@ -377,6 +372,11 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
   __shared__ unsigned long long gbase;
   __shared__ int sscan[32];
   __shared__ int wc[NT / 32 + 1];
+  __shared__ short offs[32];  // [f]: D-box offset, [16 + f]: I-box offset of forward direction f
+  if (threadIdx.x < R::NF) {
+    offs[threadIdx.x] = (short)R::oL(Conn<CONN>::nfwd + threadIdx.x);
+    offs[16 + threadIdx.x] = (short)R::oI(Conn<CONN>::nfwd + threadIdx.x);
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (tma && threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -404,8 +404,9 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
       __syncthreads();
     }
     // 1. detection into the per-warp lists
-    const int n = tile_interior<CONN>(c, g) ? rag_pairs<CONN, false>(sI, sD, pk, pw, stg, g, c, edges, ecount, cap, best)
-                                            : rag_pairs<CONN, true>(sI, sD, pk, pw, stg, g, c, edges, ecount, cap, best);
+    const int n = tile_interior<CONN>(c, g)
+                      ? rag_pairs<CONN, false>(sI, sD, pk, pw, stg, offs, g, c, edges, ecount, cap, best)
+                      : rag_pairs<CONN, true>(sI, sD, pk, pw, stg, offs, g, c, edges, ecount, cap, best);
     if (lane == 0) wc[warp] = n;
     __syncthreads();
     // 2. dedup: the records of all warps spread evenly over the block
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
           w = u;
           base = pre[u];
         }
-      fold_rec<CONN>(stg[w * R::WCAP + (r - base)], w * 32, sI, sD, pk, pw, edges, ecount, cap, best);
+      fold_rec<CONN>(stg[w * R::WCAP + (r - base)], offs, sI, sD, pk, pw, edges, ecount, cap, best);
     }
     __syncthreads();  // boxes consumed, hash complete
     const int tn = t + gridDim.x;
