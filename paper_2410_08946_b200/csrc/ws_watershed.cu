@@ -709,6 +709,17 @@ __global__ void k_root_label(int* P, const int* __restrict__ L, const int* __res
     rootc[i] = INT_MAX - L[uf_find(P, roots[i])];
 }
 
+// fast path (unions before the chase): every listed root is final and L[r] already holds
+// INT_MAX - (smallest voxel index of its region); P[r] = -1 - canonical label
+__global__ void k_root_canon(int* P, const int* __restrict__ L, const int* __restrict__ roots, const int* nptr,
+                             int cap) {
+  const int n = min(*nptr, cap);
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+    const int r = roots[i];
+    P[r] = -1 - (INT_MAX - L[r]);
+  }
+}
+
 // P[root] = -1 - canonical label (no finds run any more)
 __global__ void k_root_store(int* P, const int* __restrict__ roots, const int* __restrict__ rootc, int n) {
   for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) P[roots[i]] = -1 - rootc[i];
@@ -821,46 +832,79 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
   launched(ctx, PH_WS_SELECT);
   tmark(ctx, st, PH_WS_SELECT);
 
-  // step III across tiles + root list
+  // step IV Union of the minimal plateaus across tile faces FIRST (k_resolve merged them
+  // inside the tiles and left every minimal voxel pointing at its in-tile root), then step III
+  // across tiles: the chase ends at the FINAL roots, whose minima k_jump folds directly
   size_t cap = ctx->roots.bytes / sizeof(int);
   const size_t want = (size_t)g.N / 16 + 1024;
   if (cap < want) {
     WS_TRY(ctx->roots.ensure(want * sizeof(int), "roots"));
     WS_TRY(ctx->rootc.ensure(want * sizeof(int), "root labels"));
-    cap = want;
+    cap = ctx->roots.bytes / sizeof(int);
   }
   int* nr = ctx->flags.as<int>() + 8;
   unsigned long long* nfinal = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 64);
   WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(nfinal, 0, sizeof(unsigned long long), st));
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, po.npairs, sizeof(int), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaStreamSynchronize(st));
+  const int n_pairs = (int)reinterpret_cast<const int*>(ctx->pinned)[0];
   const int gN = grid1d(g.N, ctx->num_sms);
+  const int* roots = ctx->roots.as<int>();
+  bool fast = n_pairs <= po.cap;
+  if (fast) {
+    if (n_pairs > 0) {
+      k_union_pairs<<<grid1d(n_pairs, ctx->num_sms), NT, 0, st>>>(P, po.pairs, n_pairs);
+      launched(ctx, PH_WS_UNION);
+    }
+    tmark(ctx, st, PH_WS_UNION);
+    k_jump<<<gN, NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
+    launched(ctx, PH_WS_JUMP);
+    tmark(ctx, st, PH_WS_JUMP);
+    k_root_canon<<<grid1d((long long)g.N / 32, ctx->num_sms), NT, 0, st>>>(P, L, roots, nr, (int)cap);
+    launched(ctx, PH_WS_FIND);
+    tmark(ctx, st, PH_WS_FIND);
+    k_relabel<<<gN, NT, 0, st>>>(P, L, g.N);
+    launched(ctx, PH_WS_RELABEL);
+    tmark(ctx, st, PH_WS_RELABEL);
+    WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
+    WS_CUDA(cudaStreamSynchronize(st));
+    const int n_roots = reinterpret_cast<const int*>(ctx->pinned)[0];
+    if ((size_t)n_roots <= cap) {
+      ctx->stats.n_regions = n_roots;
+      if (num_regions) *num_regions = n_roots;
+      WS_CUDA(cudaGetLastError());
+      return WS_OK;
+    }
+    // root list overflow (more than N/16 regions): P no longer holds the roots' self-loops,
+    // so the watershed is redone on the full-scan path below
+    WS_TRY(ctx->roots.ensure((size_t)n_roots * sizeof(int), "roots"));
+    WS_TRY(ctx->rootc.ensure((size_t)n_roots * sizeof(int), "root labels"));
+    return watershed_t<CONN>(ctx, grad, g, L, num_regions, st);
+  }
+  // pair list overflow (near-flat inputs): chase first, then the full q > p union scan, then
+  // merge the per-root minima into the final roots
   k_jump<<<gN, NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
   launched(ctx, PH_WS_JUMP);
-  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));  // nr, -, npairs
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaStreamSynchronize(st));
   const int n_roots = (int)reinterpret_cast<const int*>(ctx->pinned)[0];
-  const int n_pairs = (int)reinterpret_cast<const int*>(ctx->pinned)[2];
   if ((size_t)n_roots > cap) {  // list overflow: grow and rebuild it from P
     WS_TRY(ctx->roots.ensure((size_t)n_roots * sizeof(int), "roots"));
     WS_TRY(ctx->rootc.ensure((size_t)n_roots * sizeof(int), "root labels"));
     WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
     k_collect_roots<<<gN, NT, 0, st>>>(P, g.N, ctx->roots.as<int>(), nr);
     launched(ctx, PH_WS_JUMP);
+    roots = ctx->roots.as<int>();
   }
   tmark(ctx, st, PH_WS_JUMP);
-  if (n_pairs <= po.cap) {
-    if (n_pairs > 0) {
-      k_union_pairs<<<grid1d(n_pairs, ctx->num_sms), NT, 0, st>>>(P, po.pairs, n_pairs);
-      launched(ctx, PH_WS_UNION);
-    }
-  } else {  // pair list overflow (near-flat inputs): the full q > p scan
+  {
     const L3 l = launch3(g);
     k_union<CONN><<<l.grid, l.block, 0, st>>>(grad, P, g);
     launched(ctx, PH_WS_UNION);
   }
   tmark(ctx, st, PH_WS_UNION);
   const int gR = grid1d(n_roots, ctx->num_sms);
-  const int* roots = ctx->roots.as<int>();
   k_root_merge<<<gR, NT, 0, st>>>(P, L, roots, n_roots, nfinal);
   k_root_label<<<gR, NT, 0, st>>>(P, L, roots, n_roots, ctx->rootc.as<int>());
   k_root_store<<<gR, NT, 0, st>>>(P, roots, ctx->rootc.as<int>(), n_roots);
