@@ -870,15 +870,22 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
     WS_TRY(ctx->edges.ensure((size_t)want * sizeof(uint64_t), "edges"));
     cap = want;
   }
+  // The edge count of a congested input varies slightly from run to run (tiles whose pair
+  // hash overflows emit their records directly), so a retry gets headroom and repeats until
+  // the list fits; best[] is reset before every repeat.
   int64_t E = 0;
-  for (int attempt = 0; attempt < 2; ++attempt) {
+  for (int attempt = 0;; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ecount, 0, sizeof(unsigned long long), st));
     WS_TRY(rag(conn, D, I, g, ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), st));
     launched(ctx, PH_WF_RAG);
     WS_TRY(read_i64(ctx, ecount, &E, st));
     if (E <= cap) break;
-    WS_TRY(ctx->edges.ensure((size_t)E * sizeof(uint64_t), "edges"));
-    cap = E;
+    if (attempt >= 4) {
+      set_error(WS_ERR_INTERNAL, "ws_waterfall: edge list does not fit after %d attempts", attempt + 1);
+      return WS_ERR_INTERNAL;
+    }
+    cap = E + E / 4 + 4096;
+    WS_TRY(ctx->edges.ensure((size_t)cap * sizeof(uint64_t), "edges"));
     WS_CUDA(cudaMemsetAsync(ctx->best.p, 0xFF, (size_t)ctx->wf.R * sizeof(uint64_t), st));
   }
   tmark(ctx, st, PH_WF_RAG);

@@ -214,3 +214,21 @@ def test_gradient_sigmas_and_loaders(sigma, shape, ndim, monkeypatch):
     agreed_gradient(raw, sigma, ndim)
     monkeypatch.setenv("WS_NO_TMA", "1")
     agreed_gradient(raw, sigma, ndim)
+
+
+@pytest.mark.parametrize("conn", [6, 26])
+def test_overflow_fallback_paths(conn):
+    """The rare host-side fallbacks of ws_watershed, each against the oracle: i.i.d. noise has
+    more than N/16 regions (root-list overflow: the watershed is redone with a larger list);
+    a constant volume has every tile-face pair on one minimal plateau (cross-tile pair list
+    overflow: full union scan after the chase, then the per-root minima are merged)."""
+    gen = torch.Generator().manual_seed(conn)
+    noise = torch.randint(0, 256, (12, 40, 64), generator=gen, dtype=torch.uint8)
+    const = torch.full((24, 48, 64), 7, dtype=torch.uint8)
+    for g in (noise, const):
+        qn = g.numpy()
+        q = g.cuda()
+        lab, ref = check_watershed(q, qn, conn, 3)
+        if g is noise and conn == 6:
+            assert int(np.unique(ref).size) > ref.size // 16  # the overflow case is exercised
+        check_waterfall(lab, q, qn, ref, conn, 3, 4)
