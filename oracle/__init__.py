@@ -37,7 +37,8 @@ def _load():
         lib.oracle_gradient.argtypes = [vp, i32, i64, i64, i64, dbl, vp, vp, vp]
         lib.oracle_watershed.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp]
         lib.oracle_waterfall.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
-        for f in (lib.oracle_gradient, lib.oracle_watershed, lib.oracle_waterfall):
+        lib.oracle_waterfall_reconstruct.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
+        for f in (lib.oracle_gradient, lib.oracle_watershed, lib.oracle_waterfall, lib.oracle_waterfall_reconstruct):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -106,4 +107,21 @@ def waterfall(labels: np.ndarray, grad: np.ndarray, conn: int, NL: int, ndim: in
                                   _p(counts))
     if rc != 0:
         raise ValueError("oracle_waterfall: invalid arguments")
+    return levels.reshape((NL,) + orig), counts
+
+
+def waterfall_reconstruct(labels: np.ndarray, grad: np.ndarray, conn: int, NL: int, ndim: int = None):
+    """O9, the paper-literal waterfall (Alg. 4 steps V-VI + watershed per layer, Alg. 5):
+    (levels int32 [NL, *shape], counts int64 [NL])."""
+    orig = grad.shape
+    if ndim is None:
+        ndim = 3 if conn in (6, 26) else 2
+    g, (n0, n1, n2) = _shape3(np.asarray(grad, dtype=np.uint8), ndim)
+    lab = np.ascontiguousarray(np.asarray(labels, dtype=np.int32).reshape(g.shape))
+    levels = np.empty((max(NL, 1),) + g.shape, np.int32)
+    counts = np.empty(max(NL, 1), np.int64)
+    rc = _load().oracle_waterfall_reconstruct(_p(lab), _p(g), ndim, n0, n1, n2, int(conn), int(NL), _p(levels),
+                                              _p(counts))
+    if rc != 0:
+        raise ValueError("oracle_waterfall_reconstruct: invalid arguments")
     return levels.reshape((NL,) + orig), counts

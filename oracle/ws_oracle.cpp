@@ -17,6 +17,8 @@
 //                             canonical label = min voxel index (C7)
 //    oracle_waterfall  O6+O7  RAG with per-pair min pass height (Alg. 4 l.2-7),
 //                             strict edge order K (C14), Boruvka levels (C13)
+//    oracle_waterfall_reconstruct  O9  the paper-literal waterfall: newmin + image raise
+//                             (Alg. 4 steps V-VI), watershed re-run per layer (Alg. 5)
 //  Pins (tests/test_oracle_*.py): SciPy/NumPy for O1-O2, closed forms, the paper's worked
 //  examples, literal Alg. 1 on exhaustive tiny images, Kruskal-MST
 //  waterfall, invariants.  No function here is "parity unpinned".
@@ -317,6 +319,51 @@ int oracle_waterfall(const int32_t* labels, const uint8_t* I, int ndim, int64_t 
     for (int64_t r : reps) if (find(r) == r) ++R;
     if (counts) counts[k] = R;
     for (int64_t p = 0; p < N; ++p) levels[(int64_t)k * N + p] = (int32_t)find(labels[p]);
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------------
+// O9: the paper-literal waterfall by image reconstruction (Alg. 4; Alg. 5,
+// P:630-656).  Level 0 = labels on the input image I_0 = I.  Level k
+// (1..NL-1), from I_{k-1} and L_{k-1}:
+//   V  newmin(l) = M, then for every p and q in N(p) with L(q) != L(p):
+//        newmin(L(p)) = min(newmin(L(p)), max(I(p), I(q)))          (Alg. 4 l.1-7)
+//   VI I_k(p) = max(I_{k-1}(p), newmin(L(p)))                        (Alg. 4 l.8-12)
+//   L_k = watershed of I_k (O3-O4: the same definition as level 0)   (Alg. 5 l.4-8)
+// M = 255, the upper bound of the u8 greyscale range ("at least the upper bound";
+// reading C23).  levels[k*N + p] = L_k(p) (canonical labels); counts[k] = #regions.
+// Returns 0 ok, 1 invalid args.
+// ---------------------------------------------------------------------------------
+int oracle_waterfall_reconstruct(const int32_t* labels, const uint8_t* I, int ndim, int64_t n0, int64_t n1,
+                                 int64_t n2, int conn, int NL, int32_t* levels, int64_t* counts) {
+  Grid g{ndim, n0, n1, n2};
+  if (!valid(g, conn) || NL < 1) return 1;
+  const int64_t N = g.N();
+  const int M = 255;
+  std::vector<uint8_t> img(I, I + N);
+  std::vector<int32_t> L(labels, labels + N);
+  int64_t R0 = 0;
+  for (int64_t p = 0; p < N; ++p) {
+    levels[p] = L[p];
+    R0 += L[p] == p;
+  }
+  if (counts) counts[0] = R0;
+  std::vector<int> newmin(N);
+  for (int k = 1; k < NL; ++k) {
+    std::fill(newmin.begin(), newmin.end(), M);  // step V
+    for (int64_t p = 0; p < N; ++p)
+      for (int64_t q : neighbours(g, conn, p)) {
+        if (L[q] == L[p]) continue;
+        const int h = std::max<int>(img[p], img[q]);
+        if (h < newmin[L[p]]) newmin[L[p]] = h;
+      }
+    for (int64_t p = 0; p < N; ++p)  // step VI
+      if (img[p] < newmin[L[p]]) img[p] = (uint8_t)newmin[L[p]];
+    int64_t R = 0;
+    if (oracle_watershed(img.data(), ndim, n0, n1, n2, conn, L.data(), nullptr, nullptr, &R) != 0) return 1;
+    for (int64_t p = 0; p < N; ++p) levels[(int64_t)k * N + p] = L[p];
+    if (counts) counts[k] = R;
   }
   return 0;
 }
