@@ -445,6 +445,25 @@ def run_ours(args):
     step_roof = {"alg_bytes_per_voxel": step_bytes, "achieved_GBps": step_bytes * N / (ms / 1e3) / 1e9,
                  "frac": step_bytes * N / (ms / 1e3) / 1e9 / peak}
 
+    # ---- the paper-literal waterfall (Alg. 4 V-VI + watershed per layer,
+    # Alg. 5) on the same labels, for context: not the metric (outside the timed region)
+    literal = None
+    if not args.no_paper_protocol:
+        lv2 = torch.empty_like(levels)
+        for _ in range(2):
+            _, lc = ws.waterfall(labels, grad, conn, NL, ndim=cfg.ndim, ctx=ctx, out=lv2, mode="reconstruct")
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            _, lc = ws.waterfall(labels, grad, conn, NL, ndim=cfg.ndim, ctx=ctx, out=lv2, mode="reconstruct")
+        e1.record(stream)
+        torch.cuda.synchronize()
+        lms = e0.elapsed_time(e1) / 3
+        literal = {"what": "ws_waterfall_reconstruct, NL=%d, on the step's level-0 labels (Alg. 4 V-VI + Alg. 5)" % NL,
+                   "ms": lms, "Mvoxel_per_s": N / (lms / 1e3) / 1e6, "level_counts": list(lc)}
+        del lv2
+        torch.cuda.empty_cache()
+
     # ---- end to end through the public API with HOST buffers (ws_segment_host)
     e2e = None
     if not args.no_e2e:
@@ -486,6 +505,7 @@ def run_ours(args):
             "gpu_launches": launches, "clocks": clk,
             "gradient_prepass": {"ms": grad_ms, "Mvoxel_per_s": N / (grad_ms / 1e3) / 1e6},
             "paper_protocol_watershed_raw": paper_protocol,
+            "paper_literal_waterfall": literal,
             "phases_ms_per_step": {k: v / args.steps for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
             "input_stats": {"regions": s1["n_regions"], "edges": s2["n_edges"],
                             "plateau_rounds": s1["plateau_rounds"], "level_counts": s2["level_counts"][:NL],

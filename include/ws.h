@@ -138,6 +138,21 @@ ws_status ws_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, 
                        int32_t connectivity, int32_t NL, int32_t* levels, int64_t* counts,
                        void* stream);
 
+/* ws_waterfall_reconstruct — the paper's own waterfall by image reconstruction (Sec. 4,
+ * P:593-656), single GPU.  Level 0 = labels on I_0 = grad; level k = 1..NL-1:
+ *   Step V   newmin(l) = M = 255 (reading C23), then for every p and q in N(p) with
+ *            L(q) != L(p): newmin(L(p)) = min(newmin(L(p)), max(I(p), I(q)))  (Alg. 4 l.1-7)
+ *   Step VI  I_k(p) = max(I_{k-1}(p), newmin(L_{k-1}(p)))                    (Alg. 4 l.8-12)
+ *   then L_k = ws_watershed(I_k) (Alg. 5 l.4-8), canonical labels (C7).
+ *   Unlike the graph waterfall (C13) the layers are NOT nested.
+ * Arguments as ws_waterfall: labels i32[N] (in, canonical ws_watershed output of grad), grad
+ * u8[N] (in, not modified: the raised images live in the context), NL >= 1, levels
+ * i32[NL*N] (out, level-major; levels[0..N) = labels), counts (HOST i64[NL], optional).
+ * Errors: WS_ERR_INVALID (dims/conn/NL, NULL), WS_ERR_LIMIT as ws_watershed. */
+ws_status ws_waterfall_reconstruct(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, ws_dims dims,
+                                   int32_t connectivity, int32_t NL, int32_t* levels, int64_t* counts,
+                                   void* stream);
+
 /* ws_segment_host — the end-to-end user call on HOST buffers: copies grad (host, ideally
  * pinned) to the device, runs ws_watershed + ws_waterfall, copies levels back to the host
  * (host i32[NL*N]).  Device buffers come from the context workspace.  Synchronous. */

@@ -71,8 +71,12 @@ def watershed(grad: torch.Tensor, conn: int, ndim: int = None, ctx: Context = No
 
 
 def waterfall(labels: torch.Tensor, grad: torch.Tensor, conn: int, NL: int, ndim: int = None,
-              ctx: Context = None, out: torch.Tensor = None):
-    """ws_waterfall: levels (int32 [NL, *shape], level 0 = labels) and per-level counts."""
+              ctx: Context = None, out: torch.Tensor = None, mode: str = "graph"):
+    """ws_waterfall: levels (int32 [NL, *shape], level 0 = labels) and per-level counts.
+    mode="graph": the nested graph waterfall (C13); mode="reconstruct": the paper-literal
+    waterfall by image reconstruction (ws_waterfall_reconstruct, Alg. 4 V-VI + Alg. 5)."""
+    if mode not in ("graph", "reconstruct"):
+        raise ValueError("mode must be 'graph' or 'reconstruct'")
     _req(labels, torch.int32, "labels")
     _req(grad, torch.uint8, "grad")
     if labels.shape != grad.shape:
@@ -82,8 +86,9 @@ def waterfall(labels: torch.Tensor, grad: torch.Tensor, conn: int, NL: int, ndim
     levels = out if out is not None else torch.empty((max(int(NL), 1),) + tuple(grad.shape), dtype=torch.int32,
                                                       device=grad.device)
     counts = (ctypes.c_int64 * max(int(NL), 1))()
-    _b.check(_b.load().ws_waterfall(ctx.handle, _b.ptr(labels), _b.ptr(grad), _b.dims_of(grad.shape, ndim),
-                                    int(conn), int(NL), _b.ptr(levels), counts, _b.stream_of(grad)))
+    fn = _b.load().ws_waterfall if mode == "graph" else _b.load().ws_waterfall_reconstruct
+    _b.check(fn(ctx.handle, _b.ptr(labels), _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn), int(NL),
+                _b.ptr(levels), counts, _b.stream_of(grad)))
     return levels, list(counts)
 
 

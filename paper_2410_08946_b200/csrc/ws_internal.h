@@ -80,6 +80,8 @@ struct ws_ctx {
   ws::Buf levelmap;   // i32[R*stride]  canonical label of each dense id at levels 0..NL-1
   ws::Buf dimg;       // i32[N]   dense id of every voxel's label (waterfall)
   ws::Buf rank;       // uint2[N/32+1] dense-id rank structure (k_dense, unsharded)
+  ws::Buf wimg;       // u8[N]    reconstructed image (paper-literal waterfall)
+  ws::Buf nmin;       // u32[N]   255 - newmin per label (paper-literal waterfall)
   ws::Buf lvcount;    // i64[NL]  device-side region counts
   ws::Buf h_grad, h_labels, h_levels;  // device copies used by ws_segment_host
   int64_t* pinned = nullptr;           // small pinned host scratch (flags / counts)
@@ -147,6 +149,8 @@ ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, 
 
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g,
                         int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
+ws_status run_waterfall_reconstruct(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g, int conn,
+                                    int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
 
 // TMA tensor map for a row-major (n0, n1, n2) array of `esize`-byte elements with box
 // {bx, by, bz} (x fastest).  Returns false when the layout cannot be described (global
@@ -158,6 +162,14 @@ bool encode_tmap_3d(void* map /* CUtensorMap* */, int esize, const void* base, c
 struct L3 {
   dim3 grid, block;
 };
+#define ZLOOP_BEGIN_R                                                       \
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;                      \
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;                      \
+  if (x >= g.n2 || y >= g.n1) return;                                       \
+  for (int z = blockIdx.z; z < g.n0; z += gridDim.z) {                      \
+    const int p = z * g.plane + y * g.n2 + x;
+#define ZLOOP_END_R }
+
 inline L3 launch3(const Geo& g, int bx = 32, int by = 8) {
   L3 l;
   l.block = dim3(bx, by, 1);

@@ -232,3 +232,36 @@ def test_overflow_fallback_paths(conn):
         if g is noise and conn == 6:
             assert int(np.unique(ref).size) > ref.size // 16  # the overflow case is exercised
         check_waterfall(lab, q, qn, ref, conn, 3, 4)
+
+
+@pytest.mark.parametrize("conn,ndim,shape,levels", [(4, 2, (2, 45, 61), 6), (8, 2, (1, 70, 90), 10),
+                                                    (6, 3, (11, 37, 70), 8), (26, 3, (9, 21, 35), 16),
+                                                    (4, 2, (1, 1, 300), 5)])
+def test_waterfall_reconstruct_parity(conn, ndim, shape, levels):
+    """ws_waterfall_reconstruct (paper-literal Alg. 4 V-VI + Alg. 5) vs oracle O9: every layer
+    bit-exact, counts equal; the input gradient is left untouched."""
+    ws = _ws()
+    g = synth.random_plateau_image(shape, levels, seed=conn + levels)
+    qn = g.numpy()
+    q = g.cuda()
+    lab, ref = check_watershed(q, qn, conn, ndim)
+    NL = 6
+    lv, counts = ws.waterfall(lab, q, conn, NL, ndim=ndim, mode="reconstruct")
+    rlv, rcounts = oracle.waterfall_reconstruct(ref, qn, conn, NL, ndim=ndim)
+    got = lv.cpu().numpy()
+    for k in range(NL):
+        assert np.array_equal(got[k], rlv[k]), "reconstruct level %d" % k
+    assert list(counts) == [int(c) for c in rcounts]
+    assert np.array_equal(q.cpu().numpy(), qn)
+
+
+def test_waterfall_reconstruct_config_c1():
+    """C1 (cameraman-like, sigma 1, 4-conn, NL=6) through the literal reconstruction."""
+    ws = _ws()
+    raw = synth.make_config_image("C1", device="cuda").cpu().numpy()
+    q, qn = agreed_gradient(raw, 1.0, 2)
+    lab, ref = check_watershed(q, qn, 4, 2)
+    lv, counts = ws.waterfall(lab, q, 4, 6, ndim=2, mode="reconstruct")
+    rlv, rcounts = oracle.waterfall_reconstruct(ref, qn, 4, 6, ndim=2)
+    assert np.array_equal(lv.cpu().numpy(), rlv)
+    assert list(counts) == [int(c) for c in rcounts]
