@@ -464,6 +464,28 @@ def run_ours(args):
         del lv2
         torch.cuda.empty_cache()
 
+    # ---- the paper's own one-thread-per-voxel watershed kernels on the same gradient (SURVEY
+    # NEXT f3: the baseline design the tiled ws_watershed replaces), for context
+    variants = None
+    if not args.no_paper_protocol:
+        variants = {"what": "ws_watershed_variant on the step's gradient, same partition as ws_watershed",
+                    "tiled_ws_watershed_ms": sum(v for k, v in phase_ms.items() if k.startswith("watershed.")) / args.steps}
+        lab_v = torch.empty_like(labels)
+        for vname in ("pruf_sync", "prw_sync", "apruf_sync"):
+            ws.watershed(grad, conn, ndim=cfg.ndim, ctx=ctx, out=lab_v, variant=vname)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(2):
+                _, Rv = ws.watershed(grad, conn, ndim=cfg.ndim, ctx=ctx, out=lab_v, variant=vname)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            vms = e0.elapsed_time(e1) / 2
+            variants[vname] = {"ms": vms, "Mvoxel_per_s": N / (vms / 1e3) / 1e6, "regions": Rv,
+                               "same_labels": bool(torch.equal(lab_v, labels)),
+                               "step2_rounds": ctx.stats()["plateau_rounds"]}
+        del lab_v
+        torch.cuda.empty_cache()
+
     # ---- end to end through the public API with HOST buffers (ws_segment_host)
     e2e = None
     if not args.no_e2e:
@@ -506,6 +528,7 @@ def run_ours(args):
             "gradient_prepass": {"ms": grad_ms, "Mvoxel_per_s": N / (grad_ms / 1e3) / 1e6},
             "paper_protocol_watershed_raw": paper_protocol,
             "paper_literal_waterfall": literal,
+            "paper_kernel_variants": variants,
             "phases_ms_per_step": {k: v / args.steps for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
             "input_stats": {"regions": s1["n_regions"], "edges": s2["n_edges"],
                             "plateau_rounds": s1["plateau_rounds"], "level_counts": s2["level_counts"][:NL],

@@ -123,6 +123,21 @@ ws_status ws_gradient(ws_ctx* ctx, const uint8_t* img, ws_dims dims, float sigma
 ws_status ws_watershed(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity,
                        int32_t* labels, int64_t* num_regions, void* stream);
 
+/* ws_watershed_variant — the paper's own one-thread-per-voxel watershed kernels (SURVEY NEXT
+ * f3), the baseline for the tiled ws_watershed; every variant yields the same partition
+ * and the same canonical labels (C7):
+ *   WS_VARIANT_PRUF_SYNC   Alg. 1 as written: step I, Jacobi step II (S -> S',
+ *                          host loop until no change), step III by RR = 6 jumps
+ *                          per launch until no change, step IV Union + Find.
+ *   WS_VARIANT_PRW_SYNC    step IV of Alg. 2: min-merging of representatives +
+ *                          path reduction, repeated until no change.
+ *   WS_VARIANT_APRUF_SYNC  step III replaced by one independent Find per voxel.
+ * Arguments as ws_watershed; errors as ws_watershed plus WS_ERR_INVALID for an unknown
+ * variant. */
+enum { WS_VARIANT_PRUF_SYNC = 0, WS_VARIANT_PRW_SYNC = 1, WS_VARIANT_APRUF_SYNC = 2 };
+ws_status ws_watershed_variant(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity,
+                               int32_t variant, int32_t* labels, int64_t* num_regions, void* stream);
+
 /* ws_waterfall — the hierarchical segmentation as the graph waterfall (C13):
  *   RAG edges {a, b} between adjacent regions with height max(I(p), I(q)), per pair
  *   the minimum (Alg. 4 l.2-7); strict edge order K = (w asc, max(a,b) desc, min(a,b) desc)

@@ -57,16 +57,28 @@ def gradient(img: torch.Tensor, sigma: float = 1.0, ndim: int = None, verify: bo
     return (q, blur, grad) if verify else q
 
 
+VARIANTS = {"pruf_sync": 0, "prw_sync": 1, "apruf_sync": 2}
+
+
 def watershed(grad: torch.Tensor, conn: int, ndim: int = None, ctx: Context = None,
-              out: torch.Tensor = None):
-    """ws_watershed: canonical labels (int32, shaped like grad) and the region count R."""
+              out: torch.Tensor = None, variant: str = None):
+    """ws_watershed: canonical labels (int32, shaped like grad) and the region count R.
+    variant="pruf_sync" | "prw_sync" | "apruf_sync": the paper's one-thread-per-voxel kernels
+    (ws_watershed_variant, Alg. 1 / Alg. 2 / APRUF) instead of the tiled design."""
     _req(grad, torch.uint8, "grad")
     ndim = _ndim_for(conn, ndim)
     ctx = ctx or default_context(grad.device.index)
     labels = out if out is not None else torch.empty(grad.shape, dtype=torch.int32, device=grad.device)
     R = ctypes.c_int64(0)
-    _b.check(_b.load().ws_watershed(ctx.handle, _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn),
-                                    _b.ptr(labels), ctypes.byref(R), _b.stream_of(grad)))
+    if variant is None:
+        _b.check(_b.load().ws_watershed(ctx.handle, _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn),
+                                        _b.ptr(labels), ctypes.byref(R), _b.stream_of(grad)))
+    else:
+        if variant not in VARIANTS:
+            raise ValueError("variant must be one of %s" % sorted(VARIANTS))
+        _b.check(_b.load().ws_watershed_variant(ctx.handle, _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn),
+                                                VARIANTS[variant], _b.ptr(labels), ctypes.byref(R),
+                                                _b.stream_of(grad)))
     return labels, R.value
 
 

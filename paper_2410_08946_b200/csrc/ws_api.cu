@@ -224,7 +224,7 @@ ws_status ws_ctx_destroy(ws_ctx* ctx) {
   cudaSetDevice(ctx->device);
   ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->tiles, &ctx->roots, &ctx->rootc, &ctx->blockcnt, &ctx->edges, &ctx->ebufA, &ctx->ebufB, &ctx->rootsA, &ctx->rootsB, &ctx->lvl,
                      &ctx->comp, &ctx->best, &ctx->rep_of, &ctx->levelmap, &ctx->lvcount,
-                     &ctx->h_grad, &ctx->h_labels, &ctx->h_levels, &ctx->dimg, &ctx->rank, &ctx->wimg, &ctx->nmin, &ctx->tlist, &ctx->upairs, &ctx->exitmx,
+                     &ctx->h_grad, &ctx->h_labels, &ctx->h_levels, &ctx->dimg, &ctx->rank, &ctx->wimg, &ctx->vstate, &ctx->nmin, &ctx->tlist, &ctx->upairs, &ctx->exitmx,
                      &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap};
   for (auto* b : bufs) b->release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -301,6 +301,25 @@ ws_status ws_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, 
   begin_call(ctx, g);
   tbegin(ctx, (cudaStream_t)stream);
   ws_status s = run_waterfall(ctx, labels, grad, g, connectivity, NL, levels, counts, (cudaStream_t)stream);
+  tfinish(ctx);
+  return s;
+}
+
+ws_status ws_watershed_variant(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity, int32_t variant,
+                               int32_t* labels, int64_t* num_regions, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  WS_TRY(check_conn(dims, connectivity));
+  if (variant != WS_VARIANT_PRUF_SYNC && variant != WS_VARIANT_PRW_SYNC && variant != WS_VARIANT_APRUF_SYNC) {
+    set_error(WS_ERR_INVALID, "unknown watershed variant %d", variant);
+    return WS_ERR_INVALID;
+  }
+  if (!grad) return null_arg("grad");
+  if (!labels) return null_arg("labels");
+  begin_call(ctx, g);
+  tbegin(ctx, (cudaStream_t)stream);
+  ws_status s = run_watershed_variant(ctx, grad, g, connectivity, variant, labels, num_regions, (cudaStream_t)stream);
   tfinish(ctx);
   return s;
 }

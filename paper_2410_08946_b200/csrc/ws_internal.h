@@ -81,6 +81,7 @@ struct ws_ctx {
   ws::Buf dimg;       // i32[N]   dense id of every voxel's label (waterfall)
   ws::Buf rank;       // uint2[N/32+1] dense-id rank structure (k_dense, unsharded)
   ws::Buf wimg;       // u8[N]    reconstructed image (paper-literal waterfall)
+  ws::Buf vstate;     // u8[2N]   states S, S' of the paper's one-thread-per-voxel variants
   ws::Buf nmin;       // u32[N]   255 - newmin per label (paper-literal waterfall)
   ws::Buf lvcount;    // i64[NL]  device-side region counts
   ws::Buf h_grad, h_labels, h_levels;  // device copies used by ws_segment_host
@@ -149,6 +150,8 @@ ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, 
 
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g,
                         int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
+ws_status run_watershed_variant(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int variant,
+                                int32_t* labels, int64_t* num_regions, cudaStream_t st);
 ws_status run_waterfall_reconstruct(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g, int conn,
                                     int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
 

@@ -265,3 +265,19 @@ def test_waterfall_reconstruct_config_c1():
     rlv, rcounts = oracle.waterfall_reconstruct(ref, qn, 4, 6, ndim=2)
     assert np.array_equal(lv.cpu().numpy(), rlv)
     assert list(counts) == [int(c) for c in rcounts]
+
+
+@pytest.mark.parametrize("variant", ["pruf_sync", "prw_sync", "apruf_sync"])
+@pytest.mark.parametrize("conn,ndim,shape,levels", [(4, 2, (2, 45, 61), 3), (8, 2, (1, 70, 90), 5),
+                                                    (6, 3, (11, 37, 70), 4), (26, 3, (9, 21, 35), 3),
+                                                    (4, 2, (1, 1, 300), 2), (6, 3, (7, 19, 23), 16)])
+def test_paper_variants_parity(variant, conn, ndim, shape, levels):
+    """The paper's own one-thread-per-voxel kernels (Alg. 1 PRUF_sync, Alg. 2 PRW step IV,
+    APRUF step III) give the oracle's partition and canonical labels exactly."""
+    ws = _ws()
+    g = synth.random_plateau_image(shape, levels, seed=conn * 7 + levels)
+    qn = g.numpy()
+    lab, R = ws.watershed(g.cuda(), conn, ndim=ndim, variant=variant)
+    ref, _, _, Rref = oracle.watershed(qn, conn, ndim=ndim, dumps=True)
+    assert np.array_equal(lab.cpu().numpy(), ref)
+    assert R == Rref
