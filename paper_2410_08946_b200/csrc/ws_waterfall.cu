@@ -995,6 +995,8 @@ static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn
   tmark(ctx, st, PH_WF_LEVELS);
   const int N = g.N;
   const int gN = grid_for(N, ctx->num_sms);
+  // (a linear 4-voxels-per-thread variant with 16-byte stores measured 6.0 vs 4.7 ms on C4:
+  // the tiled kernel shares each gathered row across the lanes of a run and along z)
   if (stride == 4 || stride == 8) {
     const bool is3d = (conn == 6 || conn == 26);
     const int TX = is3d ? TL<6>::TX : TL<4>::TX, TY = is3d ? TL<6>::TY : TL<4>::TY, TZ = is3d ? TL<6>::TZ : TL<4>::TZ;
