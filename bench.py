@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-paper-protocol", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=32)
     ap.add_argument("--ref-sample-slices", type=int, default=4)
     return ap.parse_args()
@@ -410,7 +411,9 @@ def run_ours(args):
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     phase_ms, phase_launch, launches, stats = {}, {}, 0, []
-    for _ in range(args.steps):
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    for i in range(args.steps):
+        step_ev[i].record(stream)
         s1, s2 = step()
         stats.append((s1, s2))
         for s in (s1, s2):
@@ -418,12 +421,16 @@ def run_ours(args):
             for k, v in s["phases"].items():
                 phase_ms[k] = phase_ms.get(k, 0.0) + v["ms"]
                 phase_launch[k] = phase_launch.get(k, 0) + v["launches"]
+    step_ev[args.steps].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     clk = clocks.stop()
     ctx.set_timing(False)
     ms_local = t_start.elapsed_time(t_end) / args.steps
+    per_step = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
+    step_stats = {"mean": ms_local, "min": min(per_step), "median": statistics.median(per_step),
+                  "note": "per-step CUDA events inside the timed region; min = the paper's protocol (P:742)"}
     ms = max_over_ranks(ms_local, world)
     value = N * world / (ms / 1e3) / 1e6
 
@@ -486,6 +493,52 @@ def run_ours(args):
         del lab_v
         torch.cuda.empty_cache()
 
+    # ---- the other configs of BASELINE.json at full size, one GPU (SURVEY §8(d) "also
+    # reported"): gradient pre-pass timed separately, then the step; min and median of 5
+    others = None
+    if world == 1 and not args.no_other_configs and args.shape is None and cfg.name == "C4":
+        others = {}
+        del labels, levels
+        torch.cuda.empty_cache()
+        for name in ("C1", "C2", "C3", "C5"):
+            oc = synth.CONFIGS[name]
+            oraw = synth.make_config_image(name, device=dev)
+            og = torch.empty_like(oraw)
+            for _ in range(2):
+                ws.gradient(oraw, oc.sigma, ndim=oc.ndim, ctx=ctx, out=og)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(3):
+                ws.gradient(oraw, oc.sigma, ndim=oc.ndim, ctx=ctx, out=og)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            gms = e0.elapsed_time(e1) / 3
+            olab = torch.empty(oraw.shape, dtype=torch.int32, device=dev)
+            olev = torch.empty((oc.NL,) + tuple(oraw.shape), dtype=torch.int32, device=dev)
+            for _ in range(2):
+                ws.watershed(og, oc.conn, ndim=oc.ndim, ctx=ctx, out=olab)
+                ws.waterfall(olab, og, oc.conn, oc.NL, ndim=oc.ndim, ctx=ctx, out=olev)
+            torch.cuda.synchronize()
+            times = []
+            for _ in range(5):
+                e0.record(stream)
+                _, oR = ws.watershed(og, oc.conn, ndim=oc.ndim, ctx=ctx, out=olab)
+                _, ocounts = ws.waterfall(olab, og, oc.conn, oc.NL, ndim=oc.ndim, ctx=ctx, out=olev)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+            on = oraw.numel()
+            med = statistics.median(times)
+            others[name] = {"workload": oc.desc, "shape": list(oraw.shape), "conn": oc.conn, "NL": oc.NL,
+                            "gradient_ms": gms, "step_ms_min": min(times), "step_ms_median": med,
+                            "Mvoxel_per_s": on / (med / 1e3) / 1e6,
+                            "Mvoxel_per_s_incl_gradient": on / ((med + gms) / 1e3) / 1e6,
+                            "regions": oR, "level_counts": list(ocounts)}
+            del oraw, og, olab, olev
+            torch.cuda.empty_cache()
+        labels = torch.empty(shape, dtype=torch.int32, device=dev)
+        levels = torch.empty((NL,) + tuple(shape), dtype=torch.int32, device=dev)
+
     # ---- end to end through the public API with HOST buffers (ws_segment_host)
     e2e = None
     if not args.no_e2e:
@@ -529,6 +582,8 @@ def run_ours(args):
             "paper_protocol_watershed_raw": paper_protocol,
             "paper_literal_waterfall": literal,
             "paper_kernel_variants": variants,
+            "step_ms": step_stats,
+            "other_configs": others,
             "phases_ms_per_step": {k: v / args.steps for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
             "input_stats": {"regions": s1["n_regions"], "edges": s2["n_edges"],
                             "plateau_rounds": s1["plateau_rounds"], "level_counts": s2["level_counts"][:NL],
