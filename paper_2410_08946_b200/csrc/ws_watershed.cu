@@ -828,7 +828,7 @@ static ws_status plateau_phase(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
 // cross-tile step IV pair list of k_resolve: ctx->upairs, counter at flags int 10
 static ws_status pair_out(ws_ctx* ctx, const Geo& g, PairOut& po, cudaStream_t st) {
   const size_t own = (size_t)(g.zhi - g.zlo) * g.plane;
-  const size_t want = own / 64 + 65536;
+  const size_t want = own / 8 + 65536;  // plateau-heavy volumes (C3 air) have many face pairs
   if (ctx->upairs.bytes / sizeof(int2) < want) WS_TRY(ctx->upairs.ensure(want * sizeof(int2), "union pairs"));
   WS_TRY(ctx->flags.ensure(256, "flags"));
   po.pairs = ctx->upairs.as<int2>();
@@ -873,7 +873,10 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
   const int n_pairs = (int)reinterpret_cast<const int*>(ctx->pinned)[0];
   const int gN = grid1d(g.N, ctx->num_sms);
   const int* roots = ctx->roots.as<int>();
-  bool fast = n_pairs <= po.cap;
+  // Unions before the chase put every voxel of a region on its FINAL root; for a giant
+  // minimal plateau (many cross-tile pairs, e.g. the air of C3) the chase's per-root minimum
+  // atomics would then all hit one address, so such inputs chase first and union after
+  bool fast = n_pairs <= po.cap && (long long)n_pairs <= (long long)g.N / 64;
   if (fast) {
     if (n_pairs > 0) {
       k_union_pairs<<<grid1d(n_pairs, ctx->num_sms), NT, 0, st>>>(P, po.pairs, n_pairs);
@@ -907,8 +910,9 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
     WS_TRY(ctx->rootc.ensure((size_t)n_roots * sizeof(int), "root labels"));
     return watershed_t<CONN>(ctx, grad, g, L, num_regions, st);
   }
-  // pair list overflow (near-flat inputs): chase first, then the full q > p union scan, then
-  // merge the per-root minima into the final roots
+  // many cross-tile pairs: chase first (per-root minima on the tiles' roots), then the union
+  // (the pair list, or the full q > p scan when it overflowed), then merge the minima into
+  // the final roots
   k_jump<<<gN, NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
   launched(ctx, PH_WS_JUMP);
   WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -923,7 +927,12 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
     roots = ctx->roots.as<int>();
   }
   tmark(ctx, st, PH_WS_JUMP);
-  {
+  if (n_pairs <= po.cap) {
+    if (n_pairs > 0) {
+      k_union_pairs<<<grid1d(n_pairs, ctx->num_sms), NT, 0, st>>>(P, po.pairs, n_pairs);
+      launched(ctx, PH_WS_UNION);
+    }
+  } else {
     const L3 l = launch3(g);
     k_union<CONN><<<l.grid, l.block, 0, st>>>(grad, P, g);
     launched(ctx, PH_WS_UNION);
