@@ -95,7 +95,9 @@ class LocalTransport:
 
 
 class DistTransport:
-    """One rank per process over torch.distributed (NCCL on GPUs; gloo on CPU)."""
+    """One rank per process over torch.distributed (NCCL on GPUs; gloo on CPU).  With gloo,
+    device tensors are staged through host memory (a functional test of the multi-process
+    path when several ranks share one GPU; NCCL refuses that)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -104,11 +106,15 @@ class DistTransport:
         self.rank = dist.get_rank(group)
         self.K = dist.get_world_size(group)
         self.held = [self.rank]
+        self.host = dist.get_backend(group) == "gloo"
+
+    def _out(self, t):
+        return t.cpu() if (self.host and t is not None) else t
 
     def exchange(self, send_lo, send_hi):
         dist = self.dist
         r, K = self.rank, self.K
-        lo, hi = send_lo[0], send_hi[0]
+        lo, hi = self._out(send_lo[0]), self._out(send_hi[0])
         ref = lo if lo is not None else hi
         below = torch.empty_like(ref) if r > 0 else None
         above = torch.empty_like(ref) if r < K - 1 else None
@@ -122,10 +128,18 @@ class DistTransport:
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        dev = (send_lo[0] if send_lo[0] is not None else send_hi[0]).device
+        if self.host:
+            below = below.to(dev) if below is not None else None
+            above = above.to(dev) if above is not None else None
         return [below], [above]
 
     def allgather(self, xs):
         x = xs[0].reshape(-1)
+        if self.host:
+            parts = [torch.empty_like(x, device="cpu") for _ in range(self.K)]
+            self.dist.all_gather(parts, x.cpu(), group=self.group)
+            return [torch.cat(parts).to(x.device)]
         out = torch.empty(self.K * x.numel(), dtype=x.dtype, device=x.device)
         self.dist.all_gather_into_tensor(out, x, group=self.group)
         return [out]
@@ -143,13 +157,20 @@ class DistTransport:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return bool(t.item())
 
-    def allreduce_min(self, xs):
-        self.dist.all_reduce(xs[0], op=self.dist.ReduceOp.MIN, group=self.group)
+    def _allreduce(self, xs, op):
+        if self.host and xs[0].is_cuda:
+            h = xs[0].cpu()
+            self.dist.all_reduce(h, op=op, group=self.group)
+            xs[0].copy_(h)
+        else:
+            self.dist.all_reduce(xs[0], op=op, group=self.group)
         return xs
 
+    def allreduce_min(self, xs):
+        return self._allreduce(xs, self.dist.ReduceOp.MIN)
+
     def allreduce_max(self, xs):
-        self.dist.all_reduce(xs[0], op=self.dist.ReduceOp.MAX, group=self.group)
-        return xs
+        return self._allreduce(xs, self.dist.ReduceOp.MAX)
 
 
 # ------------------------------------------------------------------------ watershed
