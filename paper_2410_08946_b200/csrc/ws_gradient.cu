@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) k_grad_stream(const uint8_t* __restrict__
   constexpr int AX = GSX + 2, AXP = (AX + 3) / 4 * 4, BY = GSY + 2, PL = BY * AX;
   constexpr int RG = 3, NRG = BY / RG;  // a y/z thread owns RG consecutive rows of one column
   static_assert(BY % RG == 0 && AX * NRG <= 256, "y/z thread layout");
-  __shared__ __align__(16) uint8_t sIn[SY * SX];
+  __shared__ __align__(16) uint8_t sIn[SY * SX + 16];  // +16: the last x-blur group reads past the row (padding outputs)
   __shared__ float X[SY * AXP];
   __shared__ float B[3 * PL];
   const int t0 = blockIdx.x;

@@ -419,7 +419,7 @@ ws_status shard_local(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, 
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->exitmx.ensure((size_t)2 * g.plane * sizeof(int), "exit minima"));
   int* nr = ctx->flags.as<int>() + 8;
-  WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
+  WS_CUDA(cudaMemsetAsync(nr, 0, 2 * sizeof(int), st));  // [0] roots, [1] unused ([2] = pairs, set by pair_out)
   WS_CUDA(cudaMemsetAsync(ctx->exitmx.p, 0, (size_t)2 * g.plane * sizeof(int), st));
   const int gN = grid_s((long long)own, ctx->num_sms);
   k_jump_shard<<<gN, NTS, 0, st>>>(P, L, g, ctx->exitmx.as<int>(), ctx->roots.as<int>(), (int)cap, nr);

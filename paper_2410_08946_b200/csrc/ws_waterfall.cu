@@ -665,6 +665,7 @@ __global__ void k_levelmap(const int* __restrict__ comp, const uint8_t* __restri
       while (__ldg(lvl + x) <= k) x = __ldg(comp + x);
       row[k] = __ldg(rep_of + x);
     }
+    for (int k = NL; k < stride; ++k) row[k] = 0;  // padding of the row (read by 16-byte loads)
   }
 }
 

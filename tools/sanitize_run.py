@@ -1,0 +1,33 @@
+"""Small end-to-end run for compute-sanitizer: C1 and a small C4-like volume through
+ws_gradient -> ws_watershed -> ws_waterfall (graph and reconstruct), the paper's variants and the
+sharded path with a local transport; parity against the oracle at the end."""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import oracle
+import synth
+import paper_2410_08946_b200 as ws
+from paper_2410_08946_b200 import shard
+
+for name, shape, conn, nd in (("C1", None, 4, 2), ("C4", (20, 48, 64), 6, 3)):
+    raw = synth.make_config_image(name, device="cuda", shape=shape)
+    q = ws.gradient(raw, 1.0, ndim=nd)
+    lab, R = ws.watershed(q, conn, ndim=nd)
+    lv, c = ws.waterfall(lab, q, conn, 6, ndim=nd)
+    lv2, c2 = ws.waterfall(lab, q, conn, 6, ndim=nd, mode="reconstruct")
+    lab3, _ = ws.watershed(q, conn, ndim=nd, variant="prw_sync")
+    qn = q.cpu().numpy()
+    ref = oracle.watershed(qn, conn, ndim=nd)
+    assert np.array_equal(lab.cpu().numpy(), ref) and np.array_equal(lab3.cpu().numpy(), ref)
+    assert np.array_equal(lv.cpu().numpy(), oracle.waterfall(ref, qn, conn, 6, ndim=nd)[0])
+    assert np.array_equal(lv2.cpu().numpy(), oracle.waterfall_reconstruct(ref, qn, conn, 6, ndim=nd)[0])
+    if nd == 3:
+        K = 3
+        slabs = shard.make_slabs(q.shape[0], K)
+        tr = shard.LocalTransport(K)
+        ctxs = [ws.Context() for _ in range(K)]
+        grads = [q[s.e0:s.e1].contiguous() for s in slabs]
+        labs, levs, counts, Rs, _ = shard.sharded_segment(tr, ctxs, slabs, grads, 6, conn)
+        assert np.array_equal(torch.cat(labs).cpu().numpy(), ref)
+    print(name, "ok", R, c, c2)
