@@ -1,7 +1,7 @@
 # quick GPU iteration: parity tests + a short bench (no e2e / cpu baseline)
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/q_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/q_pytest.log
 tail -3 gpurun_out/q_pytest.log
-timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-paper-protocol $BENCH_ARGS > gpurun_out/q_bench.log 2>&1
+timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-paper-protocol --no-other-configs $BENCH_ARGS > gpurun_out/q_bench.log 2>&1
 python - <<'PY'
 import json
 for l in open('gpurun_out/q_bench.log'):

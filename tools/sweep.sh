@@ -2,7 +2,7 @@
 name=$1; shift
 for v in "$@"; do
   export $name=$v
-  timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-paper-protocol > gpurun_out/sw_$v.log 2>&1
+  timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-paper-protocol --no-other-configs > gpurun_out/sw_$v.log 2>&1
   python -c "
 import json
 for l in open('gpurun_out/sw_$v.log'):
