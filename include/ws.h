@@ -250,8 +250,12 @@ ws_status ws_shard_wf_bfill(ws_ctx* ctx, const int32_t* btables_all, int32_t nra
 ws_status ws_shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* grad_ext, ws_dims dims_ext,
                             int32_t connectivity, ws_slab slab, const int32_t* dense_of, int64_t R, int32_t NL,
                             int64_t* best_out, void* stream);
-/* one level: best_in = all ranks' minima (reduced); count (HOST) = regions after the level;
- * more (HOST) = 1 if another level follows, then best_out = this rank's minima for it */
+/* one level: best_in = all ranks' minima (reduced) of the current components -- level 1: all R
+ * regions in dense-id order (ws_shard_wf_begin's output); later levels: the previous level's
+ * roots in increasing dense id (the same order on every rank: the union-find is replicated);
+ * count (HOST) = regions after the level; more (HOST) = 1 if another level follows, then
+ * best_out[0..count) = this rank's minima at this level's roots in increasing dense id
+ * (best_out must hold the previous count) */
 ws_status ws_shard_wf_step(ws_ctx* ctx, const int64_t* best_in, int64_t* best_out, int64_t* count, int32_t* more,
                            void* stream);
 /* level maps + the NL level arrays of the owned voxels: levels_own i32[NL][(z1-z0)*n1*n2] */

@@ -47,6 +47,7 @@ struct Buf {
 struct WSState {
   int64_t R = 0, E = 0, ne_in = 0, nr_in = 0, prev = 0;
   long long dofs = 0;  // offset of the owned planes in ctx->dimg
+  long long sorted_n = 0;  // sharded: length of the exchanged minima (current roots, sorted)
   int NL = 1, stride = 4, lv = 0, k = 1, eflip = 0, rflip = -1;
 };
 
@@ -79,6 +80,7 @@ struct ws_ctx {
   ws::Buf rep_of;     // i32[R]   dense id -> canonical voxel label
   ws::Buf levelmap;   // i32[R*stride]  canonical label of each dense id at levels 0..NL-1
   ws::Buf dimg;       // i32[N]   dense id of every voxel's label (waterfall)
+  ws::Buf sroots, sblocks;  // sharded waterfall: sorted roots of the level, compaction block counts
   ws::Buf rank;       // uint2[N/32+1] dense-id rank structure (k_dense, unsharded)
   ws::Buf wimg;       // u8[N]    reconstructed image (paper-literal waterfall)
   ws::Buf vstate;     // u8[2N]   states S, S' of the paper's one-thread-per-voxel variants

@@ -1113,12 +1113,88 @@ ws_status shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* 
   return WS_OK;
 }
 
+// Sharded levels exchange only the minima of the CURRENT roots, in increasing dense-id order
+// (every rank holds the same replicated union-find, so the order is the same on all ranks):
+// level 1 = all R regions (identity), then the roots of each level, compacted by a
+// deterministic scan over comp (comp[c] == c <=> c is a root).
+constexpr int SCH = 2048;  // entries per compaction block
+
+__global__ void __launch_bounds__(NTW) k_root_count(const int* __restrict__ comp, int R, int* __restrict__ bc) {
+  const int b0 = blockIdx.x * SCH;
+  int c = 0;
+  for (int i = b0 + threadIdx.x; i < min(b0 + SCH, R); i += NTW) c += comp[i] == i;
+  __shared__ int sm[32];
+  int tot;
+  block_excl_scan(c, sm, tot);
+  if (threadIdx.x == 0) bc[blockIdx.x] = tot;
+}
+
+// exclusive scan of the nb block counts in place (one block); total -> bc[nb]
+__global__ void __launch_bounds__(NTW) k_scan_counts(int* bc, int nb) {
+  __shared__ int sm[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nb; b0 += NTW) {
+    const int i = b0 + threadIdx.x;
+    const int v = i < nb ? bc[i] : 0;
+    int tot;
+    const int ex = block_excl_scan(v, sm, tot);
+    if (i < nb) bc[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bc[nb] = carry;
+}
+
+// sorted roots and the flipped minima of this rank at them
+__global__ void __launch_bounds__(NTW) k_root_scatter(const int* __restrict__ comp, int R, const int* __restrict__ bc,
+                                                       int* __restrict__ sroots, uint64_t* __restrict__ best_out,
+                                                       const uint64_t* __restrict__ best) {
+  const int b0 = blockIdx.x * SCH;
+  __shared__ int sm[32];
+  int base = bc[blockIdx.x];
+  for (int i0 = b0; i0 < min(b0 + SCH, R); i0 += NTW) {
+    const int i = i0 + threadIdx.x;
+    const bool r = i < R && comp[i] == i;
+    int tot;
+    const int ex = block_excl_scan(r ? 1 : 0, sm, tot);
+    if (r) {
+      sroots[base + ex] = i;
+      best_out[base + ex] = best[i] ^ (1ull << 63);
+    }
+    base += tot;
+  }
+}
+
+__global__ void k_best_scatter(uint64_t* best, const int* __restrict__ sroots, const uint64_t* __restrict__ best_in,
+                               int n) {
+  for (int i = blockIdx.x * NTW + threadIdx.x; i < n; i += gridDim.x * NTW) best[sroots[i]] = best_in[i] ^ (1ull << 63);
+}
+
 ws_status shard_wf_step(ws_ctx* ctx, const uint64_t* best_in, uint64_t* best_out, int64_t* count, int* more,
                         cudaStream_t st) {
   const long long R = ctx->wf.R;
-  k_flip_copy<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(ctx->best.as<uint64_t>(), best_in, R);
+  WS_TRY(ctx->sroots.ensure((size_t)R * sizeof(int), "sorted level roots"));
+  const int nb = (int)((R + SCH - 1) / SCH);
+  WS_TRY(ctx->sblocks.ensure((size_t)(nb + 1) * sizeof(int), "root compaction counts"));
+  int* sr = ctx->sroots.as<int>();
+  if (ctx->wf.k == 1) {  // level 1: the minima of all R regions, in dense-id order
+    k_flip_copy<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(ctx->best.as<uint64_t>(), best_in, R);
+  } else {
+    const int n = (int)ctx->wf.sorted_n;
+    if (n > 0) k_best_scatter<<<grid_for(n, ctx->num_sms), NTW, 0, st>>>(ctx->best.as<uint64_t>(), sr, best_in, n);
+  }
   WS_TRY(wf_step(ctx, count, more, st));
-  k_flip_copy<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(best_out, ctx->best.as<uint64_t>(), R);
+  if (*more) {
+    int* bc = ctx->sblocks.as<int>();
+    k_root_count<<<nb, NTW, 0, st>>>(ctx->comp.as<int>(), (int)R, bc);
+    k_scan_counts<<<1, NTW, 0, st>>>(bc, nb);
+    k_root_scatter<<<nb, NTW, 0, st>>>(ctx->comp.as<int>(), (int)R, bc, sr, best_out, ctx->best.as<uint64_t>());
+    launched(ctx, PH_WF_LEVELS, 3);
+    ctx->wf.sorted_n = *count;  // the roots of this level are the next level's components
+  }
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }

@@ -304,14 +304,15 @@ def sharded_waterfall(tr, ctxs, slabs, grads_ext, labels_own, nreps, NL: int, co
     cnt = R
     for k in range(1, NL):
         if more:
-            nxt = [torch.empty(R, dtype=torch.int64, device=dev) for _ in slabs]
+            # the exchanged minima shrink with the levels: only the current roots' (sorted)
+            nxt = [torch.empty(max(cnt, 1), dtype=torch.int64, device=dev) for _ in slabs]
             for i, s in enumerate(slabs):
                 c, m = ctypes.c_int64(0), ctypes.c_int32(0)
                 _b.check(lib.ws_shard_wf_step(ctxs[i].handle, _b.ptr(best[i]), _b.ptr(nxt[i]), ctypes.byref(c),
                                               ctypes.byref(m), _stream()))
                 cnt, more = c.value, m.value
             if more:
-                best = tr.allreduce_min(nxt)
+                best = tr.allreduce_min([x[:cnt].contiguous() for x in nxt])
         counts.append(cnt)
     levels = []
     for i, s in enumerate(slabs):
