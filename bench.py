@@ -349,7 +349,7 @@ def run_ours(args):
 
     world, rank, local = dist_setup(args)
     cfg, shape = workload(args)
-    if world > 1 and cfg.ndim == 3 and cfg.conn == 6:
+    if world > 1 and cfg.ndim == 3 and cfg.conn in (6, 26):
         return run_sharded(args, world, rank, cfg, shape)
     dev = torch.device("cuda", torch.cuda.current_device())
     N = int(np.prod(shape))

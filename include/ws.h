@@ -186,7 +186,7 @@ ws_status ws_plateau_debug(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32
 /* ==================================================================================
  * z-slab sharding (north_star: "3D volumes are partitioned along z into slabs across the 8
  * GPUs of one box, with NCCL halo exchange over NVLink and a cross-slab boundary union-find
- * merge").  Volumes (ndim 3), 6-connectivity.  Rank r of K owns global planes
+ * merge").  Volumes (ndim 3), 6- or 26-connectivity.  Rank r of K owns global planes
  * [z0, z1) and holds an EXTENDED slab [e0, e1) = [max(0, z0-2), min(D, z1+2)) of grad and of
  * the working array L_ext (i32); every dims argument below is the extended slab
  * (n0 = e1 - e0, n1, n2).  The caller moves the planes between ranks (NCCL through

@@ -392,8 +392,8 @@ ws_status ws_plateau_debug(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32
 // ------------------------------------------------------------------ z-slab sharding
 static ws_status check_slab(const ws_dims& d, const ws_slab& sl, int conn, Geo* g) {
   WS_TRY(check_dims(d, g));
-  if (d.ndim != 3 || conn != 6) {
-    set_error(WS_ERR_INVALID, "the sharded path supports 3-D volumes with 6-connectivity");
+  if (d.ndim != 3 || (conn != 6 && conn != 26)) {
+    set_error(WS_ERR_INVALID, "the sharded path supports 3-D volumes with 6- or 26-connectivity");
     return WS_ERR_INVALID;
   }
   const int64_t plane = d.n1 * d.n2;

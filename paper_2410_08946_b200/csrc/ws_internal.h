@@ -73,6 +73,7 @@ struct ws_ctx {
   WSState wf;
   int64_t total_launches = 0;
   int shard_nroots = 0;
+  int shard_conn = 6;     // connectivity of the last ws_shard_local (6 or 26)
   int shard_tiles = 0;    // tile count of the current sharded plateau phase
   int shard_flip = 0;     // which tile-flag buffer holds "next"
   ws::Buf comp;       // i32[R]   component parent (union-find over dense ids)

@@ -304,23 +304,32 @@ __global__ void k_merge_insert(const int* R0, long long n, RootMap M) {
   }
 }
 
-// cut-plane unions: last plane of rank r vs first plane of rank r + 1 (6-connectivity: the
-// voxel straight above), both on one minimal plateau (I equal and I(root) == I)
-__global__ void k_merge_union(Slabs S, const int* R0, RootMap M) {
+// cut-plane unions: last plane of rank r vs first plane of rank r + 1 -- the voxel straight
+// above (6-connectivity) or the 3 x 3 voxels above (26) -- both on one minimal plateau
+// (I equal and I(root) == I: an equal-valued neighbour lies on the same plateau)
+__global__ void k_merge_union(Slabs S, const int* R0, RootMap M, int n2, int diag) {
   const long long n = (long long)(S.K - 1) * S.plane;
+  const int n1 = S.plane / n2;
   for (long long i = blockIdx.x * (long long)NTS + threadIdx.x; i < n; i += (long long)gridDim.x * NTS) {
     const int r = (int)(i / S.plane), xy = (int)(i % S.plane);
     const Table A = tab(S, r), B = tab(S, r + 1);
-    const int ia = S.plane + xy, ib = xy;  // slot 1 of r, slot 0 of r + 1
-    if (A.I[ia] != B.I[ib] || A.term[ia] < 0 || A.rootI[ia] != A.I[ia]) continue;
-    int a = R0[(long long)r * 2 * S.plane + ia], b = R0[(long long)(r + 1) * 2 * S.plane + ib];
-    while (true) {
-      a = rm_find(M, a);
-      b = rm_find(M, b);
-      if (a == b) break;
-      if (a > b) { const int t = a; a = b; b = t; }
-      if (atomicCAS(M.parent + rm_slot(M, b), b, a) == b) break;
-    }
+    const int ia = S.plane + xy;  // slot 1 of r
+    if (A.term[ia] < 0 || A.rootI[ia] != A.I[ia]) continue;
+    const int x = xy % n2, y = xy / n2;
+    for (int dy = -diag; dy <= diag; ++dy)
+      for (int dx = -diag; dx <= diag; ++dx) {
+        if ((unsigned)(x + dx) >= (unsigned)n2 || (unsigned)(y + dy) >= (unsigned)n1) continue;
+        const int ib = xy + dy * n2 + dx;  // slot 0 of r + 1
+        if (A.I[ia] != B.I[ib]) continue;
+        int a = R0[(long long)r * 2 * S.plane + ia], b = R0[(long long)(r + 1) * 2 * S.plane + ib];
+        while (true) {
+          a = rm_find(M, a);
+          b = rm_find(M, b);
+          if (a == b) break;
+          if (a > b) { const int t = a; a = b; b = t; }
+          if (atomicCAS(M.parent + rm_slot(M, b), b, a) == b) break;
+        }
+      }
   }
 }
 
@@ -442,7 +451,8 @@ ws_status shard_local(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, 
   } else {
     L3 l = launch3(g);
     l.grid.z = (g.zhi - g.zlo) < 65535 ? (g.zhi - g.zlo) : 65535;
-    k_union_shard<6><<<l.grid, l.block, 0, st>>>(grad, P, g);  // resolve_shard checked conn == 6
+    if (conn == 26) k_union_shard<26><<<l.grid, l.block, 0, st>>>(grad, P, g);
+    else k_union_shard<6><<<l.grid, l.block, 0, st>>>(grad, P, g);
     launched(ctx, PH_WS_UNION);
   }
   tmark(ctx, st, PH_WS_UNION);
@@ -454,6 +464,7 @@ ws_status shard_local(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, 
   tmark(ctx, st, PH_WS_FIND);
   ctx->stats.n_regions = n_roots;
   ctx->shard_nroots = n_roots;
+  ctx->shard_conn = conn;  // ws_shard_merge's cut-plane adjacency
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
@@ -490,7 +501,9 @@ ws_status shard_merge(ws_ctx* ctx, const void* tables, const int64_t* z0s, const
   const int gg = grid_s(n, ctx->num_sms);
   k_merge_resolve<<<gg, NTS, 0, st>>>(S, R0);
   k_merge_insert<<<gg, NTS, 0, st>>>(R0, n, M);
-  if (K > 1) k_merge_union<<<grid_s((long long)(K - 1) * g.plane, ctx->num_sms), NTS, 0, st>>>(S, R0, M);
+  if (K > 1)
+    k_merge_union<<<grid_s((long long)(K - 1) * g.plane, ctx->num_sms), NTS, 0, st>>>(S, R0, M, g.n2,
+                                                                                     ctx->shard_conn == 26 ? 1 : 0);
   k_merge_min<<<gg, NTS, 0, st>>>(S, R0, M);
   k_merge_apply<<<grid_s(2LL * g.plane, ctx->num_sms), NTS, 0, st>>>(S, R0, M, rank, g, L, exitcanon);
   launched(ctx, PH_WS_FIND, K > 1 ? 5 : 4);

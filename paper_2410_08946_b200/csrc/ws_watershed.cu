@@ -1026,33 +1026,40 @@ static ws_status shard_round_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
 ws_status plateau_first_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int* pending,
                               cudaStream_t st) {
   if (conn == 6) return shard_first_t<6>(ctx, grad, g, L, pending, st);
-  set_error(WS_ERR_INVALID, "the sharded path supports 6-connectivity only");
+  if (conn == 26) return shard_first_t<26>(ctx, grad, g, L, pending, st);
+  set_error(WS_ERR_INVALID, "the sharded path supports 6- and 26-connectivity");
   return WS_ERR_INVALID;
 }
 
 ws_status plateau_round_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int act_lo,
                               int act_hi, int* pending, cudaStream_t st) {
   if (conn == 6) return shard_round_t<6>(ctx, grad, g, L, act_lo, act_hi, pending, st);
-  set_error(WS_ERR_INVALID, "the sharded path supports 6-connectivity only");
+  if (conn == 26) return shard_round_t<26>(ctx, grad, g, L, act_lo, act_hi, pending, st);
+  set_error(WS_ERR_INVALID, "the sharded path supports 6- and 26-connectivity");
   return WS_ERR_INVALID;
 }
 
-ws_status resolve_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, const int32_t* L, int32_t* P,
-                        cudaStream_t st) {
-  if (conn != 6) {
-    set_error(WS_ERR_INVALID, "the sharded path supports 6-connectivity only");
-    return WS_ERR_INVALID;
-  }
-  const TileGrid tg = tiles_of<6>(g);
+template <int CONN>
+static ws_status resolve_shard_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, const int32_t* L, int32_t* P,
+                                 cudaStream_t st) {
+  const TileGrid tg = tiles_of<CONN>(g);
   Maps mp;
-  make_maps<6>(grad, L, g, mp);
+  make_maps<CONN>(grad, L, g, mp);
   PairOut po;
   WS_TRY(pair_out(ctx, g, po, st));
-  k_resolve<6, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr, po);
+  k_resolve<CONN, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr, po);
   launched(ctx, PH_WS_SELECT);
   tmark(ctx, st, PH_WS_SELECT);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
+}
+
+ws_status resolve_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, const int32_t* L, int32_t* P,
+                        cudaStream_t st) {
+  if (conn == 6) return resolve_shard_t<6>(ctx, grad, g, L, P, st);
+  if (conn == 26) return resolve_shard_t<26>(ctx, grad, g, L, P, st);
+  set_error(WS_ERR_INVALID, "the sharded path supports 6- and 26-connectivity");
+  return WS_ERR_INVALID;
 }
 
 ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* labels,

@@ -9,7 +9,7 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-def _run(grad, K):
+def _run(grad, K, conn=6):
     import paper_2410_08946_b200 as ws
     from paper_2410_08946_b200 import shard
     D = grad.shape[0]
@@ -17,16 +17,16 @@ def _run(grad, K):
     tr = shard.LocalTransport(K)
     ctxs = [ws.Context(0) for _ in range(K)]
     grads = [grad[s.e0:s.e1].contiguous() for s in slabs]
-    labels, R, rounds = shard.sharded_watershed(tr, ctxs, slabs, grads, 6)
+    labels, R, rounds = shard.sharded_watershed(tr, ctxs, slabs, grads, conn)
     for c in ctxs:
         c.close()
     return torch.cat(labels, 0), R, rounds
 
 
-def _check(grad, K):
+def _check(grad, K, conn=6):
     import paper_2410_08946_b200 as ws
-    ref, Rref = ws.watershed(grad, 6)
-    got, R, rounds = _run(grad, K)
+    ref, Rref = ws.watershed(grad, conn)
+    got, R, rounds = _run(grad, K, conn)
     if not torch.equal(got, ref):
         bad = (got != ref).nonzero()
         pytest.fail("K=%d: %d voxels differ, first %s got %s want %s" % (
@@ -42,12 +42,14 @@ def test_sharded_equals_unsharded_microct(K):
     _check(grad, K)
 
 
+@pytest.mark.parametrize("conn", [6, 26])
 @pytest.mark.parametrize("K,shape,levels", [(2, (12, 33, 47), 3), (4, (16, 32, 64), 2), (6, (6, 20, 30), 3),
                                             (3, (9, 17, 23), 5)])
-def test_sharded_plateau_volumes(K, shape, levels):
-    """values in {0..levels-1}: plateaux (minimal and not) crossing every cut; 1-plane slabs."""
+def test_sharded_plateau_volumes(K, shape, levels, conn):
+    """values in {0..levels-1}: plateaux (minimal and not) crossing every cut; 1-plane slabs;
+    26-connectivity adds the diagonal neighbours across every cut."""
     g = synth.random_plateau_image(shape, levels, seed=K * 10 + levels).cuda()
-    _check(g, K)
+    _check(g, K, conn)
 
 
 def test_sharded_constant_and_corridor():
@@ -64,15 +66,15 @@ def test_sharded_constant_and_corridor():
     _check(ws.gradient(raw, 1.0, ndim=3), 3)
 
 
-def _check_segment(grad, K, NL=6):
+def _check_segment(grad, K, NL=6, conn=6):
     import paper_2410_08946_b200 as ws
     from paper_2410_08946_b200 import shard
-    ref, Rref = ws.watershed(grad, 6)
-    rlv, rcounts = ws.waterfall(ref, grad, 6, NL)
+    ref, Rref = ws.watershed(grad, conn)
+    rlv, rcounts = ws.waterfall(ref, grad, conn, NL)
     slabs = shard.make_slabs(grad.shape[0], K)
     ctxs = [ws.Context(0) for _ in range(K)]
     labels, levels, counts, R, rounds = shard.sharded_segment(
-        shard.LocalTransport(K), ctxs, slabs, [grad[s.e0:s.e1].contiguous() for s in slabs], NL)
+        shard.LocalTransport(K), ctxs, slabs, [grad[s.e0:s.e1].contiguous() for s in slabs], NL, conn)
     for c in ctxs:
         c.close()
     assert torch.equal(torch.cat(labels, 0), ref) and R == Rref
@@ -90,7 +92,18 @@ def test_sharded_waterfall_microct(K):
     _check_segment(ws.gradient(raw, 1.0, ndim=3), K)
 
 
+@pytest.mark.parametrize("conn", [6, 26])
 @pytest.mark.parametrize("K,shape,levels,NL", [(2, (10, 24, 40), 4, 6), (5, (5, 16, 32), 3, 4), (3, (12, 20, 28), 6, 9)])
-def test_sharded_waterfall_plateaux(K, shape, levels, NL):
+def test_sharded_waterfall_plateaux(K, shape, levels, NL, conn):
     g = synth.random_plateau_image(shape, levels, seed=K + levels).cuda()
-    _check_segment(g, K, NL)
+    _check_segment(g, K, NL, conn)
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_sharded_26conn_microct_and_constant(K):
+    """26-connectivity through the whole sharded pipeline on a C4-like volume, and one
+    minimal plateau spanning every slab."""
+    import paper_2410_08946_b200 as ws
+    raw = synth.make_config_image("C4", shape=(24, 48, 64), device="cuda")
+    _check_segment(ws.gradient(raw, 1.0, ndim=3), K, 6, 26)
+    _check(torch.full((12, 16, 24), 5, dtype=torch.uint8, device="cuda"), K, 26)
