@@ -107,3 +107,27 @@ def test_sharded_26conn_microct_and_constant(K):
     raw = synth.make_config_image("C4", shape=(24, 48, 64), device="cuda")
     _check_segment(ws.gradient(raw, 1.0, ndim=3), K, 6, 26)
     _check(torch.full((12, 16, 24), 5, dtype=torch.uint8, device="cuda"), K, 26)
+
+
+@pytest.mark.parametrize("conn2d,conn3d,K", [(8, 26, 3), (4, 6, 4)])
+def test_2d_y_band_sharding(conn2d, conn3d, K):
+    """NEXT f4, 2-D y-band sharding: an H x W image is the (H, 1, W) volume, whose 26- (6-)
+    connectivity is the image's 8- (4-) connectivity and whose linear order is the image's
+    (C1, C21), so its z-slabs are y-bands.  The sharded segmentation of the bands must equal
+    the unsharded 2-D one."""
+    import paper_2410_08946_b200 as ws
+    from paper_2410_08946_b200 import shard
+    raw = synth.make_config_image("C2", shape=(1, 96, 160), device="cuda")
+    q = ws.gradient(raw, 1.0, ndim=2)
+    ref, Rref = ws.watershed(q, conn2d, ndim=2)
+    rlv, rc = ws.waterfall(ref, q, conn2d, 6, ndim=2)
+    H, W = q.shape[1], q.shape[2]
+    q3 = q.view(H, 1, W)
+    slabs = shard.make_slabs(H, K)
+    ctxs = [ws.Context(0) for _ in range(K)]
+    labels, levels, counts, R, _ = shard.sharded_segment(
+        shard.LocalTransport(K), ctxs, slabs, [q3[s.e0:s.e1].contiguous() for s in slabs], 6, conn3d)
+    for c in ctxs:
+        c.close()
+    assert torch.equal(torch.cat(labels, 0).view(1, H, W), ref) and R == Rref
+    assert torch.equal(torch.cat(levels, 1).view(6, 1, H, W), rlv) and counts == list(rc)
