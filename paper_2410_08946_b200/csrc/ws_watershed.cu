@@ -526,7 +526,7 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     }
     if (minimal) {
       minmask |= 1u << k;
-      sP[j] = (short)j;
+      sP[j] = -2;  // root (set after the in-tile union below)
       sG[j] = j;  // union-find parent (local index)
     } else {
       int dz, dy, dx;
@@ -582,7 +582,8 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     for (int k = 0; k < T::VPT; ++k)
       if ((minmask >> k) & 1) {
         const int j = threadIdx.x + k * NT;
-        sP[j] = (short)s_find(sG, j);
+        const int r = s_find(sG, j);
+        sP[j] = (short)(r == j ? -2 : r);
       }
     __syncthreads();
     for (int i = threadIdx.x; i < nq; i += NT)
@@ -600,12 +601,12 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi)) continue;
     int j = threadIdx.x + k * NT;
     int jn = sP[j];
-    while (jn >= 0 && jn != j) {
+    while (jn >= 0) {
       j = jn;
       jn = sP[j];
     }
     int out;
-    if (jn < 0) {
+    if (jn == -1) {
       out = sG[j];
     } else {
       const int rx = j % T::TX, ry = (j / T::TX) % T::TY, rz = j / (T::TX * T::TY);
@@ -624,7 +625,7 @@ __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensor
   using T = TL<CONN>;
   __shared__ alignas(128) uint8_t sI[T::SI];
   __shared__ alignas(128) int sD[T::SL];
-  __shared__ short sP[T::V];  // local target, -1 = leaves the tile
+  __shared__ short sP[T::V];  // local target, -1 = leaves the tile, -2 = root
   __shared__ int sG[T::V];    // global target when leaving the tile / union-find of minimal voxels
   __shared__ int2 sQ[QCAP];   // cross-tile step IV pairs
   __shared__ int sQn, sQb;
