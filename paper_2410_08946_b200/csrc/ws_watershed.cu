@@ -472,11 +472,13 @@ __device__ __forceinline__ void s_unite(int* U, int a, int b) {
 }
 
 template <int CONN, bool DEBUG, bool BORDER>
-__device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, short* sP, int* sG, int2* sQ,
+__device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, short* sP, int* sG /* aliases sD */, int2* sQ,
                                              int* sQn, int* sQb, const Geo& g, const TileCoord& c,
                                              int* __restrict__ P, int* __restrict__ dist, const PairOut& po) {
   using T = TL<CONN>;
   uint32_t minmask = 0;  // bit k: voxel k of this thread is on a minimal plateau (or a strict minimum)
+  uint32_t gmask = 0;    // bit k: gk[k] holds sG[j] (stored once sD is dead: sG aliases sD)
+  int gk[T::VPT];
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
@@ -485,7 +487,8 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     if (BORDER && !(c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi)) {
       // not owned (halo plane of a z-slab, or outside the volume): a tile exit, never a root
       sP[j] = -1;
-      sG[j] = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx) + g.gofs;
+      gk[k] = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx) + g.gofs;
+      gmask |= 1u << k;
       continue;
     }
     const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
@@ -527,7 +530,8 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     if (minimal) {
       minmask |= 1u << k;
       sP[j] = -2;  // root (set after the in-tile union below)
-      sG[j] = j;  // union-find parent (local index)
+      gk[k] = j;   // union-find parent (local index)
+      gmask |= 1u << k;
     } else {
       int dz, dy, dx;
       nb_delta(CONN, dir, dz, dy, dx);
@@ -536,7 +540,8 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
         sP[j] = (short)(j + (dz * T::TY + dy) * T::TX + dx);
       } else {
         sP[j] = -1;
-        sG[j] = p + nb_off<CONN>(g, dir) + g.gofs;
+        gk[k] = p + nb_off<CONN>(g, dir) + g.gofs;
+        gmask |= 1u << k;
       }
     }
   }
@@ -544,7 +549,11 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
   // step IV inside the tile + the cross-tile pairs (q > p: the forward half).  Only
   // the (few) minimal voxels loop; cross-tile pairs are staged in shared memory (sQ) and
   // flushed with one global atomic per tile.
-  const bool anymin = __syncthreads_or(minmask != 0);
+  const bool anymin = __syncthreads_or(minmask != 0);  // sD is dead from here on
+#pragma unroll
+  for (int k = 0; k < T::VPT; ++k)
+    if (gmask & (1u << k)) sG[threadIdx.x + k * NT] = gk[k];
+  __syncthreads();
   if (anymin) {
     for (uint32_t mm = minmask; mm; mm &= mm - 1) {
       const int k = __ffs(mm) - 1;
@@ -625,8 +634,8 @@ __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensor
   using T = TL<CONN>;
   __shared__ alignas(128) uint8_t sI[T::SI];
   __shared__ alignas(128) int sD[T::SL];
+  static_assert(T::SL >= T::V, "sG aliases sD");
   __shared__ short sP[T::V];  // local target, -1 = leaves the tile, -2 = root
-  __shared__ int sG[T::V];    // global target when leaving the tile / union-find of minimal voxels
   __shared__ int2 sQ[QCAP];   // cross-tile step IV pairs
   __shared__ int sQn, sQb;
   __shared__ uint64_t bar;
@@ -634,9 +643,9 @@ __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensor
   if (threadIdx.x == 0) sQn = 0;
   stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);  // raw step II codes (no decoding)
   if (tile_interior<CONN>(c, g))
-    resolve_body<CONN, DEBUG, false>(sI, sD, sP, sG, sQ, &sQn, &sQb, g, c, P, dist, po);
+    resolve_body<CONN, DEBUG, false>(sI, sD, sP, sD, sQ, &sQn, &sQb, g, c, P, dist, po);
   else
-    resolve_body<CONN, DEBUG, true>(sI, sD, sP, sG, sQ, &sQn, &sQb, g, c, P, dist, po);
+    resolve_body<CONN, DEBUG, true>(sI, sD, sP, sD, sQ, &sQn, &sQb, g, c, P, dist, po);
 }
 
 // --------------------------- step III across tiles + per-root minimum + root list
