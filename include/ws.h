@@ -123,6 +123,16 @@ ws_status ws_gradient(ws_ctx* ctx, const uint8_t* img, ws_dims dims, float sigma
 ws_status ws_watershed(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity,
                        int32_t* labels, int64_t* num_regions, void* stream);
 
+/* ws_watershed_u16 — ws_watershed on a 16-bit image (NEXT f4; microCT volumes are often
+ * 16-bit; the paper's headline protocol runs on raw images).  Identical
+ * definition, steps and output; intensities compare as unsigned 16-bit values.
+ * Arguments: grad u16[N] (in, 2-byte aligned), labels i32[N] (out), num_regions (HOST i64,
+ * optional).  TMA staging needs a 16-byte aligned grad and n2 % 8 == 0, else a plain loader
+ * runs (same result).  Unsharded only (the ws_shard_* calls take u8).
+ * Errors: as ws_watershed. */
+ws_status ws_watershed_u16(ws_ctx* ctx, const uint16_t* grad, ws_dims dims, int32_t connectivity,
+                           int32_t* labels, int64_t* num_regions, void* stream);
+
 /* ws_watershed_variant — the paper's own one-thread-per-voxel watershed kernels (SURVEY NEXT
  * f3), the baseline for the tiled ws_watershed; every variant yields the same partition
  * and the same canonical labels (C7):

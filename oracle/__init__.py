@@ -38,7 +38,9 @@ def _load():
         lib.oracle_watershed.argtypes = [vp, i32, i64, i64, i64, i32, vp, vp, vp, vp]
         lib.oracle_waterfall.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
         lib.oracle_waterfall_reconstruct.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
-        for f in (lib.oracle_gradient, lib.oracle_watershed, lib.oracle_waterfall, lib.oracle_waterfall_reconstruct):
+        lib.oracle_watershed_u16.argtypes = lib.oracle_watershed.argtypes
+        for f in (lib.oracle_gradient, lib.oracle_watershed, lib.oracle_watershed_u16, lib.oracle_waterfall,
+                  lib.oracle_waterfall_reconstruct):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -76,17 +78,20 @@ def gradient(img: np.ndarray, sigma: float, ndim: int = None):
 
 
 def watershed(grad: np.ndarray, conn: int, ndim: int = None, dumps: bool = False):
-    """O3+O4: canonical labels (int32).  With ``dumps`` also (dist int32, ptr int64, R)."""
+    """O3+O4: canonical labels (int32).  With ``dumps`` also (dist int32, ptr int64, R).
+    A np.uint16 image runs the same definition on 16-bit intensities (O10, NEXT f4)."""
     orig = grad.shape
     if ndim is None:
         ndim = 3 if conn in (6, 26) else 2
-    a, (n0, n1, n2) = _shape3(np.asarray(grad, dtype=np.uint8), ndim)
+    wide = isinstance(grad, np.ndarray) and grad.dtype == np.uint16
+    a, (n0, n1, n2) = _shape3(np.asarray(grad, dtype=np.uint16 if wide else np.uint8), ndim)
     labels = np.empty(a.shape, np.int32)
     dist = np.empty(a.shape, np.int32) if dumps else None
     ptr = np.empty(a.shape, np.int64) if dumps else None
     R = ctypes.c_int64(0)
-    rc = _load().oracle_watershed(_p(a), ndim, n0, n1, n2, int(conn), _p(labels), _p(dist), _p(ptr),
-                                  ctypes.byref(R))
+    fn = _load().oracle_watershed_u16 if wide else _load().oracle_watershed
+    rc = fn(_p(a), ndim, n0, n1, n2, int(conn), _p(labels), _p(dist), _p(ptr),
+            ctypes.byref(R))
     if rc != 0:
         raise ValueError("oracle_watershed: invalid arguments")
     if dumps:

@@ -171,8 +171,11 @@ int oracle_gradient(const uint8_t* img, int ndim, int64_t n0, int64_t n1, int64_
 // ptr (parent; p itself for minimal-plateau voxels), n_regions.
 // Returns 0 on success, 1 on invalid arguments.
 // ---------------------------------------------------------------------------------
-int oracle_watershed(const uint8_t* I, int ndim, int64_t n0, int64_t n1, int64_t n2, int conn,
-                     int32_t* labels, int32_t* dist_out, int64_t* ptr_out, int64_t* n_regions) {
+}  // extern "C"
+
+template <class Px>
+int watershed_impl(const Px* I, int ndim, int64_t n0, int64_t n1, int64_t n2, int conn,
+                   int32_t* labels, int32_t* dist_out, int64_t* ptr_out, int64_t* n_regions) {
   Grid g{ndim, n0, n1, n2};
   if (!valid(g, conn)) return 1;
   int64_t N = g.N();
@@ -199,7 +202,7 @@ int oracle_watershed(const uint8_t* I, int ndim, int64_t n0, int64_t n1, int64_t
   for (int64_t p = 0; p < N; ++p) {
     auto nb = neighbours(g, conn, p);
     if (nb.empty()) continue;  // single-voxel image: terminal (C4)
-    int m = 256;
+    int m = 1 << 16;  // above every u8 / u16 intensity
     for (int64_t q : nb) m = std::min<int>(m, I[q]);
     if (m < I[p]) {
       lower[p] = 1;
@@ -254,6 +257,19 @@ int oracle_watershed(const uint8_t* I, int ndim, int64_t n0, int64_t n1, int64_t
   }
   if (n_regions) *n_regions = R;
   return 0;
+}
+
+extern "C" {
+
+int oracle_watershed(const uint8_t* I, int ndim, int64_t n0, int64_t n1, int64_t n2, int conn,
+                     int32_t* labels, int32_t* dist_out, int64_t* ptr_out, int64_t* n_regions) {
+  return watershed_impl(I, ndim, n0, n1, n2, conn, labels, dist_out, ptr_out, n_regions);
+}
+
+// The same definition on a 16-bit image (NEXT f4): intensities compare as u16.
+int oracle_watershed_u16(const uint16_t* I, int ndim, int64_t n0, int64_t n1, int64_t n2, int conn,
+                         int32_t* labels, int32_t* dist_out, int64_t* ptr_out, int64_t* n_regions) {
+  return watershed_impl(I, ndim, n0, n1, n2, conn, labels, dist_out, ptr_out, n_regions);
 }
 
 // ---------------------------------------------------------------------------------

@@ -64,13 +64,20 @@ def watershed(grad: torch.Tensor, conn: int, ndim: int = None, ctx: Context = No
               out: torch.Tensor = None, variant: str = None):
     """ws_watershed: canonical labels (int32, shaped like grad) and the region count R.
     variant="pruf_sync" | "prw_sync" | "apruf_sync": the paper's one-thread-per-voxel kernels
-    (ws_watershed_variant, Alg. 1 / Alg. 2 / APRUF) instead of the tiled design."""
-    _req(grad, torch.uint8, "grad")
+    (ws_watershed_variant, Alg. 1 / Alg. 2 / APRUF) instead of the tiled design.
+    A torch.uint16 grad runs ws_watershed_u16 (16-bit images, NEXT f4; tiled design only)."""
+    wide = isinstance(grad, torch.Tensor) and grad.dtype == torch.uint16
+    _req(grad, torch.uint16 if wide else torch.uint8, "grad")
     ndim = _ndim_for(conn, ndim)
     ctx = ctx or default_context(grad.device.index)
     labels = out if out is not None else torch.empty(grad.shape, dtype=torch.int32, device=grad.device)
     R = ctypes.c_int64(0)
-    if variant is None:
+    if wide:
+        if variant is not None:
+            raise ValueError("the paper's kernel variants take u8 images")
+        _b.check(_b.load().ws_watershed_u16(ctx.handle, _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn),
+                                            _b.ptr(labels), ctypes.byref(R), _b.stream_of(grad)))
+    elif variant is None:
         _b.check(_b.load().ws_watershed(ctx.handle, _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn),
                                         _b.ptr(labels), ctypes.byref(R), _b.stream_of(grad)))
     else:

@@ -171,7 +171,8 @@ bool encode_tmap_3d(void* map, int esize, const void* base, const Geo& g, unsign
   cuuint32_t box[3] = {bx, by, bz};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(reinterpret_cast<CUtensorMap*>(map),
-                  esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3,
+                  esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                  : esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3,
                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -281,6 +282,25 @@ ws_status ws_watershed(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t c
   begin_call(ctx, g);
   tbegin(ctx, (cudaStream_t)stream);
   ws_status s = run_watershed(ctx, grad, g, connectivity, labels, num_regions, (cudaStream_t)stream);
+  tfinish(ctx);
+  return s;
+}
+
+ws_status ws_watershed_u16(ws_ctx* ctx, const uint16_t* grad, ws_dims dims, int32_t connectivity,
+                           int32_t* labels, int64_t* num_regions, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  WS_TRY(check_conn(dims, connectivity));
+  if (!grad) return null_arg("grad");
+  if (!labels) return null_arg("labels");
+  if (reinterpret_cast<uintptr_t>(grad) & 1) {
+    set_error(WS_ERR_INVALID, "grad must be 2-byte aligned");
+    return WS_ERR_INVALID;
+  }
+  begin_call(ctx, g);
+  tbegin(ctx, (cudaStream_t)stream);
+  ws_status s = px16::run_watershed(ctx, grad, g, connectivity, labels, num_regions, (cudaStream_t)stream);
   tfinish(ctx);
   return s;
 }

@@ -11,7 +11,7 @@ namespace ws {
 constexpr int NT = 256;
 
 // Tile layout.  3-D tiles 32x8x8, 2-D tiles 64x32 (2048 voxels, 8 per thread).
-//   I box (u8):  x in [bx-16, bx+TX+16), y in [by-2, by+TY+2), z in [bz-2, bz+TZ+2) (3-D)
+//   I box (u8 or u16 pixels):  x in [bx-16, bx+TX+16), y in [by-2, by+TY+2), z in [bz-2, bz+TZ+2) (3-D)
 //   L box (i32): x in [bx-4, bx+TX+4),   y in [by-1, by+TY+1), z in [bz-1, bz+TZ+1) (3-D)
 // TMA rules (measured on sm_100a): box widths AND the innermost start coordinate must be
 // multiples of 16 bytes, hence the wide x halos; 2-D tiles have no halo across axis 0.
@@ -89,16 +89,16 @@ __device__ __forceinline__ unsigned valid_mask(const Geo& g, int gz, int gy, int
 // Stage the I box (and optionally the L box, as raw L values) into shared memory: one
 // cp.async.bulk.tensor per box (TMA zero-fills outside the volume), or a plain loader when
 // the layout has no tensor map.
-template <int CONN>
+template <int CONN, class Px>
 __device__ __forceinline__ void stage(const CUtensorMap* mI, const CUtensorMap* mL, bool tma,
-                                      const uint8_t* __restrict__ I, const int* __restrict__ L, const Geo& g,
-                                      const TileCoord& c, uint8_t* sI, int* sL, uint64_t* bar) {
+                                      const Px* __restrict__ I, const int* __restrict__ L, const Geo& g,
+                                      const TileCoord& c, Px* sI, int* sL, uint64_t* bar) {
   using T = TL<CONN>;
   if (tma) {
     if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
-      mbar_expect_tx(bar, T::SI + (sL ? T::SL * 4 : 0));
+      mbar_expect_tx(bar, T::SI * (int)sizeof(Px) + (sL ? T::SL * 4 : 0));
       tma_load_3d(sI, mI, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, bar);
       if (sL) tma_load_3d(sL, mL, c.bx - T::LXO, c.by - T::LYO, c.bz - T::LZO, bar);
     }
@@ -107,7 +107,7 @@ __device__ __forceinline__ void stage(const CUtensorMap* mI, const CUtensorMap* 
     for (int s = threadIdx.x; s < T::SI; s += NT) {
       const int sx = s % T::SXI, sy = (s / T::SXI) % T::SYI, sz = s / (T::SXI * T::SYI);
       const int gx = c.bx + sx - T::IXO, gy = c.by + sy - T::IYO, gz = c.bz + sz - T::IZO;
-      uint8_t v = 0;
+      Px v = 0;
       if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
         v = __ldg(I + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
       sI[s] = v;
@@ -134,13 +134,13 @@ struct Maps {
   int tma;
 };
 
-template <int CONN>
-static inline void make_maps(const uint8_t* grad, const int* L, const Geo& g, Maps& m) {
+template <int CONN, class Px>
+static inline void make_maps(const Px* grad, const int* L, const Geo& g, Maps& m) {
   using T = TL<CONN>;
   const char* env = getenv("WS_NO_TMA");
   const bool off = env && env[0] == '1';
   std::memset(&m, 0, sizeof(m));
-  const bool a = !off && encode_tmap_3d(&m.mI, 1, grad, g, T::SXI, T::SYI, T::SZI);
+  const bool a = !off && encode_tmap_3d(&m.mI, (int)sizeof(Px), grad, g, T::SXI, T::SYI, T::SZI);
   const bool b = !off && encode_tmap_3d(&m.mL, 4, L, g, T::SXL, T::SYL, T::SZL);
   m.tma = (a && b) ? 1 : 0;
 }

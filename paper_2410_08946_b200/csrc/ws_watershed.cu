@@ -1,9 +1,10 @@
 // ws_watershed.cu — steps I-IV of PRUF (Alg. 1) + canonical relabel, sm_100a.
 //
 // Tile design: the volume is cut into tiles of 2048 voxels
-// (3-D 32x8x8, 2-D 64x32) staged in shared memory with a halo.  Intensities are staged as
-// 16-bit values with an out-of-volume sentinel (0xFFFF: never lower, never equal), so the
-// stencil loops carry no bounds checks.
+// (3-D 32x8x8, 2-D 64x32) staged in shared memory with a halo by TMA (zero fill outside the
+// volume); tiles whose halo leaves the volume use neighbour-validity masks (BORDER bodies).
+// Pixel type Px: u8 here; ws_watershed16.cu compiles this file again with u16 pixels
+// (NEXT f4) into namespace ws::px16.
 //
 //   k_relax_first  step I classification (Alg. 1 l.1-10) fused with the first round of the
 //                  step II distance relaxation (Alg. 3 l.7-8) inside each tile      [all tiles]
@@ -31,6 +32,12 @@
 #include "ws_tile.cuh"
 
 namespace ws {
+#ifdef WS_PX16
+namespace px16 {
+using Px = uint16_t;
+#else
+using Px = uint8_t;
+#endif
 
 constexpr int INF = DUNREACHED;
 
@@ -269,8 +276,8 @@ __device__ __forceinline__ void classify_box_swar(const uint8_t* sI, int* sD) {
 // step I classification of the tile + 1-voxel halo into sD (L layout):
 // lower -> 0, plateau without lower -> INF, strict minimum -> 0 (Alg. 1 l.1-10)
 template <int CONN, bool BORDER>
-__device__ __forceinline__ void classify_box(const uint8_t* sI, int* sD, const Geo& g, const TileCoord& c) {
-  if constexpr (!BORDER) {
+__device__ __forceinline__ void classify_box(const Px* sI, int* sD, const Geo& g, const TileCoord& c) {
+  if constexpr (!BORDER && sizeof(Px) == 1) {
     classify_box_swar<CONN>(sI, sD);
     return;
   } else {
@@ -305,7 +312,7 @@ __device__ __forceinline__ void classify_box(const uint8_t* sI, int* sD, const G
 
 // ------------------------------------------- step I + first step II round (all tiles)
 template <int CONN, bool BORDER>
-__device__ __forceinline__ void relax_first_body(const uint8_t* sI, int* sD, int* __restrict__ L, const Geo& g,
+__device__ __forceinline__ void relax_first_body(const Px* sI, int* sD, int* __restrict__ L, const Geo& g,
                                                  const TileCoord& c, int t, int ntx, int nty, uint8_t* next,
                                                  uint8_t* hasplat, int* flags, RQ& q) {
   using T = TL<CONN>;
@@ -349,10 +356,10 @@ __device__ __forceinline__ void relax_first_body(const uint8_t* sI, int* sD, int
 
 template <int CONN>
 __global__ void __launch_bounds__(NT) k_relax_first(const __grid_constant__ CUtensorMap mI, int tma,
-                                                     const uint8_t* __restrict__ I, int* __restrict__ L, Geo g,
+                                                     const Px* __restrict__ I, int* __restrict__ L, Geo g,
                                                      int ntx, int nty, uint8_t* next, uint8_t* hasplat, int* flags) {
   using T = TL<CONN>;
-  __shared__ alignas(128) uint8_t sI[T::SI];
+  __shared__ alignas(128) Px sI[T::SI];
   __shared__ alignas(16) int sD[T::SL];
   __shared__ uint64_t bar;
   __shared__ RQ q;
@@ -368,7 +375,7 @@ __global__ void __launch_bounds__(NT) k_relax_first(const __grid_constant__ CUte
 
 // ------------------------------------------------ further step II rounds (active tiles)
 template <int CONN, bool BORDER>
-__device__ __forceinline__ void relax_round_body(const uint8_t* sI, int* sD, int* __restrict__ L, const Geo& g,
+__device__ __forceinline__ void relax_round_body(const Px* sI, int* sD, int* __restrict__ L, const Geo& g,
                                                  const TileCoord& c, int t, int ntx, int nty, uint8_t* next,
                                                  int* flags, RQ& q) {
   using T = TL<CONN>;
@@ -398,13 +405,13 @@ __device__ __forceinline__ void relax_round_body(const uint8_t* sI, int* sD, int
 template <int CONN>
 __global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUtensorMap mI,
                                                      const __grid_constant__ CUtensorMap mL, int tma,
-                                                     const uint8_t* __restrict__ I, int* __restrict__ L, Geo g,
+                                                     const Px* __restrict__ I, int* __restrict__ L, Geo g,
                                                      int ntx, int nty, const uint8_t* cur, uint8_t* next,
                                                      const uint8_t* hasplat, int* flags, const int* list) {
   using T = TL<CONN>;
   const int t = list ? list[blockIdx.x] : blockIdx.x;  // list: the compacted active tiles
   if (!list && (!cur[t] || !hasplat[t])) return;
-  __shared__ alignas(128) uint8_t sI[T::SI];
+  __shared__ alignas(128) Px sI[T::SI];
   __shared__ alignas(128) int sD[T::SL];
   __shared__ uint64_t bar;
   __shared__ RQ q;
@@ -472,7 +479,7 @@ __device__ __forceinline__ void s_unite(int* U, int a, int b) {
 }
 
 template <int CONN, bool DEBUG, bool BORDER>
-__device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, short* sP, int* sG /* aliases sD */, int2* sQ,
+__device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short* sP, int* sG /* aliases sD */, int2* sQ,
                                              int* sQn, int* sQb, const Geo& g, const TileCoord& c,
                                              int* __restrict__ P, int* __restrict__ dist, const PairOut& po) {
   using T = TL<CONN>;
@@ -494,7 +501,7 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
     const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
     const int si = T::iI(lz, ly, lx), sl = T::iL(lz, ly, lx);
     const int v = sI[si];
-    int m = 256, dm = -1;
+    int m = 1 << (8 * sizeof(Px)), dm = -1;
     unsigned eqm = 0;
 #pragma unroll
     for (int i = 0; i < CONN; ++i) {
@@ -628,11 +635,11 @@ __device__ __forceinline__ void resolve_body(const uint8_t* sI, const int* sD, s
 template <int CONN, bool DEBUG>
 __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensorMap mI,
                                                 const __grid_constant__ CUtensorMap mL, int tma,
-                                                const uint8_t* __restrict__ I, const int* __restrict__ L, Geo g,
+                                                const Px* __restrict__ I, const int* __restrict__ L, Geo g,
                                                 int ntx, int nty, int* __restrict__ P, int* __restrict__ dist,
                                                 PairOut po) {
   using T = TL<CONN>;
-  __shared__ alignas(128) uint8_t sI[T::SI];
+  __shared__ alignas(128) Px sI[T::SI];
   __shared__ alignas(128) int sD[T::SL];
   static_assert(T::SL >= T::V, "sG aliases sD");
   __shared__ short sP[T::V];  // local target, -1 = leaves the tile, -2 = root
@@ -765,7 +772,7 @@ __device__ __forceinline__ void uf_unite(int* P, int a, int b) {
 // p is on a minimal plateau  <=>  I(root(p)) == I(p): the descent path into a regional
 // minimum keeps the intensity only inside that minimum's plateau.
 template <int CONN>
-__global__ void k_union(const uint8_t* __restrict__ I, int* P, Geo g) {
+__global__ void k_union(const Px* __restrict__ I, int* P, Geo g) {
   ZLOOP_BEGIN
   const int v = I[p];
   const int r = ld_cg(P + p);
@@ -878,7 +885,7 @@ static int grid1d(long long n, int sms, int per_sm = 8) {
 }
 
 template <int CONN>
-static ws_status plateau_phase(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, const TileGrid& tg,
+static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* L, const TileGrid& tg,
                                const Maps& mp, cudaStream_t st) {
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->tiles.ensure((size_t)tg.n * 3, "tile flags"));
@@ -939,7 +946,7 @@ static ws_status pair_out(ws_ctx* ctx, const Geo& g, PairOut& po, cudaStream_t s
 }
 
 template <int CONN>
-static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, int64_t* num_regions,
+static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* L, int64_t* num_regions,
                              cudaStream_t st) {
   const TileGrid tg = tiles_of<CONN>(g);
   Maps mp;
@@ -1055,6 +1062,7 @@ static ws_status watershed_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int
   return WS_OK;
 }
 
+#ifndef WS_PX16
 // ------------------------------------------------------------- z-slab sharded phases
 __global__ void k_mark_layer(uint8_t* cur, int layer, int per_layer) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per_layer; i += gridDim.x * blockDim.x)
@@ -1062,7 +1070,7 @@ __global__ void k_mark_layer(uint8_t* cur, int layer, int per_layer) {
 }
 
 template <int CONN>
-static ws_status shard_first_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, int* pending,
+static ws_status shard_first_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* L, int* pending,
                                cudaStream_t st) {
   const TileGrid tg = tiles_of<CONN>(g);
   Maps mp;
@@ -1090,7 +1098,7 @@ static ws_status shard_first_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
 }
 
 template <int CONN>
-static ws_status shard_round_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* L, int act_lo, int act_hi,
+static ws_status shard_round_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* L, int act_lo, int act_hi,
                                int* pending, cudaStream_t st) {
   const TileGrid tg = tiles_of<CONN>(g);
   if (tg.n != ctx->shard_tiles) {
@@ -1123,7 +1131,7 @@ static ws_status shard_round_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, i
   return WS_OK;
 }
 
-ws_status plateau_first_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int* pending,
+ws_status plateau_first_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* L, int* pending,
                               cudaStream_t st) {
   if (conn == 6) return shard_first_t<6>(ctx, grad, g, L, pending, st);
   if (conn == 26) return shard_first_t<26>(ctx, grad, g, L, pending, st);
@@ -1131,7 +1139,7 @@ ws_status plateau_first_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, in
   return WS_ERR_INVALID;
 }
 
-ws_status plateau_round_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int act_lo,
+ws_status plateau_round_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* L, int act_lo,
                               int act_hi, int* pending, cudaStream_t st) {
   if (conn == 6) return shard_round_t<6>(ctx, grad, g, L, act_lo, act_hi, pending, st);
   if (conn == 26) return shard_round_t<26>(ctx, grad, g, L, act_lo, act_hi, pending, st);
@@ -1140,7 +1148,7 @@ ws_status plateau_round_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, in
 }
 
 template <int CONN>
-static ws_status resolve_shard_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, const int32_t* L, int32_t* P,
+static ws_status resolve_shard_t(ws_ctx* ctx, const Px* grad, const Geo& g, const int32_t* L, int32_t* P,
                                  cudaStream_t st) {
   const TileGrid tg = tiles_of<CONN>(g);
   Maps mp;
@@ -1154,7 +1162,7 @@ static ws_status resolve_shard_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g,
   return WS_OK;
 }
 
-ws_status resolve_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, const int32_t* L, int32_t* P,
+ws_status resolve_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, const int32_t* L, int32_t* P,
                         cudaStream_t st) {
   if (conn == 6) return resolve_shard_t<6>(ctx, grad, g, L, P, st);
   if (conn == 26) return resolve_shard_t<26>(ctx, grad, g, L, P, st);
@@ -1162,7 +1170,9 @@ ws_status resolve_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn
   return WS_ERR_INVALID;
 }
 
-ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* labels,
+#endif  // !WS_PX16
+
+ws_status run_watershed(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* labels,
                         int64_t* num_regions, cudaStream_t st) {
   switch (conn) {
     case 4: return watershed_t<4>(ctx, grad, g, labels, num_regions, st);
@@ -1174,8 +1184,9 @@ ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn
   return WS_ERR_INVALID;
 }
 
+#ifndef WS_PX16
 template <int CONN>
-static ws_status debug_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t* dist, int32_t* parent,
+static ws_status debug_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* dist, int32_t* parent,
                          cudaStream_t st) {
   WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
   int* L = ctx->aux.as<int>();
@@ -1190,7 +1201,7 @@ static ws_status debug_t(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int32_t
   return WS_OK;
 }
 
-ws_status run_plateau_debug(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* dist,
+ws_status run_plateau_debug(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* dist,
                             int32_t* parent, cudaStream_t st) {
   switch (conn) {
     case 4: return debug_t<4>(ctx, grad, g, dist, parent, st);
@@ -1202,4 +1213,9 @@ ws_status run_plateau_debug(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int 
   return WS_ERR_INVALID;
 }
 
+#endif  // !WS_PX16
+
+#ifdef WS_PX16
+}  // namespace px16
+#endif
 }  // namespace ws
