@@ -106,6 +106,16 @@ const char* ws_phase_name(int32_t i);
 ws_status ws_gradient(ws_ctx* ctx, const uint8_t* img, ws_dims dims, float sigma,
                       uint8_t* grad_q, float* blur_f32, float* grad_f32, void* stream);
 
+/* ws_gradient_u16 — ws_gradient on a 16-bit image (NEXT f4; microCT volumes are often
+ * 16-bit): b = G_sigma * (img / 65535) with the same Gaussian (C8) and differences
+ * (C9); grad_q[p] = min(65535, floor(65535 g + 0.5)) (C10 at 16 bits: finer levels, smaller
+ * plateaux).  A u8 image widened by x257 has exactly the same b and g.
+ * Arguments: img u16[N] (in), grad_q u16[N] (out, required), blur_f32 / grad_f32 f32[N]
+ * (optional verify mode), all 2-byte aligned.  Arithmetic is fp32 (separable passes through
+ * two f32[N] workspace arrays).  Errors: as ws_gradient. */
+ws_status ws_gradient_u16(ws_ctx* ctx, const uint16_t* img, ws_dims dims, float sigma,
+                          uint16_t* grad_q, float* blur_f32, float* grad_f32, void* stream);
+
 /* ws_watershed — steps I-IV of PRUF (Alg. 1) + canonical relabel.
  *   Step I   steepest-descent pointer, Eq. 1: among the minimal neighbours
  *            the one with the largest index (C3).

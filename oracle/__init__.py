@@ -39,6 +39,8 @@ def _load():
         lib.oracle_waterfall.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
         lib.oracle_waterfall_reconstruct.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
         lib.oracle_watershed_u16.argtypes = lib.oracle_watershed.argtypes
+        lib.oracle_gradient_u16.argtypes = lib.oracle_gradient.argtypes
+        lib.oracle_gradient_u16.restype = ctypes.c_int
         for f in (lib.oracle_gradient, lib.oracle_watershed, lib.oracle_watershed_u16, lib.oracle_waterfall,
                   lib.oracle_waterfall_reconstruct):
             f.restype = ctypes.c_int
@@ -63,15 +65,18 @@ def _p(a):
 
 
 def gradient(img: np.ndarray, sigma: float, ndim: int = None):
-    """O1+O2: returns (blur f64, grad f64, grad_q u8), each shaped like ``img``."""
+    """O1+O2: returns (blur f64, grad f64, grad_q u8), each shaped like ``img``.  A np.uint16
+    image uses x / 65535 and 16-bit quantisation (O11, NEXT f4; grad_q u16)."""
     orig = img.shape
     if ndim is None:
         ndim = 3 if img.ndim == 3 else 2
-    a, (n0, n1, n2) = _shape3(np.asarray(img, dtype=np.uint8), ndim)
+    wide = isinstance(img, np.ndarray) and img.dtype == np.uint16
+    a, (n0, n1, n2) = _shape3(np.asarray(img, dtype=np.uint16 if wide else np.uint8), ndim)
     blur = np.empty(a.shape, np.float64)
     grad = np.empty(a.shape, np.float64)
-    q = np.empty(a.shape, np.uint8)
-    rc = _load().oracle_gradient(_p(a), ndim, n0, n1, n2, float(sigma), _p(blur), _p(grad), _p(q))
+    q = np.empty(a.shape, np.uint16 if wide else np.uint8)
+    fn = _load().oracle_gradient_u16 if wide else _load().oracle_gradient
+    rc = fn(_p(a), ndim, n0, n1, n2, float(sigma), _p(blur), _p(grad), _p(q))
     if rc != 0:
         raise ValueError("oracle_gradient: invalid arguments")
     return blur.reshape(orig), grad.reshape(orig), q.reshape(orig)

@@ -124,13 +124,16 @@ extern "C" {
 
 // Returns 0 on success, 1 on invalid arguments.  Outputs: blur, grad (fp64, may be NULL),
 // grad_q (u8, may be NULL): q = min(255, floor(255 g + 0.5)) (C10).
-int oracle_gradient(const uint8_t* img, int ndim, int64_t n0, int64_t n1, int64_t n2,
-                    double sigma, double* blur_out, double* grad_out, uint8_t* grad_q) {
+}  // extern "C"
+
+template <class Tin, class Tq>
+int gradient_impl(const Tin* img, int ndim, int64_t n0, int64_t n1, int64_t n2, double sigma, double vmax,
+                  double* blur_out, double* grad_out, Tq* grad_q) {
   Grid g{ndim, n0, n1, n2};
   if ((ndim != 2 && ndim != 3) || n0 < 1 || n1 < 1 || n2 < 1 || !(sigma >= 0)) return 1;
   int64_t N = g.N();
   std::vector<double> b(N);
-  for (int64_t p = 0; p < N; ++p) b[p] = img[p] / 255.0;
+  for (int64_t p = 0; p < N; ++p) b[p] = img[p] / vmax;  // x / 255 (C8); x / 65535 for 16-bit images
   if (sigma > 0) {
     if (ndim == 3) blur_axis(g, b, 0, sigma);
     blur_axis(g, b, 1, sigma);
@@ -149,11 +152,24 @@ int oracle_gradient(const uint8_t* img, int ndim, int64_t n0, int64_t n1, int64_
         if (blur_out) blur_out[p] = b[p];
         if (grad_out) grad_out[p] = gm;
         if (grad_q) {
-          double q = std::floor(255.0 * gm + 0.5);
-          grad_q[p] = (uint8_t)(q > 255.0 ? 255.0 : q);
+          double q = std::floor(vmax * gm + 0.5);  // C10 (vmax = 255); 65535 for 16 bits
+          grad_q[p] = (Tq)(q > vmax ? vmax : q);
         }
       }
   return 0;
+}
+
+extern "C" {
+
+int oracle_gradient(const uint8_t* img, int ndim, int64_t n0, int64_t n1, int64_t n2,
+                    double sigma, double* blur_out, double* grad_out, uint8_t* grad_q) {
+  return gradient_impl(img, ndim, n0, n1, n2, sigma, 255.0, blur_out, grad_out, grad_q);
+}
+
+// 16-bit images (NEXT f4): b = G * (img / 65535), q = min(65535, floor(65535 g + 0.5)).
+int oracle_gradient_u16(const uint16_t* img, int ndim, int64_t n0, int64_t n1, int64_t n2,
+                        double sigma, double* blur_out, double* grad_out, uint16_t* grad_q) {
+  return gradient_impl(img, ndim, n0, n1, n2, sigma, 65535.0, blur_out, grad_out, grad_q);
 }
 
 // ---------------------------------------------------------------------------------

@@ -45,14 +45,17 @@ def _req(t, dtype, name):
 
 def gradient(img: torch.Tensor, sigma: float = 1.0, ndim: int = None, verify: bool = False,
              ctx: Context = None, out: torch.Tensor = None):
-    """ws_gradient: u8 image -> agreed u8 gradient image (and fp32 blur/grad if ``verify``)."""
-    _req(img, torch.uint8, "img")
+    """ws_gradient: u8 image -> agreed u8 gradient image (and fp32 blur/grad if ``verify``).
+    A torch.uint16 image runs ws_gradient_u16 (16-bit in, 16-bit gradient out, NEXT f4)."""
+    wide = isinstance(img, torch.Tensor) and img.dtype == torch.uint16
+    _req(img, torch.uint16 if wide else torch.uint8, "img")
     ndim = ndim if ndim is not None else (3 if img.dim() == 3 and img.shape[0] > 1 else 2)
     ctx = ctx or default_context(img.device.index)
     q = out if out is not None else torch.empty_like(img)
     blur = torch.empty(img.shape, dtype=torch.float32, device=img.device) if verify else None
     grad = torch.empty(img.shape, dtype=torch.float32, device=img.device) if verify else None
-    _b.check(_b.load().ws_gradient(ctx.handle, _b.ptr(img), _b.dims_of(img.shape, ndim), float(sigma),
+    fn = _b.load().ws_gradient_u16 if wide else _b.load().ws_gradient
+    _b.check(fn(ctx.handle, _b.ptr(img), _b.dims_of(img.shape, ndim), float(sigma),
                                    _b.ptr(q), _b.ptr(blur), _b.ptr(grad), _b.stream_of(img)))
     return (q, blur, grad) if verify else q
 

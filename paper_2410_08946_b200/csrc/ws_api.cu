@@ -271,6 +271,29 @@ ws_status ws_gradient(ws_ctx* ctx, const uint8_t* img, ws_dims dims, float sigma
   return s;
 }
 
+ws_status ws_gradient_u16(ws_ctx* ctx, const uint16_t* img, ws_dims dims, float sigma, uint16_t* grad_q,
+                          float* blur_f32, float* grad_f32, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  if (!(sigma >= 0.f) || sigma > 20.f) {
+    set_error(WS_ERR_INVALID, "sigma must be in [0, 20] (got %g)", (double)sigma);
+    return WS_ERR_INVALID;
+  }
+  if (!img) return null_arg("img");
+  if (!grad_q) return null_arg("grad_q");
+  if ((reinterpret_cast<uintptr_t>(img) | reinterpret_cast<uintptr_t>(grad_q)) & 1) {
+    set_error(WS_ERR_INVALID, "img and grad_q must be 2-byte aligned");
+    return WS_ERR_INVALID;
+  }
+  begin_call(ctx, g);
+  tbegin(ctx, (cudaStream_t)stream);
+  ws_status s =
+      run_gradient_u16(ctx, img, g, dims.ndim == 3, sigma, grad_q, blur_f32, grad_f32, (cudaStream_t)stream);
+  tfinish(ctx);
+  return s;
+}
+
 ws_status ws_watershed(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity, int32_t* labels,
                        int64_t* num_regions, void* stream) {
   WS_TRY(check_ctx(ctx));

@@ -22,6 +22,10 @@ __device__ __forceinline__ float load_norm<uint8_t>(const uint8_t* in, size_t i)
   return (float)__ldg(in + i) / 255.0f;
 }
 template <>
+__device__ __forceinline__ float load_norm<uint16_t>(const uint16_t* in, size_t i) {
+  return (float)__ldg(in + i) / 65535.0f;  // 16-bit images (NEXT f4): x / 65535
+}
+template <>
 __device__ __forceinline__ float load_norm<float>(const float* in, size_t i) {
   return __ldg(in + i);
 }
@@ -55,8 +59,9 @@ __device__ __forceinline__ float deriv(const Tin* b, size_t p, int c, int len, i
   return 0.5f * (load_norm<Tin>(b, p + stride) - load_norm<Tin>(b, p - stride));
 }
 
-template <class Tin>
-__global__ void k_gradmag(const Tin* __restrict__ b, Geo g, int is3d, uint8_t* __restrict__ q,
+// Tq = uint8_t: q = min(255, floor(255 g + 0.5)) (C10); Tq = uint16_t: the same with 65535
+template <class Tin, class Tq>
+__global__ void k_gradmag(const Tin* __restrict__ b, Geo g, int is3d, Tq* __restrict__ q,
                           float* __restrict__ blur_out, float* __restrict__ grad_out) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -73,8 +78,9 @@ __global__ void k_gradmag(const Tin* __restrict__ b, Geo g, int is3d, uint8_t* _
     float d2 = deriv<Tin>(b, p, x, g.n2, 1);
     s = fmaf(d2, d2, s);
     const float gm = sqrtf(s);
-    const float qq = floorf(fmaf(255.0f, gm, 0.5f));
-    q[p] = (uint8_t)(qq > 255.f ? 255.f : qq);
+    constexpr float QM = sizeof(Tq) == 1 ? 255.f : 65535.f;
+    const float qq = floorf(fmaf(QM, gm, 0.5f));
+    q[p] = (Tq)(qq > QM ? QM : qq);
     if (blur_out) blur_out[p] = load_norm<Tin>(b, p);
     if (grad_out) grad_out[p] = gm;
   }
@@ -432,7 +438,7 @@ ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, 
     }
   }
   if (sigma == 0.f) {
-    k_gradmag<uint8_t><<<l.grid, l.block, 0, st>>>(img, g, is3d, grad_q, blur_f32, grad_f32);
+    k_gradmag<uint8_t, uint8_t><<<l.grid, l.block, 0, st>>>(img, g, is3d, grad_q, blur_f32, grad_f32);
     launched(ctx, PH_GRAD_MAG);
     tmark(ctx, st, PH_GRAD_MAG);
     WS_CUDA(cudaGetLastError());
@@ -463,7 +469,52 @@ ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, 
     launched(ctx, PH_GRAD_BLUR, 2);
   }
   tmark(ctx, st, PH_GRAD_BLUR);
-  k_gradmag<float><<<l.grid, l.block, 0, st>>>(fin, g, is3d, grad_q, blur_f32, grad_f32);
+  k_gradmag<float, uint8_t><<<l.grid, l.block, 0, st>>>(fin, g, is3d, grad_q, blur_f32, grad_f32);
+  launched(ctx, PH_GRAD_MAG);
+  tmark(ctx, st, PH_GRAD_MAG);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
+// 16-bit images (NEXT f4): b = G_sigma * (img / 65535), q = min(65535, floor(65535 g
+// + 0.5)).  The generic separable path (fp32 scratch between the axis passes, then one
+// gradient + quantise pass); the fused u8 tile / streaming kernels are not instantiated for u16.
+ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma,
+                           uint16_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st) {
+  L3 l = launch3(g);
+  if (sigma == 0.f) {
+    k_gradmag<uint16_t, uint16_t><<<l.grid, l.block, 0, st>>>(img, g, is3d, grad_q, blur_f32, grad_f32);
+    launched(ctx, PH_GRAD_MAG);
+    tmark(ctx, st, PH_GRAD_MAG);
+    WS_CUDA(cudaGetLastError());
+    return WS_OK;
+  }
+  const int r = (int)floor(3.0 * (double)sigma + 0.5);
+  float w[2 * RMAX + 1];
+  double ws = 0, wd[2 * RMAX + 1];
+  for (int i = -r; i <= r; ++i) { wd[i + r] = exp(-(double)i * i / (2.0 * sigma * (double)sigma)); ws += wd[i + r]; }
+  for (int i = 0; i <= 2 * r; ++i) w[i] = (float)(wd[i] / ws);
+  WS_CUDA(cudaMemcpyToSymbolAsync(c_w, w, sizeof(float) * (2 * r + 1), 0, cudaMemcpyHostToDevice, st));
+  const size_t nb = (size_t)g.N * sizeof(float);
+  WS_TRY(ctx->tmpA.ensure(nb, "gradient scratch A"));
+  WS_TRY(ctx->tmpB.ensure(nb, "gradient scratch B"));
+  float* A = ctx->tmpA.as<float>();
+  float* B = ctx->tmpB.as<float>();
+  const float* fin;
+  if (is3d) {
+    k_blur_axis<uint16_t><<<l.grid, l.block, 0, st>>>(img, A, g, 0, r);
+    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(A, B, g, 1, r);
+    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(B, A, g, 2, r);
+    fin = A;
+    launched(ctx, PH_GRAD_BLUR, 3);
+  } else {
+    k_blur_axis<uint16_t><<<l.grid, l.block, 0, st>>>(img, A, g, 1, r);
+    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(A, B, g, 2, r);
+    fin = B;
+    launched(ctx, PH_GRAD_BLUR, 2);
+  }
+  tmark(ctx, st, PH_GRAD_BLUR);
+  k_gradmag<float, uint16_t><<<l.grid, l.block, 0, st>>>(fin, g, is3d, grad_q, blur_f32, grad_f32);
   launched(ctx, PH_GRAD_MAG);
   tmark(ctx, st, PH_GRAD_MAG);
   WS_CUDA(cudaGetLastError());

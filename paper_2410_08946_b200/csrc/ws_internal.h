@@ -123,6 +123,8 @@ ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, 
                        uint8_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st);
 ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
                         int32_t* labels, int64_t* num_regions, cudaStream_t st);
+ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma,
+                           uint16_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st);
 namespace px16 {  // ws_watershed16.cu: the same watershed on u16 pixels (unsharded)
 ws_status run_watershed(ws_ctx* ctx, const uint16_t* grad, const Geo& g, int conn, int32_t* labels,
                         int64_t* num_regions, cudaStream_t st);

@@ -43,3 +43,42 @@ def test_hand_cases_need_16_bits():
     # full-range extremes: 65535 descends to 0 on both sides; 65534 is a strict minimum
     c = np.array([[65535, 0, 65535, 65534]], np.uint16)
     assert oracle.watershed(c, 4, ndim=2).tolist() == [[0, 0, 0, 3]]
+
+
+# ---- O11: the 16-bit gradient (x / 65535, q = min(65535, floor(65535 g + 0.5)))
+@pytest.mark.parametrize("sigma", [0.0, 0.6, 1.0, 2.0])
+@pytest.mark.parametrize("ndim,shape", [(2, (2, 9, 14)), (3, (6, 7, 9))])
+def test_u8_widened_by_257_has_the_same_blur_and_gradient(sigma, ndim, shape):
+    """img / 255 == (257 img) / 65535 exactly, so blur and g equal the pinned u8 oracle's."""
+    rng = np.random.default_rng(int(sigma * 10) + ndim)
+    a = rng.integers(0, 256, shape).astype(np.uint8)
+    b8, g8, _ = oracle.gradient(a, sigma, ndim=ndim)
+    b16, g16, q16 = oracle.gradient(a.astype(np.uint16) * 257, sigma, ndim=ndim)
+    assert np.max(np.abs(b8 - b16)) <= 1e-12 and np.max(np.abs(g8 - g16)) <= 1e-12
+    assert q16.dtype == np.uint16
+
+
+@pytest.mark.parametrize("slope", [1, 37, 1234])
+def test_ramp_closed_form_16bit(slope):
+    """img = slope * x: central and one-sided differences both give g = slope / 65535, so
+    q = slope exactly (no blur); with a symmetric normalised blur the ramp is preserved away
+    from the clamped ends, so the interior keeps q = slope."""
+    n = 48
+    img = (np.arange(n, dtype=np.int64) * slope).astype(np.uint16).reshape(1, 1, n)
+    _, g, q = oracle.gradient(img, 0.0, ndim=2)
+    assert np.all(q == slope)
+    assert np.allclose(g, slope / 65535.0, rtol=0, atol=1e-15)
+    _, g1, q1 = oracle.gradient(img, 1.0, ndim=2)  # r = 3: x in [4, n - 5] is interior
+    assert np.all(q1.ravel()[4:n - 4] == slope)
+    vol = np.broadcast_to(img.reshape(1, 1, n), (5, 6, n)).copy()
+    _, _, q3 = oracle.gradient(vol, 0.0, ndim=3)  # constant along z and y: d0 = d1 = 0
+    assert np.all(q3 == slope)
+
+
+def test_steep_ramp_clips_at_65535():
+    img = np.array([[0, 65535, 0, 65535]], np.uint16)
+    _, g, q = oracle.gradient(img, 0.0, ndim=2)
+    assert q.tolist() == [[65535, 0, 0, 65535]]  # one-sided ends g = 1; centres (b[x+1]-b[x-1])/2 = 0
+    chk = np.array([[0, 65535], [65535, 0]], np.uint16)  # |dx| = |dy| = 1 everywhere: g = sqrt 2
+    _, g2, q2 = oracle.gradient(chk, 0.0, ndim=2)
+    assert np.allclose(g2, np.sqrt(2.0)) and np.all(q2 == 65535)  # clipped (C10 at 16 bits)

@@ -70,3 +70,40 @@ def test_u16_edge_cases():
     for img, conn, ndim in [(np.zeros((1, 1, 1), np.uint16), 6, 3), (np.full((3, 5, 7), 65535, np.uint16), 26, 3),
                             (np.arange(64, dtype=np.uint16).reshape(1, 1, 64) * 1000, 4, 2)]:
         _check(img, conn, ndim)
+
+
+FTOL = 1e-5  # north_star float tolerance (as for the u8 gradient)
+
+
+@pytest.mark.parametrize("sigma", [0.0, 1.0, 1.7])
+@pytest.mark.parametrize("ndim,shape", [(3, (13, 19, 37)), (2, (2, 45, 70))])
+def test_u16_gradient_parity_and_pipeline(sigma, ndim, shape):
+    """ws_gradient_u16 vs O11: floats within 1e-5, q equal except on boundary straddles
+    (C11 at 16 bits: |65535 g - (k + 1/2)| <= 65535 tol, off by one); then the watershed of
+    the agreed u16 image is bit-exact vs O10."""
+    ws = _ws()
+    rng = np.random.default_rng(int(sigma * 10) + ndim)
+    f = rng.standard_normal(shape)
+    img = np.floor((f - f.min()) / (np.ptp(f) + 1e-12) * 65535).astype(np.uint16)
+    q, blur, grad = ws.gradient(torch.from_numpy(img).cuda(), sigma, ndim=ndim, verify=True)
+    ob, og, oq = oracle.gradient(img, sigma, ndim=ndim)
+    assert q.dtype == torch.uint16
+    assert np.max(np.abs(blur.cpu().numpy() - ob)) <= FTOL
+    assert np.max(np.abs(grad.cpu().numpy() - og)) <= FTOL
+    qn = q.cpu().numpy()
+    diff = qn != oq
+    if diff.any():
+        t = 65535.0 * og[diff]
+        assert np.all(np.abs(t - np.floor(t) - 0.5) <= 65535 * FTOL), "u16 quantisation mismatch"
+        assert np.all(np.abs(qn[diff].astype(int) - oq[diff].astype(int)) == 1)
+    conn = 6 if ndim == 3 else 8
+    _check(qn, conn, ndim)
+
+
+def test_u16_gradient_of_widened_u8_matches_u8_floats():
+    ws = _ws()
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, 256, (9, 20, 33)).astype(np.uint8)
+    _, b8, g8 = ws.gradient(torch.from_numpy(a).cuda(), 1.0, ndim=3, verify=True)
+    _, b16, g16 = ws.gradient(torch.from_numpy(a.astype(np.uint16) * 257).cuda(), 1.0, ndim=3, verify=True)
+    assert torch.max(torch.abs(b8 - b16)).item() <= 1e-6 and torch.max(torch.abs(g8 - g16)).item() <= 1e-6
