@@ -633,10 +633,7 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
 }
 
 template <int CONN, bool DEBUG>
-#ifndef WS_RESOLVE_MINB
-#define WS_RESOLVE_MINB 1
-#endif
-__global__ void __launch_bounds__(NT, WS_RESOLVE_MINB) k_resolve(const __grid_constant__ CUtensorMap mI,
+__global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensorMap mI,
                                                 const __grid_constant__ CUtensorMap mL, int tma,
                                                 const Px* __restrict__ I, const int* __restrict__ L, Geo g,
                                                 int ntx, int nty, int* __restrict__ P, int* __restrict__ dist,
