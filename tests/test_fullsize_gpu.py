@@ -73,6 +73,10 @@ def _shift(a, axis, d, fill):
 
 def test_watershed_properties(c4):
     _, q, _, _, lab, R, _, _ = c4
+    _check_watershed_properties(q, lab, R)
+
+
+def _check_watershed_properties(q, lab, R):
     N = lab.numel()
     idx = torch.arange(N, device="cuda", dtype=torch.int64).view(SHAPE)
     l64 = lab.long()
@@ -83,7 +87,7 @@ def test_watershed_properties(c4):
     # Eq. 1 target of every voxel: among the 6 neighbours with the minimum value, the largest
     # index; neighbours in increasing index order are (z-1), (y-1), (x-1), (x+1), (y+1), (z+1)
     order = [(0, -1), (1, -1), (2, -1), (2, 1), (1, 1), (0, 1)]
-    best = torch.full_like(I, 256)
+    best = torch.full_like(I, 1 << 16)  # above every u8 / u16 value
     tgt = torch.full_like(l64, -1)
     for axis, d in order:
         nv = _shift(I, axis, d, 1 << 20)
@@ -115,3 +119,40 @@ def test_waterfall_properties(c4):
         assert int((cur == ar).sum()) == counts[k]
         assert counts[k] <= counts[k - 1] and (counts[k - 1] <= 1 or 2 * counts[k] <= counts[k - 1])
     assert torch.equal(levels[0], lab)
+
+
+# ---- NEXT f4 at the full C4 shape: a 16-bit volume (the u8 volume as the high byte, seeded
+# low byte, as in bench.py), ws_gradient_u16 sampled crops vs O11 and the properties of
+# ws_watershed_u16 on its gradient
+def test_u16_fullsize_gradient_crops_and_watershed():
+    import paper_2410_08946_b200 as ws
+    raw = synth.make_config_image("C4", device="cuda", shape=SHAPE)
+    gen = torch.Generator(device="cuda").manual_seed(4242)
+    raw16 = (raw.to(torch.int32) * 256 + torch.randint(0, 256, SHAPE, generator=gen, device="cuda",
+                                                       dtype=torch.int32)).to(torch.uint16)
+    del raw
+    q, blur, grad = ws.gradient(raw16, 1.0, ndim=3, verify=True)
+    rng = np.random.default_rng(16)
+    D, H, W = SHAPE
+    M, C = 4, 10
+    corners = [(0, 0, 0), (D - C, H - C, W - C)] + [tuple(int(rng.integers(0, s - C + 1)) for s in SHAPE)
+                                                   for _ in range(6)]
+    for z, y, x in corners:
+        z0, y0, x0 = max(z - M, 0), max(y - M, 0), max(x - M, 0)
+        z1, y1, x1 = min(z + C + M, D), min(y + C + M, H), min(x + C + M, W)
+        crop = raw16[z0:z1, y0:y1, x0:x1].cpu().numpy()
+        ob, og, oq = oracle.gradient(crop, 1.0, ndim=3)
+        sl = (slice(z - z0, z - z0 + C), slice(y - y0, y - y0 + C), slice(x - x0, x - x0 + C))
+        gs = (slice(z, z + C), slice(y, y + C), slice(x, x + C))
+        assert np.max(np.abs(blur[gs].cpu().numpy() - ob[sl])) <= FTOL
+        assert np.max(np.abs(grad[gs].cpu().numpy() - og[sl])) <= FTOL
+        qg, qo, go = q[gs].cpu().numpy(), oq[sl], og[sl]
+        diff = qg != qo
+        if diff.any():
+            t = 65535.0 * go[diff]
+            assert np.all(np.abs(t - np.floor(t) - 0.5) <= 65535 * FTOL)
+            assert np.all(np.abs(qg[diff].astype(int) - qo[diff].astype(int)) == 1)
+    del blur, grad, raw16
+    torch.cuda.empty_cache()
+    lab, R = ws.watershed(q, 6, ndim=3)
+    _check_watershed_properties(q, lab, R)
