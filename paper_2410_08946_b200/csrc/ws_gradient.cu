@@ -5,6 +5,7 @@
 // then one fused gradient + quantise pass.  HBM-bound; see DESIGN.md §Kernels.
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "ws_internal.h"
 #include "ws_tma.cuh"
@@ -14,6 +15,7 @@ namespace ws {
 constexpr int RMAX = 60;  // sigma <= 20  ->  r = floor(3 sigma + 0.5) <= 60
 __constant__ float c_w[2 * RMAX + 1];
 __constant__ float c_w255[2 * RMAX + 1];  // w / 255: the x pass reads raw u8
+__constant__ float c_w65535[2 * RMAX + 1];  // w / 65535: the same for 16-bit images (NEXT f4)
 
 template <class Tin>
 __device__ __forceinline__ float load_norm(const Tin* in, size_t i);
@@ -233,41 +235,45 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
 // while the current one is blurred.  HBM traffic: 1 B in + 1 B out per voxel.
 constexpr int GSX = 32, GSY = 16, GZC = 64;
 
-template <int R>
-__global__ void __launch_bounds__(256) k_grad_stream(const uint8_t* __restrict__ img, Geo g, int ntx, int nty,
-                                                     uint8_t* __restrict__ q, float* __restrict__ blur_out,
+// Px = uint8_t (C10) or uint16_t (16-bit images, NEXT f4: x / 65535, 16-bit quantisation);
+// a load "word" is 4 consecutive pixels either way (u32 / u64).
+template <int R, class Px>
+__global__ void __launch_bounds__(256) k_grad_stream(const Px* __restrict__ img, Geo g, int ntx, int nty,
+                                                     Px* __restrict__ q, float* __restrict__ blur_out,
                                                      float* __restrict__ grad_out) {
+  using Wd = typename std::conditional<sizeof(Px) == 1, uint32_t, unsigned long long>::type;
   constexpr int H = R + 1, K = 2 * R + 1;
   constexpr int XO = H <= 4 ? 4 : 8, SX = GSX + 2 * XO, SY = GSY + 2 * H, WPR = SX / 4;
   constexpr int AX = GSX + 2, AXP = (AX + 3) / 4 * 4, BY = GSY + 2, PL = BY * AX;
   constexpr int RG = 3, NRG = BY / RG;  // a y/z thread owns RG consecutive rows of one column
   static_assert(BY % RG == 0 && AX * NRG <= 256, "y/z thread layout");
-  __shared__ __align__(16) uint8_t sIn[SY * SX + 16];  // +16: the last x-blur group reads past the row (padding outputs)
+  __shared__ __align__(16) Px sIn[SY * SX + 16];  // +16: the last x-blur group reads past the row (padding outputs)
   __shared__ float X[SY * AXP];
   __shared__ float B[3 * PL];
   const int t0 = blockIdx.x;
   const int bx = (t0 % ntx) * GSX, by = ((t0 / ntx) % nty) * GSY, z0 = (t0 / (ntx * nty)) * GZC;
   const int z1 = min(z0 + GZC, g.n0);
-  const bool wide = bx >= XO && bx + GSX + XO <= g.n2 && (g.n2 & 3) == 0;  // aligned word loads
+  const bool wide = bx >= XO && bx + GSX + XO <= g.n2 && (g.n2 & 3) == 0 &&
+                    (reinterpret_cast<uintptr_t>(img) & (sizeof(Wd) - 1)) == 0;  // aligned word loads
   const bool inner = bx > 0 && bx + GSX < g.n2 && by > 0 && by + GSY < g.n1;  // no x/y border voxel
   constexpr int LJ = (SY * WPR + 255) / 256;  // load jobs (words) per thread
-  uint32_t pre[LJ];
+  Wd pre[LJ];
   auto load = [&](int zi) {  // words of input plane clamp(zi) into registers
     const int zc = min(max(zi, 0), g.n0 - 1);
 #pragma unroll
     for (int u = 0; u < LJ; ++u) {
       const int job = threadIdx.x + u * 256;
-      uint32_t v = 0;
+      Wd v = 0;
       if (job < SY * WPR) {
         const int row = job / WPR, w = job % WPR;
         const int gy = min(max(by + row - H, 0), g.n1 - 1);
-        const uint8_t* rowp = img + (size_t)zc * g.plane + (size_t)gy * g.n2;
+        const Px* rowp = img + (size_t)zc * g.plane + (size_t)gy * g.n2;
         const int gx = bx - XO + 4 * w;
         if (wide) {
-          v = __ldg(reinterpret_cast<const uint32_t*>(rowp + gx));
+          v = __ldg(reinterpret_cast<const Wd*>(rowp + gx));
         } else {
 #pragma unroll
-          for (int b = 0; b < 4; ++b) v |= (uint32_t)__ldg(rowp + min(max(gx + b, 0), g.n2 - 1)) << (8 * b);
+          for (int b = 0; b < 4; ++b) v |= (Wd)__ldg(rowp + min(max(gx + b, 0), g.n2 - 1)) << (8 * sizeof(Px) * b);
         }
       }
       pre[u] = v;
@@ -290,14 +296,14 @@ __global__ void __launch_bounds__(256) k_grad_stream(const uint8_t* __restrict__
 #pragma unroll
     for (int u = 0; u < LJ; ++u) {
       const int job = threadIdx.x + u * 256;
-      if (job < SY * WPR) reinterpret_cast<uint32_t*>(sIn)[job] = pre[u];
+      if (job < SY * WPR) reinterpret_cast<Wd*>(sIn)[job] = pre[u];
     }
     __syncthreads();
     if (t + 1 < nin) load(zi + 1);  // in flight during the blur of this plane
     // x blur: 4 consecutive outputs x' = 4 grp - 1 .. + 3 (x' in [-1, GSX]) per job
     for (int job = threadIdx.x; job < SY * (AXP / 4); job += 256) {
       const int grp = job % (AXP / 4), row = job / (AXP / 4);
-      const uint8_t* src = sIn + row * SX + XO - 1 + 4 * grp - R;
+      const Px* src = sIn + row * SX + XO - 1 + 4 * grp - R;
       float v[4 + 2 * R];
 #pragma unroll
       for (int jj = 0; jj < 4 + 2 * R; ++jj) v[jj] = (float)src[jj];
@@ -307,7 +313,8 @@ __global__ void __launch_bounds__(256) k_grad_stream(const uint8_t* __restrict__
       for (int oo = 0; oo < 4; ++oo) {
         float acc = 0.f;
 #pragma unroll
-        for (int i = 0; i <= 2 * R; ++i) acc = fmaf(c_w255[i], v[oo + i], acc);  // w / 255 folded in
+        for (int i = 0; i <= 2 * R; ++i)  // w / 255 (w / 65535) folded in
+          acc = fmaf(sizeof(Px) == 1 ? c_w255[i] : c_w65535[i], v[oo + i], acc);
         o[oo] = acc;
       }
       *reinterpret_cast<float4*>(X + row * AXP + 4 * grp) = o4;
@@ -370,20 +377,21 @@ __global__ void __launch_bounds__(256) k_grad_stream(const uint8_t* __restrict__
       ss = fmaf(dy, dy, ss);
       ss = fmaf(dz, dz, ss);
       const float gm = sqrtf(ss);
-      const float qq = floorf(fmaf(255.0f, gm, 0.5f));
+      constexpr float QM = sizeof(Px) == 1 ? 255.f : 65535.f;
+      const float qq = floorf(fmaf(QM, gm, 0.5f));
       const size_t p = (size_t)zo * g.plane + (size_t)gy * g.n2 + gx;
-      q[p] = (uint8_t)(qq > 255.f ? 255.f : qq);
+      q[p] = (Px)(qq > QM ? QM : qq);
       if (blur_out) blur_out[p] = v;
       if (grad_out) grad_out[p] = gm;
     }
   }
 }
 
-template <int R>
-static ws_status grad_stream_t(ws_ctx* ctx, const uint8_t* img, const Geo& g, uint8_t* q, float* blur, float* grad,
+template <int R, class Px>
+static ws_status grad_stream_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, float* blur, float* grad,
                                cudaStream_t st) {
   const int ntx = (g.n2 + GSX - 1) / GSX, nty = (g.n1 + GSY - 1) / GSY, ntz = (g.n0 + GZC - 1) / GZC;
-  k_grad_stream<R><<<ntx * nty * ntz, 256, 0, st>>>(img, g, ntx, nty, q, blur, grad);
+  k_grad_stream<R, Px><<<ntx * nty * ntz, 256, 0, st>>>(img, g, ntx, nty, q, blur, grad);
   launched(ctx, PH_GRAD_MAG);
   tmark(ctx, st, PH_GRAD_MAG);
   WS_CUDA(cudaGetLastError());
@@ -482,6 +490,24 @@ ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, 
 ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma,
                            uint16_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st) {
   L3 l = launch3(g);
+  const int rr = sigma > 0.f ? (int)floor(3.0 * (double)sigma + 0.5) : 0;
+  if (is3d && rr >= 1 && rr <= 4) {  // volumes: the 2.5-D streaming kernel on u16 pixels
+    float w[2 * RMAX + 1], wq[2 * RMAX + 1];
+    double wsum = 0, wd[2 * RMAX + 1];
+    for (int i = -rr; i <= rr; ++i) { wd[i + rr] = exp(-(double)i * i / (2.0 * sigma * (double)sigma)); wsum += wd[i + rr]; }
+    for (int i = 0; i <= 2 * rr; ++i) {
+      w[i] = (float)(wd[i] / wsum);
+      wq[i] = (float)(wd[i] / wsum / 65535.0);
+    }
+    WS_CUDA(cudaMemcpyToSymbolAsync(c_w, w, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
+    WS_CUDA(cudaMemcpyToSymbolAsync(c_w65535, wq, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
+    switch (rr) {
+      case 1: return grad_stream_t<1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 2: return grad_stream_t<2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 3: return grad_stream_t<3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      default: return grad_stream_t<4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+    }
+  }
   if (sigma == 0.f) {
     k_gradmag<uint16_t, uint16_t><<<l.grid, l.block, 0, st>>>(img, g, is3d, grad_q, blur_f32, grad_f32);
     launched(ctx, PH_GRAD_MAG);
