@@ -660,6 +660,21 @@ __global__ void k_levelmap(const int* __restrict__ comp, const uint8_t* __restri
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < R; d += gridDim.x * blockDim.x) {
     int x = d;
     int* row = levelmap + (size_t)d * stride;
+    if (stride == 4 || stride == 8) {  // the row in registers, written with 16-byte stores
+      int r[8];
+      r[0] = __ldg(rep_of + d);
+#pragma unroll
+      for (int k = 1; k < 8; ++k) {
+        r[k] = 0;  // padding of the row (read by 16-byte loads)
+        if (k < NL) {
+          while (__ldg(lvl + x) <= k) x = __ldg(comp + x);
+          r[k] = __ldg(rep_of + x);
+        }
+      }
+      reinterpret_cast<int4*>(row)[0] = make_int4(r[0], r[1], r[2], r[3]);
+      if (stride == 8) reinterpret_cast<int4*>(row)[1] = make_int4(r[4], r[5], r[6], r[7]);
+      continue;
+    }
     row[0] = __ldg(rep_of + d);
     for (int k = 1; k < NL; ++k) {
       while (__ldg(lvl + x) <= k) x = __ldg(comp + x);
