@@ -607,18 +607,21 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
   } else {
     __syncthreads();
   }
-  // one in-place pointer-jumping round (sP[j] = sP[sP[j]] where that is again an in-tile
+  // two in-place pointer-jumping rounds (sP[j] = sP[sP[j]] where that is again an in-tile
   // pointer; a racing reader sees the old or the new value, both ancestors), then the walk
+#pragma unroll 1
+  for (int round = 0; round < 2; ++round) {
 #pragma unroll
-  for (int k = 0; k < T::VPT; ++k) {
-    const int j = threadIdx.x + k * NT;
-    const int jn = sP[j];
-    if (jn >= 0) {
-      const int jj = sP[jn];
-      if (jj >= 0) sP[j] = (short)jj;
+    for (int k = 0; k < T::VPT; ++k) {
+      const int j = threadIdx.x + k * NT;
+      const int jn = sP[j];
+      if (jn >= 0) {
+        const int jj = sP[jn];
+        if (jj >= 0) sP[j] = (short)jj;
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
   // tile-local path reduction: follow in-tile pointers to a root or to the tile exit (a
   // serial walk per voxel measured faster than pointer doubling with block-wide rounds)
   const int base = (int)((size_t)c.bz * g.plane + (size_t)c.by * g.n2 + c.bx);
