@@ -349,9 +349,10 @@ __device__ __forceinline__ void relax_first_body(const Px* sI, int* sD, int* __r
     L[(size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx] = 0;
   }
   const bool marked = write_back<CONN>(sD, s0, eqm, plat, L, g, c, t, ntx, nty, next);
-  const int hp = __syncthreads_or(plat != 0);
-  if (threadIdx.x == 0) hasplat[t] = hp ? 1 : 0;
-  if (__syncthreads_or(marked) && threadIdx.x == 0) flags[0] = 1;
+  // no block barriers: one idempotent store per warp (hasplat is zeroed by the host)
+  const bool lane0 = (threadIdx.x & 31) == 0;
+  if (__any_sync(0xffffffffu, plat != 0) && lane0) hasplat[t] = 1;
+  if (__any_sync(0xffffffffu, marked) && lane0) flags[0] = 1;
 }
 
 template <int CONN>
@@ -912,7 +913,7 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   int* list = ctx->tlist.as<int>();
   const int gl = std::max(1, std::min((tg.n + NT - 1) / NT, ctx->num_sms * 8));
   WS_CUDA(cudaMemsetAsync(flags, 0, 5 * sizeof(int), st));
-  WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
+  WS_CUDA(cudaMemsetAsync(next, 0, 2 * (size_t)tg.n, st));  // next and hasplat
   k_relax_first<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, next, hasplat, flags);
   k_tile_list<<<gl, NT, 0, st>>>(next, hasplat, tg.n, list, flags + 4);
   launched(ctx, PH_WS_INIT, 2);
@@ -1097,6 +1098,7 @@ static ws_status shard_first_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   uint8_t* hasplat = a + 2 * tg.n;
   WS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(a, 0, tg.n, st));
+  WS_CUDA(cudaMemsetAsync(hasplat, 0, tg.n, st));
   k_relax_first<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, a, hasplat, flags);
   launched(ctx, PH_WS_INIT);
   ctx->shard_tiles = tg.n;
