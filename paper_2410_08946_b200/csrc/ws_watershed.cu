@@ -400,7 +400,7 @@ __device__ __forceinline__ void relax_round_body(const Px* sI, int* sD, int* __r
   }
   const unsigned changed = relax_tile_q<CONN, true>(sD, s0, eqm, flags + 1, q);
   const bool marked = write_back<CONN>(sD, s0, eqm, changed, L, g, c, t, ntx, nty, next);
-  if (__syncthreads_or(marked) && threadIdx.x == 0) flags[0] = 1;
+  if (__any_sync(0xffffffffu, marked) && (threadIdx.x & 31) == 0) flags[0] = 1;  // idempotent, no barrier
 }
 
 template <int CONN>
