@@ -31,3 +31,14 @@ for name, shape, conn, nd in (("C1", None, 4, 2), ("C4", (20, 48, 64), 6, 3)):
         labs, levs, counts, Rs, _ = shard.sharded_segment(tr, ctxs, slabs, grads, 6, conn)
         assert np.array_equal(torch.cat(labs).cpu().numpy(), ref)
     print(name, "ok", R, c, c2)
+
+# 16-bit images (NEXT f4): gradient (streaming kernel and generic path) + watershed
+rng = np.random.default_rng(7)
+for shape, conn, nd, sig in (((20, 48, 64), 6, 3, 1.0), ((18, 40, 36), 26, 3, 2.0), ((2, 70, 96), 8, 2, 1.0)):
+    f = rng.standard_normal(shape)
+    img = np.floor((f - f.min()) / (np.ptp(f) + 1e-12) * 65535).astype(np.uint16)
+    q16 = ws.gradient(torch.from_numpy(img).cuda(), sig, ndim=nd)
+    lab16, R16 = ws.watershed(q16, conn, ndim=nd)
+    qn16 = q16.cpu().numpy()
+    assert np.array_equal(lab16.cpu().numpy(), oracle.watershed(qn16, conn, ndim=nd))
+    print("u16", shape, conn, "ok", R16)
