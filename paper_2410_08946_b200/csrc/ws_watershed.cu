@@ -867,7 +867,7 @@ __global__ void __launch_bounds__(NT) k_relabel4(const int* __restrict__ P, int*
   const int4* P4 = reinterpret_cast<const int4*>(P);
   int4* L4 = reinterpret_cast<int4*>(L);
   for (int i = blockIdx.x * NT + threadIdx.x; i < n4; i += gridDim.x * NT) {
-    const int4 t = __ldcs(P4 + i);
+    const int4 t = __ldg(P4 + i);  // not evict-first: the root entries it gathers share these lines
     int4 o;
     o.x = relabel_one(P, t.x);
     o.y = t.y == t.x ? o.x : relabel_one(P, t.y);
