@@ -111,9 +111,10 @@ ws_status ws_gradient(ws_ctx* ctx, const uint8_t* img, ws_dims dims, float sigma
  * (C9); grad_q[p] = min(65535, floor(65535 g + 0.5)) (C10 at 16 bits: finer levels, smaller
  * plateaux).  A u8 image widened by x257 has exactly the same b and g.
  * Arguments: img u16[N] (in), grad_q u16[N] (out, required), blur_f32 / grad_f32 f32[N]
- * (optional verify mode), all 2-byte aligned.  Arithmetic is fp32: volumes with
- * r = floor(3 sigma + 0.5) in 1..4 use the streaming kernel of ws_gradient, other cases
- * separable passes through two f32[N] workspace arrays.  Errors: as ws_gradient. */
+ * (optional verify mode), all 2-byte aligned.  Arithmetic is fp32: with r = floor(3 sigma
+ * + 0.5) in 1..4 the kernels of ws_gradient run on u16 pixels (volumes: streaming kernel,
+ * 2-D: tile kernel), other cases separable passes through two f32[N] workspace arrays.
+ * Errors: as ws_gradient. */
 ws_status ws_gradient_u16(ws_ctx* ctx, const uint16_t* img, ws_dims dims, float sigma,
                           uint16_t* grad_q, float* blur_f32, float* grad_f32, void* stream);
 

@@ -100,10 +100,10 @@ template <bool IS3D> struct GT {
   static constexpr int XO = 16, SXB = TX + 32;  // box x: [bx - 16, bx + TX + 16)
 };
 
-template <bool IS3D, int R>
+template <bool IS3D, int R, class Px>  // Px: u8 (C10) or u16 (NEXT f4: x / 65535, 16-bit q)
 __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUtensorMap mImg, int tma,
-                                                    const uint8_t* __restrict__ img, Geo g, int ntx, int nty,
-                                                    uint8_t* __restrict__ q, float* __restrict__ blur_out,
+                                                    const Px* __restrict__ img, Geo g, int ntx, int nty,
+                                                    Px* __restrict__ q, float* __restrict__ blur_out,
                                                     float* __restrict__ grad_out) {
   using T = GT<IS3D>;
   constexpr int H = R + 1;
@@ -111,8 +111,8 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
   constexpr int AX = T::TX + 2;                                 // blurred x range [-1, TX]
   constexpr int BY = T::TY + 2, CZ = IS3D ? T::TZ + 2 : 1;
   extern __shared__ __align__(128) unsigned char gsm[];
-  uint8_t* sIn = gsm;                                           // [SZB][SYB][SXB] u8
-  float* A = reinterpret_cast<float*>(gsm + ((SZB * SYB * T::SXB + 127) / 128) * 128);  // [SZB][SYB][AX]
+  Px* sIn = reinterpret_cast<Px*>(gsm);                         // [SZB][SYB][SXB] pixels
+  float* A = reinterpret_cast<float*>(gsm + ((SZB * SYB * T::SXB * (int)sizeof(Px) + 127) / 128) * 128);  // [SZB][SYB][AX]
   float* B = A + SZB * SYB * AX;                                // [SZB][BY][AX]
   float* C = IS3D ? A : B;                                      // [CZ][BY][AX] (reuses A in 3-D)
   __shared__ uint64_t bar;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
-      mbar_expect_tx(&bar, SZB * SYB * T::SXB);
+      mbar_expect_tx(&bar, SZB * SYB * T::SXB * (int)sizeof(Px));
       tma_load_3d(sIn, &mImg, bx - T::XO, by - H, IS3D ? bz - H : bz, &bar);
     }
     mbar_wait(&bar, 0);
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
   constexpr int AXP = (AX + 3) / 4 * 4;
   for (int job = threadIdx.x; job < SZB * SYB * (AXP / 4); job += 256) {
     const int grp = job % (AXP / 4), row = job / (AXP / 4);
-    const uint8_t* src = sIn + row * T::SXB + T::XO - 1 + 4 * grp - R;
+    const Px* src = sIn + row * T::SXB + T::XO - 1 + 4 * grp - R;
     float v[4 + 2 * R];
 #pragma unroll
     for (int j = 0; j < 4 + 2 * R; ++j) v[j] = (float)src[j];
@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
       if (x >= AX) break;
       float acc = 0.f;
 #pragma unroll
-      for (int i = 0; i <= 2 * R; ++i) acc = fmaf(c_w255[i], v[o + i], acc);  // w / 255 folded in
+      for (int i = 0; i <= 2 * R; ++i)  // w / 255 (w / 65535) folded in
+        acc = fmaf(sizeof(Px) == 1 ? c_w255[i] : c_w65535[i], v[o + i], acc);
       A[row * AX + x] = acc;
     }
   }
@@ -214,9 +215,10 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
       ss = fmaf(d, d, ss);
     }
     const float gm = sqrtf(ss);
-    const float qq = floorf(fmaf(255.0f, gm, 0.5f));
+    constexpr float QM = sizeof(Px) == 1 ? 255.f : 65535.f;
+    const float qq = floorf(fmaf(QM, gm, 0.5f));
     const size_t p = (size_t)gz * g.plane + (size_t)gy * g.n2 + gx;
-    q[p] = (uint8_t)(qq > 255.f ? 255.f : qq);
+    q[p] = (Px)(qq > QM ? QM : qq);
     if (blur_out) blur_out[p] = v;
     if (grad_out) grad_out[p] = gm;
   }
@@ -398,21 +400,21 @@ static ws_status grad_stream_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, 
   return WS_OK;
 }
 
-template <bool IS3D, int R>
-static ws_status grad_fused_t(ws_ctx* ctx, const uint8_t* img, const Geo& g, uint8_t* q, float* blur, float* grad,
+template <bool IS3D, int R, class Px>
+static ws_status grad_fused_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, float* blur, float* grad,
                               cudaStream_t st) {
   using T = GT<IS3D>;
   constexpr int H = R + 1;
   constexpr int SYB = T::TY + 2 * H, SZB = IS3D ? T::TZ + 2 * H : 1;
   constexpr int AX = T::TX + 2, BY = T::TY + 2;
-  const int smem = ((SZB * SYB * T::SXB + 127) / 128) * 128 + 4 * (SZB * SYB * AX + SZB * BY * AX);
+  const int smem = ((SZB * SYB * T::SXB * (int)sizeof(Px) + 127) / 128) * 128 + 4 * (SZB * SYB * AX + SZB * BY * AX);
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
   const char* env = getenv("WS_NO_TMA");
-  const int tma = !(env && env[0] == '1') && encode_tmap_3d(&m, 1, img, g, T::SXB, SYB, SZB);
+  const int tma = !(env && env[0] == '1') && encode_tmap_3d(&m, (int)sizeof(Px), img, g, T::SXB, SYB, SZB);
   const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY, ntz = (g.n0 + T::TZ - 1) / T::TZ;
-  WS_CUDA(cudaFuncSetAttribute(k_grad_fused<IS3D, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_grad_fused<IS3D, R><<<ntx * nty * ntz, 256, smem, st>>>(m, tma, img, g, ntx, nty, q, blur, grad);
+  WS_CUDA(cudaFuncSetAttribute(k_grad_fused<IS3D, R, Px>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_grad_fused<IS3D, R, Px><<<ntx * nty * ntz, 256, smem, st>>>(m, tma, img, g, ntx, nty, q, blur, grad);
   launched(ctx, PH_GRAD_MAG);
   tmark(ctx, st, PH_GRAD_MAG);
   WS_CUDA(cudaGetLastError());
@@ -491,7 +493,7 @@ ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int i
                            uint16_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st) {
   L3 l = launch3(g);
   const int rr = sigma > 0.f ? (int)floor(3.0 * (double)sigma + 0.5) : 0;
-  if (is3d && rr >= 1 && rr <= 4) {  // volumes: the 2.5-D streaming kernel on u16 pixels
+  if (rr >= 1 && rr <= 4) {  // volumes: the 2.5-D streaming kernel; 2-D: the fused tile kernel
     float w[2 * RMAX + 1], wq[2 * RMAX + 1];
     double wsum = 0, wd[2 * RMAX + 1];
     for (int i = -rr; i <= rr; ++i) { wd[i + rr] = exp(-(double)i * i / (2.0 * sigma * (double)sigma)); wsum += wd[i + rr]; }
@@ -501,10 +503,14 @@ ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int i
     }
     WS_CUDA(cudaMemcpyToSymbolAsync(c_w, w, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
     WS_CUDA(cudaMemcpyToSymbolAsync(c_w65535, wq, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
-    switch (rr) {
-      case 1: return grad_stream_t<1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 2: return grad_stream_t<2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 3: return grad_stream_t<3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+    switch (rr + (is3d ? 10 : 0)) {
+      case 1: return grad_fused_t<false, 1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 2: return grad_fused_t<false, 2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 3: return grad_fused_t<false, 3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 4: return grad_fused_t<false, 4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 11: return grad_stream_t<1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 12: return grad_stream_t<2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+      case 13: return grad_stream_t<3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
       default: return grad_stream_t<4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
     }
   }

@@ -76,7 +76,8 @@ FTOL = 1e-5  # north_star float tolerance (as for the u8 gradient)
 
 
 @pytest.mark.parametrize("sigma", [0.0, 1.0, 1.7])
-@pytest.mark.parametrize("ndim,shape", [(3, (13, 19, 37)), (3, (9, 34, 72)), (2, (2, 45, 70))])  # 72: aligned word loads
+@pytest.mark.parametrize("ndim,shape", [(3, (13, 19, 37)), (3, (9, 34, 72)), (2, (2, 45, 70)), (2, (3, 96, 200))])
+# 72: aligned word loads (3-D streaming kernel); (3, 96, 200): TMA-staged 2-D tiles (row pitch % 16 == 0)
 def test_u16_gradient_parity_and_pipeline(sigma, ndim, shape):
     """ws_gradient_u16 vs O11: floats within 1e-5, q equal except on boundary straddles
     (C11 at 16 bits: |65535 g - (k + 1/2)| <= 65535 tol, off by one); then the watershed of
