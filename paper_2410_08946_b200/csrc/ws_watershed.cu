@@ -605,9 +605,7 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
     __syncthreads();
     for (int i = threadIdx.x; i < nq; i += NT)
       if (*sQb + i < po.cap) po.pairs[*sQb + i] = sQ[i];
-  } else {
-    __syncthreads();
-  }
+  }  // no minimal voxel: the barrier after the sG stores already orders sP / sG for the walk
   // two in-place pointer-jumping rounds (sP[j] = sP[sP[j]] where that is again an in-tile
   // pointer; a racing reader sees the old or the new value, both ancestors), then the walk
 #pragma unroll 1
