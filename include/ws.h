@@ -79,6 +79,14 @@ typedef struct ws_stats {
   int32_t reserved0;
   int64_t level_edges[16];    /* live RAG edge records entering each waterfall level       */
   int64_t total_launches;     /* kernels launched by this context since its creation       */
+  /* size-dependent code paths the last call took (the full-size parity tests assert them) */
+  int32_t union_order;        /* ws_watershed step IV: 0 = cross-tile pair list before the chase,
+                                 1 = chase first + pair list (many pairs: giant minimal plateaux),
+                                 2 = chase first + full k_union scan (pair list overflow)        */
+  int32_t root_overflow;      /* ws_watershed: 1 if the step III root list overflowed (rebuilt) */
+  int32_t lookback_max;       /* ws_waterfall: deepest look-back (blocks) of the dense-id scan   */
+  int32_t edge_chunks_max;    /* ws_waterfall: most edge chunks one k_edges block walked         */
+  int64_t rag_global_emits;   /* ws_waterfall: RAG records emitted past a full tile pair hash    */
 } ws_stats;
 
 ws_status ws_ctx_create(int32_t device, ws_ctx** out);

@@ -43,6 +43,15 @@ def _req(t, dtype, name):
         raise ValueError("%s must be contiguous" % name)
 
 
+def _req_out(t, dtype, shape, like, name):
+    """Validate a caller-supplied output tensor before its pointer reaches the library."""
+    _req(t, dtype, name)
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError("%s must have shape %s (got %s)" % (name, tuple(shape), tuple(t.shape)))
+    if t.device != like.device:
+        raise ValueError("%s must be on %s (got %s)" % (name, like.device, t.device))
+
+
 def gradient(img: torch.Tensor, sigma: float = 1.0, ndim: int = None, verify: bool = False,
              ctx: Context = None, out: torch.Tensor = None):
     """ws_gradient: u8 image -> agreed u8 gradient image (and fp32 blur/grad if ``verify``).
@@ -51,6 +60,8 @@ def gradient(img: torch.Tensor, sigma: float = 1.0, ndim: int = None, verify: bo
     _req(img, torch.uint16 if wide else torch.uint8, "img")
     ndim = ndim if ndim is not None else (3 if img.dim() == 3 and img.shape[0] > 1 else 2)
     ctx = ctx or default_context(img.device.index)
+    if out is not None:
+        _req_out(out, img.dtype, img.shape, img, "out")
     q = out if out is not None else torch.empty_like(img)
     blur = torch.empty(img.shape, dtype=torch.float32, device=img.device) if verify else None
     grad = torch.empty(img.shape, dtype=torch.float32, device=img.device) if verify else None
@@ -73,6 +84,8 @@ def watershed(grad: torch.Tensor, conn: int, ndim: int = None, ctx: Context = No
     _req(grad, torch.uint16 if wide else torch.uint8, "grad")
     ndim = _ndim_for(conn, ndim)
     ctx = ctx or default_context(grad.device.index)
+    if out is not None:
+        _req_out(out, torch.int32, grad.shape, grad, "out")
     labels = out if out is not None else torch.empty(grad.shape, dtype=torch.int32, device=grad.device)
     R = ctypes.c_int64(0)
     if wide:
@@ -105,6 +118,10 @@ def waterfall(labels: torch.Tensor, grad: torch.Tensor, conn: int, NL: int, ndim
         raise ValueError("labels and grad shapes differ")
     ndim = _ndim_for(conn, ndim)
     ctx = ctx or default_context(grad.device.index)
+    if labels.device != grad.device:
+        raise ValueError("labels and grad must be on the same device")
+    if out is not None:
+        _req_out(out, torch.int32, (max(int(NL), 1),) + tuple(grad.shape), grad, "out")
     levels = out if out is not None else torch.empty((max(int(NL), 1),) + tuple(grad.shape), dtype=torch.int32,
                                                       device=grad.device)
     counts = (ctypes.c_int64 * max(int(NL), 1))()
@@ -121,6 +138,9 @@ def segment_host(grad_host: torch.Tensor, conn: int, NL: int, ndim: int = None, 
         raise TypeError("grad_host must be a contiguous CPU uint8 tensor")
     ndim = _ndim_for(conn, ndim)
     ctx = ctx or default_context(device)
+    if out is not None and (out.is_cuda or out.dtype != torch.int32 or not out.is_contiguous()
+                            or tuple(out.shape) != (int(NL),) + tuple(grad_host.shape)):
+        raise ValueError("out must be a contiguous CPU int32 tensor of shape %s" % (((int(NL),) + tuple(grad_host.shape)),))
     levels = out if out is not None else torch.empty((int(NL),) + tuple(grad_host.shape), dtype=torch.int32,
                                                       pin_memory=True)
     counts = (ctypes.c_int64 * max(int(NL), 1))()

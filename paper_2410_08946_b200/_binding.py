@@ -41,7 +41,9 @@ class WsStats(ctypes.Structure):
                 ("level_counts", ctypes.c_int64 * 16), ("kernel_launches", ctypes.c_int64),
                 ("phase_ms", ctypes.c_double * 16), ("phase_launches", ctypes.c_int32 * 16),
                 ("tma", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("level_edges", ctypes.c_int64 * 16),
-                ("total_launches", ctypes.c_int64)]
+                ("total_launches", ctypes.c_int64), ("union_order", ctypes.c_int32),
+                ("root_overflow", ctypes.c_int32), ("lookback_max", ctypes.c_int32),
+                ("edge_chunks_max", ctypes.c_int32), ("rag_global_emits", ctypes.c_int64)]
 
     def as_dict(self):
         lib = load()
@@ -54,7 +56,9 @@ class WsStats(ctypes.Structure):
                 "plateau_rounds": self.plateau_rounds, "waterfall_levels": self.waterfall_levels,
                 "level_counts": list(self.level_counts), "kernel_launches": self.kernel_launches,
                 "phases": phases, "tma": self.tma, "level_edges": list(self.level_edges),
-                "total_launches": self.total_launches}
+                "total_launches": self.total_launches, "union_order": self.union_order,
+                "root_overflow": self.root_overflow, "lookback_max": self.lookback_max,
+                "edge_chunks_max": self.edge_chunks_max, "rag_global_emits": self.rag_global_emits}
 
 
 class WsError(RuntimeError):

@@ -226,7 +226,7 @@ ws_status ws_ctx_destroy(ws_ctx* ctx) {
   ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->tiles, &ctx->roots, &ctx->rootc, &ctx->blockcnt, &ctx->edges, &ctx->ebufA, &ctx->ebufB, &ctx->rootsA, &ctx->rootsB, &ctx->lvl,
                      &ctx->comp, &ctx->best, &ctx->rep_of, &ctx->levelmap, &ctx->lvcount,
                      &ctx->h_grad, &ctx->h_labels, &ctx->h_levels, &ctx->dimg, &ctx->sroots, &ctx->sblocks, &ctx->rank, &ctx->wimg, &ctx->vstate, &ctx->nmin, &ctx->tlist, &ctx->upairs, &ctx->exitmx,
-                     &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap};
+                     &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc};
   for (auto* b : bufs) b->release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (int i = 0; i < ws_ctx::MAXEV; ++i)

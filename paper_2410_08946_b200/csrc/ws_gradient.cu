@@ -3,6 +3,7 @@
 //
 // v1 design: one separable pass per blurred axis (fp32, clamp-to-edge) through fp32 scratch,
 // then one fused gradient + quantise pass.  HBM-bound; see DESIGN.md §Kernels.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -13,9 +14,27 @@
 namespace ws {
 
 constexpr int RMAX = 60;  // sigma <= 20  ->  r = floor(3 sigma + 0.5) <= 60
-__constant__ float c_w[2 * RMAX + 1];
-__constant__ float c_w255[2 * RMAX + 1];  // w / 255: the x pass reads raw u8
-__constant__ float c_w65535[2 * RMAX + 1];  // w / 65535: the same for 16-bit images (NEXT f4)
+// The blur weights of one call travel as a __grid_constant__ kernel parameter (not shared
+// __constant__ symbols): calls on different streams or contexts never see each other's sigma.
+struct BlurW {
+  float w[2 * RMAX + 1];   // normalised Gaussian weights w_i, i = -r..r (C8)
+  float wn[2 * RMAX + 1];  // w_i / 255 (u8) or w_i / 65535 (u16): the x pass reads raw pixels
+};
+
+static BlurW blur_weights(float sigma, int r, double scale) {
+  BlurW b;
+  std::memset(&b, 0, sizeof(b));
+  double wd[2 * RMAX + 1], sum = 0;
+  for (int i = -r; i <= r; ++i) {
+    wd[i + r] = exp(-(double)i * i / (2.0 * sigma * (double)sigma));
+    sum += wd[i + r];
+  }
+  for (int i = 0; i <= 2 * r; ++i) {
+    b.w[i] = (float)(wd[i] / sum);
+    b.wn[i] = (float)(wd[i] / sum / scale);
+  }
+  return b;
+}
 
 template <class Tin>
 __device__ __forceinline__ float load_norm(const Tin* in, size_t i);
@@ -34,7 +53,8 @@ __device__ __forceinline__ float load_norm<float>(const float* in, size_t i) {
 
 // out = (1-D Gaussian along `axis`) * in ; axis 0 = n0, 1 = n1, 2 = n2.
 template <class Tin>
-__global__ void k_blur_axis(const Tin* __restrict__ in, float* __restrict__ out, Geo g, int axis, int r) {
+__global__ void k_blur_axis(const Tin* __restrict__ in, float* __restrict__ out, Geo g, int axis, int r,
+                            const __grid_constant__ BlurW W) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= g.n2 || y >= g.n1) return;
@@ -47,7 +67,7 @@ __global__ void k_blur_axis(const Tin* __restrict__ in, float* __restrict__ out,
     for (int i = -r; i <= r; ++i) {
       int k = c + i;
       k = k < 0 ? 0 : (k >= len ? len - 1 : k);
-      acc = fmaf(c_w[i + r], load_norm<Tin>(in, p + (ptrdiff_t)(k - c) * stride), acc);
+      acc = fmaf(W.w[i + r], load_norm<Tin>(in, p + (ptrdiff_t)(k - c) * stride), acc);
     }
     out[p] = acc;
   }
@@ -104,7 +124,7 @@ template <bool IS3D, int R, class Px>  // Px: u8 (C10) or u16 (NEXT f4: x / 6553
 __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUtensorMap mImg, int tma,
                                                     const Px* __restrict__ img, Geo g, int ntx, int nty,
                                                     Px* __restrict__ q, float* __restrict__ blur_out,
-                                                    float* __restrict__ grad_out) {
+                                                    float* __restrict__ grad_out, const __grid_constant__ BlurW W) {
   using T = GT<IS3D>;
   constexpr int H = R + 1;
   constexpr int SYB = T::TY + 2 * H, SZB = IS3D ? T::TZ + 2 * H : 1;
@@ -154,7 +174,7 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
       float acc = 0.f;
 #pragma unroll
       for (int i = 0; i <= 2 * R; ++i)  // w / 255 (w / 65535) folded in
-        acc = fmaf(sizeof(Px) == 1 ? c_w255[i] : c_w65535[i], v[o + i], acc);
+        acc = fmaf(W.wn[i], v[o + i], acc);
       A[row * AX + x] = acc;
     }
   }
@@ -169,7 +189,7 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
     for (int y = 0; y < BY; ++y) {
       float acc = 0.f;
 #pragma unroll
-      for (int i = 0; i <= 2 * R; ++i) acc = fmaf(c_w[i], v[H - 1 + y - R + i], acc);
+      for (int i = 0; i <= 2 * R; ++i) acc = fmaf(W.w[i], v[H - 1 + y - R + i], acc);
       B[(z * BY + y) * AX + x] = acc;
     }
   }
@@ -184,7 +204,7 @@ __global__ void __launch_bounds__(256) k_grad_fused(const __grid_constant__ CUte
       for (int z = 0; z < CZ; ++z) {
         float acc = 0.f;
 #pragma unroll
-        for (int i = 0; i <= 2 * R; ++i) acc = fmaf(c_w[i], v[H - 1 + z - R + i], acc);
+        for (int i = 0; i <= 2 * R; ++i) acc = fmaf(W.w[i], v[H - 1 + z - R + i], acc);
         C[(z * BY + y) * AX + x] = acc;
       }
     }
@@ -242,7 +262,7 @@ constexpr int GSX = 32, GSY = 16, GZC = 64;
 template <int R, class Px>
 __global__ void __launch_bounds__(256) k_grad_stream(const Px* __restrict__ img, Geo g, int ntx, int nty,
                                                      Px* __restrict__ q, float* __restrict__ blur_out,
-                                                     float* __restrict__ grad_out) {
+                                                     float* __restrict__ grad_out, const __grid_constant__ BlurW W) {
   using Wd = typename std::conditional<sizeof(Px) == 1, uint32_t, unsigned long long>::type;
   constexpr int H = R + 1, K = 2 * R + 1;
   constexpr int XO = H <= 4 ? 4 : 8, SX = GSX + 2 * XO, SY = GSY + 2 * H, WPR = SX / 4;
@@ -316,7 +336,7 @@ __global__ void __launch_bounds__(256) k_grad_stream(const Px* __restrict__ img,
         float acc = 0.f;
 #pragma unroll
         for (int i = 0; i <= 2 * R; ++i)  // w / 255 (w / 65535) folded in
-          acc = fmaf(sizeof(Px) == 1 ? c_w255[i] : c_w65535[i], v[oo + i], acc);
+          acc = fmaf(W.wn[i], v[oo + i], acc);
         o[oo] = acc;
       }
       *reinterpret_cast<float4*>(X + row * AXP + 4 * grp) = o4;
@@ -333,7 +353,7 @@ __global__ void __launch_bounds__(256) k_grad_stream(const Px* __restrict__ img,
       for (int r = 0; r < RG; ++r) {
         float acc = 0.f;
 #pragma unroll
-        for (int i = 0; i <= 2 * R; ++i) acc = fmaf(c_w[i], xv[r + i], acc);
+        for (int i = 0; i <= 2 * R; ++i) acc = fmaf(W.w[i], xv[r + i], acc);
 #pragma unroll
         for (int i = 0; i < K - 1; ++i) zr[r][i] = zr[r][i + 1];
         zr[r][K - 1] = acc;
@@ -344,7 +364,7 @@ __global__ void __launch_bounds__(256) k_grad_stream(const Px* __restrict__ img,
         for (int r = 0; r < RG; ++r) {
           float acc = 0.f;
 #pragma unroll
-          for (int i = 0; i < K; ++i) acc = fmaf(c_w[i], zr[r][i], acc);
+          for (int i = 0; i < K; ++i) acc = fmaf(W.w[i], zr[r][i], acc);
           Bt[(RG * rg + r) * AX + j] = acc;
         }
       }
@@ -391,9 +411,9 @@ __global__ void __launch_bounds__(256) k_grad_stream(const Px* __restrict__ img,
 
 template <int R, class Px>
 static ws_status grad_stream_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, float* blur, float* grad,
-                               cudaStream_t st) {
+                               const BlurW& W, cudaStream_t st) {
   const int ntx = (g.n2 + GSX - 1) / GSX, nty = (g.n1 + GSY - 1) / GSY, ntz = (g.n0 + GZC - 1) / GZC;
-  k_grad_stream<R, Px><<<ntx * nty * ntz, 256, 0, st>>>(img, g, ntx, nty, q, blur, grad);
+  k_grad_stream<R, Px><<<ntx * nty * ntz, 256, 0, st>>>(img, g, ntx, nty, q, blur, grad, W);
   launched(ctx, PH_GRAD_MAG);
   tmark(ctx, st, PH_GRAD_MAG);
   WS_CUDA(cudaGetLastError());
@@ -402,7 +422,7 @@ static ws_status grad_stream_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, 
 
 template <bool IS3D, int R, class Px>
 static ws_status grad_fused_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, float* blur, float* grad,
-                              cudaStream_t st) {
+                              const BlurW& W, cudaStream_t st) {
   using T = GT<IS3D>;
   constexpr int H = R + 1;
   constexpr int SYB = T::TY + 2 * H, SZB = IS3D ? T::TZ + 2 * H : 1;
@@ -414,52 +434,45 @@ static ws_status grad_fused_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, f
   const int tma = !(env && env[0] == '1') && encode_tmap_3d(&m, (int)sizeof(Px), img, g, T::SXB, SYB, SZB);
   const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY, ntz = (g.n0 + T::TZ - 1) / T::TZ;
   WS_CUDA(cudaFuncSetAttribute(k_grad_fused<IS3D, R, Px>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_grad_fused<IS3D, R, Px><<<ntx * nty * ntz, 256, smem, st>>>(m, tma, img, g, ntx, nty, q, blur, grad);
+  k_grad_fused<IS3D, R, Px><<<ntx * nty * ntz, 256, smem, st>>>(m, tma, img, g, ntx, nty, q, blur, grad, W);
   launched(ctx, PH_GRAD_MAG);
   tmark(ctx, st, PH_GRAD_MAG);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
 
-ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, float sigma,
-                       uint8_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st) {
+// Px = u8: b = G_sigma * (img / 255), q = min(255, floor(255 g + 0.5)) (C8-C10).
+// Px = u16 (NEXT f4): b = G_sigma * (img / 65535), q = min(65535, floor(65535 g + 0.5)).
+// r = floor(3 sigma + 0.5) in 1..4: volumes run the 2.5-D streaming kernel k_grad_stream, 2-D
+// images the TMA tile kernel k_grad_fused (both on either pixel type); sigma == 0: the gradient
+// kernel alone; larger r: separable k_blur_axis passes through two f32[N] workspace arrays,
+// then k_gradmag.
+template <class Px>
+static ws_status run_gradient_t(ws_ctx* ctx, const Px* img, const Geo& g, int is3d, float sigma, Px* grad_q,
+                                float* blur_f32, float* grad_f32, cudaStream_t st) {
   L3 l = launch3(g);
-  const int rr = sigma > 0.f ? (int)floor(3.0 * (double)sigma + 0.5) : 0;
-  if (rr >= 1 && rr <= 4) {  // fused tile kernel
-    float w[2 * RMAX + 1];
-    double wsum = 0, wd[2 * RMAX + 1];
-    for (int i = -rr; i <= rr; ++i) { wd[i + rr] = exp(-(double)i * i / (2.0 * sigma * (double)sigma)); wsum += wd[i + rr]; }
-    float w255[2 * RMAX + 1];
-    for (int i = 0; i <= 2 * rr; ++i) {
-      w[i] = (float)(wd[i] / wsum);
-      w255[i] = (float)(wd[i] / wsum / 255.0);
-    }
-    WS_CUDA(cudaMemcpyToSymbolAsync(c_w, w, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
-    WS_CUDA(cudaMemcpyToSymbolAsync(c_w255, w255, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
-    switch (rr + (is3d ? 10 : 0)) {
-      case 1: return grad_fused_t<false, 1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 2: return grad_fused_t<false, 2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 3: return grad_fused_t<false, 3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 4: return grad_fused_t<false, 4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 11: return grad_stream_t<1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 12: return grad_stream_t<2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 13: return grad_stream_t<3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      default: return grad_stream_t<4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
+  const double scale = sizeof(Px) == 1 ? 255.0 : 65535.0;
+  const int r = sigma > 0.f ? (int)floor(3.0 * (double)sigma + 0.5) : 0;
+  const BlurW W = blur_weights(sigma, r, scale);
+  if (r >= 1 && r <= 4) {
+    switch (r + (is3d ? 10 : 0)) {
+      case 1: return grad_fused_t<false, 1>(ctx, img, g, grad_q, blur_f32, grad_f32, W, st);
+      case 2: return grad_fused_t<false, 2>(ctx, img, g, grad_q, blur_f32, grad_f32, W, st);
+      case 3: return grad_fused_t<false, 3>(ctx, img, g, grad_q, blur_f32, grad_f32, W, st);
+      case 4: return grad_fused_t<false, 4>(ctx, img, g, grad_q, blur_f32, grad_f32, W, st);
+      case 11: return grad_stream_t<1>(ctx, img, g, grad_q, blur_f32, grad_f32, W, st);
+      case 12: return grad_stream_t<2>(ctx, img, g, grad_q, blur_f32, grad_f32, W, st);
+      case 13: return grad_stream_t<3>(ctx, img, g, grad_q, blur_f32, grad_f32, W, st);
+      default: return grad_stream_t<4>(ctx, img, g, grad_q, blur_f32, grad_f32, W, st);
     }
   }
-  if (sigma == 0.f) {
-    k_gradmag<uint8_t, uint8_t><<<l.grid, l.block, 0, st>>>(img, g, is3d, grad_q, blur_f32, grad_f32);
+  if (r == 0) {
+    k_gradmag<Px, Px><<<l.grid, l.block, 0, st>>>(img, g, is3d, grad_q, blur_f32, grad_f32);
     launched(ctx, PH_GRAD_MAG);
     tmark(ctx, st, PH_GRAD_MAG);
     WS_CUDA(cudaGetLastError());
     return WS_OK;
   }
-  const int r = (int)floor(3.0 * (double)sigma + 0.5);
-  float w[2 * RMAX + 1];
-  double ws = 0, wd[2 * RMAX + 1];
-  for (int i = -r; i <= r; ++i) { wd[i + r] = exp(-(double)i * i / (2.0 * sigma * (double)sigma)); ws += wd[i + r]; }
-  for (int i = 0; i <= 2 * r; ++i) w[i] = (float)(wd[i] / ws);
-  WS_CUDA(cudaMemcpyToSymbolAsync(c_w, w, sizeof(float) * (2 * r + 1), 0, cudaMemcpyHostToDevice, st));
   const size_t nb = (size_t)g.N * sizeof(float);
   WS_TRY(ctx->tmpA.ensure(nb, "gradient scratch A"));
   WS_TRY(ctx->tmpB.ensure(nb, "gradient scratch B"));
@@ -467,90 +480,33 @@ ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, 
   float* B = ctx->tmpB.as<float>();
   const float* fin;
   if (is3d) {
-    k_blur_axis<uint8_t><<<l.grid, l.block, 0, st>>>(img, A, g, 0, r);
-    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(A, B, g, 1, r);
-    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(B, A, g, 2, r);
+    k_blur_axis<Px><<<l.grid, l.block, 0, st>>>(img, A, g, 0, r, W);
+    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(A, B, g, 1, r, W);
+    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(B, A, g, 2, r, W);
     fin = A;
     launched(ctx, PH_GRAD_BLUR, 3);
   } else {
-    k_blur_axis<uint8_t><<<l.grid, l.block, 0, st>>>(img, A, g, 1, r);
-    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(A, B, g, 2, r);
+    k_blur_axis<Px><<<l.grid, l.block, 0, st>>>(img, A, g, 1, r, W);
+    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(A, B, g, 2, r, W);
     fin = B;
     launched(ctx, PH_GRAD_BLUR, 2);
   }
   tmark(ctx, st, PH_GRAD_BLUR);
-  k_gradmag<float, uint8_t><<<l.grid, l.block, 0, st>>>(fin, g, is3d, grad_q, blur_f32, grad_f32);
+  k_gradmag<float, Px><<<l.grid, l.block, 0, st>>>(fin, g, is3d, grad_q, blur_f32, grad_f32);
   launched(ctx, PH_GRAD_MAG);
   tmark(ctx, st, PH_GRAD_MAG);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
 
-// 16-bit images (NEXT f4): b = G_sigma * (img / 65535), q = min(65535, floor(65535 g
-// + 0.5)).  The generic separable path (fp32 scratch between the axis passes, then one
-// gradient + quantise pass); the fused u8 tile / streaming kernels are not instantiated for u16.
-ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma,
-                           uint16_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st) {
-  L3 l = launch3(g);
-  const int rr = sigma > 0.f ? (int)floor(3.0 * (double)sigma + 0.5) : 0;
-  if (rr >= 1 && rr <= 4) {  // volumes: the 2.5-D streaming kernel; 2-D: the fused tile kernel
-    float w[2 * RMAX + 1], wq[2 * RMAX + 1];
-    double wsum = 0, wd[2 * RMAX + 1];
-    for (int i = -rr; i <= rr; ++i) { wd[i + rr] = exp(-(double)i * i / (2.0 * sigma * (double)sigma)); wsum += wd[i + rr]; }
-    for (int i = 0; i <= 2 * rr; ++i) {
-      w[i] = (float)(wd[i] / wsum);
-      wq[i] = (float)(wd[i] / wsum / 65535.0);
-    }
-    WS_CUDA(cudaMemcpyToSymbolAsync(c_w, w, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
-    WS_CUDA(cudaMemcpyToSymbolAsync(c_w65535, wq, sizeof(float) * (2 * rr + 1), 0, cudaMemcpyHostToDevice, st));
-    switch (rr + (is3d ? 10 : 0)) {
-      case 1: return grad_fused_t<false, 1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 2: return grad_fused_t<false, 2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 3: return grad_fused_t<false, 3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 4: return grad_fused_t<false, 4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 11: return grad_stream_t<1>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 12: return grad_stream_t<2>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      case 13: return grad_stream_t<3>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-      default: return grad_stream_t<4>(ctx, img, g, grad_q, blur_f32, grad_f32, st);
-    }
-  }
-  if (sigma == 0.f) {
-    k_gradmag<uint16_t, uint16_t><<<l.grid, l.block, 0, st>>>(img, g, is3d, grad_q, blur_f32, grad_f32);
-    launched(ctx, PH_GRAD_MAG);
-    tmark(ctx, st, PH_GRAD_MAG);
-    WS_CUDA(cudaGetLastError());
-    return WS_OK;
-  }
-  const int r = (int)floor(3.0 * (double)sigma + 0.5);
-  float w[2 * RMAX + 1];
-  double ws = 0, wd[2 * RMAX + 1];
-  for (int i = -r; i <= r; ++i) { wd[i + r] = exp(-(double)i * i / (2.0 * sigma * (double)sigma)); ws += wd[i + r]; }
-  for (int i = 0; i <= 2 * r; ++i) w[i] = (float)(wd[i] / ws);
-  WS_CUDA(cudaMemcpyToSymbolAsync(c_w, w, sizeof(float) * (2 * r + 1), 0, cudaMemcpyHostToDevice, st));
-  const size_t nb = (size_t)g.N * sizeof(float);
-  WS_TRY(ctx->tmpA.ensure(nb, "gradient scratch A"));
-  WS_TRY(ctx->tmpB.ensure(nb, "gradient scratch B"));
-  float* A = ctx->tmpA.as<float>();
-  float* B = ctx->tmpB.as<float>();
-  const float* fin;
-  if (is3d) {
-    k_blur_axis<uint16_t><<<l.grid, l.block, 0, st>>>(img, A, g, 0, r);
-    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(A, B, g, 1, r);
-    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(B, A, g, 2, r);
-    fin = A;
-    launched(ctx, PH_GRAD_BLUR, 3);
-  } else {
-    k_blur_axis<uint16_t><<<l.grid, l.block, 0, st>>>(img, A, g, 1, r);
-    k_blur_axis<float><<<l.grid, l.block, 0, st>>>(A, B, g, 2, r);
-    fin = B;
-    launched(ctx, PH_GRAD_BLUR, 2);
-  }
-  tmark(ctx, st, PH_GRAD_BLUR);
-  k_gradmag<float, uint16_t><<<l.grid, l.block, 0, st>>>(fin, g, is3d, grad_q, blur_f32, grad_f32);
-  launched(ctx, PH_GRAD_MAG);
-  tmark(ctx, st, PH_GRAD_MAG);
-  WS_CUDA(cudaGetLastError());
-  return WS_OK;
+ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, float sigma, uint8_t* grad_q,
+                       float* blur_f32, float* grad_f32, cudaStream_t st) {
+  return run_gradient_t<uint8_t>(ctx, img, g, is3d, sigma, grad_q, blur_f32, grad_f32, st);
+}
+
+ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma, uint16_t* grad_q,
+                           float* blur_f32, float* grad_f32, cudaStream_t st) {
+  return run_gradient_t<uint16_t>(ctx, img, g, is3d, sigma, grad_q, blur_f32, grad_f32, st);
 }
 
 }  // namespace ws

@@ -87,6 +87,7 @@ struct ws_ctx {
   ws::Buf vstate;     // u8[2N]   states S, S' of the paper's one-thread-per-voxel variants
   ws::Buf nmin;       // u32[N]   255 - newmin per label (paper-literal waterfall)
   ws::Buf lvcount;    // i64[NL]  device-side region counts
+  ws::Buf pathc;      // u64[4]   code-path counters of the waterfall (look-back depth, k_edges chunks, RAG emits)
   ws::Buf h_grad, h_labels, h_levels;  // device copies used by ws_segment_host
   int64_t* pinned = nullptr;           // small pinned host scratch (flags / counts)
   ws_stats stats{};

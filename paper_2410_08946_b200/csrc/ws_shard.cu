@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(NTS) k_jump_shard(int* P, int* L, Geo g, int* 
   const int lane = threadIdx.x & 31;
   const int lo = g.zlo * g.plane, hi = g.zhi * g.plane;
   const int stride = gridDim.x * NTS;
+  int cnt = 0;  // staged roots: block-uniform (a register, never re-read from scount)
   for (int p0 = lo + blockIdx.x * NTS; p0 < hi; p0 += stride) {
     const int p = p0 + threadIdx.x;
     const bool valid = p < hi;
@@ -105,8 +106,7 @@ __global__ void __launch_bounds__(NTS) k_jump_shard(int* P, int* L, Geo g, int* 
       base = __shfl_sync(0xffffffffu, base, 0);
       if (isr) sbuf[base + __popc(rb & ((1u << lane) - 1))] = p + g.gofs;
     }
-    __syncthreads();
-    const int cnt = scount;
+    cnt += __syncthreads_count(isr);
     if (cnt > 2048 - NTS || p0 + stride >= hi) {
       if (cnt > 0) {
         if (threadIdx.x == 0) sbase = atomicAdd(nroots, cnt);
@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(NTS) k_jump_shard(int* P, int* L, Geo g, int* 
       __syncthreads();
       if (threadIdx.x == 0) scount = 0;
       __syncthreads();
+      cnt = 0;
     }
   }
 }

@@ -65,7 +65,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int* smem, int& total) {
 __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, int N, int aligned,
                                                 unsigned long long* status, int* ticket, int* __restrict__ dense_of,
                                                 int* __restrict__ rep_of, int rep_cap, long long* R, int pofs,
-                                                int doff, uint2* __restrict__ rk) {
+                                                int doff, uint2* __restrict__ rk, unsigned long long* depth_max,
+                                                int agg_only) {
   __shared__ int sm[32];
   __shared__ int sb;
   __shared__ long long sprefix;
@@ -121,10 +122,15 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         prefix += v;
-        if (pre) break;
+        if (pre) {
+          if (lane == 0) atomicMax(depth_max, (unsigned long long)(b - (q - first)));  // blocks looked back
+          break;
+        }
         q -= 32;
       }
-      if (lane == 0) atomicExch(status + b, ST_PRE | (unsigned long long)(prefix + total));
+      // (agg_only, a test knob: keep only the aggregate published, so every successor looks
+      // back to block 0 across many 32-block windows)
+      if (lane == 0 && !agg_only) atomicExch(status + b, ST_PRE | (unsigned long long)(prefix + total));
     }
     if (lane == 0) {
       sprefix = prefix;
@@ -253,11 +259,21 @@ __device__ __forceinline__ void fold_best(uint64_t* best, uint64_t k) {
   atomicMin((unsigned long long*)(best + key_hi(k)), (unsigned long long)k);
 }
 
-__device__ __noinline__ void emit_global(uint64_t k, uint64_t* edges, unsigned long long* ecount, long long cap,
-                                         uint64_t* best) {
-  const unsigned long long i = atomicAdd(ecount, 1ull);
-  if ((long long)i < cap) edges[i] = k;
-  fold_best(best, k);
+// where the RAG's unique tile edges go (level-1 key list + best[]); emits counts the records
+// that bypassed a full tile hash (ws_stats.rag_global_emits)
+struct EdgeOut {
+  uint64_t* edges;
+  unsigned long long* ecount;
+  long long cap;
+  uint64_t* best;
+  unsigned long long* emits;
+};
+
+__device__ __noinline__ void emit_global(uint64_t k, const EdgeOut& eo) {
+  const unsigned long long i = atomicAdd(eo.ecount, 1ull);
+  if ((long long)i < eo.cap) eo.edges[i] = k;
+  fold_best(eo.best, k);
+  atomicAdd(eo.emits, 1ull);
 }
 
 // fold staged records into the tile's pair hash.  wst/wcnt: one list of a warp (wsel >= 0:
@@ -265,8 +281,7 @@ __device__ __noinline__ void emit_global(uint64_t k, uint64_t* edges, unsigned l
 // wc[], exclusive prefixes in wp[]) spread evenly over all threads.
 template <int CONN>
 __device__ __forceinline__ void fold_rec(unsigned rec, const short* offs, const uint8_t* sI, const int* sD,
-                                         unsigned long long* pk, unsigned* pw, uint64_t* edges,
-                                         unsigned long long* ecount, long long cap, uint64_t* best) {
+                                         unsigned long long* pk, unsigned* pw, const EdgeOut& eo) {
   using R = RL<CONN>;
   const int sl = rec >> 4, f = rec & 15;  // [sl:12][f:4]: D-box index of p, forward direction
   const int si = sl + (sl / R::SXL) * (R::SXI - R::SXL) + (R::IXO - R::LXO);  // same voxel in the I box
@@ -285,20 +300,19 @@ __device__ __forceinline__ void fold_rec(unsigned rec, const short* offs, const 
     }
     h = (h + 1) & (R::HP - 1);
   }
-  emit_global(make_key(w, dp, dq), edges, ecount, cap, best);  // congested tile
+  emit_global(make_key(w, dp, dq), eo);  // congested tile
 }
 
 template <int CONN>
 __device__ __forceinline__ void fold_warp(const uint16_t* wst, int wcnt, const short* offs, const uint8_t* sI,
-                                          const int* sD, unsigned long long* pk, unsigned* pw, uint64_t* edges,
-                                          unsigned long long* ecount, long long cap, uint64_t* best) {
-  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN>(wst[r], offs, sI, sD, pk, pw, edges, ecount, cap, best);
+                                          const int* sD, unsigned long long* pk, unsigned* pw, const EdgeOut& eo) {
+  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN>(wst[r], offs, sI, sD, pk, pw, eo);
 }
 
 template <int CONN, bool BORDER>
 __device__ __forceinline__ int rag_pairs(const uint8_t* sI, const int* sD, unsigned long long* pk, unsigned* pw,
-                                          uint16_t* stg, const short* offs, const Geo& g, const TileCoord& c, uint64_t* edges,
-                                          unsigned long long* ecount, long long cap, uint64_t* best) {
+                                          uint16_t* stg, const short* offs, const Geo& g, const TileCoord& c,
+                                          const EdgeOut& eo) {
   using R = RL<CONN>;
   using T = TL<CONN>;
   constexpr int NF = R::NF;
@@ -324,7 +338,7 @@ __device__ __forceinline__ int rag_pairs(const uint8_t* sI, const int* sD, unsig
     }
     if (R::MIDFOLD && wcnt > R::WCAP - NF * 32) {
       __syncwarp();
-      fold_warp<CONN>(wst, wcnt, offs, sI, sD, pk, pw, edges, ecount, cap, best);
+      fold_warp<CONN>(wst, wcnt, offs, sI, sD, pk, pw, eo);
       __syncwarp();
       wcnt = 0;
     }
@@ -359,8 +373,7 @@ __device__ __forceinline__ void rag_load_plain(const int* __restrict__ D, const 
 template <int CONN>
 __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mD,
                                             int tma, const int* __restrict__ D, const uint8_t* __restrict__ I, Geo g,
-                                            int ntx, int nty, int ntiles, uint64_t* __restrict__ edges,
-                                            unsigned long long* ecount, long long cap, uint64_t* best) {
+                                            int ntx, int nty, int ntiles, EdgeOut eo) {
   using R = RL<CONN>;
   extern __shared__ __align__(128) unsigned char rag_smem[];
   uint8_t* sI = rag_smem;                                                         // R::SI bytes
@@ -405,8 +418,8 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
     }
     // 1. detection into the per-warp lists
     const int n = tile_interior<CONN>(c, g)
-                      ? rag_pairs<CONN, false>(sI, sD, pk, pw, stg, offs, g, c, edges, ecount, cap, best)
-                      : rag_pairs<CONN, true>(sI, sD, pk, pw, stg, offs, g, c, edges, ecount, cap, best);
+                      ? rag_pairs<CONN, false>(sI, sD, pk, pw, stg, offs, g, c, eo)
+                      : rag_pairs<CONN, true>(sI, sD, pk, pw, stg, offs, g, c, eo);
     if (lane == 0) wc[warp] = n;
     __syncthreads();
     // 2. dedup: the records of all warps spread evenly over the block
@@ -423,7 +436,7 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
           w = u;
           base = pre[u];
         }
-      fold_rec<CONN>(stg[w * R::WCAP + (r - base)], offs, sI, sD, pk, pw, edges, ecount, cap, best);
+      fold_rec<CONN>(stg[w * R::WCAP + (r - base)], offs, sI, sD, pk, pw, eo);
     }
     __syncthreads();  // boxes consumed, hash complete
     const int tn = t + gridDim.x;
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
     for (int m = 0; m < M; ++m) cnt += pk[threadIdx.x * M + m] != KEY_NONE;
     int tot;
     const int ex = block_excl_scan(cnt, sscan, tot);
-    if (threadIdx.x == 0) gbase = tot ? atomicAdd(ecount, (unsigned long long)tot) : 0;
+    if (threadIdx.x == 0) gbase = tot ? atomicAdd(eo.ecount, (unsigned long long)tot) : 0;
     __syncthreads();
     long long i = (long long)gbase + ex;
 #pragma unroll
@@ -448,9 +461,9 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
       const unsigned long long key = pk[threadIdx.x * M + m];
       if (key == KEY_NONE) continue;
       const uint64_t k = make_key(pw[threadIdx.x * M + m], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
-      if (i < cap) edges[i] = k;
+      if (i < eo.cap) eo.edges[i] = k;
       ++i;
-      fold_best(best, k);
+      fold_best(eo.best, k);
     }
     __syncthreads();  // flush done before the hash is reset
   }
@@ -505,6 +518,7 @@ __global__ void __launch_bounds__(NTW) k_flatten(int* comp, const int* __restric
   if (threadIdx.x == 0) scount = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  int cnt = 0;  // staged roots: block-uniform (a register, never re-read from scount)
   for (int i0 = blockIdx.x * NTW; i0 < n; i0 += gridDim.x * NTW) {
     const int i = i0 + threadIdx.x;
     int c = -1, r = -1;
@@ -520,12 +534,11 @@ __global__ void __launch_bounds__(NTW) k_flatten(int* comp, const int* __restric
       base = __shfl_sync(0xffffffffu, base, 0);
       if (isr) sbuf[base + __popc(rb & ((1u << lane) - 1))] = c;
     }
-    __syncthreads();
+    cnt += __syncthreads_count(isr);
     if (i < n && r != c) {
       comp[c] = r;
       lvl[c] = (uint8_t)level;  // c stops being a root at this level
     }
-    const int cnt = scount;
     if (cnt > NTW || i0 + gridDim.x * NTW >= n) {
       if (cnt > 0) {
         if (threadIdx.x == 0) sbase = atomicAdd(nout, (unsigned long long)cnt);
@@ -535,6 +548,7 @@ __global__ void __launch_bounds__(NTW) k_flatten(int* comp, const int* __restric
       __syncthreads();
       if (threadIdx.x == 0) scount = 0;
       __syncthreads();
+      cnt = 0;
     }
   }
 }
@@ -555,7 +569,7 @@ constexpr int EHC = 2048;  // shared hash slots (>= ECH distinct pairs: probing 
 __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_keys, const Edge* __restrict__ in,
                                                 long long n, const unsigned long long* nptr,
                                                 const int* __restrict__ comp, uint64_t* best, Edge* __restrict__ out,
-                                                unsigned long long* nout) {
+                                                unsigned long long* nout, unsigned long long* chunks_max) {
   extern __shared__ __align__(16) unsigned long long esm[];
   unsigned long long* tp = esm;                         // component pair (lo << 32 | hi)
   unsigned* khi = reinterpret_cast<unsigned*>(esm + EHC);  // min K of the pair: high word,
@@ -565,6 +579,8 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
   if (nptr) n = (long long)*nptr;  // device-resident count of the previous level's live edges
   constexpr int M = EHC / NTW;     // thread t owns the consecutive slots M t .. M t + M - 1
   constexpr int J = ECH / NTW;
+  if (threadIdx.x == 0 && (long long)blockIdx.x * ECH < n)
+    atomicMax(chunks_max, (unsigned long long)((n - 1 - (long long)blockIdx.x * ECH) / ((long long)gridDim.x * ECH) + 1));
 #pragma unroll 1
   for (long long e0 = (long long)blockIdx.x * ECH; e0 < n; e0 += (long long)gridDim.x * ECH) {
     for (int i = threadIdx.x; i < EHC; i += NTW) {
@@ -745,8 +761,7 @@ __global__ void k_levels_any(const int* __restrict__ D, const int* __restrict__ 
 
 // --------------------------------------------------------------------------- driver
 template <int CONN>
-static ws_status rag_t(const int* D, const uint8_t* I, const Geo& g, uint64_t* edges, unsigned long long* ecount,
-                       long long cap, uint64_t* best, cudaStream_t st) {
+static ws_status rag_t(const int* D, const uint8_t* I, const Geo& g, const EdgeOut& eo, cudaStream_t st) {
   using T = TL<CONN>;
   using R = RL<CONN>;
   const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY,
@@ -764,18 +779,17 @@ static ws_status rag_t(const int* D, const uint8_t* I, const Geo& g, uint64_t* e
   // persistent grid interleaves distant tiles and measured slower overall)
   const int ntiles = ntx * nty * ntz;
   const int grid = ntiles;
-  k_rag<CONN><<<grid, NT, R::SMEM, st>>>(mp.mI, mp.mL, mp.tma, D, I, g, ntx, nty, ntiles, edges, ecount, cap, best);
+  k_rag<CONN><<<grid, NT, R::SMEM, st>>>(mp.mI, mp.mL, mp.tma, D, I, g, ntx, nty, ntiles, eo);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
 
-static ws_status rag(int conn, const int* D, const uint8_t* I, const Geo& g, uint64_t* edges,
-                     unsigned long long* ecount, long long cap, uint64_t* best, cudaStream_t st) {
+static ws_status rag(int conn, const int* D, const uint8_t* I, const Geo& g, const EdgeOut& eo, cudaStream_t st) {
   switch (conn) {
-    case 4: return rag_t<4>(D, I, g, edges, ecount, cap, best, st);
-    case 8: return rag_t<8>(D, I, g, edges, ecount, cap, best, st);
-    case 6: return rag_t<6>(D, I, g, edges, ecount, cap, best, st);
-    case 26: return rag_t<26>(D, I, g, edges, ecount, cap, best, st);
+    case 4: return rag_t<4>(D, I, g, eo, st);
+    case 8: return rag_t<8>(D, I, g, eo, st);
+    case 6: return rag_t<6>(D, I, g, eo, st);
+    case 26: return rag_t<26>(D, I, g, eo, st);
   }
   return WS_ERR_INVALID;
 }
@@ -797,6 +811,10 @@ static ws_status read_i64(ws_ctx* ctx, const void* dptr, int64_t* out, cudaStrea
 static ws_status wf_dense(ws_ctx* ctx, const int32_t* labels, int n, int pofs, int doff, int* dense_of,
                           int64_t* count, cudaStream_t st, uint2* rk = nullptr) {
   const int nb = (n + DCHUNK - 1) / DCHUNK;
+  if (!ctx->pathc.p) {
+    WS_TRY(ctx->pathc.ensure(4 * sizeof(unsigned long long), "path counters"));
+    WS_CUDA(cudaMemsetAsync(ctx->pathc.p, 0, 4 * sizeof(unsigned long long), st));
+  }
   WS_TRY(ctx->blockcnt.ensure((size_t)nb * sizeof(unsigned long long), "scan status"));
   char* fl = ctx->flags.as<char>();
   long long* dR = reinterpret_cast<long long*>(fl + 128);
@@ -806,12 +824,14 @@ static ws_status wf_dense(ws_ctx* ctx, const int32_t* labels, int n, int pofs, i
     WS_TRY(ctx->rep_of.ensure(((size_t)n / 16 + 1024) * sizeof(int), "rep_of"));
     rep_cap = ctx->rep_of.bytes / sizeof(int);
   }
+  const char* knob = getenv("WS_TEST_LOOKBACK");  // test only: force look-backs to block 0
+  const int agg_only = knob && knob[0] == '1';
   for (int attempt = 0; attempt < 2; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ctx->blockcnt.p, 0, (size_t)nb * sizeof(unsigned long long), st));
     WS_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     k_dense<<<nb, NTW, 0, st>>>(labels, n, !(reinterpret_cast<uintptr_t>(labels) & 15),
                                 ctx->blockcnt.as<unsigned long long>(), ticket, dense_of, ctx->rep_of.as<int>(),
-                                (int)rep_cap, dR, pofs, doff, rk);
+                                (int)rep_cap, dR, pofs, doff, rk, ctx->pathc.as<unsigned long long>(), agg_only);
     launched(ctx, PH_WF_DENSE);
     WS_TRY(read_i64(ctx, dR, count, st));
     if ((size_t)*count <= rep_cap) break;
@@ -861,6 +881,7 @@ static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
 static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn,
                         const int* dense_of, cudaStream_t st, const uint2* rk = nullptr) {
   unsigned long long* ecount = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 136);
+  unsigned long long* pathc = ctx->pathc.as<unsigned long long>();
   WS_TRY(ctx->dimg.ensure((size_t)g.N * sizeof(int), "dense-id image"));
   int* D = ctx->dimg.as<int>();
   {
@@ -892,7 +913,8 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   int64_t E = 0;
   for (int attempt = 0;; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ecount, 0, sizeof(unsigned long long), st));
-    WS_TRY(rag(conn, D, I, g, ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), st));
+    WS_CUDA(cudaMemsetAsync(pathc + 2, 0, sizeof(unsigned long long), st));
+    WS_TRY(rag(conn, D, I, g, EdgeOut{ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), pathc + 2}, st));
     launched(ctx, PH_WF_RAG);
     WS_TRY(read_i64(ctx, ecount, &E, st));
     if (E <= cap) break;
@@ -952,7 +974,8 @@ static ws_status wf_level(ws_ctx* ctx, bool edges_next, cudaStream_t st) {
     const long long chunks = (w.E + ECH - 1) / ECH;
     const int grid = (int)std::min<long long>(chunks, (long long)ctx->num_sms * std::max(1, occ));
     k_edges<<<grid, NTW, esmem, st>>>(k == 1 ? ctx->edges.as<uint64_t>() : nullptr, ein, w.E,
-                                      k == 1 ? nullptr : cnt + LVC + k, comp, best, eout, cnt + LVC + k + 1);
+                                      k == 1 ? nullptr : cnt + LVC + k, comp, best, eout, cnt + LVC + k + 1,
+                                      ctx->pathc.as<unsigned long long>() + 1);
     launched(ctx, PH_WF_LEVELS);
   }
   w.eflip = 1 - w.eflip;  // eout becomes the next input
@@ -966,8 +989,13 @@ static ws_status wf_read_counts(ws_ctx* ctx, int k_last, int64_t* counts, cudaSt
   static_assert(2 * LVC <= 256, "pinned scratch");
   WS_CUDA(cudaMemcpyAsync(ctx->pinned, ctx->lvcount.p, 2 * LVC * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           st));
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned + 2 * LVC, ctx->pathc.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          st));
   WS_CUDA(cudaStreamSynchronize(st));
   const unsigned long long* h = reinterpret_cast<const unsigned long long*>(ctx->pinned);
+  ctx->stats.lookback_max = (int32_t)h[2 * LVC];
+  ctx->stats.edge_chunks_max = (int32_t)h[2 * LVC + 1];
+  ctx->stats.rag_global_emits = (int64_t)h[2 * LVC + 2];
   long long prev = w.R;
   for (int k = 1; k <= k_last && k < LVC; ++k) {
     const long long c = (long long)h[k];
@@ -1039,6 +1067,8 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   }
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
+  WS_TRY(ctx->pathc.ensure(4 * sizeof(unsigned long long), "path counters"));
+  WS_CUDA(cudaMemsetAsync(ctx->pathc.p, 0, 4 * sizeof(unsigned long long), st));
   int* dense_of = ctx->aux.as<int>();
   int64_t R = 0;
   WS_TRY(ctx->rank.ensure(((size_t)g.N / 32 + 1) * sizeof(uint2), "dense rank structure"));
@@ -1086,6 +1116,8 @@ __global__ void k_wf_bfill(const int* __restrict__ tabs, int K, int plane, int* 
 ws_status shard_wf_dense(ws_ctx* ctx, const int32_t* labels_own, int n, int pofs, int doff, int* dense_of,
                          int* rep_of_global, int64_t* count, cudaStream_t st) {
   WS_TRY(ctx->flags.ensure(256, "flags"));
+  WS_TRY(ctx->pathc.ensure(4 * sizeof(unsigned long long), "path counters"));
+  WS_CUDA(cudaMemsetAsync(ctx->pathc.p, 0, 4 * sizeof(unsigned long long), st));
   WS_TRY(wf_dense(ctx, labels_own, n, pofs, doff, dense_of, count, st));
   if (*count > 0)
     WS_CUDA(cudaMemcpyAsync(rep_of_global + doff, ctx->rep_of.p, (size_t)*count * sizeof(int),

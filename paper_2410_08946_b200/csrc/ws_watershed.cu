@@ -687,6 +687,7 @@ __global__ void __launch_bounds__(NT) k_jump(int* P, int* __restrict__ L, int N,
   if (threadIdx.x == 0) scount = 0;
   __syncthreads();
   const int stride = gridDim.x * NT;
+  int cnt = 0;  // staged roots: block-uniform (a register, never re-read from scount)
   for (int p0 = blockIdx.x * NT; p0 < N; p0 += stride) {
     const int p = p0 + threadIdx.x;
     const bool valid = p < N;
@@ -714,8 +715,7 @@ __global__ void __launch_bounds__(NT) k_jump(int* P, int* __restrict__ L, int N,
       base = __shfl_sync(0xffffffffu, base, 0);
       if (isr) sbuf[base + __popc(rb & ((1u << lane) - 1))] = p;
     }
-    __syncthreads();
-    const int cnt = scount;
+    cnt += __syncthreads_count(isr);  // the barrier that orders the appends before the flush
     if (cnt > RBUF - NT || p0 + stride >= N) {  // flush the staged roots
       if (cnt > 0) {
         if (threadIdx.x == 0) sbase = atomicAdd(nroots, cnt);
@@ -726,6 +726,7 @@ __global__ void __launch_bounds__(NT) k_jump(int* P, int* __restrict__ L, int N,
       __syncthreads();
       if (threadIdx.x == 0) scount = 0;
       __syncthreads();
+      cnt = 0;
     }
   }
 }
@@ -998,6 +999,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   // minimal plateau (many cross-tile pairs, e.g. the air of C3) the chase's per-root minimum
   // atomics would then all hit one address, so such inputs chase first and union after
   bool fast = n_pairs <= po.cap && (long long)n_pairs <= (long long)g.N / 64;
+  ctx->stats.union_order = fast ? 0 : (n_pairs <= po.cap ? 1 : 2);
   if (fast) {
     if (n_pairs > 0) {
       k_union_pairs<<<grid1d(n_pairs, ctx->num_sms), NT, 0, st>>>(P, po.pairs, n_pairs);
@@ -1026,10 +1028,12 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
       return WS_OK;
     }
     // root list overflow (more than N/16 regions): P no longer holds the roots' self-loops,
-    // so the watershed is redone on the full-scan path below
+    // so the watershed is redone with a list large enough
     WS_TRY(ctx->roots.ensure((size_t)n_roots * sizeof(int), "roots"));
     WS_TRY(ctx->rootc.ensure((size_t)n_roots * sizeof(int), "root labels"));
-    return watershed_t<CONN>(ctx, grad, g, L, num_regions, st);
+    const ws_status s = watershed_t<CONN>(ctx, grad, g, L, num_regions, st);
+    ctx->stats.root_overflow = 1;
+    return s;
   }
   // many cross-tile pairs: chase first (per-root minima on the tiles' roots), then the union
   // (the pair list, or the full q > p scan when it overflowed), then merge the minima into
@@ -1040,6 +1044,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   WS_CUDA(cudaStreamSynchronize(st));
   const int n_roots = (int)reinterpret_cast<const int*>(ctx->pinned)[0];
   if ((size_t)n_roots > cap) {  // list overflow: grow and rebuild it from P
+    ctx->stats.root_overflow = 1;
     WS_TRY(ctx->roots.ensure((size_t)n_roots * sizeof(int), "roots"));
     WS_TRY(ctx->rootc.ensure((size_t)n_roots * sizeof(int), "root labels"));
     WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
