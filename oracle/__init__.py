@@ -39,6 +39,8 @@ def _load():
         lib.oracle_waterfall.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
         lib.oracle_waterfall_reconstruct.argtypes = [vp, vp, i32, i64, i64, i64, i32, i32, vp, vp]
         lib.oracle_watershed_u16.argtypes = lib.oracle_watershed.argtypes
+        lib.oracle_waterfall_u16.argtypes = lib.oracle_waterfall.argtypes
+        lib.oracle_waterfall_u16.restype = ctypes.c_int
         lib.oracle_gradient_u16.argtypes = lib.oracle_gradient.argtypes
         lib.oracle_gradient_u16.restype = ctypes.c_int
         for f in (lib.oracle_gradient, lib.oracle_watershed, lib.oracle_watershed_u16, lib.oracle_waterfall,
@@ -105,16 +107,18 @@ def watershed(grad: np.ndarray, conn: int, ndim: int = None, dumps: bool = False
 
 
 def waterfall(labels: np.ndarray, grad: np.ndarray, conn: int, NL: int, ndim: int = None):
-    """O6+O7: (levels int32 [NL, *shape], counts int64 [NL])."""
+    """O6+O7: (levels int32 [NL, *shape], counts int64 [NL]).  A np.uint16 image uses 16-bit
+    pass heights (O12, NEXT f4)."""
     orig = grad.shape
     if ndim is None:
         ndim = 3 if conn in (6, 26) else 2
-    g, (n0, n1, n2) = _shape3(np.asarray(grad, dtype=np.uint8), ndim)
+    wide = isinstance(grad, np.ndarray) and grad.dtype == np.uint16
+    g, (n0, n1, n2) = _shape3(np.asarray(grad, dtype=np.uint16 if wide else np.uint8), ndim)
     lab = np.ascontiguousarray(np.asarray(labels, dtype=np.int32).reshape(g.shape))
     levels = np.empty((max(NL, 1),) + g.shape, np.int32)
     counts = np.empty(max(NL, 1), np.int64)
-    rc = _load().oracle_waterfall(_p(lab), _p(g), ndim, n0, n1, n2, int(conn), int(NL), _p(levels),
-                                  _p(counts))
+    fn = _load().oracle_waterfall_u16 if wide else _load().oracle_waterfall
+    rc = fn(_p(lab), _p(g), ndim, n0, n1, n2, int(conn), int(NL), _p(levels), _p(counts))
     if rc != 0:
         raise ValueError("oracle_waterfall: invalid arguments")
     return levels.reshape((NL,) + orig), counts

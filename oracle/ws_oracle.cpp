@@ -17,6 +17,7 @@
 //                             canonical label = min voxel index (C7)
 //    oracle_waterfall  O6+O7  RAG with per-pair min pass height (Alg. 4 l.2-7),
 //                             strict edge order K (C14), Boruvka levels (C13)
+//    oracle_waterfall_u16  O12  O6+O7 on a 16-bit image (NEXT f4)
 //    oracle_waterfall_reconstruct  O9  the paper-literal waterfall: newmin + image raise
 //                             (Alg. 4 steps V-VI), watershed re-run per layer (Alg. 5)
 //  Pins (tests/test_oracle_*.py): SciPy/NumPy for O1-O2, closed forms, the paper's worked
@@ -299,8 +300,11 @@ int oracle_watershed_u16(const uint16_t* I, int ndim, int64_t n0, int64_t n1, in
 //   levels[k*N + p] = smallest voxel index of p's level-k region; counts[k] = #regions.
 // `labels` must be a canonical watershed labelling.  Returns 0 ok, 1 invalid args.
 // ---------------------------------------------------------------------------------
-int oracle_waterfall(const int32_t* labels, const uint8_t* I, int ndim, int64_t n0, int64_t n1,
-                     int64_t n2, int conn, int NL, int32_t* levels, int64_t* counts) {
+}  // extern "C"
+
+template <class Px>
+int waterfall_impl(const int32_t* labels, const Px* I, int ndim, int64_t n0, int64_t n1,
+                   int64_t n2, int conn, int NL, int32_t* levels, int64_t* counts) {
   Grid g{ndim, n0, n1, n2};
   if (!valid(g, conn) || NL < 1) return 1;
   int64_t N = g.N();
@@ -353,6 +357,20 @@ int oracle_waterfall(const int32_t* labels, const uint8_t* I, int ndim, int64_t 
     for (int64_t p = 0; p < N; ++p) levels[(int64_t)k * N + p] = (int32_t)find(labels[p]);
   }
   return 0;
+}
+
+extern "C" {
+
+int oracle_waterfall(const int32_t* labels, const uint8_t* I, int ndim, int64_t n0, int64_t n1,
+                     int64_t n2, int conn, int NL, int32_t* levels, int64_t* counts) {
+  return waterfall_impl<uint8_t>(labels, I, ndim, n0, n1, n2, conn, NL, levels, counts);
+}
+
+// O12, the same definition on a 16-bit image (NEXT f4): pass heights max(I(p), I(q))
+// compare as u16, so K (C14) orders 16-bit heights first.
+int oracle_waterfall_u16(const int32_t* labels, const uint16_t* I, int ndim, int64_t n0, int64_t n1,
+                         int64_t n2, int conn, int NL, int32_t* levels, int64_t* counts) {
+  return waterfall_impl<uint16_t>(labels, I, ndim, n0, n1, n2, conn, NL, levels, counts);
 }
 
 // ---------------------------------------------------------------------------------

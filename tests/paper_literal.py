@@ -197,7 +197,7 @@ def rag_bruteforce(labels, I, nbrs):
             if labels[p] != labels[q]:
                 a, b = min(labels[p], labels[q]), max(labels[p], labels[q])
                 h = max(I[p], I[q])
-                E[(a, b)] = min(E.get((a, b), 256), h)
+                E[(a, b)] = min(E[(a, b)], h) if (a, b) in E else h
     return E
 
 

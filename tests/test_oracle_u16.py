@@ -82,3 +82,52 @@ def test_steep_ramp_clips_at_65535():
     chk = np.array([[0, 65535], [65535, 0]], np.uint16)  # |dx| = |dy| = 1 everywhere: g = sqrt 2
     _, g2, q2 = oracle.gradient(chk, 0.0, ndim=2)
     assert np.allclose(g2, np.sqrt(2.0)) and np.all(q2 == 65535)  # clipped (C10 at 16 bits)
+
+
+# ---- O12: the 16-bit waterfall (pass heights max(I(p), I(q)) as u16, K of C14)
+@pytest.mark.parametrize("conn,shape", [(4, (3, 17, 23)), (8, (2, 19, 21)), (6, (7, 9, 11)), (26, (5, 8, 9))])
+@pytest.mark.parametrize("nlev", [4, 40, 256])
+def test_waterfall_monotone_invariance_vs_u8_oracle(conn, shape, nlev):
+    """The waterfall compares pass heights only (max of two intensities, the per-pair min,
+    then K), so a strictly increasing map of the intensities leaves every level unchanged:
+    the u16 levels equal the (separately pinned) u8 oracle's on the rank image."""
+    rng = np.random.default_rng(2000 + conn * 7 + nlev)
+    table = np.sort(rng.choice(65536, size=nlev, replace=False)).astype(np.uint16)
+    img = table[rng.integers(0, nlev, shape)]
+    ndim = 3 if conn in (6, 26) else 2
+    r8 = _rank_u8(img)
+    lab = oracle.watershed(img, conn, ndim=ndim)
+    lv16, c16 = oracle.waterfall(lab, img, conn, 6, ndim=ndim)
+    lv8, c8 = oracle.waterfall(oracle.watershed(r8, conn, ndim=ndim), r8, conn, 6, ndim=ndim)
+    assert np.array_equal(lv16, lv8) and list(c16) == list(c8)
+
+
+@pytest.mark.parametrize("shape,conn,ndim", [((1, 9, 9), 4, 2), ((1, 8, 11), 8, 2), ((3, 4, 5), 6, 3),
+                                             ((3, 3, 4), 26, 3)])
+def test_waterfall_u16_vs_kruskal_mst(shape, conn, ndim):
+    """O8 (independent Kruskal-MST waterfall) on images with many more than 256
+    distinct 16-bit values, so no u8 reduction is involved."""
+    from paper_literal import as_list, kruskal_waterfall, neighbour_table
+    rng = np.random.default_rng(300 + conn)
+    nbrs = neighbour_table(shape, conn, ndim)
+    for _ in range(30):
+        img = rng.integers(0, 65536, size=shape).astype(np.uint16)
+        lab = oracle.watershed(img, conn, ndim=ndim)
+        lv, counts = oracle.waterfall(lab, img, conn, 6, ndim=ndim)
+        ref = kruskal_waterfall(as_list(lab), as_list(img), nbrs, 6)
+        for k in range(6):
+            assert as_list(lv[k]) == ref[k], k
+
+
+def test_waterfall_hand_case_needs_16_bits():
+    # 1-D [0, 256, 10, 300, 20, 255, 30]: regions {0,1} {2,3} {4,5} {6} (each wall descends to
+    # its smaller neighbour, Eq. 1); pass heights 256 (R0-R2), 300 (R2-R4), 255 (R4-R6).  Level
+    # 1: R0 and R2 pick 256, R4 and R6 pick 255, the 300 pass is never picked -> {0..3} {4..6}.
+    # Clipped to 255 all three passes tie and K's max-label tie-break chains them into one
+    # region; wrapped to 8 bits the watershed itself differs.
+    a = np.array([[0, 256, 10, 300, 20, 255, 30]], np.uint16)
+    lab = oracle.watershed(a, 4, ndim=2)
+    assert lab.tolist() == [[0, 0, 2, 2, 4, 4, 6]]
+    lv, counts = oracle.waterfall(lab, a, 4, 3, ndim=2)
+    assert lv[1].tolist() == [[0, 0, 0, 0, 4, 4, 4]] and lv[2].tolist() == [[0] * 7]
+    assert list(counts) == [4, 2, 1]
