@@ -183,6 +183,16 @@ ws_status ws_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, 
                        int32_t connectivity, int32_t NL, int32_t* levels, int64_t* counts,
                        void* stream);
 
+/* ws_waterfall_u16 — ws_waterfall on a 16-bit image (NEXT f4): the same graph waterfall
+ * (C13) with 16-bit pass heights max(I(p), I(q)) and the same strict order K (C14).
+ * K needs 16 + 28 + 28 bits, so per-component minima take two passes (the high word
+ * w << 28 | ~max, then ~min among the edges with the minimum high word).
+ * Arguments as ws_waterfall; labels MUST be canonical ws_watershed_u16 output for the same
+ * grad; grad u16[N] (in, 2-byte aligned).
+ * Errors: as ws_waterfall. */
+ws_status ws_waterfall_u16(ws_ctx* ctx, const int32_t* labels, const uint16_t* grad, ws_dims dims,
+                           int32_t connectivity, int32_t NL, int32_t* levels, int64_t* counts, void* stream);
+
 /* ws_waterfall_reconstruct — the paper's own waterfall by image reconstruction (Sec. 4,
  * P:593-656), single GPU.  Level 0 = labels on I_0 = grad; level k = 1..NL-1:
  *   Step V   newmin(l) = M = 255 (reading C23), then for every p and q in N(p) with

@@ -109,11 +109,15 @@ def waterfall(labels: torch.Tensor, grad: torch.Tensor, conn: int, NL: int, ndim
               ctx: Context = None, out: torch.Tensor = None, mode: str = "graph"):
     """ws_waterfall: levels (int32 [NL, *shape], level 0 = labels) and per-level counts.
     mode="graph": the nested graph waterfall (C13); mode="reconstruct": the paper-literal
-    waterfall by image reconstruction (ws_waterfall_reconstruct, Alg. 4 V-VI + Alg. 5)."""
+    waterfall by image reconstruction (ws_waterfall_reconstruct, Alg. 4 V-VI + Alg. 5).
+    A torch.uint16 grad runs ws_waterfall_u16 (16-bit pass heights, NEXT f4; graph mode)."""
     if mode not in ("graph", "reconstruct"):
         raise ValueError("mode must be 'graph' or 'reconstruct'")
     _req(labels, torch.int32, "labels")
-    _req(grad, torch.uint8, "grad")
+    wide = isinstance(grad, torch.Tensor) and grad.dtype == torch.uint16
+    if wide and mode != "graph":
+        raise ValueError("the reconstruct waterfall takes u8 images")
+    _req(grad, torch.uint16 if wide else torch.uint8, "grad")
     if labels.shape != grad.shape:
         raise ValueError("labels and grad shapes differ")
     ndim = _ndim_for(conn, ndim)
@@ -126,6 +130,8 @@ def waterfall(labels: torch.Tensor, grad: torch.Tensor, conn: int, NL: int, ndim
                                                       device=grad.device)
     counts = (ctypes.c_int64 * max(int(NL), 1))()
     fn = _b.load().ws_waterfall if mode == "graph" else _b.load().ws_waterfall_reconstruct
+    if wide:
+        fn = _b.load().ws_waterfall_u16
     _b.check(fn(ctx.handle, _b.ptr(labels), _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn), int(NL),
                 _b.ptr(levels), counts, _b.stream_of(grad)))
     return levels, list(counts)

@@ -226,7 +226,7 @@ ws_status ws_ctx_destroy(ws_ctx* ctx) {
   ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->tiles, &ctx->roots, &ctx->rootc, &ctx->blockcnt, &ctx->edges, &ctx->ebufA, &ctx->ebufB, &ctx->rootsA, &ctx->rootsB, &ctx->lvl,
                      &ctx->comp, &ctx->best, &ctx->rep_of, &ctx->levelmap, &ctx->lvcount,
                      &ctx->h_grad, &ctx->h_labels, &ctx->h_levels, &ctx->dimg, &ctx->sroots, &ctx->sblocks, &ctx->rank, &ctx->wimg, &ctx->vstate, &ctx->nmin, &ctx->tlist, &ctx->upairs, &ctx->exitmx,
-                     &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc};
+                     &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc, &ctx->best_lo};
   for (auto* b : bufs) b->release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (int i = 0; i < ws_ctx::MAXEV; ++i)
@@ -344,6 +344,30 @@ ws_status ws_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, 
   begin_call(ctx, g);
   tbegin(ctx, (cudaStream_t)stream);
   ws_status s = run_waterfall(ctx, labels, grad, g, connectivity, NL, levels, counts, (cudaStream_t)stream);
+  tfinish(ctx);
+  return s;
+}
+
+ws_status ws_waterfall_u16(ws_ctx* ctx, const int32_t* labels, const uint16_t* grad, ws_dims dims, int32_t connectivity,
+                           int32_t NL, int32_t* levels, int64_t* counts, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  WS_TRY(check_conn(dims, connectivity));
+  if (NL < 1) {
+    set_error(WS_ERR_INVALID, "NL must be >= 1 (got %d)", NL);
+    return WS_ERR_INVALID;
+  }
+  if (!labels) return null_arg("labels");
+  if (!grad) return null_arg("grad");
+  if (!levels) return null_arg("levels");
+  if (reinterpret_cast<uintptr_t>(grad) & 1) {
+    set_error(WS_ERR_INVALID, "grad must be 2-byte aligned");
+    return WS_ERR_INVALID;
+  }
+  begin_call(ctx, g);
+  tbegin(ctx, (cudaStream_t)stream);
+  ws_status s = run_waterfall_u16(ctx, labels, grad, g, connectivity, NL, levels, counts, (cudaStream_t)stream);
   tfinish(ctx);
   return s;
 }

@@ -77,7 +77,8 @@ struct ws_ctx {
   int shard_tiles = 0;    // tile count of the current sharded plateau phase
   int shard_flip = 0;     // which tile-flag buffer holds "next"
   ws::Buf comp;       // i32[R]   component parent (union-find over dense ids)
-  ws::Buf best;       // u64[R]   per-component min-K edge
+  ws::Buf best;       // u64[R]   per-component min-K edge (u16: the hi word of K)
+  ws::Buf best_lo;    // u32[R]   u16 waterfall: the lo word of the per-component min-K edge
   ws::Buf rep_of;     // i32[R]   dense id -> canonical voxel label
   ws::Buf levelmap;   // i32[R*stride]  canonical label of each dense id at levels 0..NL-1
   ws::Buf dimg;       // i32[N]   dense id of every voxel's label (waterfall)
@@ -160,6 +161,8 @@ ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, 
 
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g,
                         int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
+ws_status run_waterfall_u16(ws_ctx* ctx, const int32_t* labels, const uint16_t* grad, const Geo& g,
+                            int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
 ws_status run_watershed_variant(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int variant,
                                 int32_t* labels, int64_t* num_regions, cudaStream_t st);
 ws_status run_waterfall_reconstruct(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g, int conn,

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(NTW) k_dimage_rk(const int* __restrict__ label
 //   3. flush: every unique tile pair becomes its edge key K = [w:8][~max:28][~min:28] (C14),
 //      is appended (block scan + one global atomic per tile) and folded into best[] (the
 //      level-1 per-region min-K edge, RED atomicMin).
-template <int CONN> struct RL {
+template <int CONN, class Px = uint8_t> struct RL {
   using T = TL<CONN>;
   static constexpr bool is3d = T::is3d;
   static constexpr int TX = T::TX, TY = T::TY, TZ = T::TZ;
@@ -249,7 +249,7 @@ template <int CONN> struct RL {
   }
   static_assert((SXI % 16) == 0 && ((SXL * 4) % 16) == 0, "TMA");
   static_assert(SL <= 4096 && NF <= 16, "record encoding [sl:12][f:4]");
-  static constexpr int SIA = (SI + 127) / 128 * 128;           // TMA destinations are 128-byte aligned
+  static constexpr int SIA = (SI * (int)sizeof(Px) + 127) / 128 * 128;  // TMA destinations are 128-byte aligned
   static constexpr int SLA = (4 * SL + 127) / 128 * 128;
   static constexpr int SMEM = SIA + SLA + 12 * HP + 2 * STG;
 };
@@ -261,28 +261,56 @@ __device__ __forceinline__ void fold_best(uint64_t* best, uint64_t k) {
 
 // where the RAG's unique tile edges go (level-1 key list + best[]); emits counts the records
 // that bypassed a full tile hash (ws_stats.rag_global_emits)
+struct E16;
 struct EdgeOut {
   uint64_t* edges;
   unsigned long long* ecount;
   long long cap;
   uint64_t* best;
   unsigned long long* emits;
+  E16* e16;  // 16-bit images: the edge list (w, ids) instead of 64-bit keys (no best[] fold)
 };
 
-__device__ __noinline__ void emit_global(uint64_t k, const EdgeOut& eo) {
+// A waterfall edge of a 16-bit image (ws_waterfall_u16).  K (C14) = (w asc, max desc, min
+// desc) on the level-0 dense ids needs 16 + 28 + 28 bits, more than one u64 holds, so it is
+// the pair (hi, lo): hi = w << 28 | (IDMASK - max), lo = IDMASK - min; per-component minima
+// take two passes (hi, then lo among the edges with the minimum hi).  ca, cb: the endpoints'
+// current components.
+struct E16 {
+  uint64_t hi;
+  uint32_t lo;
+  int ca, cb, pad;
+};
+__host__ __device__ __forceinline__ E16 make_e16(uint32_t w, uint32_t a, uint32_t b) {
+  const uint32_t mx = a > b ? a : b, mn = a > b ? b : a;
+  E16 e;
+  e.hi = ((uint64_t)w << 28) | (uint64_t)(IDMASK - mx);
+  e.lo = IDMASK - mn;
+  e.ca = (int)mn;
+  e.cb = (int)mx;
+  e.pad = 0;
+  return e;
+}
+
+__device__ __noinline__ void emit_global(uint32_t w, uint32_t a, uint32_t b, const EdgeOut& eo) {
   const unsigned long long i = atomicAdd(eo.ecount, 1ull);
-  if ((long long)i < eo.cap) eo.edges[i] = k;
-  fold_best(eo.best, k);
+  if (eo.e16) {
+    if ((long long)i < eo.cap) eo.e16[i] = make_e16(w, a, b);
+  } else {
+    const uint64_t k = make_key(w, a, b);
+    if ((long long)i < eo.cap) eo.edges[i] = k;
+    fold_best(eo.best, k);
+  }
   atomicAdd(eo.emits, 1ull);
 }
 
 // fold staged records into the tile's pair hash.  wst/wcnt: one list of a warp (wsel >= 0:
 // that warp's lane base), or, with wsel < 0, the lists of all warps of the block (counts in
 // wc[], exclusive prefixes in wp[]) spread evenly over all threads.
-template <int CONN>
-__device__ __forceinline__ void fold_rec(unsigned rec, const short* offs, const uint8_t* sI, const int* sD,
+template <int CONN, class Px>
+__device__ __forceinline__ void fold_rec(unsigned rec, const short* offs, const Px* sI, const int* sD,
                                          unsigned long long* pk, unsigned* pw, const EdgeOut& eo) {
-  using R = RL<CONN>;
+  using R = RL<CONN, Px>;
   const int sl = rec >> 4, f = rec & 15;  // [sl:12][f:4]: D-box index of p, forward direction
   const int si = sl + (sl / R::SXL) * (R::SXI - R::SXL) + (R::IXO - R::LXO);  // same voxel in the I box
   const uint32_t dp = (uint32_t)sD[sl], dq = (uint32_t)sD[sl + offs[f]];
@@ -300,20 +328,20 @@ __device__ __forceinline__ void fold_rec(unsigned rec, const short* offs, const 
     }
     h = (h + 1) & (R::HP - 1);
   }
-  emit_global(make_key(w, dp, dq), eo);  // congested tile
+  emit_global(w, dp, dq, eo);  // congested tile
 }
 
-template <int CONN>
-__device__ __forceinline__ void fold_warp(const uint16_t* wst, int wcnt, const short* offs, const uint8_t* sI,
+template <int CONN, class Px>
+__device__ __forceinline__ void fold_warp(const uint16_t* wst, int wcnt, const short* offs, const Px* sI,
                                           const int* sD, unsigned long long* pk, unsigned* pw, const EdgeOut& eo) {
-  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN>(wst[r], offs, sI, sD, pk, pw, eo);
+  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN, Px>(wst[r], offs, sI, sD, pk, pw, eo);
 }
 
-template <int CONN, bool BORDER>
-__device__ __forceinline__ int rag_pairs(const uint8_t* sI, const int* sD, unsigned long long* pk, unsigned* pw,
+template <int CONN, bool BORDER, class Px>
+__device__ __forceinline__ int rag_pairs(const Px* sI, const int* sD, unsigned long long* pk, unsigned* pw,
                                           uint16_t* stg, const short* offs, const Geo& g, const TileCoord& c,
                                           const EdgeOut& eo) {
-  using R = RL<CONN>;
+  using R = RL<CONN, Px>;
   using T = TL<CONN>;
   constexpr int NF = R::NF;
   uint16_t* wst = stg + (threadIdx.x >> 5) * R::WCAP;
@@ -338,7 +366,7 @@ __device__ __forceinline__ int rag_pairs(const uint8_t* sI, const int* sD, unsig
     }
     if (R::MIDFOLD && wcnt > R::WCAP - NF * 32) {
       __syncwarp();
-      fold_warp<CONN>(wst, wcnt, offs, sI, sD, pk, pw, eo);
+      fold_warp<CONN, Px>(wst, wcnt, offs, sI, sD, pk, pw, eo);
       __syncwarp();
       wcnt = 0;
     }
@@ -346,14 +374,14 @@ __device__ __forceinline__ int rag_pairs(const uint8_t* sI, const int* sD, unsig
   return wcnt;
 }
 
-template <int CONN>
-__device__ __forceinline__ void rag_load_plain(const int* __restrict__ D, const uint8_t* __restrict__ I, const Geo& g,
-                                               const TileCoord& c, uint8_t* sI, int* sD) {
-  using R = RL<CONN>;
+template <int CONN, class Px>
+__device__ __forceinline__ void rag_load_plain(const int* __restrict__ D, const Px* __restrict__ I, const Geo& g,
+                                               const TileCoord& c, Px* sI, int* sD) {
+  using R = RL<CONN, Px>;
   for (int s = threadIdx.x; s < R::SI; s += NT) {
     const int sx = s % R::SXI, sy = (s / R::SXI) % R::SY, sz = s / (R::SXI * R::SY);
     const int gx = c.bx + sx - R::IXO, gy = c.by + sy - R::YO, gz = c.bz + sz;
-    uint8_t v = 0;
+    Px v = 0;
     if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
       v = __ldg(I + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
     sI[s] = v;
@@ -370,13 +398,13 @@ __device__ __forceinline__ void rag_load_plain(const int* __restrict__ D, const 
 
 // Persistent CTAs walk the tiles t = blockIdx.x, + gridDim.x, ...; with TMA the next tile's
 // boxes are requested as soon as the current ones are consumed, so the load overlaps the flush.
-template <int CONN>
+template <int CONN, class Px>
 __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mD,
-                                            int tma, const int* __restrict__ D, const uint8_t* __restrict__ I, Geo g,
+                                            int tma, const int* __restrict__ D, const Px* __restrict__ I, Geo g,
                                             int ntx, int nty, int ntiles, EdgeOut eo) {
-  using R = RL<CONN>;
+  using R = RL<CONN, Px>;
   extern __shared__ __align__(128) unsigned char rag_smem[];
-  uint8_t* sI = rag_smem;                                                         // R::SI bytes
+  Px* sI = reinterpret_cast<Px*>(rag_smem);                                       // R::SI pixels
   int* sD = reinterpret_cast<int*>(rag_smem + R::SIA);                            // R::SL dense ids
   unsigned long long* pk = reinterpret_cast<unsigned long long*>(rag_smem + R::SIA + R::SLA);  // R::HP pair keys
   unsigned* pw = reinterpret_cast<unsigned*>(pk + R::HP);                         // R::HP min pass heights
@@ -395,7 +423,7 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
     mbar_init(&bar, 1);
     if ((int)blockIdx.x < ntiles) {
       const TileCoord c0 = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
-      mbar_expect_tx(&bar, R::SI + R::SL * 4);
+      mbar_expect_tx(&bar, R::SI * (int)sizeof(Px) + R::SL * 4);
       tma_load_3d(sI, &mI, c0.bx - R::IXO, c0.by - R::YO, c0.bz, &bar);
       tma_load_3d(sD, &mD, c0.bx - R::LXO, c0.by - R::YO, c0.bz, &bar);
     }
@@ -413,13 +441,13 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
       mbar_wait(&bar, phase);
       phase ^= 1u;
     } else {
-      rag_load_plain<CONN>(D, I, g, c, sI, sD);
+      rag_load_plain<CONN, Px>(D, I, g, c, sI, sD);
       __syncthreads();
     }
     // 1. detection into the per-warp lists
     const int n = tile_interior<CONN>(c, g)
-                      ? rag_pairs<CONN, false>(sI, sD, pk, pw, stg, offs, g, c, eo)
-                      : rag_pairs<CONN, true>(sI, sD, pk, pw, stg, offs, g, c, eo);
+                      ? rag_pairs<CONN, false, Px>(sI, sD, pk, pw, stg, offs, g, c, eo)
+                      : rag_pairs<CONN, true, Px>(sI, sD, pk, pw, stg, offs, g, c, eo);
     if (lane == 0) wc[warp] = n;
     __syncthreads();
     // 2. dedup: the records of all warps spread evenly over the block
@@ -436,13 +464,13 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
           w = u;
           base = pre[u];
         }
-      fold_rec<CONN>(stg[w * R::WCAP + (r - base)], offs, sI, sD, pk, pw, eo);
+      fold_rec<CONN, Px>(stg[w * R::WCAP + (r - base)], offs, sI, sD, pk, pw, eo);
     }
     __syncthreads();  // boxes consumed, hash complete
     const int tn = t + gridDim.x;
     if (tma && threadIdx.x == 0 && tn < ntiles) {
       const TileCoord cn = tile_coord<CONN>(tn, ntx, nty, g);
-      mbar_expect_tx(&bar, R::SI + R::SL * 4);
+      mbar_expect_tx(&bar, R::SI * (int)sizeof(Px) + R::SL * 4);
       tma_load_3d(sI, &mI, cn.bx - R::IXO, cn.by - R::YO, cn.bz, &bar);
       tma_load_3d(sD, &mD, cn.bx - R::LXO, cn.by - R::YO, cn.bz, &bar);
     }
@@ -460,10 +488,14 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
     for (int m = 0; m < M; ++m) {
       const unsigned long long key = pk[threadIdx.x * M + m];
       if (key == KEY_NONE) continue;
-      const uint64_t k = make_key(pw[threadIdx.x * M + m], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
-      if (i < eo.cap) eo.edges[i] = k;
+      if constexpr (sizeof(Px) == 1) {
+        const uint64_t k = make_key(pw[threadIdx.x * M + m], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
+        if (i < eo.cap) eo.edges[i] = k;
+        fold_best(eo.best, k);
+      } else {
+        if (i < eo.cap) eo.e16[i] = make_e16(pw[threadIdx.x * M + m], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
+      }
       ++i;
-      fold_best(eo.best, k);
     }
     __syncthreads();  // flush done before the hash is reset
   }
@@ -760,36 +792,37 @@ __global__ void k_levels_any(const int* __restrict__ D, const int* __restrict__ 
 }
 
 // --------------------------------------------------------------------------- driver
-template <int CONN>
-static ws_status rag_t(const int* D, const uint8_t* I, const Geo& g, const EdgeOut& eo, cudaStream_t st) {
+template <int CONN, class Px>
+static ws_status rag_t(const int* D, const Px* I, const Geo& g, const EdgeOut& eo, cudaStream_t st) {
   using T = TL<CONN>;
-  using R = RL<CONN>;
+  using R = RL<CONN, Px>;
   const int ntx = (g.n2 + T::TX - 1) / T::TX, nty = (g.n1 + T::TY - 1) / T::TY,
             ntz = (g.zhi - g.zlo + T::TZ - 1) / T::TZ;
   Maps mp;
   std::memset(&mp, 0, sizeof(mp));
   const char* env = getenv("WS_NO_TMA");
   const bool off = env && env[0] == '1';
-  const bool a = !off && encode_tmap_3d(&mp.mI, 1, I, g, R::SXI, R::SY, R::SZ);
+  const bool a = !off && encode_tmap_3d(&mp.mI, (int)sizeof(Px), I, g, R::SXI, R::SY, R::SZ);
   const bool b = !off && encode_tmap_3d(&mp.mL, 4, D, g, R::SXL, R::SY, R::SZ);
   mp.tma = (a && b) ? 1 : 0;
-  WS_CUDA(cudaFuncSetAttribute(k_rag<CONN>, cudaFuncAttributeMaxDynamicSharedMemorySize, R::SMEM));
+  WS_CUDA(cudaFuncSetAttribute(k_rag<CONN, Px>, cudaFuncAttributeMaxDynamicSharedMemorySize, R::SMEM));
   // one tile per CTA: CTAs running together hold neighbouring tiles, so the edge list comes
   // out in tile order (the level loop's per-chunk dedup and comp gathers depend on it; a
   // persistent grid interleaves distant tiles and measured slower overall)
   const int ntiles = ntx * nty * ntz;
   const int grid = ntiles;
-  k_rag<CONN><<<grid, NT, R::SMEM, st>>>(mp.mI, mp.mL, mp.tma, D, I, g, ntx, nty, ntiles, eo);
+  k_rag<CONN, Px><<<grid, NT, R::SMEM, st>>>(mp.mI, mp.mL, mp.tma, D, I, g, ntx, nty, ntiles, eo);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
 
-static ws_status rag(int conn, const int* D, const uint8_t* I, const Geo& g, const EdgeOut& eo, cudaStream_t st) {
+template <class Px>
+static ws_status rag(int conn, const int* D, const Px* I, const Geo& g, const EdgeOut& eo, cudaStream_t st) {
   switch (conn) {
-    case 4: return rag_t<4>(D, I, g, eo, st);
-    case 8: return rag_t<8>(D, I, g, eo, st);
-    case 6: return rag_t<6>(D, I, g, eo, st);
-    case 26: return rag_t<26>(D, I, g, eo, st);
+    case 4: return rag_t<4, Px>(D, I, g, eo, st);
+    case 8: return rag_t<8, Px>(D, I, g, eo, st);
+    case 6: return rag_t<6, Px>(D, I, g, eo, st);
+    case 26: return rag_t<26, Px>(D, I, g, eo, st);
   }
   return WS_ERR_INVALID;
 }
@@ -878,8 +911,12 @@ static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
 // RAG edges of the owned planes, tile-deduplicated, folded into best[] (level-1 minima).
 // First the dense-id image D of the owned planes and the plane above (the forward halo) is
 // written into ctx->dimg (same layout as labels).
-static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, const Geo& g, int conn,
+// Px = u16 (ws_waterfall_u16): the unique tile edges go to ctx->edges as E16 records (no
+// best[] fold; the u16 level loop takes its minima in two passes).
+template <class Px = uint8_t>
+static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const Geo& g, int conn,
                         const int* dense_of, cudaStream_t st, const uint2* rk = nullptr) {
+  constexpr size_t ESZ = sizeof(Px) == 1 ? sizeof(uint64_t) : sizeof(E16);
   unsigned long long* ecount = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 136);
   unsigned long long* pathc = ctx->pathc.as<unsigned long long>();
   WS_TRY(ctx->dimg.ensure((size_t)g.N * sizeof(int), "dense-id image"));
@@ -901,10 +938,10 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   }
   tmark(ctx, st, PH_WF_DENSE);
   const long long own = (long long)(g.zhi - g.zlo) * g.plane;
-  long long cap = (long long)(ctx->edges.bytes / sizeof(uint64_t));
+  long long cap = (long long)(ctx->edges.bytes / ESZ);
   const long long want = own / 4 + 4096;
   if (cap < want) {
-    WS_TRY(ctx->edges.ensure((size_t)want * sizeof(uint64_t), "edges"));
+    WS_TRY(ctx->edges.ensure((size_t)want * ESZ, "edges"));
     cap = want;
   }
   // The edge count of a congested input varies slightly from run to run (tiles whose pair
@@ -914,7 +951,9 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   for (int attempt = 0;; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ecount, 0, sizeof(unsigned long long), st));
     WS_CUDA(cudaMemsetAsync(pathc + 2, 0, sizeof(unsigned long long), st));
-    WS_TRY(rag(conn, D, I, g, EdgeOut{ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), pathc + 2}, st));
+    WS_TRY(rag<Px>(conn, D, I, g,
+                   EdgeOut{ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), pathc + 2,
+                           sizeof(Px) == 1 ? nullptr : ctx->edges.as<E16>()}, st));
     launched(ctx, PH_WF_RAG);
     WS_TRY(read_i64(ctx, ecount, &E, st));
     if (E <= cap) break;
@@ -923,14 +962,15 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
       return WS_ERR_INTERNAL;
     }
     cap = E + E / 4 + 4096;
-    WS_TRY(ctx->edges.ensure((size_t)cap * sizeof(uint64_t), "edges"));
+    WS_TRY(ctx->edges.ensure((size_t)cap * ESZ, "edges"));
     WS_CUDA(cudaMemsetAsync(ctx->best.p, 0xFF, (size_t)ctx->wf.R * sizeof(uint64_t), st));
   }
   tmark(ctx, st, PH_WF_RAG);
   ctx->stats.n_edges = E;
   ctx->stats.n_regions = ctx->wf.R;
-  WS_TRY(ctx->ebufA.ensure((size_t)(E > 0 ? E : 1) * sizeof(Edge), "edge buffer A"));
-  WS_TRY(ctx->ebufB.ensure((size_t)(E > 0 ? E : 1) * sizeof(Edge), "edge buffer B"));
+  constexpr size_t LSZ = sizeof(Px) == 1 ? sizeof(Edge) : sizeof(E16);
+  WS_TRY(ctx->ebufA.ensure((size_t)(E > 0 ? E : 1) * LSZ, "edge buffer A"));
+  WS_TRY(ctx->ebufB.ensure((size_t)(E > 0 ? E : 1) * LSZ, "edge buffer B"));
   ctx->wf.E = E;
   ctx->wf.ne_in = E;
   ctx->wf.nr_in = ctx->wf.R;
@@ -1084,6 +1124,124 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   for (int k = 1; k < NL; ++k) WS_TRY(wf_level(ctx, k + 1 < NL, st));
   WS_TRY(wf_finish(ctx, ctx->dimg.as<int>(), g, conn, levels, st));
   if (NL > 1) WS_TRY(wf_read_counts(ctx, NL - 1, counts, st));
+  ctx->stats.waterfall_levels = ctx->wf.lv;
+  return WS_OK;
+}
+
+// ------------------------------------------------- 16-bit waterfall (ws_waterfall_u16)
+// Level k = 1..NL-1 on the E16 list of level k-1 (level 1: the RAG list, endpoints = dense
+// ids): k_e16_live re-labels both endpoints to the current components (one comp hop: the
+// previous level's roots were flattened onto their new roots), drops internal edges, appends
+// the survivors and folds hi into best[c]; k_e16_lo folds lo among the edges whose hi is the
+// component's minimum; k_hook16 merges every component along (hi, lo) = its min-K edge (C14,
+// min-root union C16); k_flatten as for u8.  Counts stay on the device.
+__global__ void __launch_bounds__(NTW) k_e16_live(const E16* __restrict__ in, long long n,
+                                                   const unsigned long long* nptr, const int* __restrict__ comp,
+                                                   uint64_t* best_hi, E16* __restrict__ out, unsigned long long* nout) {
+  if (nptr) n = (long long)*nptr;
+  const int lane = threadIdx.x & 31;
+  for (long long i0 = blockIdx.x * (long long)NTW; i0 < n; i0 += (long long)gridDim.x * NTW) {
+    const long long i = i0 + threadIdx.x;
+    E16 e;
+    bool live = false;
+    if (i < n) {
+      e = in[i];
+      e.ca = __ldg(comp + e.ca);
+      e.cb = __ldg(comp + e.cb);
+      live = e.ca != e.cb;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, live);
+    if (!b) continue;
+    unsigned long long base = 0;
+    if (lane == __ffs(b) - 1) base = atomicAdd(nout, (unsigned long long)__popc(b));
+    base = __shfl_sync(0xffffffffu, base, __ffs(b) - 1);
+    if (live) {
+      out[base + __popc(b & ((1u << lane) - 1))] = e;
+      atomicMin((unsigned long long*)(best_hi + e.ca), (unsigned long long)e.hi);
+      atomicMin((unsigned long long*)(best_hi + e.cb), (unsigned long long)e.hi);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NTW) k_e16_lo(const E16* __restrict__ list, const unsigned long long* nptr,
+                                                 const uint64_t* __restrict__ best_hi, unsigned* best_lo) {
+  const long long n = (long long)*nptr;
+  for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n; i += (long long)gridDim.x * NTW) {
+    const E16 e = list[i];
+    if (__ldcg(reinterpret_cast<const unsigned long long*>(best_hi) + e.ca) == e.hi) atomicMin(best_lo + e.ca, e.lo);
+    if (__ldcg(reinterpret_cast<const unsigned long long*>(best_hi) + e.cb) == e.hi) atomicMin(best_lo + e.cb, e.lo);
+  }
+}
+
+__global__ void k_hook16(uint64_t* best_hi, unsigned* best_lo, int* comp, const int* __restrict__ roots, int n,
+                         const unsigned long long* nptr) {
+  if (nptr) n = (int)*nptr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = roots ? roots[i] : i;
+    const uint64_t hi = best_hi[c];
+    if (hi == KEY_NONE) continue;  // isolated component (C17)
+    const unsigned lo = best_lo[c];
+    best_hi[c] = KEY_NONE;
+    best_lo[c] = 0xffffffffu;
+    int a = (int)(IDMASK - lo), b = (int)(IDMASK - (uint32_t)(hi & IDMASK));
+    while (true) {
+      a = c_find_ro(comp, a);
+      b = c_find_ro(comp, b);
+      if (a == b) break;
+      if (a > b) { const int t = a; a = b; b = t; }
+      if (atomicCAS(comp + b, b, a) == b) break;
+    }
+  }
+}
+
+ws_status run_waterfall_u16(ws_ctx* ctx, const int32_t* labels, const uint16_t* I, const Geo& g, int conn, int NL,
+                            int32_t* levels, int64_t* counts, cudaStream_t st) {
+  if (NL > LVC) {
+    set_error(WS_ERR_LIMIT, "ws_waterfall_u16: NL must be <= %d", LVC);
+    return WS_ERR_LIMIT;
+  }
+  WS_TRY(ctx->flags.ensure(256, "flags"));
+  WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
+  WS_TRY(ctx->pathc.ensure(4 * sizeof(unsigned long long), "path counters"));
+  WS_CUDA(cudaMemsetAsync(ctx->pathc.p, 0, 4 * sizeof(unsigned long long), st));
+  int64_t R = 0;
+  WS_TRY(ctx->rank.ensure(((size_t)g.N / 32 + 1) * sizeof(uint2), "dense rank structure"));
+  uint2* rk = ctx->rank.as<uint2>();
+  WS_TRY(wf_dense(ctx, labels, g.N, 0, 0, ctx->aux.as<int>(), &R, st, rk));
+  WS_TRY(wf_alloc(ctx, R, NL, st));
+  WS_TRY(ctx->best_lo.ensure((size_t)R * sizeof(unsigned), "best lo"));
+  WS_CUDA(cudaMemsetAsync(ctx->best_lo.p, 0xFF, (size_t)R * sizeof(unsigned), st));
+  WS_TRY(wf_rag<uint16_t>(ctx, labels, I, g, conn, nullptr, st, rk));
+  if (counts) counts[0] = R;
+  ctx->stats.level_counts[0] = R;
+  ctx->stats.level_edges[1] = ctx->wf.E;
+  WSState& w = ctx->wf;
+  unsigned long long* cnt = ctx->lvcount.as<unsigned long long>();
+  int* comp = ctx->comp.as<int>();
+  uint64_t* best_hi = ctx->best.as<uint64_t>();
+  unsigned* best_lo = ctx->best_lo.as<unsigned>();
+  int* rA = ctx->rootsA.as<int>();
+  int* rB = ctx->rootsB.as<int>();
+  const E16* ein = ctx->edges.as<E16>();
+  const int ge = grid_for(w.E, ctx->num_sms, 8);
+  for (int k = 1; k < NL; ++k) {
+    E16* eout = (k & 1) ? ctx->ebufA.as<E16>() : ctx->ebufB.as<E16>();
+    int* rin = k == 1 ? nullptr : ((k & 1) ? rB : rA);  // roots of level k-1 (level 1: all R)
+    int* rout = (k & 1) ? rA : rB;
+    const unsigned long long* nin = k == 1 ? nullptr : cnt + (k - 1);
+    k_e16_live<<<ge, NTW, 0, st>>>(ein, w.E, k == 1 ? nullptr : cnt + LVC + k - 1, comp, best_hi, eout,
+                                   cnt + LVC + k);
+    k_e16_lo<<<ge, NTW, 0, st>>>(eout, cnt + LVC + k, best_hi, best_lo);
+    k_hook16<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(best_hi, best_lo, comp, rin, (int)R, nin);
+    k_flatten<<<grid_for(R, ctx->num_sms, 8), NTW, 0, st>>>(comp, rin, (int)R, nin, rout, cnt + k,
+                                                           ctx->lvl.as<uint8_t>(), k);
+    launched(ctx, PH_WF_LEVELS, 4);
+    ein = eout;
+  }
+  WS_CUDA(cudaGetLastError());
+  WS_TRY(wf_finish(ctx, ctx->dimg.as<int>(), g, conn, levels, st));
+  if (NL > 1) WS_TRY(wf_read_counts(ctx, NL - 1, counts, st));
+  for (int k = 1; k < NL && k < 16; ++k) ctx->stats.level_edges[k] = (long long)reinterpret_cast<const unsigned long long*>(ctx->pinned)[LVC + k];
   ctx->stats.waterfall_levels = ctx->wf.lv;
   return WS_OK;
 }

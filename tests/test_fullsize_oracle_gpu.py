@@ -15,6 +15,8 @@ Cases (the configs of BASELINE.json at full or slab size):
   C2       1 x 8192 x 8192  (the full config, 8-conn, NL=6)
   C3       512^3            (the full config, 6-conn, NL=6: giant minimal plateaux in the air)
   C5       1024 x 145 x 145 (the full batch, 4-conn, NL=4)
+  C4 u16   32 x 1024 x 1024 16-bit slab (NEXT f4: ws_gradient_u16 -> ws_watershed_u16 ->
+           ws_waterfall_u16 vs O11, O10, O12)
 
 The size-only code paths are asserted through ws_stats: the dense-id scan looks back beyond
 one 32-block window, k_edges blocks walk more than one chunk, and both step IV union orders
@@ -38,21 +40,26 @@ CASES = {
     "C2": ("C2", None),
     "C3": ("C3", None),
     "C5": ("C5", None),
+    "C4u16slab": ("C4", (32, 1024, 1024)),  # 16-bit volume (NEXT f4): the u8 C4 slab x 256 + a seeded low byte
 }
 
 
-def _gpu_side(name, shape):
+def _gpu_side(case, name, shape):
     import paper_2410_08946_b200 as ws
     c = synth.CONFIGS[name]
     ctx = ws.Context(0)
     raw = synth.make_config_image(name, device="cuda", shape=shape)
+    if case.endswith("u16slab"):  # as bench.py's 16-bit context line
+        gen = torch.Generator(device="cuda").manual_seed(4242)
+        raw = (raw.to(torch.int32) * 256 + torch.randint(0, 256, tuple(raw.shape), generator=gen, device="cuda",
+                                                         dtype=torch.int32)).to(torch.uint16)
     q, blur, grad = ws.gradient(raw, c.sigma, ndim=c.ndim, verify=True, ctx=ctx)
     lab, R = ws.watershed(q, c.conn, ndim=c.ndim, ctx=ctx)
     s_ws = ctx.stats()
     levels, counts = ws.waterfall(lab, q, c.conn, c.NL, ndim=c.ndim, ctx=ctx)
     s_wf = ctx.stats()
     torch.cuda.synchronize()
-    out = {"cfg": c, "raw": raw.cpu().numpy(), "q": q.cpu().numpy(), "blur": blur.cpu().numpy(),
+    out = {"cfg": c, "qmax": 65535.0 if raw.dtype == torch.uint16 else 255.0, "raw": raw.cpu().numpy(), "q": q.cpu().numpy(), "blur": blur.cpu().numpy(),
            "grad": grad.cpu().numpy(), "labels": lab.cpu().numpy(), "R": R, "levels": levels.cpu().numpy(),
            "counts": list(counts), "s_ws": s_ws, "s_wf": s_wf}
     del raw, q, blur, grad, lab, levels
@@ -67,8 +74,8 @@ def _oracle_side(g):
     g["err_grad"] = float(np.max(np.abs(g["grad"] - og)))
     diff = g["q"] != oq
     g["straddles"] = int(diff.sum())
-    t = 255.0 * og[diff]
-    g["straddle_ok"] = bool(np.all(np.abs(t - np.floor(t) - 0.5) <= 255 * FTOL)) and \
+    t = g["qmax"] * og[diff]
+    g["straddle_ok"] = bool(np.all(np.abs(t - np.floor(t) - 0.5) <= g["qmax"] * FTOL)) and \
         bool(np.all(np.abs(g["q"][diff].astype(int) - oq[diff].astype(int)) == 1))
     del ob, og, oq, g["blur"], g["grad"], g["raw"]
     ref = oracle.watershed(g["q"], c.conn, ndim=c.ndim)
@@ -80,7 +87,7 @@ def _oracle_side(g):
 @pytest.fixture(scope="module")
 def results():
     oracle.build()
-    gpu = {k: _gpu_side(*v) for k, v in CASES.items()}
+    gpu = {k: _gpu_side(k, *v) for k, v in CASES.items()}
     with ThreadPoolExecutor(max_workers=len(gpu)) as ex:
         futs = {k: ex.submit(_oracle_side, g) for k, g in gpu.items()}
         return {k: f.result() for k, f in futs.items()}

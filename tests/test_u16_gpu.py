@@ -1,6 +1,7 @@
-"""GPU parity of ws_watershed_u16 (NEXT f4, 16-bit images) against the 16-bit oracle
-(O10), bit-exact labels and region counts; TMA (n2 % 8 == 0) and plain loaders; tiles
-spanning several tiles with ragged tails; and u16 == u8 on order-isomorphic images."""
+"""GPU parity of ws_watershed_u16 and ws_waterfall_u16 (NEXT f4, 16-bit images) against
+the 16-bit oracles (O10, O12): bit-exact labels, every waterfall level and the region counts;
+TMA (n2 % 8 == 0) and plain loaders; several tiles with ragged tails; u16 == u8 on
+order-isomorphic images."""
 import numpy as np
 import pytest
 import torch
@@ -29,15 +30,23 @@ def _img(shape, kind, seed):
     return np.floor(f * 65535).astype(np.uint16)
 
 
-def _check(img, conn, ndim):
+def _check(img, conn, ndim, NL=6):
     ws = _ws()
-    lab, R = ws.watershed(torch.from_numpy(img).cuda(), conn, ndim=ndim)
+    q = torch.from_numpy(img).cuda()
+    lab, R = ws.watershed(q, conn, ndim=ndim)
     ref, _, _, Rref = oracle.watershed(img, conn, ndim=ndim, dumps=True)
     got = lab.cpu().numpy()
     if not np.array_equal(got, ref):
         bad = np.flatnonzero(got.ravel() != ref.ravel())
         pytest.fail("u16 watershed mismatch at %d voxels, first %s" % (bad.size, bad[:5]))
     assert R == Rref
+    lv, counts = ws.waterfall(lab, q, conn, NL, ndim=ndim)  # ws_waterfall_u16
+    rlv, rcounts = oracle.waterfall(ref, img, conn, NL, ndim=ndim)
+    glv = lv.cpu().numpy()
+    for k in range(NL):
+        if not np.array_equal(glv[k], rlv[k]):
+            pytest.fail("u16 waterfall level %d mismatch at %d voxels" % (k, int((glv[k] != rlv[k]).sum())))
+    assert list(counts) == [int(c) for c in rcounts]
 
 
 @pytest.mark.parametrize("kind", ["few", "many", "smooth"])
@@ -61,9 +70,28 @@ def test_u16_equals_u8_on_order_isomorphic_images(conn, ndim, shape):
     rng = np.random.default_rng(5)
     img8 = rng.integers(0, 9, shape).astype(np.uint8)
     img16 = (img8.astype(np.uint16) * 7919 + 11).astype(np.uint16)  # strictly increasing map
-    l8, r8 = ws.watershed(torch.from_numpy(img8).cuda(), conn, ndim=ndim)
-    l16, r16 = ws.watershed(torch.from_numpy(img16).cuda(), conn, ndim=ndim)
+    g8, g16 = torch.from_numpy(img8).cuda(), torch.from_numpy(img16).cuda()
+    l8, r8 = ws.watershed(g8, conn, ndim=ndim)
+    l16, r16 = ws.watershed(g16, conn, ndim=ndim)
     assert r8 == r16 and torch.equal(l8, l16)
+    v8, c8 = ws.waterfall(l8, g8, conn, 6, ndim=ndim)
+    v16, c16 = ws.waterfall(l16, g16, conn, 6, ndim=ndim)
+    assert c8 == c16 and torch.equal(v8, v16)
+
+
+@pytest.mark.parametrize("NL", [1, 2, 4, 9])
+@pytest.mark.parametrize("conn,ndim,shape", [(6, 3, (12, 40, 72)), (4, 2, (3, 64, 100))])
+def test_u16_waterfall_levels(NL, conn, ndim, shape):
+    _check(_img(shape, "smooth", 11 + NL), conn, ndim, NL)
+
+
+def test_u16_waterfall_hand_case():
+    """O12's hand case on the GPU: {0..3} {4..6} at level 1, one region at level 2."""
+    ws = _ws()
+    a = torch.tensor([[[0, 256, 10, 300, 20, 255, 30]]], dtype=torch.uint16).cuda()
+    lab, R = ws.watershed(a, 4, ndim=2)
+    lv, counts = ws.waterfall(lab, a, 4, 3, ndim=2)
+    assert lv[1].cpu().tolist() == [[[0, 0, 0, 0, 4, 4, 4]]] and counts == [4, 2, 1]
 
 
 def test_u16_edge_cases():
