@@ -32,18 +32,19 @@ UNIT = "Mvoxel/s"
 PAPER_CONTEXT = ("paper (P:819 Table 3): 4000x4000x50 raw u8 microCT, watershed only, PRUF 6-conn on an "
                  "RTX 3060 Ti: 1357.75 ms = 589 Mvox/s; no waterfall timings are printed (Figs. 9-10 stripped)")
 
-# algorithmic (compulsory) bytes per voxel of each phase's kernel(s), per launch
+# algorithmic (compulsory) bytes per voxel of each phase's kernel(s), per launch (DESIGN.md
+# §6), for the step's ws_segment call; None = graph / list work (no per-voxel pass)
 ALG_BYTES = {
-    "watershed.init": 5,        # read I (1) + write L (4)
-    "watershed.relax": 5,       # read I + L per round
-    "watershed.select": 9,      # read I + L, write L
-    "watershed.jump": 8,        # read L, write L
-    "watershed.union": 5,       # read I + L
-    "watershed.find": 8,        # read L, write L
-    "watershed.relabel": 8,     # read L, write L
-    "waterfall.dense_ids": 4,   # read labels
-    "waterfall.rag": 5,         # read labels + I
-    "waterfall.materialise": None,  # read labels + write NL levels: 4 + 4 NL
+    "watershed.init": 5,        # k_relax_first: read I (1) + write L (4)
+    "watershed.relax": None,    # active tiles only
+    "watershed.select": 9,      # k_resolve: read I + L, write P
+    "watershed.jump": 8,        # k_jump: read P, write P
+    "watershed.union": None,    # the cross-tile pair list
+    "watershed.find": None,     # the root list
+    "watershed.relabel": 12,    # k_relabel_seg: read P, write level 0 + the dense-id image D
+    "waterfall.dense_ids": None,  # bitmap scan over N/32 words + the root list
+    "waterfall.rag": 5,         # k_rag: read D + I
+    "waterfall.materialise": None,  # k_levels: read D + write levels 1..NL-1: 4 + 4 (NL - 1)
 }
 
 
@@ -76,12 +77,25 @@ def load_peak():
 
 
 def load_traffic():
+    """profiles/ncu_traffic.json (tools/make_traffic.py from an ncu launch list of one step):
+    per-phase DRAM bytes per launch, the step's total and the sha256 of the library captured;
+    `matches_build` says whether that capture is of the library this run loaded."""
+    import hashlib
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f)
+            d = json.load(f)
     except Exception:
         return {}
+    try:
+        lib = os.path.join(ROOT, "paper_2410_08946_b200", "libws_b200.so")
+        cur = hashlib.sha256(open(lib, "rb").read()).hexdigest()
+        prov = d.get("_provenance", {})
+        prov["matches_build"] = prov.get("lib_sha256") == cur
+        d["_provenance"] = prov
+    except Exception:
+        pass
+    return d
 
 
 class Clocks:
@@ -188,6 +202,57 @@ def cpu_oracle_rate(grad_np, cfg, slices):
     dt = time.perf_counter() - t0
     return sub.size / dt / 1e6, dt, "first %d slices %s of the same gradient volume (%d voxels)" % (
         sub.shape[0], "x".join(map(str, sub.shape)), sub.size)
+
+
+def host_cpu():
+    """CPU model and core count of the host (reported next to the oracle)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for l in f:
+                if l.startswith("model name"):
+                    model = l.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+def _c5_worker(args):
+    import oracle
+    q, conn, NL = args
+    lab = oracle.watershed(q, conn, ndim=2)
+    oracle.waterfall(lab, q, conn, NL, ndim=2)
+    return q.size
+
+
+def c5_parallel_oracle(q_np, conn, NL):
+    """The oracle on C5 with one process per host core, a chunk of the independent images each
+    (process-parallel C5 oracle).  Returns (Mvox/s, processes, seconds)."""
+    import multiprocessing as mp
+    import numpy as np
+    import oracle
+    oracle.build()
+    n = os.cpu_count() or 1
+    chunks = [c for c in np.array_split(q_np, n) if c.shape[0] > 0]
+    with mp.get_context("fork").Pool(len(chunks)) as pool:
+        t0 = time.perf_counter()
+        total = sum(pool.map(_c5_worker, [(np.ascontiguousarray(c), conn, NL) for c in chunks]))
+        dt = time.perf_counter() - t0
+    return total / dt / 1e6, len(chunks), dt
+
+
+def straddle_count(raw_head, q_head, sigma, ndim, sl):
+    """C11 on a sample: the oracle's u8 gradient on the first sl slices (computed from sl + 4
+    raw slices: blur radius 3 + 1) vs the GPU's; returns (differing voxels, all straddles?)."""
+    import numpy as np
+    import oracle
+    _, og, oq = oracle.gradient(raw_head, sigma, ndim=ndim)
+    og, oq = og[:sl], oq[:sl]
+    diff = q_head != oq
+    t = 255.0 * og[diff]
+    ok = bool(np.all(np.abs(t - np.floor(t) - 0.5) <= 255 * 1e-5))
+    return int(diff.sum()), ok
 
 
 def run_reference(args):
@@ -394,6 +459,23 @@ def run_ours(args):
             torch.cuda.synchronize()
             pms = e0.elapsed_time(e1) / 3
             paper_protocol[str(c3)] = {"ms": pms, "Mvoxel_per_s": N / (pms / 1e3) / 1e6, "regions": Rraw}
+        # the paper's 128-Mvoxel microCT shape 500x500x512 (207.99 ms 6-conn, 453.55 ms 26-conn
+        # PRUF on an RTX 3060 Ti), the same recipe at that shape, raw, watershed only
+        r128 = synth.make_config_image(cfg.name, device=dev, shape=(512, 500, 500))
+        l128 = torch.empty(r128.shape, dtype=torch.int32, device=dev)
+        ctx128 = {"shape": [512, 500, 500], "paper_ms": {"6": 207.99, "26": 453.554}, "cite": "P:819, P:825 (Table 3)"}
+        for c3 in (6, 26):
+            ws.watershed(r128, c3, ndim=3, ctx=ctx, out=l128)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(5):
+                _, R128 = ws.watershed(r128, c3, ndim=3, ctx=ctx, out=l128)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            pms = e0.elapsed_time(e1) / 5
+            ctx128[str(c3)] = {"ms": pms, "Mvoxel_per_s": r128.numel() / (pms / 1e3) / 1e6, "regions": R128}
+        paper_protocol["raw_500x500x512"] = ctx128
+        del r128, l128
         # 16-bit acquisition (NEXT f4): the u8 volume as the high byte, seeded uniform
         # low byte -> ws_watershed_u16 on the same shape, 6-connectivity
         gen = torch.Generator(device=dev).manual_seed(4242 + rank)
@@ -429,22 +511,34 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         wms16 = e0.elapsed_time(e1) / 3
-        paper_protocol["u16_gradient"] = {"what": "ws_gradient_u16 (sigma of the config) then ws_watershed_u16 6-conn",
-                                          "gradient_ms": gms16, "watershed_ms": wms16, "regions": Rq16,
-                                          "plateau_rounds": ctx.stats()["plateau_rounds"]}
-        del lab_raw, raw16, q16
+        rounds16 = ctx.stats()["plateau_rounds"]
+        lv16 = torch.empty((NL,) + tuple(shape), dtype=torch.int32, device=dev)
+        ws.waterfall(lab_raw, q16, 6, NL, ndim=3, ctx=ctx, out=lv16)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            _, c16 = ws.waterfall(lab_raw, q16, 6, NL, ndim=3, ctx=ctx, out=lv16)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        fms16 = e0.elapsed_time(e1) / 3
+        paper_protocol["u16_gradient"] = {"what": "ws_gradient_u16 (sigma of the config), ws_watershed_u16 6-conn, "
+                                                  "ws_waterfall_u16 NL=%d" % NL,
+                                          "gradient_ms": gms16, "watershed_ms": wms16, "waterfall_ms": fms16,
+                                          "Mvoxel_per_s_watershed_waterfall": N / ((wms16 + fms16) / 1e3) / 1e6,
+                                          "regions": Rq16, "plateau_rounds": rounds16, "level_counts": list(c16)}
+        del lab_raw, raw16, q16, lv16
+    sl_cpu = max(1, min(args.cpu_sample_slices, shape[0])) if cfg.ndim == 3 else shape[0]
+    raw_head = raw[:sl_cpu + 4].cpu().numpy() if cfg.ndim == 3 else raw.cpu().numpy()
     del raw
     torch.cuda.empty_cache()
 
-    labels = torch.empty(shape, dtype=torch.int32, device=dev)
     levels = torch.empty((NL,) + tuple(shape), dtype=torch.int32, device=dev)
+    labels = levels[0]
 
-    def step():
-        ws.watershed(grad, conn, ndim=cfg.ndim, ctx=ctx, out=labels)
-        s1 = ctx.stats()
-        ws.waterfall(labels, grad, conn, NL, ndim=cfg.ndim, ctx=ctx, out=levels)
-        s2 = ctx.stats()
-        return s1, s2
+    def step():  # ws_segment = ws_watershed + ws_waterfall(NL) in one call (levels[0] = labels)
+        ws.segment(grad, conn, NL, ndim=cfg.ndim, ctx=ctx, out=levels)
+        s = ctx.stats()
+        return s, s
 
     for _ in range(args.warmup):
         step()
@@ -461,7 +555,7 @@ def run_ours(args):
         step_ev[i].record(stream)
         s1, s2 = step()
         stats.append((s1, s2))
-        for s in (s1, s2):
+        for s in ((s1,) if s1 is s2 else (s1, s2)):
             launches += s["kernel_launches"]
             for k, v in s["phases"].items():
                 phase_ms[k] = phase_ms.get(k, 0.0) + v["ms"]
@@ -483,7 +577,7 @@ def run_ours(args):
     peak, peak_src = load_peak()
     traffic = load_traffic()
     alg = dict(ALG_BYTES)
-    alg["waterfall.materialise"] = 4 + 4 * NL
+    alg["waterfall.materialise"] = 4 + 4 * (NL - 1)
     cand = {k: v for k, v in phase_ms.items() if alg.get(k)}
     dom = max(cand, key=cand.get)
     per_launch_ms = phase_ms[dom] / max(1, phase_launch[dom])
@@ -491,11 +585,17 @@ def run_ours(args):
     tr = traffic.get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": tr.get("bytes_per_launch") if tr else None,
+                "traffic_source": dict(traffic.get("_provenance", {}), file="profiles/ncu_traffic.json") if tr else None,
                 "alg_bytes_per_voxel": alg[dom], "avg_launch_ms": per_launch_ms,
                 "share_of_step": phase_ms[dom] / (ms_local * args.steps), "peak_source": peak_src}
     step_bytes = 38 if NL == 6 else (5 + 9 + 4 * NL)
     step_roof = {"alg_bytes_per_voxel": step_bytes, "achieved_GBps": step_bytes * N / (ms / 1e3) / 1e9,
                  "frac": step_bytes * N / (ms / 1e3) / 1e9 / peak}
+    if traffic.get("_step") and cfg.name == "C4" and args.shape is None:
+        st = traffic["_step"]
+        step_roof["measured_dram_bytes_per_voxel"] = st.get("dram_bytes_per_voxel")
+        step_roof["amplification_vs_alg"] = st.get("amplification_vs_38B")
+        step_roof["measured_source"] = dict(traffic.get("_provenance", {}), file="profiles/ncu_traffic.json")
 
     # ---- the paper-literal waterfall (Alg. 4 V-VI + watershed per layer,
     # Alg. 5) on the same labels, for context: not the metric (outside the timed region)
@@ -558,31 +658,34 @@ def run_ours(args):
             e1.record(stream)
             torch.cuda.synchronize()
             gms = e0.elapsed_time(e1) / 3
-            olab = torch.empty(oraw.shape, dtype=torch.int32, device=dev)
-            olev = torch.empty((oc.NL,) + tuple(oraw.shape), dtype=torch.int32, device=dev)
-            for _ in range(2):
-                ws.watershed(og, oc.conn, ndim=oc.ndim, ctx=ctx, out=olab)
-                ws.waterfall(olab, og, oc.conn, oc.NL, ndim=oc.ndim, ctx=ctx, out=olev)
-            torch.cuda.synchronize()
-            times = []
-            for _ in range(5):
-                e0.record(stream)
-                _, oR = ws.watershed(og, oc.conn, ndim=oc.ndim, ctx=ctx, out=olab)
-                _, ocounts = ws.waterfall(olab, og, oc.conn, oc.NL, ndim=oc.ndim, ctx=ctx, out=olev)
-                e1.record(stream)
+            for oNL in ((oc.NL, 6) if oc.NL != 6 else (6,)):  # C5: NL = 4 and NL = 6
+                olev = torch.empty((oNL,) + tuple(oraw.shape), dtype=torch.int32, device=dev)
+                for _ in range(2):
+                    ws.segment(og, oc.conn, oNL, ndim=oc.ndim, ctx=ctx, out=olev)
                 torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1))
-            on = oraw.numel()
-            med = statistics.median(times)
-            others[name] = {"workload": oc.desc, "shape": list(oraw.shape), "conn": oc.conn, "NL": oc.NL,
-                            "gradient_ms": gms, "step_ms_min": min(times), "step_ms_median": med,
-                            "Mvoxel_per_s": on / (med / 1e3) / 1e6,
-                            "Mvoxel_per_s_incl_gradient": on / ((med + gms) / 1e3) / 1e6,
-                            "regions": oR, "level_counts": list(ocounts)}
-            del oraw, og, olab, olev
+                times = []
+                for _ in range(10):
+                    e0.record(stream)
+                    _, ocounts = ws.segment(og, oc.conn, oNL, ndim=oc.ndim, ctx=ctx, out=olev)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    times.append(e0.elapsed_time(e1))
+                on = oraw.numel()
+                med = statistics.median(times)
+                sb = 14 + 4 * oNL  # 5 + (9 + 4 NL) algorithmic bytes per voxel
+                key = name if oNL == oc.NL else "%s_NL%d" % (name, oNL)
+                others[key] = {"workload": oc.desc, "shape": list(oraw.shape), "conn": oc.conn, "NL": oNL,
+                               "gradient_ms": gms, "step_ms_min": min(times), "step_ms_median": med,
+                               "Mvoxel_per_s": on / (med / 1e3) / 1e6,
+                               "Mvoxel_per_s_incl_gradient": on / ((med + gms) / 1e3) / 1e6,
+                               "hbm_frac": sb * on / (min(times) / 1e3) / 1e9 / load_peak()[0],
+                               "alg_bytes_per_voxel": sb, "regions": ocounts[0], "level_counts": list(ocounts),
+                               "launches_per_step": ctx.stats()["kernel_launches"]}
+                del olev
+            del oraw, og
             torch.cuda.empty_cache()
-        labels = torch.empty(shape, dtype=torch.int32, device=dev)
         levels = torch.empty((NL,) + tuple(shape), dtype=torch.int32, device=dev)
+        labels = levels[0]
 
     # ---- end to end through the public API with HOST buffers (ws_segment_host)
     e2e = None
@@ -607,8 +710,24 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, sample = cpu_oracle_rate(grad.cpu().numpy(), cfg, args.cpu_sample_slices)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, "seconds": dt}
+        gnp = grad.cpu().numpy()
+        v, dt, sample = cpu_oracle_rate(gnp, cfg, args.cpu_sample_slices)
+        model, ncpu = host_cpu()
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, "seconds": dt,
+               "cpu_model": model, "nproc": ncpu, "note": "single-threaded C++ oracle (-O2), 1 of nproc cores"}
+        nst, st_ok = straddle_count(raw_head, gnp[:sl_cpu], cfg.sigma, cfg.ndim, sl_cpu)
+        cpu["c11_straddles"] = {"voxels": nst, "all_boundary_straddles": st_ok, "sample_voxels": int(gnp[:sl_cpu].size),
+                                "what": "u8 gradient voxels where ws_gradient and the fp64 oracle differ (C11)"}
+        del gnp
+        if world == 1 and args.shape is None and not args.no_other_configs:
+            c5 = synth.CONFIGS["C5"]
+            c5raw = synth.make_config_image("C5", device=dev)
+            c5q = ws.gradient(c5raw, c5.sigma, ndim=2, ctx=ctx).cpu().numpy()
+            pv, pn, pdt = c5_parallel_oracle(c5q, c5.conn, c5.NL)
+            cpu["process_parallel_C5"] = {"value": pv, "unit": UNIT, "cores": pn, "seconds": pdt, "NL": c5.NL,
+                                          "sample": "the full C5 batch %s, one chunk of images per process" %
+                                                    "x".join(map(str, c5q.shape))}
+            del c5raw, c5q
 
     s1, s2 = stats[-1]
     if rank == 0:

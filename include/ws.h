@@ -208,9 +208,20 @@ ws_status ws_waterfall_reconstruct(ws_ctx* ctx, const int32_t* labels, const uin
                                    int32_t connectivity, int32_t NL, int32_t* levels, int64_t* counts,
                                    void* stream);
 
+/* ws_segment — ws_watershed followed by ws_waterfall as ONE call (Alg. 5 is one procedure,
+ * P:629-656): identical outputs, fewer full-volume passes.  The watershed stops before its
+ * relabel; dense region ids come from the root list (a scan over a bitmap of the canonical
+ * labels, N/32 words, instead of a scan over the labels); one pass writes level 0 and the
+ * dense-id image; the level pass writes levels 1..NL-1.
+ * Arguments: grad u8[N] (in), NL >= 1 (C12), levels i32[NL*N] (out, level-major, 16-byte
+ * aligned; levels[0..N) = the canonical watershed labels), counts (HOST i64[NL], optional).
+ * Errors: as ws_watershed and ws_waterfall. */
+ws_status ws_segment(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity, int32_t NL,
+                     int32_t* levels, int64_t* counts, void* stream);
+
 /* ws_segment_host — the end-to-end user call on HOST buffers: copies grad (host, ideally
- * pinned) to the device, runs ws_watershed + ws_waterfall, copies levels back to the host
- * (host i32[NL*N]).  Device buffers come from the context workspace.  Synchronous. */
+ * pinned) to the device, runs ws_segment, copies levels back to the host (host i32[NL*N]).
+ * Device buffers come from the context workspace.  Synchronous. */
 ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims,
                           int32_t connectivity, int32_t NL, int32_t* levels_host,
                           int64_t* counts, void* stream);

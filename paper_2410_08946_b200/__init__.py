@@ -5,6 +5,7 @@ Python API (same names as the C ABI in include/ws.h; argument marshalling only):
     grad_q              = gradient(img, sigma, ndim)             # ws_gradient
     labels, R           = watershed(grad, conn)                  # ws_watershed
     levels, counts      = waterfall(labels, grad, conn, NL)      # ws_waterfall
+    levels, counts      = segment(grad, conn, NL)                # ws_segment (both, one call)
     levels_h, counts    = segment_host(grad_host, conn, NL)      # ws_segment_host (host buffers)
 
 Tensors live on a CUDA device (PyTorch is used for device memory and streams only); work is
@@ -20,7 +21,7 @@ import torch
 from . import _binding as _b
 from ._binding import Context, WsError, default_context  # noqa: F401
 
-__all__ = ["gradient", "watershed", "waterfall", "segment_host", "plateau_debug", "stats", "Context",
+__all__ = ["gradient", "watershed", "waterfall", "segment", "segment_host", "plateau_debug", "stats", "Context",
            "WsError", "version"]
 
 
@@ -134,6 +135,23 @@ def waterfall(labels: torch.Tensor, grad: torch.Tensor, conn: int, NL: int, ndim
         fn = _b.load().ws_waterfall_u16
     _b.check(fn(ctx.handle, _b.ptr(labels), _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn), int(NL),
                 _b.ptr(levels), counts, _b.stream_of(grad)))
+    return levels, list(counts)
+
+
+def segment(grad: torch.Tensor, conn: int, NL: int, ndim: int = None, ctx: Context = None,
+            out: torch.Tensor = None):
+    """ws_segment: ws_watershed + ws_waterfall(NL) as one call (Alg. 5).  Returns
+    (levels int32 [NL, *shape] with levels[0] = the canonical labels, counts)."""
+    _req(grad, torch.uint8, "grad")
+    ndim = _ndim_for(conn, ndim)
+    ctx = ctx or default_context(grad.device.index)
+    if out is not None:
+        _req_out(out, torch.int32, (max(int(NL), 1),) + tuple(grad.shape), grad, "out")
+    levels = out if out is not None else torch.empty((max(int(NL), 1),) + tuple(grad.shape), dtype=torch.int32,
+                                                      device=grad.device)
+    counts = (ctypes.c_int64 * max(int(NL), 1))()
+    _b.check(_b.load().ws_segment(ctx.handle, _b.ptr(grad), _b.dims_of(grad.shape, ndim), int(conn), int(NL),
+                                  _b.ptr(levels), counts, _b.stream_of(grad)))
     return levels, list(counts)
 
 

@@ -226,7 +226,7 @@ ws_status ws_ctx_destroy(ws_ctx* ctx) {
   ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->tiles, &ctx->roots, &ctx->rootc, &ctx->blockcnt, &ctx->edges, &ctx->ebufA, &ctx->ebufB, &ctx->rootsA, &ctx->rootsB, &ctx->lvl,
                      &ctx->comp, &ctx->best, &ctx->rep_of, &ctx->levelmap, &ctx->lvcount,
                      &ctx->h_grad, &ctx->h_labels, &ctx->h_levels, &ctx->dimg, &ctx->sroots, &ctx->sblocks, &ctx->rank, &ctx->wimg, &ctx->vstate, &ctx->nmin, &ctx->tlist, &ctx->upairs, &ctx->exitmx,
-                     &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc, &ctx->best_lo};
+                     &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc, &ctx->best_lo, &ctx->repbits};
   for (auto* b : bufs) b->release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (int i = 0; i < ws_ctx::MAXEV; ++i)
@@ -411,6 +411,25 @@ ws_status ws_waterfall_reconstruct(ws_ctx* ctx, const int32_t* labels, const uin
   return s;
 }
 
+ws_status ws_segment(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity, int32_t NL,
+                     int32_t* levels, int64_t* counts, void* stream) {
+  WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_dims(dims, &g));
+  WS_TRY(check_conn(dims, connectivity));
+  if (NL < 1) {
+    set_error(WS_ERR_INVALID, "NL must be >= 1 (got %d)", NL);
+    return WS_ERR_INVALID;
+  }
+  if (!grad) return null_arg("grad");
+  if (!levels) return null_arg("levels");
+  begin_call(ctx, g);
+  tbegin(ctx, (cudaStream_t)stream);
+  ws_status s = run_segment(ctx, grad, g, connectivity, NL, levels, counts, (cudaStream_t)stream);
+  tfinish(ctx);
+  return s;
+}
+
 ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims, int32_t connectivity, int32_t NL,
                           int32_t* levels_host, int64_t* counts, void* stream) {
   WS_TRY(check_ctx(ctx));
@@ -426,15 +445,12 @@ ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims, i
   cudaStream_t st = (cudaStream_t)stream;
   const size_t N = (size_t)g.N;
   WS_TRY(ctx->h_grad.ensure(N, "segment grad"));
-  WS_TRY(ctx->h_labels.ensure(N * sizeof(int32_t), "segment labels"));
   WS_TRY(ctx->h_levels.ensure(N * (size_t)NL * sizeof(int32_t), "segment levels"));
   begin_call(ctx, g);
   tbegin(ctx, st);
   WS_CUDA(cudaMemcpyAsync(ctx->h_grad.p, grad_host, N, cudaMemcpyHostToDevice, st));
   tmark(ctx, st, PH_COPY);
-  WS_TRY(run_watershed(ctx, ctx->h_grad.as<uint8_t>(), g, connectivity, ctx->h_labels.as<int32_t>(), nullptr, st));
-  WS_TRY(run_waterfall(ctx, ctx->h_labels.as<int32_t>(), ctx->h_grad.as<uint8_t>(), g, connectivity, NL,
-                       ctx->h_levels.as<int32_t>(), counts, st));
+  WS_TRY(run_segment(ctx, ctx->h_grad.as<uint8_t>(), g, connectivity, NL, ctx->h_levels.as<int32_t>(), counts, st));
   WS_CUDA(cudaMemcpyAsync(levels_host, ctx->h_levels.p, N * (size_t)NL * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   tmark(ctx, st, PH_COPY);
   WS_CUDA(cudaStreamSynchronize(st));

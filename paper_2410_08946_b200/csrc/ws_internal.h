@@ -73,6 +73,8 @@ struct ws_ctx {
   WSState wf;
   int64_t total_launches = 0;
   int shard_nroots = 0;
+  int seg_nroots = 0;     // ws_segment: listed roots left by the watershed (ctx->roots)
+  ws::Buf repbits;        // u32[N/32+1] ws_segment: bit c set <=> c is a canonical label
   int shard_conn = 6;     // connectivity of the last ws_shard_local (6 or 26)
   int shard_tiles = 0;    // tile count of the current sharded plateau phase
   int shard_flip = 0;     // which tile-flag buffer holds "next"
@@ -124,12 +126,12 @@ inline void launched(ws_ctx* ctx, int phase, int n = 1) {
 ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, float sigma,
                        uint8_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st);
 ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
-                        int32_t* labels, int64_t* num_regions, cudaStream_t st);
+                        int32_t* labels, int64_t* num_regions, cudaStream_t st, bool relabel = true);
 ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma,
                            uint16_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st);
 namespace px16 {  // ws_watershed16.cu: the same watershed on u16 pixels (unsharded)
 ws_status run_watershed(ws_ctx* ctx, const uint16_t* grad, const Geo& g, int conn, int32_t* labels,
-                        int64_t* num_regions, cudaStream_t st);
+                        int64_t* num_regions, cudaStream_t st, bool relabel = true);
 }
 ws_status run_plateau_debug(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
                             int32_t* dist, int32_t* parent, cudaStream_t st);
@@ -161,6 +163,8 @@ ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, 
 
 ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, const Geo& g,
                         int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
+ws_status run_segment(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int NL, int32_t* levels,
+                      int64_t* counts, cudaStream_t st);
 ws_status run_waterfall_u16(ws_ctx* ctx, const int32_t* labels, const uint16_t* grad, const Geo& g,
                             int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
 ws_status run_watershed_variant(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int variant,

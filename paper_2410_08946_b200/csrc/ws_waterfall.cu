@@ -741,7 +741,7 @@ __global__ void k_levelmap(const int* __restrict__ comp, const uint8_t* __restri
 // stores (evict-first).
 template <int CONN, int STRIDE>
 __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ D, const int* __restrict__ levelmap, int NL,
-                                                 Geo g, int ntx, int nty, int* __restrict__ levels) {
+                                                 Geo g, int ntx, int nty, int* __restrict__ levels, int kfirst) {
   using T = TL<CONN>;
   const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
   const int lane = threadIdx.x & 31;
@@ -777,17 +777,17 @@ __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ D, const
     if (valid) {
 #pragma unroll
       for (int j = 0; j < STRIDE; ++j)
-        if (j < NL) __stcs(levels + (size_t)j * N + p, row[j]);
+        if (j >= kfirst && j < NL) __stcs(levels + (size_t)j * N + p, row[j]);
     }
   }
 }
 
 // scalar variant for large NL (stride not specialised)
 __global__ void k_levels_any(const int* __restrict__ D, const int* __restrict__ levelmap, int NL, int stride,
-                             long long N, int* __restrict__ levels) {
+                             long long N, int* __restrict__ levels, int kfirst) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
     const int* m = levelmap + (size_t)__ldg(D + p) * stride;
-    for (int k = 0; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k);
+    for (int k = kfirst; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k);
   }
 }
 
@@ -921,7 +921,9 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const G
   unsigned long long* pathc = ctx->pathc.as<unsigned long long>();
   WS_TRY(ctx->dimg.ensure((size_t)g.N * sizeof(int), "dense-id image"));
   int* D = ctx->dimg.as<int>();
-  {
+  if (!labels) {  // ws_segment: the relabel pass already wrote D
+    ctx->wf.dofs = 0;
+  } else {
     const int z1 = g.zhi < g.n0 ? g.zhi + 1 : g.zhi;
     const size_t o = (size_t)g.zlo * g.plane;
     const long long n = (long long)(z1 - g.zlo) * g.plane;
@@ -1068,7 +1070,9 @@ static ws_status wf_step(ws_ctx* ctx, int64_t* count, int* more, cudaStream_t st
 }
 
 // level maps (replicated) + level arrays of the voxels of the dense-id image D (n0 planes of g)
-static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn, int32_t* levels, cudaStream_t st) {
+// kfirst = 1 (ws_segment): level 0 was written by the relabel pass
+static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn, int32_t* levels, cudaStream_t st,
+                           int kfirst = 0) {
   WSState& w = ctx->wf;
   const int NL = w.NL, stride = w.stride;
   ctx->stats.waterfall_levels = w.lv;
@@ -1086,12 +1090,12 @@ static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn
     const int TX = is3d ? TL<6>::TX : TL<4>::TX, TY = is3d ? TL<6>::TY : TL<4>::TY, TZ = is3d ? TL<6>::TZ : TL<4>::TZ;
     const int ntx = (g.n2 + TX - 1) / TX, nty = (g.n1 + TY - 1) / TY, ntz = (g.zhi - g.zlo + TZ - 1) / TZ;
     const int nt = ntx * nty * ntz;
-    if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
-    else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
-    else if (stride == 4) k_levels<4, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
-    else k_levels<4, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels, kfirst);
+    else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels, kfirst);
+    else if (stride == 4) k_levels<4, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels, kfirst);
+    else k_levels<4, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels, kfirst);
   } else {
-    k_levels_any<<<gN, NTW, 0, st>>>(D, levelmap, NL, stride, N, levels);
+    k_levels_any<<<gN, NTW, 0, st>>>(D, levelmap, NL, stride, N, levels, kfirst);
   }
   launched(ctx, PH_WF_MATERIALISE);
   tmark(ctx, st, PH_WF_MATERIALISE);
@@ -1123,6 +1127,181 @@ ws_status run_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* I, co
   // the counts are read once, after the level arrays are enqueued
   for (int k = 1; k < NL; ++k) WS_TRY(wf_level(ctx, k + 1 < NL, st));
   WS_TRY(wf_finish(ctx, ctx->dimg.as<int>(), g, conn, levels, st));
+  if (NL > 1) WS_TRY(wf_read_counts(ctx, NL - 1, counts, st));
+  ctx->stats.waterfall_levels = ctx->wf.lv;
+  return WS_OK;
+}
+
+// exclusive scan of the nb block counts in place (one block); total -> bc[nb]
+__global__ void __launch_bounds__(NTW) k_scan_counts(int* bc, int nb) {
+  __shared__ int sm[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nb; b0 += NTW) {
+    const int i = b0 + threadIdx.x;
+    const int v = i < nb ? bc[i] : 0;
+    int tot;
+    const int ex = block_excl_scan(v, sm, tot);
+    if (i < nb) bc[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bc[nb] = carry;
+}
+
+// ------------------------------------------------------ ws_segment (watershed + waterfall)
+// One procedure, as Alg. 5: the watershed stops before its relabel pass, the
+// dense ids come from the root list instead of a scan over the labels, and ONE relabel pass
+// writes both level 0 (the canonical labels) and the dense-id image D:
+//   k_root_bits   bit c of the representative bitmap for the canonical label c of every
+//                 listed root (C7; duplicates on the chase-first path set the same bit)
+//   k_rank_sum / k_scan_counts / k_rank_write   reduce-then-scan over the N/32 bitmap words:
+//                 rk[w] = (reps before voxel 32 w, bits of word w) -> dense(c) = rank of c
+//                 (dense ids keep the canonical label order, C14)
+//   k_root_dense  D[r] = dense id of root r, rep_of[dense] = its canonical label
+//   k_relabel_seg levels[0][p] = canonical label, D[p] = dense id of p's region
+// then the RAG, the level loop and k_levels (levels 1..NL-1) exactly as ws_waterfall.
+__global__ void k_root_bits(const int* __restrict__ P, const int* __restrict__ roots, int n, unsigned* bits) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = -1 - P[roots[i]];
+    atomicOr(bits + (c >> 5), 1u << (c & 31));
+  }
+}
+
+constexpr int RKW = 16;            // bitmap words per thread
+constexpr int RKB = NTW * RKW;     // words per block
+
+__global__ void __launch_bounds__(NTW) k_rank_sum(const unsigned* __restrict__ bits, int nw, int* __restrict__ bsum) {
+  __shared__ int sm[32];
+  const int w0 = blockIdx.x * RKB + threadIdx.x * RKW;
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < RKW; ++j)
+    if (w0 + j < nw) c += __popc(__ldg(bits + w0 + j));
+  int tot;
+  block_excl_scan(c, sm, tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(NTW) k_rank_write(const unsigned* __restrict__ bits, int nw,
+                                                    const int* __restrict__ bsum, uint2* __restrict__ rk) {
+  __shared__ int sm[32];
+  const int w0 = blockIdx.x * RKB + threadIdx.x * RKW;
+  unsigned v[RKW];
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < RKW; ++j) {
+    v[j] = w0 + j < nw ? __ldg(bits + w0 + j) : 0u;
+    c += __popc(v[j]);
+  }
+  int tot;
+  int base = bsum[blockIdx.x] + block_excl_scan(c, sm, tot);
+#pragma unroll
+  for (int j = 0; j < RKW; ++j) {
+    if (w0 + j < nw) rk[w0 + j] = make_uint2((unsigned)base, v[j]);
+    base += __popc(v[j]);
+  }
+}
+
+__global__ void k_root_dense(const int* __restrict__ P, const int* __restrict__ roots, int n,
+                             const uint2* __restrict__ rk, int* __restrict__ D, int* __restrict__ rep_of) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = roots[i];
+    const int c = -1 - P[r];
+    const int d = rank_of(rk, c);
+    D[r] = d;
+    rep_of[d] = c;
+  }
+}
+
+// 4 consecutive voxels per thread.  A root r is written D[r] = its own (already stored) dense
+// id, so the gathers of D at roots never see another value.
+__device__ __forceinline__ void seg_one(const int* __restrict__ P, const int* D, int p, int t, int& lab, int& d) {
+  if (t < 0) {
+    lab = -1 - t;
+    d = D[p];
+  } else {
+    lab = -1 - __ldg(P + t);
+    d = D[t];
+  }
+}
+
+__global__ void __launch_bounds__(NTW) k_relabel_seg(const int* __restrict__ P, int* D, int N, int* __restrict__ L) {
+  const int n4 = N >> 2;
+  const int4* P4 = reinterpret_cast<const int4*>(P);
+  for (int i = blockIdx.x * NTW + threadIdx.x; i < n4; i += gridDim.x * NTW) {
+    const int4 t = __ldg(P4 + i);
+    const int p = 4 * i;
+    int4 o, d;
+    seg_one(P, D, p, t.x, o.x, d.x);
+    if (t.y == t.x && t.x >= 0) { o.y = o.x; d.y = d.x; } else seg_one(P, D, p + 1, t.y, o.y, d.y);
+    if (t.z == t.y && t.y >= 0) { o.z = o.y; d.z = d.y; } else seg_one(P, D, p + 2, t.z, o.z, d.z);
+    if (t.w == t.z && t.z >= 0) { o.w = o.z; d.w = d.z; } else seg_one(P, D, p + 3, t.w, o.w, d.w);
+    __stcs(reinterpret_cast<int4*>(L) + i, o);
+    reinterpret_cast<int4*>(D)[i] = d;
+  }
+  for (int p = 4 * n4 + blockIdx.x * NTW + threadIdx.x; p < N; p += gridDim.x * NTW) {
+    int lab, d;
+    seg_one(P, D, p, P[p], lab, d);
+    L[p] = lab;
+    D[p] = d;
+  }
+}
+
+ws_status run_segment(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int NL, int32_t* levels,
+                      int64_t* counts, cudaStream_t st) {
+  if (NL > LVC) {
+    set_error(WS_ERR_LIMIT, "ws_segment: NL must be <= %d", LVC);
+    return WS_ERR_LIMIT;
+  }
+  if ((reinterpret_cast<uintptr_t>(levels) & 15) != 0) {
+    set_error(WS_ERR_INVALID, "ws_segment: levels must be 16-byte aligned");
+    return WS_ERR_INVALID;
+  }
+  // steps I-IV: every voxel points at a listed root, listed roots hold -1 - canonical label
+  WS_TRY(run_watershed(ctx, I, g, conn, levels, nullptr, st, false));
+  const int n_roots = ctx->seg_nroots;
+  const int* P = ctx->aux.as<int>();
+  const int* roots = ctx->roots.as<int>();
+  WS_TRY(ctx->flags.ensure(256, "flags"));
+  WS_TRY(ctx->pathc.ensure(4 * sizeof(unsigned long long), "path counters"));
+  WS_CUDA(cudaMemsetAsync(ctx->pathc.p, 0, 4 * sizeof(unsigned long long), st));
+  const int nw = g.N / 32 + 1;
+  const int nb = (nw + RKB - 1) / RKB;
+  WS_TRY(ctx->repbits.ensure((size_t)nw * sizeof(unsigned), "representative bitmap"));
+  WS_TRY(ctx->rank.ensure((size_t)nw * sizeof(uint2), "dense rank structure"));
+  WS_TRY(ctx->blockcnt.ensure((size_t)(nb + 1) * sizeof(int), "rank block sums"));
+  unsigned* bits = ctx->repbits.as<unsigned>();
+  int* bsum = ctx->blockcnt.as<int>();
+  uint2* rk = ctx->rank.as<uint2>();
+  WS_CUDA(cudaMemsetAsync(bits, 0, (size_t)nw * sizeof(unsigned), st));
+  k_root_bits<<<grid_for(n_roots, ctx->num_sms), 256, 0, st>>>(P, roots, n_roots, bits);
+  k_rank_sum<<<nb, NTW, 0, st>>>(bits, nw, bsum);
+  k_scan_counts<<<1, NTW, 0, st>>>(bsum, nb);
+  k_rank_write<<<nb, NTW, 0, st>>>(bits, nw, bsum, rk);
+  launched(ctx, PH_WF_DENSE, 4);
+  WS_CUDA(cudaMemcpyAsync(ctx->pinned, bsum + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaStreamSynchronize(st));
+  const int64_t R = reinterpret_cast<const int*>(ctx->pinned)[0];
+  ctx->stats.n_regions = R;
+  WS_TRY(wf_alloc(ctx, R, NL, st));
+  WS_TRY(ctx->rep_of.ensure((size_t)R * sizeof(int), "rep_of"));
+  WS_TRY(ctx->dimg.ensure((size_t)g.N * sizeof(int), "dense-id image"));
+  int* D = ctx->dimg.as<int>();
+  k_root_dense<<<grid_for(n_roots, ctx->num_sms), 256, 0, st>>>(P, roots, n_roots, rk, D, ctx->rep_of.as<int>());
+  launched(ctx, PH_WF_DENSE);
+  tmark(ctx, st, PH_WF_DENSE);
+  k_relabel_seg<<<grid_for(g.N / 4 + 1, ctx->num_sms), NTW, 0, st>>>(P, D, g.N, levels);
+  launched(ctx, PH_WS_RELABEL);
+  tmark(ctx, st, PH_WS_RELABEL);
+  WS_TRY(wf_rag<uint8_t>(ctx, nullptr, I, g, conn, nullptr, st));
+  if (counts) counts[0] = R;
+  ctx->stats.level_counts[0] = R;
+  ctx->stats.level_edges[1] = ctx->wf.E;
+  for (int k = 1; k < NL; ++k) WS_TRY(wf_level(ctx, k + 1 < NL, st));
+  WS_TRY(wf_finish(ctx, D, g, conn, levels, st, 1));
   if (NL > 1) WS_TRY(wf_read_counts(ctx, NL - 1, counts, st));
   ctx->stats.waterfall_levels = ctx->wf.lv;
   return WS_OK;
@@ -1332,25 +1511,6 @@ __global__ void __launch_bounds__(NTW) k_root_count(const int* __restrict__ comp
   int tot;
   block_excl_scan(c, sm, tot);
   if (threadIdx.x == 0) bc[blockIdx.x] = tot;
-}
-
-// exclusive scan of the nb block counts in place (one block); total -> bc[nb]
-__global__ void __launch_bounds__(NTW) k_scan_counts(int* bc, int nb) {
-  __shared__ int sm[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int b0 = 0; b0 < nb; b0 += NTW) {
-    const int i = b0 + threadIdx.x;
-    const int v = i < nb ? bc[i] : 0;
-    int tot;
-    const int ex = block_excl_scan(v, sm, tot);
-    if (i < nb) bc[i] = carry + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) bc[nb] = carry;
 }
 
 // sorted roots and the flipped minima of this rank at them

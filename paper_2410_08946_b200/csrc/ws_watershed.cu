@@ -960,9 +960,13 @@ static ws_status pair_out(ws_ctx* ctx, const Geo& g, PairOut& po, cudaStream_t s
   return WS_OK;
 }
 
+// relabel == false (ws_segment): stop before the relabel pass; P = ctx->aux then holds, for
+// every voxel, a listed root (or, at a listed root r, P[r] = -1 - canonical label), and the
+// listed roots are ctx->roots[0 .. ctx->seg_nroots) (a superset of the final roots on the
+// chase-first path; every listed root maps to its region's canonical label).
 template <int CONN>
 static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* L, int64_t* num_regions,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool relabel = true) {
   const TileGrid tg = tiles_of<CONN>(g);
   Maps mp;
   make_maps<CONN>(grad, L, g, mp);
@@ -1012,6 +1016,23 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
     k_root_canon<<<grid1d((long long)g.N / 32, ctx->num_sms), NT, 0, st>>>(P, L, roots, nr, (int)cap);
     launched(ctx, PH_WS_FIND);
     tmark(ctx, st, PH_WS_FIND);
+    if (!relabel) {
+      WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
+      WS_CUDA(cudaStreamSynchronize(st));
+      const int n_roots = reinterpret_cast<const int*>(ctx->pinned)[0];
+      if ((size_t)n_roots <= cap) {
+        ctx->seg_nroots = n_roots;
+        ctx->stats.n_regions = n_roots;
+        if (num_regions) *num_regions = n_roots;
+        WS_CUDA(cudaGetLastError());
+        return WS_OK;
+      }
+      WS_TRY(ctx->roots.ensure((size_t)n_roots * sizeof(int), "roots"));
+      WS_TRY(ctx->rootc.ensure((size_t)n_roots * sizeof(int), "root labels"));
+      const ws_status s = watershed_t<CONN>(ctx, grad, g, L, num_regions, st, false);
+      ctx->stats.root_overflow = 1;
+      return s;
+    }
     if (!(reinterpret_cast<uintptr_t>(P) & 15) && !(reinterpret_cast<uintptr_t>(L) & 15))
       k_relabel4<<<grid1d(g.N / 4 + 1, ctx->num_sms), NT, 0, st>>>(P, L, g.N);
     else
@@ -1070,6 +1091,15 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   k_root_store<<<gR, NT, 0, st>>>(P, roots, ctx->rootc.as<int>(), n_roots);
   launched(ctx, PH_WS_FIND, 3);
   tmark(ctx, st, PH_WS_FIND);
+  if (!relabel) {
+    ctx->seg_nroots = n_roots;
+    WS_CUDA(cudaGetLastError());
+    WS_CUDA(cudaMemcpyAsync(ctx->pinned, nfinal, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    WS_CUDA(cudaStreamSynchronize(st));
+    ctx->stats.n_regions = ctx->pinned[0];
+    if (num_regions) *num_regions = ctx->pinned[0];
+    return WS_OK;
+  }
   k_relabel<<<gN, NT, 0, st>>>(P, L, g.N);
   launched(ctx, PH_WS_RELABEL);
   tmark(ctx, st, PH_WS_RELABEL);
@@ -1193,12 +1223,12 @@ ws_status resolve_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, con
 #endif  // !WS_PX16
 
 ws_status run_watershed(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* labels,
-                        int64_t* num_regions, cudaStream_t st) {
+                        int64_t* num_regions, cudaStream_t st, bool relabel) {
   switch (conn) {
-    case 4: return watershed_t<4>(ctx, grad, g, labels, num_regions, st);
-    case 8: return watershed_t<8>(ctx, grad, g, labels, num_regions, st);
-    case 6: return watershed_t<6>(ctx, grad, g, labels, num_regions, st);
-    case 26: return watershed_t<26>(ctx, grad, g, labels, num_regions, st);
+    case 4: return watershed_t<4>(ctx, grad, g, labels, num_regions, st, relabel);
+    case 8: return watershed_t<8>(ctx, grad, g, labels, num_regions, st, relabel);
+    case 6: return watershed_t<6>(ctx, grad, g, labels, num_regions, st, relabel);
+    case 26: return watershed_t<26>(ctx, grad, g, labels, num_regions, st, relabel);
   }
   set_error(WS_ERR_INVALID, "connectivity must be 4, 8, 6 or 26");
   return WS_ERR_INVALID;

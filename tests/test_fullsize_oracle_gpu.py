@@ -149,3 +149,17 @@ def test_dense_scan_multiwindow_lookback(results, monkeypatch):
     assert st["lookback_max"] > 32 * 32, st["lookback_max"]
     assert np.array_equal(levels.cpu().numpy(), g["ref_levels"])
     assert list(counts) == [int(x) for x in g["ref_counts"]]
+
+
+@pytest.mark.parametrize("case", ["C4slab", "C2", "C3", "C5"])
+def test_segment_full_size(results, case):
+    """ws_segment (the bench's step call) on the same agreed image: every level exact."""
+    import paper_2410_08946_b200 as ws
+    g = results[case]
+    c = g["cfg"]
+    lv, counts = ws.segment(torch.from_numpy(g["q"]).cuda(), c.conn, c.NL, ndim=c.ndim)
+    got = lv.cpu().numpy()
+    for k in range(c.NL):
+        bad = np.flatnonzero(got[k].ravel() != g["ref_levels"][k].ravel())
+        assert bad.size == 0, "%s segment level %d: %d mismatches" % (case, k, bad.size)
+    assert counts == [int(x) for x in g["ref_counts"]]

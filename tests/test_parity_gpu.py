@@ -281,3 +281,43 @@ def test_paper_variants_parity(variant, conn, ndim, shape, levels):
     ref, _, _, Rref = oracle.watershed(qn, conn, ndim=ndim, dumps=True)
     assert np.array_equal(lab.cpu().numpy(), ref)
     assert R == Rref
+
+
+# ---------------------------------------------------------------- ws_segment (one call)
+def check_segment(q_dev, q_np, conn, ndim, NL):
+    """ws_segment == oracle watershed + waterfall: every level (level 0 = the labels) and the
+    counts, bit-exact."""
+    ws = _ws()
+    lv, counts = ws.segment(q_dev, conn, NL, ndim=ndim)
+    ref = oracle.watershed(q_np, conn, ndim=ndim)
+    rlv, rcounts = oracle.waterfall(ref, q_np, conn, NL, ndim=ndim)
+    got = lv.cpu().numpy()
+    for k in range(NL):
+        if not np.array_equal(got[k], rlv[k]):
+            pytest.fail("segment level %d mismatch at %d voxels" % (k, int((got[k] != rlv[k]).sum())))
+    assert list(counts) == [int(c) for c in rcounts]
+
+
+@pytest.mark.parametrize("name,shape", CASES)
+def test_segment_parity_config(name, shape):
+    c = synth.CONFIGS[name]
+    raw = synth.make_config_image(name, shape=shape, device="cuda")
+    q = _ws().gradient(raw, c.sigma, ndim=c.ndim)
+    check_segment(q, q.cpu().numpy(), c.conn, c.ndim, c.NL)
+
+
+@pytest.mark.parametrize("conn,ndim,shape", [(4, 2, (3, 37, 61)), (8, 2, (2, 45, 33)), (6, 3, (13, 17, 70)),
+                                             (26, 3, (9, 21, 35)), (4, 2, (1, 1, 301)), (6, 3, (1, 23, 29))])
+@pytest.mark.parametrize("levels,NL", [(2, 1), (3, 6), (16, 3)])
+def test_segment_random_plateau_images(conn, ndim, shape, levels, NL):
+    """Plateau-forcing inputs incl. giant minimal plateaux (the chase-first union order: listed
+    roots that are not final), ragged tails, N % 4 != 0, NL = 1."""
+    g = synth.random_plateau_image(shape, levels, seed=levels * 10 + conn)
+    check_segment(g.cuda(), g.numpy(), conn, ndim, NL)
+
+
+def test_segment_edge_cases():
+    for img, conn, ndim in [(np.zeros((1, 1, 1), np.uint8), 6, 3), (np.full((3, 5, 7), 9, np.uint8), 26, 3),
+                            (np.arange(64, dtype=np.uint8).reshape(1, 1, 64), 4, 2),
+                            (np.zeros((1, 1, 3), np.uint8), 8, 2)]:
+        check_segment(torch.from_numpy(img).cuda(), img, conn, ndim, 4)
