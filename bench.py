@@ -41,10 +41,10 @@ ALG_BYTES = {
     "watershed.jump": 8,        # k_jump: read P, write P
     "watershed.union": None,    # the cross-tile pair list
     "watershed.find": None,     # the root list
-    "watershed.relabel": 12,    # k_relabel_seg: read P, write level 0 + the dense-id image D
+    "watershed.relabel": 8,     # k_relabel_seg: read P, write the dense-id image D
     "waterfall.dense_ids": None,  # bitmap scan over N/32 words + the root list
     "waterfall.rag": 5,         # k_rag: read D + I
-    "waterfall.materialise": None,  # k_levels: read D + write levels 1..NL-1: 4 + 4 (NL - 1)
+    "waterfall.materialise": None,  # k_levels: read D + write levels 0..NL-1: 4 + 4 NL
 }
 
 
@@ -577,7 +577,7 @@ def run_ours(args):
     peak, peak_src = load_peak()
     traffic = load_traffic()
     alg = dict(ALG_BYTES)
-    alg["waterfall.materialise"] = 4 + 4 * (NL - 1)
+    alg["waterfall.materialise"] = 4 + 4 * NL
     cand = {k: v for k, v in phase_ms.items() if alg.get(k)}
     dom = max(cand, key=cand.get)
     per_launch_ms = phase_ms[dom] / max(1, phase_launch[dom])
@@ -751,7 +751,8 @@ def run_ours(args):
             "phases_ms_per_step": {k: v / args.steps for k, v in sorted(phase_ms.items(), key=lambda x: -x[1])},
             "input_stats": {"regions": s1["n_regions"], "edges": s2["n_edges"],
                             "plateau_rounds": s1["plateau_rounds"], "level_counts": s2["level_counts"][:NL],
-                            "level_edges": s2["level_edges"][1:NL]},
+                            "level_edges": s2["level_edges"][1:NL], "rag_records": s2.get("rag_records"),
+                            "rag_global_emits": s2.get("rag_global_emits")},
             "context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)

@@ -87,6 +87,7 @@ typedef struct ws_stats {
   int32_t lookback_max;       /* ws_waterfall: deepest look-back (blocks) of the dense-id scan   */
   int32_t edge_chunks_max;    /* ws_waterfall: most edge chunks one k_edges block walked         */
   int64_t rag_global_emits;   /* ws_waterfall: RAG records emitted past a full tile pair hash    */
+  int64_t rag_records;        /* ws_waterfall: boundary records the RAG staged after run merging  */
 } ws_stats;
 
 ws_status ws_ctx_create(int32_t device, ws_ctx** out);

@@ -43,7 +43,8 @@ class WsStats(ctypes.Structure):
                 ("tma", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("level_edges", ctypes.c_int64 * 16),
                 ("total_launches", ctypes.c_int64), ("union_order", ctypes.c_int32),
                 ("root_overflow", ctypes.c_int32), ("lookback_max", ctypes.c_int32),
-                ("edge_chunks_max", ctypes.c_int32), ("rag_global_emits", ctypes.c_int64)]
+                ("edge_chunks_max", ctypes.c_int32), ("rag_global_emits", ctypes.c_int64),
+                ("rag_records", ctypes.c_int64)]
 
     def as_dict(self):
         lib = load()
@@ -58,7 +59,8 @@ class WsStats(ctypes.Structure):
                 "phases": phases, "tma": self.tma, "level_edges": list(self.level_edges),
                 "total_launches": self.total_launches, "union_order": self.union_order,
                 "root_overflow": self.root_overflow, "lookback_max": self.lookback_max,
-                "edge_chunks_max": self.edge_chunks_max, "rag_global_emits": self.rag_global_emits}
+                "edge_chunks_max": self.edge_chunks_max, "rag_global_emits": self.rag_global_emits,
+                "rag_records": self.rag_records}
 
 
 class WsError(RuntimeError):

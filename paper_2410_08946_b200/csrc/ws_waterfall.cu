@@ -212,12 +212,18 @@ __global__ void __launch_bounds__(NTW) k_dimage_rk(const int* __restrict__ label
 //   1. detection: every (voxel p, forward direction f) with D(p) != D(p + f) is a boundary
 //      pair; it is appended as a 16-bit record (voxel step k, lane, f) to the warp's staging
 //      list with ballot + popc (uniform, no atomics, no divergent work);
-//   2. dedup: the warp walks its list with all lanes, re-reads D(p), D(q) and the pass height
+//   2. dedup: every warp walks its own list with all lanes (a record's box indices are the
+//      warp's base + k * step + lane), re-reads D(p), D(q) and the pass height
 //      w = max(I(p), I(q)) from shared memory, and folds the pair into the tile's
-//      shared hash (64-bit pair key, CAS insert; 32-bit w with atomicMin = the per-pair
-//      minimum pass height, Alg. 4 l.2-7);
+//      shared hash (2048 slots, linear probing).  u8 images: one 64-bit slot holds the pair
+//      AND its height, [min:28][max:28][w:8]: a CAS inserts it, and a record of a pair
+//      already present lowers the height with a 32-bit atomicMin on the slot's low word
+//      (whose upper 24 bits are the pair's, equal for all contenders) when its w is below
+//      the one just read = the per-pair minimum pass height, Alg. 4 l.2-7.  16-bit images
+//      keep the pair key and a 32-bit height in two arrays;
 //   3. flush: every unique tile pair becomes its edge key K = [w:8][~max:28][~min:28] (C14),
-//      is appended (block scan + one global atomic per tile) and folded into best[] (the
+//      is appended (block scan + one global atomic per tile; thread t owns the slots t,
+//      t + NT, ..., so the slot reads are bank-conflict free) and folded into best[] (the
 //      level-1 per-region min-K edge, RED atomicMin).
 template <int CONN, class Px = uint8_t> struct RL {
   using T = TL<CONN>;
@@ -229,11 +235,14 @@ template <int CONN, class Px = uint8_t> struct RL {
   static constexpr int IXO = XA ? 16 : 0, LXO = XA ? 4 : 0, YO = YA;
   static constexpr int SXI = TX + 16 + IXO, SXL = TX + 4 + LXO, SY = TY + 1 + YA, SZ = is3d ? TZ + 1 : 1;
   static constexpr int SI = SXI * SY * SZ, SL = SXL * SY * SZ;
-  static constexpr int HP = 1024;  // pair slots per tile (overflow -> direct global emit)
+  static constexpr int HP = 2048;  // pair slots per tile (overflow -> direct global emit)
+  static constexpr int HB = 11;    // log2(HP)
+  static constexpr bool PACK = sizeof(Px) == 1;  // u8: pair + height in one 64-bit slot
+  static constexpr int SLOT = PACK ? 8 : 12;     // bytes per slot (16-bit: key + separate height)
   static constexpr int NF = CONN - Conn<CONN>::nfwd;
-  static constexpr int WALL = T::VPT * NF * 32;             // records a warp can produce
-  static constexpr int WCAP = WALL < 1024 ? WALL : 1024;    // per-warp staging list
-  static constexpr bool MIDFOLD = WALL > WCAP;              // fold inside the detection loop
+  static constexpr int WALL = T::VPT * NF * 32;  // records a warp can produce
+  static constexpr int WCAP = WALL < 512 ? WALL : 512;  // per-warp staging list
+  static constexpr bool MIDFOLD = WALL > WCAP;           // fold inside the detection loop
   static constexpr int STG = WCAP * (NT / 32);
   __device__ static constexpr int iI(int lz, int ly, int lx) { return (lz * SY + ly + YO) * SXI + lx + IXO; }
   __device__ static constexpr int iL(int lz, int ly, int lx) { return (lz * SY + ly + YO) * SXL + lx + LXO; }
@@ -248,10 +257,11 @@ template <int CONN, class Px = uint8_t> struct RL {
     return (dz * SY + dy) * SXL + dx;
   }
   static_assert((SXI % 16) == 0 && ((SXL * 4) % 16) == 0, "TMA");
-  static_assert(SL <= 4096 && NF <= 16, "record encoding [sl:12][f:4]");
+  static_assert(T::VPT <= 8 && NF <= 16, "record encoding [k:3][lane:5][f:4]");
+  static_assert(WCAP >= NF * 32, "staging list holds one detection step");
   static constexpr int SIA = (SI * (int)sizeof(Px) + 127) / 128 * 128;  // TMA destinations are 128-byte aligned
   static constexpr int SLA = (4 * SL + 127) / 128 * 128;
-  static constexpr int SMEM = SIA + SLA + 12 * HP + 2 * STG;
+  static constexpr int SMEM = SIA + SLA + SLOT * HP + 2 * STG;
 };
 
 __device__ __forceinline__ void fold_best(uint64_t* best, uint64_t k) {
@@ -268,7 +278,8 @@ struct EdgeOut {
   long long cap;
   uint64_t* best;
   unsigned long long* emits;
-  E16* e16;  // 16-bit images: the edge list (w, ids) instead of 64-bit keys (no best[] fold)
+  E16* e16;                  // 16-bit images: the edge list (w, ids) instead of 64-bit keys (no best[] fold)
+  unsigned long long* recs;  // staged boundary records (ws_stats.rag_records), may be null
 };
 
 // A waterfall edge of a 16-bit image (ws_waterfall_u16).  K (C14) = (w asc, max desc, min
@@ -304,20 +315,65 @@ __device__ __noinline__ void emit_global(uint32_t w, uint32_t a, uint32_t b, con
   atomicAdd(eo.emits, 1ull);
 }
 
-// fold staged records into the tile's pair hash.  wst/wcnt: one list of a warp (wsel >= 0:
-// that warp's lane base), or, with wsel < 0, the lists of all warps of the block (counts in
-// wc[], exclusive prefixes in wp[]) spread evenly over all threads.
+// Box indices of a warp's voxels: voxel k of lane l is D-box index wb.x + k * wb.y + l and
+// I-box index wb.z + k * wb.w + l (lanes run along x inside one row of the tile).
 template <int CONN, class Px>
-__device__ __forceinline__ void fold_rec(unsigned rec, const short* offs, const Px* sI, const int* sD,
+__device__ __forceinline__ int4 warp_boxes() {
+  using R = RL<CONN, Px>;
+  int lx, ly, lz, lx1, ly1, lz1;
+  my_voxel<CONN>(0, lx, ly, lz);
+  my_voxel<CONN>(1, lx1, ly1, lz1);
+  const int lane = threadIdx.x & 31;
+  const int l0 = R::iL(lz, ly, lx) - lane, i0 = R::iI(lz, ly, lx) - lane;
+  return make_int4(l0, R::iL(lz1, ly1, lx1) - lane - l0, i0, R::iI(lz1, ly1, lx1) - lane - i0);
+}
+
+template <int HB>
+__device__ __forceinline__ uint32_t pair_hash(uint32_t lo, uint32_t hi) {
+  return ((lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u)) >> (32 - HB);
+}
+
+// u8: fold one packed key [min:28][max:28][w:8] into the tile's hash
+template <int HB>
+__device__ __forceinline__ void fold_key(unsigned long long* pk, unsigned long long key, const EdgeOut& eo) {
+  const uint32_t lo = (uint32_t)(key >> 36), hi = (uint32_t)(key >> 8) & IDMASK;
+  uint32_t h = pair_hash<HB>(lo, hi);
+#pragma unroll 1
+  for (int probe = 0; probe < 64; ++probe) {
+    unsigned long long cur = pk[h];
+    if (cur == KEY_NONE) {
+      cur = atomicCAS(pk + h, KEY_NONE, key);
+      if (cur == KEY_NONE) return;  // inserted with this key's height
+    }
+    if ((cur >> 8) == (key >> 8)) {
+      // same pair: lower the height (the slot's low word carries the pair's bits 0..23
+      // above w, equal for every contender, so a 32-bit min on it is the min of w)
+      if ((unsigned)(cur & 0xff) > ((unsigned)key & 0xff))
+        atomicMin(reinterpret_cast<unsigned*>(pk + h), (unsigned)key);
+      return;
+    }
+    h = (h + 1) & ((1u << HB) - 1);
+  }
+  emit_global((unsigned)key & 0xff, lo, hi, eo);  // congested tile
+}
+
+// fold one record rec = [k:3][lane:5][f:4] (re-reads the boxes).  u8: as a packed key;
+// 16-bit images: key + separate height
+template <int CONN, class Px>
+__device__ __forceinline__ void fold_rec(unsigned rec, int4 wb, const short* offs, const Px* sI, const int* sD,
                                          unsigned long long* pk, unsigned* pw, const EdgeOut& eo) {
   using R = RL<CONN, Px>;
-  const int sl = rec >> 4, f = rec & 15;  // [sl:12][f:4]: D-box index of p, forward direction
-  const int si = sl + (sl / R::SXL) * (R::SXI - R::SXL) + (R::IXO - R::LXO);  // same voxel in the I box
+  const int f = rec & 15, l = (rec >> 4) & 31, k = rec >> 9;
+  const int sl = wb.x + k * wb.y + l, si = wb.z + k * wb.w + l;
   const uint32_t dp = (uint32_t)sD[sl], dq = (uint32_t)sD[sl + offs[f]];
   const unsigned w = max((unsigned)sI[si], (unsigned)sI[si + offs[16 + f]]);
   const uint32_t lo = min(dp, dq), hi = max(dp, dq);
+  if constexpr (R::PACK) {
+    fold_key<R::HB>(pk, ((unsigned long long)lo << 36) | ((unsigned long long)hi << 8) | w, eo);
+    return;
+  }
+  uint32_t h = pair_hash<R::HB>(lo, hi);
   const unsigned long long key = ((unsigned long long)lo << 28) | hi;
-  uint32_t h = ((lo * 0x9E3779B1u) ^ (hi * 0x85EBCA77u)) >> (32 - 10);
 #pragma unroll 1
   for (int probe = 0; probe < 64; ++probe) {
     unsigned long long cur = pk[h];
@@ -331,20 +387,20 @@ __device__ __forceinline__ void fold_rec(unsigned rec, const short* offs, const 
   emit_global(w, dp, dq, eo);  // congested tile
 }
 
+// a warp folds its staged list
 template <int CONN, class Px>
-__device__ __forceinline__ void fold_warp(const uint16_t* wst, int wcnt, const short* offs, const Px* sI,
+__device__ __forceinline__ void fold_warp(const uint16_t* wst, int wcnt, int4 wb, const short* offs, const Px* sI,
                                           const int* sD, unsigned long long* pk, unsigned* pw, const EdgeOut& eo) {
-  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN, Px>(wst[r], offs, sI, sD, pk, pw, eo);
+  for (int r = threadIdx.x & 31; r < wcnt; r += 32) fold_rec<CONN, Px>(wst[r], wb, offs, sI, sD, pk, pw, eo);
 }
 
 template <int CONN, bool BORDER, class Px>
 __device__ __forceinline__ int rag_pairs(const Px* sI, const int* sD, unsigned long long* pk, unsigned* pw,
-                                          uint16_t* stg, const short* offs, const Geo& g, const TileCoord& c,
+                                          uint16_t* wst, int4 wb, const short* offs, const Geo& g, const TileCoord& c,
                                           const EdgeOut& eo) {
   using R = RL<CONN, Px>;
   using T = TL<CONN>;
   constexpr int NF = R::NF;
-  uint16_t* wst = stg + (threadIdx.x >> 5) * R::WCAP;
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1;
   int wcnt = 0;
@@ -354,19 +410,20 @@ __device__ __forceinline__ int rag_pairs(const Px* sI, const int* sD, unsigned l
     my_voxel<CONN>(k, lx, ly, lz);
     const bool own = !BORDER || (c.bx + lx < g.n2 && c.by + ly < g.n1 && c.bz + lz < g.zhi);
     const unsigned vm = !own ? 0u : (BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1);
-    const int sl = R::iL(lz, ly, lx);
+    const int sl = wb.x + k * wb.y + lane;
     const int dp = sD[sl];
 #pragma unroll
     for (int f = 0; f < NF; ++f) {
       const int i = Conn<CONN>::nfwd + f;
       const bool e = ((vm >> i) & 1u) && sD[sl + R::oL(i)] != dp;
       const unsigned b = __ballot_sync(0xffffffffu, e);
-      if (e) wst[wcnt + __popc(b & lt)] = (uint16_t)((sl << 4) | f);
+      if (e) wst[wcnt + __popc(b & lt)] = (uint16_t)(f | (lane << 4) | (k << 9));
       wcnt += __popc(b);
     }
     if (R::MIDFOLD && wcnt > R::WCAP - NF * 32) {
+      if (eo.recs && lane == 0) atomicAdd(eo.recs, (unsigned long long)wcnt);
       __syncwarp();
-      fold_warp<CONN, Px>(wst, wcnt, offs, sI, sD, pk, pw, eo);
+      fold_warp<CONN, Px>(wst, wcnt, wb, offs, sI, sD, pk, pw, eo);
       __syncwarp();
       wcnt = 0;
     }
@@ -399,26 +456,27 @@ __device__ __forceinline__ void rag_load_plain(const int* __restrict__ D, const 
 // Persistent CTAs walk the tiles t = blockIdx.x, + gridDim.x, ...; with TMA the next tile's
 // boxes are requested as soon as the current ones are consumed, so the load overlaps the flush.
 template <int CONN, class Px>
-__global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mD,
-                                            int tma, const int* __restrict__ D, const Px* __restrict__ I, Geo g,
-                                            int ntx, int nty, int ntiles, EdgeOut eo) {
+__global__ void __launch_bounds__(NT, 5) k_rag(const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mD,
+                                               int tma, const int* __restrict__ D, const Px* __restrict__ I, Geo g,
+                                               int ntx, int nty, int ntiles, EdgeOut eo) {
   using R = RL<CONN, Px>;
   extern __shared__ __align__(128) unsigned char rag_smem[];
   Px* sI = reinterpret_cast<Px*>(rag_smem);                                       // R::SI pixels
   int* sD = reinterpret_cast<int*>(rag_smem + R::SIA);                            // R::SL dense ids
-  unsigned long long* pk = reinterpret_cast<unsigned long long*>(rag_smem + R::SIA + R::SLA);  // R::HP pair keys
-  unsigned* pw = reinterpret_cast<unsigned*>(pk + R::HP);                         // R::HP min pass heights
-  uint16_t* stg = reinterpret_cast<uint16_t*>(pw + R::HP);                        // R::STG staged records
+  unsigned long long* pk = reinterpret_cast<unsigned long long*>(rag_smem + R::SIA + R::SLA);  // R::HP slots
+  unsigned* pw = reinterpret_cast<unsigned*>(pk + R::HP);    // R::HP min pass heights (16-bit images only)
+  uint16_t* stg = reinterpret_cast<uint16_t*>(rag_smem + R::SIA + R::SLA + R::SLOT * R::HP);  // staged records
   __shared__ uint64_t bar;
   __shared__ unsigned long long gbase;
   __shared__ int sscan[32];
-  __shared__ int wc[NT / 32 + 1];
   __shared__ short offs[32];  // [f]: D-box offset, [16 + f]: I-box offset of forward direction f
   if (threadIdx.x < R::NF) {
     offs[threadIdx.x] = (short)R::oL(Conn<CONN>::nfwd + threadIdx.x);
     offs[16 + threadIdx.x] = (short)R::oI(Conn<CONN>::nfwd + threadIdx.x);
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 wb = warp_boxes<CONN, Px>();
+  uint16_t* wst = stg + warp * R::WCAP;
   if (tma && threadIdx.x == 0) {
     mbar_init(&bar, 1);
     if ((int)blockIdx.x < ntiles) {
@@ -434,7 +492,7 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
     const TileCoord c = tile_coord<CONN>(t, ntx, nty, g);
     for (int i = threadIdx.x; i < R::HP; i += NT) {
       pk[i] = KEY_NONE;
-      pw[i] = 0xffffffffu;
+      if constexpr (!R::PACK) pw[i] = 0xffffffffu;
     }
     if (tma) {
       __syncthreads();  // barrier init visible; hash reset done
@@ -445,27 +503,12 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
       __syncthreads();
     }
     // 1. detection into the per-warp lists
-    const int n = tile_interior<CONN>(c, g)
-                      ? rag_pairs<CONN, false, Px>(sI, sD, pk, pw, stg, offs, g, c, eo)
-                      : rag_pairs<CONN, true, Px>(sI, sD, pk, pw, stg, offs, g, c, eo);
-    if (lane == 0) wc[warp] = n;
-    __syncthreads();
-    // 2. dedup: the records of all warps spread evenly over the block
-    int pre[NT / 32 + 1];
-    pre[0] = 0;
-#pragma unroll
-    for (int w = 0; w < NT / 32; ++w) pre[w + 1] = pre[w] + wc[w];
-    const int total = pre[NT / 32];
-    for (int r = threadIdx.x; r < total; r += NT) {
-      int w = 0, base = 0;
-#pragma unroll
-      for (int u = 1; u < NT / 32; ++u)
-        if (r >= pre[u]) {
-          w = u;
-          base = pre[u];
-        }
-      fold_rec<CONN, Px>(stg[w * R::WCAP + (r - base)], offs, sI, sD, pk, pw, eo);
-    }
+    const int n = tile_interior<CONN>(c, g) ? rag_pairs<CONN, false, Px>(sI, sD, pk, pw, wst, wb, offs, g, c, eo)
+                                             : rag_pairs<CONN, true, Px>(sI, sD, pk, pw, wst, wb, offs, g, c, eo);
+    // 2. dedup: every warp folds its own list
+    __syncwarp();
+    fold_warp<CONN, Px>(wst, n, wb, offs, sI, sD, pk, pw, eo);
+    if (eo.recs && lane == 0) atomicAdd(eo.recs, (unsigned long long)n);
     __syncthreads();  // boxes consumed, hash complete
     const int tn = t + gridDim.x;
     if (tma && threadIdx.x == 0 && tn < ntiles) {
@@ -475,10 +518,11 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
       tma_load_3d(sD, &mD, cn.bx - R::LXO, cn.by - R::YO, cn.bz, &bar);
     }
     // 3. flush: block scan of the per-thread counts, one global atomic per tile
-    constexpr int M = R::HP / NT;  // thread t owns the consecutive slots M t .. M t + M - 1
+    constexpr int M = R::HP / NT;  // thread t owns the slots t, t + NT, ... (consecutive lanes,
+                                   // consecutive slots: no bank conflicts)
     int cnt = 0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) cnt += pk[threadIdx.x * M + m] != KEY_NONE;
+    for (int m = 0; m < M; ++m) cnt += pk[threadIdx.x + m * NT] != KEY_NONE;
     int tot;
     const int ex = block_excl_scan(cnt, sscan, tot);
     if (threadIdx.x == 0) gbase = tot ? atomicAdd(eo.ecount, (unsigned long long)tot) : 0;
@@ -486,14 +530,14 @@ __global__ void __launch_bounds__(NT) k_rag(const __grid_constant__ CUtensorMap 
     long long i = (long long)gbase + ex;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const unsigned long long key = pk[threadIdx.x * M + m];
+      const unsigned long long key = pk[threadIdx.x + m * NT];
       if (key == KEY_NONE) continue;
-      if constexpr (sizeof(Px) == 1) {
-        const uint64_t k = make_key(pw[threadIdx.x * M + m], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
+      if constexpr (R::PACK) {
+        const uint64_t k = make_key((uint32_t)(key & 0xff), (uint32_t)(key >> 36), (uint32_t)(key >> 8) & IDMASK);
         if (i < eo.cap) eo.edges[i] = k;
         fold_best(eo.best, k);
       } else {
-        if (i < eo.cap) eo.e16[i] = make_e16(pw[threadIdx.x * M + m], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
+        if (i < eo.cap) eo.e16[i] = make_e16(pw[threadIdx.x + m * NT], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
       }
       ++i;
     }
@@ -609,7 +653,7 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
   __shared__ int sscan[32];
   __shared__ unsigned long long gbase;
   if (nptr) n = (long long)*nptr;  // device-resident count of the previous level's live edges
-  constexpr int M = EHC / NTW;     // thread t owns the consecutive slots M t .. M t + M - 1
+  constexpr int M = EHC / NTW;     // thread t owns the slots t, t + NTW, ... (no bank conflicts)
   constexpr int J = ECH / NTW;
   if (threadIdx.x == 0 && (long long)blockIdx.x * ECH < n)
     atomicMax(chunks_max, (unsigned long long)((n - 1 - (long long)blockIdx.x * ECH) / ((long long)gridDim.x * ECH) + 1));
@@ -677,7 +721,7 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
     __syncthreads();
     int cnt = 0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) cnt += tp[threadIdx.x * M + m] != KEY_NONE;
+    for (int m = 0; m < M; ++m) cnt += tp[threadIdx.x + m * NTW] != KEY_NONE;
     int tot;
     const int ex = block_excl_scan(cnt, sscan, tot);
     if (threadIdx.x == 0) gbase = tot ? atomicAdd(nout, (unsigned long long)tot) : 0;
@@ -685,7 +729,7 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
     unsigned long long o = gbase + ex;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const int sl = threadIdx.x * M + m;
+      const int sl = threadIdx.x + m * NTW;
       const unsigned long long pk = tp[sl];
       if (pk == KEY_NONE) continue;
       Edge ed;
@@ -741,7 +785,7 @@ __global__ void k_levelmap(const int* __restrict__ comp, const uint8_t* __restri
 // stores (evict-first).
 template <int CONN, int STRIDE>
 __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ D, const int* __restrict__ levelmap, int NL,
-                                                 Geo g, int ntx, int nty, int* __restrict__ levels, int kfirst) {
+                                                 Geo g, int ntx, int nty, int* __restrict__ levels) {
   using T = TL<CONN>;
   const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
   const int lane = threadIdx.x & 31;
@@ -777,17 +821,17 @@ __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ D, const
     if (valid) {
 #pragma unroll
       for (int j = 0; j < STRIDE; ++j)
-        if (j >= kfirst && j < NL) __stcs(levels + (size_t)j * N + p, row[j]);
+        if (j < NL) __stcs(levels + (size_t)j * N + p, row[j]);
     }
   }
 }
 
 // scalar variant for large NL (stride not specialised)
 __global__ void k_levels_any(const int* __restrict__ D, const int* __restrict__ levelmap, int NL, int stride,
-                             long long N, int* __restrict__ levels, int kfirst) {
+                             long long N, int* __restrict__ levels) {
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
     const int* m = levelmap + (size_t)__ldg(D + p) * stride;
-    for (int k = kfirst; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k);
+    for (int k = 0; k < NL; ++k) levels[(size_t)k * N + p] = __ldg(m + k);
   }
 }
 
@@ -952,10 +996,10 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const G
   int64_t E = 0;
   for (int attempt = 0;; ++attempt) {
     WS_CUDA(cudaMemsetAsync(ecount, 0, sizeof(unsigned long long), st));
-    WS_CUDA(cudaMemsetAsync(pathc + 2, 0, sizeof(unsigned long long), st));
+    WS_CUDA(cudaMemsetAsync(pathc + 2, 0, 2 * sizeof(unsigned long long), st));
     WS_TRY(rag<Px>(conn, D, I, g,
                    EdgeOut{ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), pathc + 2,
-                           sizeof(Px) == 1 ? nullptr : ctx->edges.as<E16>()}, st));
+                           sizeof(Px) == 1 ? nullptr : ctx->edges.as<E16>(), pathc + 3}, st));
     launched(ctx, PH_WF_RAG);
     WS_TRY(read_i64(ctx, ecount, &E, st));
     if (E <= cap) break;
@@ -1038,6 +1082,7 @@ static ws_status wf_read_counts(ws_ctx* ctx, int k_last, int64_t* counts, cudaSt
   ctx->stats.lookback_max = (int32_t)h[2 * LVC];
   ctx->stats.edge_chunks_max = (int32_t)h[2 * LVC + 1];
   ctx->stats.rag_global_emits = (int64_t)h[2 * LVC + 2];
+  ctx->stats.rag_records = (int64_t)h[2 * LVC + 3];
   long long prev = w.R;
   for (int k = 1; k <= k_last && k < LVC; ++k) {
     const long long c = (long long)h[k];
@@ -1070,9 +1115,7 @@ static ws_status wf_step(ws_ctx* ctx, int64_t* count, int* more, cudaStream_t st
 }
 
 // level maps (replicated) + level arrays of the voxels of the dense-id image D (n0 planes of g)
-// kfirst = 1 (ws_segment): level 0 was written by the relabel pass
-static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn, int32_t* levels, cudaStream_t st,
-                           int kfirst = 0) {
+static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn, int32_t* levels, cudaStream_t st) {
   WSState& w = ctx->wf;
   const int NL = w.NL, stride = w.stride;
   ctx->stats.waterfall_levels = w.lv;
@@ -1090,12 +1133,12 @@ static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn
     const int TX = is3d ? TL<6>::TX : TL<4>::TX, TY = is3d ? TL<6>::TY : TL<4>::TY, TZ = is3d ? TL<6>::TZ : TL<4>::TZ;
     const int ntx = (g.n2 + TX - 1) / TX, nty = (g.n1 + TY - 1) / TY, ntz = (g.zhi - g.zlo + TZ - 1) / TZ;
     const int nt = ntx * nty * ntz;
-    if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels, kfirst);
-    else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels, kfirst);
-    else if (stride == 4) k_levels<4, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels, kfirst);
-    else k_levels<4, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels, kfirst);
+    if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else if (stride == 4) k_levels<4, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else k_levels<4, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
   } else {
-    k_levels_any<<<gN, NTW, 0, st>>>(D, levelmap, NL, stride, N, levels, kfirst);
+    k_levels_any<<<gN, NTW, 0, st>>>(D, levelmap, NL, stride, N, levels);
   }
   launched(ctx, PH_WF_MATERIALISE);
   tmark(ctx, st, PH_WF_MATERIALISE);
@@ -1154,22 +1197,15 @@ __global__ void __launch_bounds__(NTW) k_scan_counts(int* bc, int nb) {
 // ------------------------------------------------------ ws_segment (watershed + waterfall)
 // One procedure, as Alg. 5: the watershed stops before its relabel pass, the
 // dense ids come from the root list instead of a scan over the labels, and ONE relabel pass
-// writes both level 0 (the canonical labels) and the dense-id image D:
-//   k_root_bits   bit c of the representative bitmap for the canonical label c of every
-//                 listed root (C7; duplicates on the chase-first path set the same bit)
+// writes the dense-id image D; k_levels then writes all NL levels from the level-map rows:
+//   (watershed) k_root_canon / k_root_store set bit c of the representative bitmap for the
+//               canonical label c of every listed root (C7)
 //   k_rank_sum / k_scan_counts / k_rank_write   reduce-then-scan over the N/32 bitmap words:
-//                 rk[w] = (reps before voxel 32 w, bits of word w) -> dense(c) = rank of c
-//                 (dense ids keep the canonical label order, C14)
-//   k_root_dense  D[r] = dense id of root r, rep_of[dense] = its canonical label
-//   k_relabel_seg levels[0][p] = canonical label, D[p] = dense id of p's region
-// then the RAG, the level loop and k_levels (levels 1..NL-1) exactly as ws_waterfall.
-__global__ void k_root_bits(const int* __restrict__ P, const int* __restrict__ roots, int n, unsigned* bits) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int c = -1 - P[roots[i]];
-    atomicOr(bits + (c >> 5), 1u << (c & 31));
-  }
-}
-
+//               rk[w] = (reps before voxel 32 w, bits of word w) -> dense(c) = rank of c
+//               (dense ids keep the canonical label order, C14)
+//   k_relabel_seg D[p] = dense id of p's region (= rank of its canonical label in the
+//               bitmap); the representative voxels write rep_of[dense] = canonical label
+// then the RAG, the level loop and k_levels exactly as ws_waterfall.
 constexpr int RKW = 16;            // bitmap words per thread
 constexpr int RKB = NTW * RKW;     // words per block
 
@@ -1205,48 +1241,39 @@ __global__ void __launch_bounds__(NTW) k_rank_write(const unsigned* __restrict__
   }
 }
 
-__global__ void k_root_dense(const int* __restrict__ P, const int* __restrict__ roots, int n,
-                             const uint2* __restrict__ rk, int* __restrict__ D, int* __restrict__ rep_of) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int r = roots[i];
-    const int c = -1 - P[r];
-    const int d = rank_of(rk, c);
-    D[r] = d;
-    rep_of[d] = c;
-  }
-}
+// 4 consecutive voxels per thread.  P[p] = t >= 0 (a listed root) or -1 - canonical label (p
+// listed); d = rank of the canonical label c in the bitmap (one P and one rk gather per run
+// of equal roots; c lies a few planes behind p, so the rk window stays in L2).  The
+// representative voxel p == c also writes rep_of[d] = c.
+__device__ __forceinline__ int seg_canon(const int* __restrict__ P, int t) { return -1 - (t < 0 ? t : __ldg(P + t)); }
 
-// 4 consecutive voxels per thread.  A root r is written D[r] = its own (already stored) dense
-// id, so the gathers of D at roots never see another value.
-__device__ __forceinline__ void seg_one(const int* __restrict__ P, const int* D, int p, int t, int& lab, int& d) {
-  if (t < 0) {
-    lab = -1 - t;
-    d = D[p];
-  } else {
-    lab = -1 - __ldg(P + t);
-    d = D[t];
-  }
-}
-
-__global__ void __launch_bounds__(NTW) k_relabel_seg(const int* __restrict__ P, int* D, int N, int* __restrict__ L) {
+__global__ void __launch_bounds__(NTW) k_relabel_seg(const int* __restrict__ P, const uint2* __restrict__ rk, int N,
+                                                     int* __restrict__ D, int* __restrict__ rep_of) {
   const int n4 = N >> 2;
   const int4* P4 = reinterpret_cast<const int4*>(P);
   for (int i = blockIdx.x * NTW + threadIdx.x; i < n4; i += gridDim.x * NTW) {
-    const int4 t = __ldg(P4 + i);
+    const int4 t = __ldg(P4 + i);  // not evict-first: the root entries it gathers share these lines
     const int p = 4 * i;
-    int4 o, d;
-    seg_one(P, D, p, t.x, o.x, d.x);
-    if (t.y == t.x && t.x >= 0) { o.y = o.x; d.y = d.x; } else seg_one(P, D, p + 1, t.y, o.y, d.y);
-    if (t.z == t.y && t.y >= 0) { o.z = o.y; d.z = d.y; } else seg_one(P, D, p + 2, t.z, o.z, d.z);
-    if (t.w == t.z && t.z >= 0) { o.w = o.z; d.w = d.z; } else seg_one(P, D, p + 3, t.w, o.w, d.w);
-    __stcs(reinterpret_cast<int4*>(L) + i, o);
+    int4 c, d;
+    c.x = seg_canon(P, t.x);
+    c.y = (t.y == t.x && t.x >= 0) ? c.x : seg_canon(P, t.y);
+    c.z = (t.z == t.y && t.y >= 0) ? c.y : seg_canon(P, t.z);
+    c.w = (t.w == t.z && t.z >= 0) ? c.z : seg_canon(P, t.w);
+    d.x = rank_of(rk, c.x);
+    d.y = c.y == c.x ? d.x : rank_of(rk, c.y);
+    d.z = c.z == c.y ? d.y : rank_of(rk, c.z);
+    d.w = c.w == c.z ? d.z : rank_of(rk, c.w);
     reinterpret_cast<int4*>(D)[i] = d;
+    if (c.x == p) rep_of[d.x] = p;
+    if (c.y == p + 1) rep_of[d.y] = p + 1;
+    if (c.z == p + 2) rep_of[d.z] = p + 2;
+    if (c.w == p + 3) rep_of[d.w] = p + 3;
   }
   for (int p = 4 * n4 + blockIdx.x * NTW + threadIdx.x; p < N; p += gridDim.x * NTW) {
-    int lab, d;
-    seg_one(P, D, p, P[p], lab, d);
-    L[p] = lab;
+    const int c = seg_canon(P, P[p]);
+    const int d = rank_of(rk, c);
     D[p] = d;
+    if (c == p) rep_of[d] = p;
   }
 }
 
@@ -1260,28 +1287,24 @@ ws_status run_segment(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int
     set_error(WS_ERR_INVALID, "ws_segment: levels must be 16-byte aligned");
     return WS_ERR_INVALID;
   }
-  // steps I-IV: every voxel points at a listed root, listed roots hold -1 - canonical label
+  // steps I-IV: every voxel points at a listed root, listed roots hold -1 - canonical label,
+  // the representative bitmap is set
   WS_TRY(run_watershed(ctx, I, g, conn, levels, nullptr, st, false));
-  const int n_roots = ctx->seg_nroots;
   const int* P = ctx->aux.as<int>();
-  const int* roots = ctx->roots.as<int>();
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->pathc.ensure(4 * sizeof(unsigned long long), "path counters"));
   WS_CUDA(cudaMemsetAsync(ctx->pathc.p, 0, 4 * sizeof(unsigned long long), st));
   const int nw = g.N / 32 + 1;
   const int nb = (nw + RKB - 1) / RKB;
-  WS_TRY(ctx->repbits.ensure((size_t)nw * sizeof(unsigned), "representative bitmap"));
   WS_TRY(ctx->rank.ensure((size_t)nw * sizeof(uint2), "dense rank structure"));
   WS_TRY(ctx->blockcnt.ensure((size_t)(nb + 1) * sizeof(int), "rank block sums"));
-  unsigned* bits = ctx->repbits.as<unsigned>();
+  const unsigned* bits = ctx->repbits.as<unsigned>();
   int* bsum = ctx->blockcnt.as<int>();
   uint2* rk = ctx->rank.as<uint2>();
-  WS_CUDA(cudaMemsetAsync(bits, 0, (size_t)nw * sizeof(unsigned), st));
-  k_root_bits<<<grid_for(n_roots, ctx->num_sms), 256, 0, st>>>(P, roots, n_roots, bits);
   k_rank_sum<<<nb, NTW, 0, st>>>(bits, nw, bsum);
   k_scan_counts<<<1, NTW, 0, st>>>(bsum, nb);
   k_rank_write<<<nb, NTW, 0, st>>>(bits, nw, bsum, rk);
-  launched(ctx, PH_WF_DENSE, 4);
+  launched(ctx, PH_WF_DENSE, 3);
   WS_CUDA(cudaMemcpyAsync(ctx->pinned, bsum + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaStreamSynchronize(st));
   const int64_t R = reinterpret_cast<const int*>(ctx->pinned)[0];
@@ -1290,10 +1313,8 @@ ws_status run_segment(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int
   WS_TRY(ctx->rep_of.ensure((size_t)R * sizeof(int), "rep_of"));
   WS_TRY(ctx->dimg.ensure((size_t)g.N * sizeof(int), "dense-id image"));
   int* D = ctx->dimg.as<int>();
-  k_root_dense<<<grid_for(n_roots, ctx->num_sms), 256, 0, st>>>(P, roots, n_roots, rk, D, ctx->rep_of.as<int>());
-  launched(ctx, PH_WF_DENSE);
   tmark(ctx, st, PH_WF_DENSE);
-  k_relabel_seg<<<grid_for(g.N / 4 + 1, ctx->num_sms), NTW, 0, st>>>(P, D, g.N, levels);
+  k_relabel_seg<<<grid_for(g.N / 4 + 1, ctx->num_sms), NTW, 0, st>>>(P, rk, g.N, D, ctx->rep_of.as<int>());
   launched(ctx, PH_WS_RELABEL);
   tmark(ctx, st, PH_WS_RELABEL);
   WS_TRY(wf_rag<uint8_t>(ctx, nullptr, I, g, conn, nullptr, st));
@@ -1301,7 +1322,7 @@ ws_status run_segment(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int
   ctx->stats.level_counts[0] = R;
   ctx->stats.level_edges[1] = ctx->wf.E;
   for (int k = 1; k < NL; ++k) WS_TRY(wf_level(ctx, k + 1 < NL, st));
-  WS_TRY(wf_finish(ctx, D, g, conn, levels, st, 1));
+  WS_TRY(wf_finish(ctx, D, g, conn, levels, st));
   if (NL > 1) WS_TRY(wf_read_counts(ctx, NL - 1, counts, st));
   ctx->stats.waterfall_levels = ctx->wf.lv;
   return WS_OK;

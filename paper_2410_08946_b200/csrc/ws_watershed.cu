@@ -833,18 +833,27 @@ __global__ void k_root_label(int* P, const int* __restrict__ L, const int* __res
 
 // fast path (unions before the chase): every listed root is final and L[r] already holds
 // INT_MAX - (smallest voxel index of its region); P[r] = -1 - canonical label
+// bits != nullptr (ws_segment): also set bit c of the representative bitmap for the canonical
+// label c of every listed root (several listed roots of one region set the same bit)
 __global__ void k_root_canon(int* P, const int* __restrict__ L, const int* __restrict__ roots, const int* nptr,
-                             int cap) {
+                             int cap, unsigned* __restrict__ bits) {
   const int n = min(*nptr, cap);
   for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
     const int r = roots[i];
-    P[r] = -1 - (INT_MAX - L[r]);
+    const int c = INT_MAX - L[r];
+    P[r] = -1 - c;
+    if (bits) atomicOr(bits + (c >> 5), 1u << (c & 31));
   }
 }
 
 // P[root] = -1 - canonical label (no finds run any more)
-__global__ void k_root_store(int* P, const int* __restrict__ roots, const int* __restrict__ rootc, int n) {
-  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) P[roots[i]] = -1 - rootc[i];
+__global__ void k_root_store(int* P, const int* __restrict__ roots, const int* __restrict__ rootc, int n,
+                             unsigned* __restrict__ bits) {
+  for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
+    const int c = rootc[i];
+    P[roots[i]] = -1 - c;
+    if (bits) atomicOr(bits + (c >> 5), 1u << (c & 31));
+  }
 }
 
 // labels[p] = canonical label of p's step III root
@@ -961,9 +970,10 @@ static ws_status pair_out(ws_ctx* ctx, const Geo& g, PairOut& po, cudaStream_t s
 }
 
 // relabel == false (ws_segment): stop before the relabel pass; P = ctx->aux then holds, for
-// every voxel, a listed root (or, at a listed root r, P[r] = -1 - canonical label), and the
+// every voxel, a listed root (or, at a listed root r, P[r] = -1 - canonical label), the
 // listed roots are ctx->roots[0 .. ctx->seg_nroots) (a superset of the final roots on the
-// chase-first path; every listed root maps to its region's canonical label).
+// chase-first path; every listed root maps to its region's canonical label), and
+// ctx->repbits (N/32 + 1 words) has bit c set for every canonical label c.
 template <int CONN>
 static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* L, int64_t* num_regions,
                              cudaStream_t st, bool relabel = true) {
@@ -992,6 +1002,13 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   }
   int* nr = ctx->flags.as<int>() + 8;
   unsigned long long* nfinal = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 64);
+  unsigned* bits = nullptr;
+  if (!relabel) {
+    const size_t nw = (size_t)g.N / 32 + 1;
+    WS_TRY(ctx->repbits.ensure(nw * sizeof(unsigned), "representative bitmap"));
+    bits = ctx->repbits.as<unsigned>();
+    WS_CUDA(cudaMemsetAsync(bits, 0, nw * sizeof(unsigned), st));
+  }
   WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(nfinal, 0, sizeof(unsigned long long), st));
   WS_CUDA(cudaMemcpyAsync(ctx->pinned, po.npairs, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1013,7 +1030,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
     k_jump<<<gN, NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
     launched(ctx, PH_WS_JUMP);
     tmark(ctx, st, PH_WS_JUMP);
-    k_root_canon<<<grid1d((long long)g.N / 32, ctx->num_sms), NT, 0, st>>>(P, L, roots, nr, (int)cap);
+    k_root_canon<<<grid1d((long long)g.N / 32, ctx->num_sms), NT, 0, st>>>(P, L, roots, nr, (int)cap, bits);
     launched(ctx, PH_WS_FIND);
     tmark(ctx, st, PH_WS_FIND);
     if (!relabel) {
@@ -1088,7 +1105,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   const int gR = grid1d(n_roots, ctx->num_sms);
   k_root_merge<<<gR, NT, 0, st>>>(P, L, roots, n_roots, nfinal);
   k_root_label<<<gR, NT, 0, st>>>(P, L, roots, n_roots, ctx->rootc.as<int>());
-  k_root_store<<<gR, NT, 0, st>>>(P, roots, ctx->rootc.as<int>(), n_roots);
+  k_root_store<<<gR, NT, 0, st>>>(P, roots, ctx->rootc.as<int>(), n_roots, bits);
   launched(ctx, PH_WS_FIND, 3);
   tmark(ctx, st, PH_WS_FIND);
   if (!relabel) {
