@@ -6,6 +6,8 @@
 
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "ws_internal.h"
 
 namespace ws {
@@ -211,6 +213,11 @@ ws_status ws_ctx_create(int32_t device, ws_ctx** out) {
   }
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&c->coop, cudaDevAttrCooperativeLaunch, device);
+  {
+    const char* nc = getenv("WS_NO_COOP");
+    if (nc && nc[0] == '1') c->coop = 0;
+  }
   e = cudaMallocHost(&c->pinned, 256 * sizeof(int64_t));
   if (e != cudaSuccess) {
     delete c;

@@ -57,6 +57,30 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int ntx, int nty, const G
   return c;
 }
 
+// Tile of this CTA.  Kernels with one CTA per tile are launched on a 3-D grid (ntx, nty, ntz)
+// (tile_grid below), so the coordinates come from blockIdx without integer division; a
+// volume with more than 65535 tile rows or layers falls back to a 1-D grid (gridDim.x != ntx).
+// t = the linear tile index (z-major), as tile_coord's.
+template <int CONN>
+__device__ __forceinline__ TileCoord tile_of_block(int ntx, int nty, const Geo& g, int& t) {
+  using T = TL<CONN>;
+  if (gridDim.x == (unsigned)ntx) {
+    t = ((int)blockIdx.z * nty + (int)blockIdx.y) * ntx + (int)blockIdx.x;
+    TileCoord c;
+    c.bx = (int)blockIdx.x * T::TX;
+    c.by = (int)blockIdx.y * T::TY;
+    c.bz = g.zlo + (int)blockIdx.z * T::TZ;
+    return c;
+  }
+  t = (int)blockIdx.x;
+  return tile_coord<CONN>(t, ntx, nty, g);
+}
+
+static inline dim3 tile_grid(int ntx, int nty, int ntz) {
+  if (nty <= 65535 && ntz <= 65535) return dim3((unsigned)ntx, (unsigned)nty, (unsigned)ntz);
+  return dim3((unsigned)((long long)ntx * nty * ntz));
+}
+
 // the tile and its 2-voxel halo lie inside the volume: no neighbour checks needed
 template <int CONN>
 __device__ __forceinline__ bool tile_interior(const TileCoord& c, const Geo& g) {

@@ -787,7 +787,8 @@ template <int CONN, int STRIDE>
 __global__ void __launch_bounds__(NTW) k_levels(const int* __restrict__ D, const int* __restrict__ levelmap, int NL,
                                                  Geo g, int ntx, int nty, int* __restrict__ levels) {
   using T = TL<CONN>;
-  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
+  int t;
+  const TileCoord c = tile_of_block<CONN>(ntx, nty, g, t);
   const int lane = threadIdx.x & 31;
   const size_t N = (size_t)g.N;
   int prev_d = -1;
@@ -1132,11 +1133,10 @@ static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn
     const bool is3d = (conn == 6 || conn == 26);
     const int TX = is3d ? TL<6>::TX : TL<4>::TX, TY = is3d ? TL<6>::TY : TL<4>::TY, TZ = is3d ? TL<6>::TZ : TL<4>::TZ;
     const int ntx = (g.n2 + TX - 1) / TX, nty = (g.n1 + TY - 1) / TY, ntz = (g.zhi - g.zlo + TZ - 1) / TZ;
-    const int nt = ntx * nty * ntz;
-    if (is3d && stride == 4) k_levels<6, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
-    else if (is3d) k_levels<6, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
-    else if (stride == 4) k_levels<4, 4><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
-    else k_levels<4, 8><<<nt, NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    if (is3d && stride == 4) k_levels<6, 4><<<tile_grid(ntx, nty, ntz), NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else if (is3d) k_levels<6, 8><<<tile_grid(ntx, nty, ntz), NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else if (stride == 4) k_levels<4, 4><<<tile_grid(ntx, nty, ntz), NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
+    else k_levels<4, 8><<<tile_grid(ntx, nty, ntz), NTW, 0, st>>>(D, levelmap, NL, g, ntx, nty, levels);
   } else {
     k_levels_any<<<gN, NTW, 0, st>>>(D, levelmap, NL, stride, N, levels);
   }

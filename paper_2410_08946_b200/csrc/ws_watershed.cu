@@ -29,6 +29,8 @@
 #include <cstring>
 
 #include "ws_internal.h"
+#include <cooperative_groups.h>
+
 #include "ws_tile.cuh"
 
 namespace ws {
@@ -60,7 +62,7 @@ __device__ __forceinline__ bool on_tile_border(int lx, int ly, int lz) {
 // loaded at kernel start; distances only decrease, so a stale value never hides a gain).
 template <int CONN>
 __device__ __forceinline__ bool mark_gains(const int* sD, int s, int d, unsigned m, int lx, int ly, int lz, int t,
-                                           int ntx, int nty, uint8_t* next, const Geo& g) {
+                                           int ntx, int nty, uint8_t* next, const Geo& g, const TileCoord& c) {
   using T = TL<CONN>;
   bool any = false;
 #pragma unroll
@@ -72,8 +74,10 @@ __device__ __forceinline__ bool mark_gains(const int* sD, int s, int d, unsigned
     const int oy = (ly + dy < 0) ? -1 : (ly + dy >= T::TY ? 1 : 0);
     const int oz = (lz + dz < 0) ? -1 : (lz + dz >= T::TZ ? 1 : 0);
     if ((ox | oy | oz) == 0) continue;
-    const int tz = t / (ntx * nty) + oz;  // no tile beyond the owned planes (slab halo)
-    if (tz < 0 || tz * T::TZ >= g.zhi - g.zlo) continue;
+    if (oz != 0) {  // no tile beyond the owned planes (slab halo)
+      const int zz = c.bz - g.zlo + oz * T::TZ;
+      if (zz < 0 || zz >= g.zhi - g.zlo) continue;
+    }
     if (sD[s + T::oL(i)] > d + 1) {
       next[t + (oz * nty + oy) * ntx + ox] = 1;
       any = true;
@@ -227,7 +231,7 @@ __device__ __forceinline__ bool write_back(const int* sD, int s0, const unsigned
 #pragma unroll
       for (int kk = 0; kk < TL<CONN>::VPT; ++kk)
         if (kk == k) m = eqm[kk];
-      marked |= mark_gains<CONN>(sD, s, d, m, lx, ly, lz, t, ntx, nty, next, g);
+      marked |= mark_gains<CONN>(sD, s, d, m, lx, ly, lz, t, ntx, nty, next, g, c);
     }
   }
   return marked;
@@ -364,8 +368,8 @@ __global__ void __launch_bounds__(NT) k_relax_first(const __grid_constant__ CUte
   __shared__ alignas(16) int sD[T::SL];
   __shared__ uint64_t bar;
   __shared__ RQ q;
-  const int t = blockIdx.x;
-  const TileCoord c = tile_coord<CONN>(t, ntx, nty, g);
+  int t;
+  const TileCoord c = tile_of_block<CONN>(ntx, nty, g, t);
   rq_zero(q);
   stage<CONN>(&mI, nullptr, tma, I, nullptr, g, c, sI, nullptr, &bar);
   if (tile_interior<CONN>(c, g))
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(NT) k_relax_first(const __grid_constant__ CUte
 template <int CONN, bool BORDER>
 __device__ __forceinline__ void relax_round_body(const Px* sI, int* sD, int* __restrict__ L, const Geo& g,
                                                  const TileCoord& c, int t, int ntx, int nty, uint8_t* next,
-                                                 int* flags, RQ& q) {
+                                                 int* changed_flag, int* limit_flag, RQ& q) {
   using T = TL<CONN>;
   const int s0 = Mine<CONN>::s0();
   unsigned eqm[T::VPT];
@@ -398,9 +402,9 @@ __device__ __forceinline__ void relax_round_body(const Px* sI, int* sD, int* __r
     }
     eqm[k] = m;
   }
-  const unsigned changed = relax_tile_q<CONN, true>(sD, s0, eqm, flags + 1, q);
+  const unsigned changed = relax_tile_q<CONN, true>(sD, s0, eqm, limit_flag, q);
   const bool marked = write_back<CONN>(sD, s0, eqm, changed, L, g, c, t, ntx, nty, next);
-  if (__any_sync(0xffffffffu, marked) && (threadIdx.x & 31) == 0) flags[0] = 1;  // idempotent, no barrier
+  if (__any_sync(0xffffffffu, marked) && (threadIdx.x & 31) == 0) *changed_flag = 1;  // idempotent, no barrier
 }
 
 template <int CONN>
@@ -421,9 +425,92 @@ __global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUte
   stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);
   decode_box<CONN>(sD);
   if (tile_interior<CONN>(c, g))
-    relax_round_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, flags, q);
+    relax_round_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, flags, flags + 1, q);
   else
-    relax_round_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, flags, q);
+    relax_round_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, flags, flags + 1, q);
+}
+
+// All further step II rounds in ONE cooperative launch (no host round trip per round, P:363
+// names the per-iteration host loop as the cost).  A grid of co-resident CTAs walks the
+// round's active tile list (the k_relax_round body per tile, boxes staged with TMA on one
+// mbarrier whose phase flips per tile); grid barrier; the tiles marked for the next round
+// (and holding plateau voxels) are compacted into the other list while next[] is cleared;
+// grid barrier; every CTA reads the same counts and stops together when no tile changed a
+// neighbour or none is active.  Loop state ls (device ints): ls[r & 1] = "a tile marked a
+// neighbour in round r", ls[2 + (r & 1)] = length of round r's list, ls[4] = rounds run (0 if
+// flags[0] says the previous round changed nothing).  A
+// round's slots are reset in the compaction phase of the round before it uses them, when no
+// CTA reads or writes them.
+template <int CONN>
+__global__ void __launch_bounds__(NT, 8) k_relax_loop(const __grid_constant__ CUtensorMap mI,
+                                                    const __grid_constant__ CUtensorMap mL, int tma,
+                                                    const Px* __restrict__ I, int* __restrict__ L, Geo g, int ntx,
+                                                    int nty, int ntiles, uint8_t* next, const uint8_t* hasplat,
+                                                    int* flags, int* ls, int* list0, int* list1, int max_rounds) {
+  using T = TL<CONN>;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ alignas(128) Px sI[T::SI];
+  __shared__ alignas(128) int sD[T::SL];
+  __shared__ uint64_t bar;
+  __shared__ RQ q;
+  volatile int* vls = ls;
+  if (!flags[0] || vls[2] == 0) return;  // the previous round changed no neighbour / no active tile
+  if (tma && threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  int r = 0;
+  for (;; ++r) {
+    const int nact = vls[2 + (r & 1)];
+    const int* cl = (r & 1) ? list1 : list0;
+    int* nl = (r & 1) ? list0 : list1;
+    for (int i = blockIdx.x; i < nact; i += gridDim.x) {
+      const int t = cl[i];
+      const TileCoord c = tile_coord<CONN>(t, ntx, nty, g);
+      rq_zero(q);
+      if (tma) {
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(&bar, T::SI * (int)sizeof(Px) + T::SL * 4);
+          tma_load_3d(sI, &mI, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, &bar);
+          tma_load_3d(sD, &mL, c.bx - T::LXO, c.by - T::LYO, c.bz - T::LZO, &bar);
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+      } else {
+        stage<CONN>(&mI, &mL, false, I, L, g, c, sI, sD, &bar);
+      }
+      decode_box<CONN>(sD);
+      if (tile_interior<CONN>(c, g))
+        relax_round_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, ls + (r & 1), flags + 1, q);
+      else
+        relax_round_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, ls + (r & 1), flags + 1, q);
+      __syncthreads();  // the boxes and q are reused by the next tile
+    }
+    grid.sync();
+    // compaction of round r + 1's list; reset the slots round r + 1 uses
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ls[(r + 1) & 1] = 0;
+      ls[2 + (r & 1)] = 0;
+    }
+    const int lane = threadIdx.x & 31;
+    for (int t0 = blockIdx.x * NT; t0 < ntiles; t0 += gridDim.x * NT) {
+      const int t = t0 + threadIdx.x;
+      bool a = false;
+      if (t < ntiles && next[t]) {
+        next[t] = 0;
+        a = hasplat[t] != 0;
+      }
+      const unsigned b = __ballot_sync(0xffffffffu, a);
+      if (!b) continue;
+      int base = 0;
+      if (lane == 0) base = atomicAdd(ls + 2 + ((r + 1) & 1), __popc(b));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (a) nl[base + __popc(b & ((1u << lane) - 1))] = t;
+    }
+    grid.sync();
+    if (!vls[r & 1] || vls[2 + ((r + 1) & 1)] == 0 || r + 1 > max_rounds || flags[1]) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ls[4] = r + 1;  // rounds this launch ran
 }
 
 // compact list of the tiles of the next round: marked by a neighbour and holding plateau voxels
@@ -660,7 +747,8 @@ __global__ void __launch_bounds__(NT) k_resolve(const __grid_constant__ CUtensor
   __shared__ int2 sQ[QCAP];   // cross-tile step IV pairs
   __shared__ int sQn, sQb;
   __shared__ uint64_t bar;
-  const TileCoord c = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
+  int t;
+  const TileCoord c = tile_of_block<CONN>(ntx, nty, g, t);
   if (threadIdx.x == 0) sQn = 0;
   stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);  // raw step II codes (no decoding)
   if (tile_interior<CONN>(c, g))
@@ -922,11 +1010,24 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   const int gl = std::max(1, std::min((tg.n + NT - 1) / NT, ctx->num_sms * 8));
   WS_CUDA(cudaMemsetAsync(flags, 0, 5 * sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(next, 0, 2 * (size_t)tg.n, st));  // next and hasplat
-  k_relax_first<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, next, hasplat, flags);
+  k_relax_first<CONN><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, next, hasplat, flags);
   k_tile_list<<<gl, NT, 0, st>>>(next, hasplat, tg.n, list, flags + 4);
   launched(ctx, PH_WS_INIT, 2);
   tmark(ctx, st, PH_WS_INIT);
   int rounds = 1;
+  // Rounds with many active tiles run as k_relax_round launches (one CTA per listed tile);
+  // once the list fits one wave of co-resident CTAs, all remaining rounds run in ONE
+  // cooperative k_relax_loop launch (no host round trip per round).  A persistent grid
+  // walking a long list measured slower than the per-round launches (C4 first round).
+  int occ = 0;
+  const bool coop = ctx->coop &&
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relax_loop<CONN>, NT, 0) == cudaSuccess &&
+                    occ > 0;
+  const int wave = occ * ctx->num_sms;
+  if (coop) {
+    WS_TRY(ctx->tlist.ensure((size_t)tg.n * 2 * sizeof(int), "active tile lists"));
+    list = ctx->tlist.as<int>();
+  }
   while (true) {
     WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 5 * sizeof(int), cudaMemcpyDeviceToHost, st));
     WS_CUDA(cudaStreamSynchronize(st));
@@ -940,6 +1041,36 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
     if (rounds > g.N + 2) {
       set_error(WS_ERR_INTERNAL, "step II did not converge");
       return WS_ERR_INTERNAL;
+    }
+    if (coop && nact <= wave) {
+      int* list1 = list + tg.n;
+      int* ls = flags + 20;
+      // ls[2] = the list k_tile_list just built (its count is flags[4]); ls[0], ls[3] = 0
+      WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
+      WS_CUDA(cudaMemsetAsync(ls, 0, 5 * sizeof(int), st));
+      WS_CUDA(cudaMemcpyAsync(ls + 2, flags + 4, sizeof(int), cudaMemcpyDeviceToDevice, st));
+      const int grid = std::max(1, std::min(nact, wave));
+      CUtensorMap mI = mp.mI, mL = mp.mL;
+      int tma = mp.tma, ntx = tg.ntx, nty = tg.nty, ntiles = tg.n, maxr = g.N + 2 - rounds;
+      Geo gg = g;
+      int32_t* LL = L;
+      const Px* II = grad;
+      void* args[] = {&mI, &mL, &tma, &II, &LL, &gg, &ntx, &nty, &ntiles, &next, &hasplat, &flags, &ls, &list, &list1,
+                      &maxr};
+      WS_CUDA(cudaLaunchCooperativeKernel((const void*)k_relax_loop<CONN>, dim3(grid), dim3(NT), args, 0, st));
+      launched(ctx, PH_WS_RELAX);
+      WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 25 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      WS_CUDA(cudaStreamSynchronize(st));
+      if (h[1]) {
+        set_error(WS_ERR_LIMIT, "a non-minimal plateau is deeper than 2^26-2 voxels");
+        return WS_ERR_LIMIT;
+      }
+      rounds += h[24];
+      if (rounds > g.N + 2) {
+        set_error(WS_ERR_INTERNAL, "step II did not converge");
+        return WS_ERR_INTERNAL;
+      }
+      break;
     }
     std::swap(cur, next);
     WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
@@ -986,7 +1117,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   int* P = ctx->aux.as<int>();
   PairOut po;
   WS_TRY(pair_out(ctx, g, po, st));
-  k_resolve<CONN, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr, po);
+  k_resolve<CONN, false><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr, po);
   launched(ctx, PH_WS_SELECT);
   tmark(ctx, st, PH_WS_SELECT);
 
@@ -1149,7 +1280,7 @@ static ws_status shard_first_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   WS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(a, 0, tg.n, st));
   WS_CUDA(cudaMemsetAsync(hasplat, 0, tg.n, st));
-  k_relax_first<CONN><<<tg.n, NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, a, hasplat, flags);
+  k_relax_first<CONN><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, a, hasplat, flags);
   launched(ctx, PH_WS_INIT);
   ctx->shard_tiles = tg.n;
   ctx->shard_flip = 0;  // "next" = buffer 0
@@ -1222,7 +1353,7 @@ static ws_status resolve_shard_t(ws_ctx* ctx, const Px* grad, const Geo& g, cons
   make_maps<CONN>(grad, L, g, mp);
   PairOut po;
   WS_TRY(pair_out(ctx, g, po, st));
-  k_resolve<CONN, false><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr, po);
+  k_resolve<CONN, false><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, P, nullptr, po);
   launched(ctx, PH_WS_SELECT);
   tmark(ctx, st, PH_WS_SELECT);
   WS_CUDA(cudaGetLastError());
@@ -1261,7 +1392,7 @@ static ws_status debug_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* dis
   Maps mp;
   make_maps<CONN>(grad, L, g, mp);
   WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, mp, st));
-  k_resolve<CONN, true><<<tg.n, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, parent, dist,
+  k_resolve<CONN, true><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, parent, dist,
                                              PairOut{nullptr, nullptr, 0});
   launched(ctx, PH_WS_SELECT);
   WS_CUDA(cudaGetLastError());
