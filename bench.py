@@ -330,10 +330,20 @@ def run_sharded(args, world, rank, cfg, shape):
     grad_ext = gfull[s.e0 - r0:s.e1 - r0].contiguous()
     del gfull, raw_ext
     torch.cuda.empty_cache()
-    tr = shard.DistTransport()
+    # the whole sharded pipeline is ONE library call per rank (ws_segment_sharded); planes move
+    # through the library's own NCCL communicator (gloo callbacks when ranks share a GPU)
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        tr = shard.NcclLibTransport(dev.index)
+        transport = "ws_transport_nccl (library-owned NCCL communicator)"
+    else:
+        tr = shard._CallbackTransport(shard.TorchCallbacks(), rank, world)
+        transport = "torch.distributed gloo callbacks (ranks sharing a GPU: functional only)"
+    levels_own = torch.empty((NL, s.z1 - s.z0) + tuple(shape[1:]), dtype=torch.int32, device=dev)
 
     def step():
-        return shard.sharded_segment(tr, [ctx], [s], [grad_ext], NL, conn)
+        lv, cts, rnd = shard.segment_sharded(tr, ctx, s, grad_ext, NL, conn, out=levels_own)
+        return lv[0], lv, cts, cts[0], rnd
 
     for _ in range(args.warmup):
         out = step()
@@ -370,8 +380,8 @@ def run_sharded(args, world, rank, cfg, shape):
 
         def e2e_step():
             gdev.copy_(gh, non_blocking=True)
-            o = shard.sharded_segment(tr, [ctx], [s], [gdev], NL, conn)
-            lh.copy_(o[1][0], non_blocking=True)
+            lv, _, _ = shard.segment_sharded(tr, ctx, s, gdev, NL, conn, out=levels_own)
+            lh.copy_(lv, non_blocking=True)
 
         e2e_step()
         barrier(world)
@@ -384,7 +394,8 @@ def run_sharded(args, world, rank, cfg, shape):
         barrier(world)
         ems = max_over_ranks(a.elapsed_time(b) / args.e2e_steps, world)
         e2e = {"value": N / (ems / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": grad_ext.numel() * world,
-               "d2h_bytes_per_step": NL * N * 4, "ms_per_step": ems, "api": "shard.sharded_segment (host buffers)"}
+               "d2h_bytes_per_step": NL * N * 4, "ms_per_step": ems,
+               "api": "ws_segment_sharded per rank, host buffers copied in/out inside the timed region"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -392,7 +403,7 @@ def run_sharded(args, world, rank, cfg, shape):
             "vs_baseline": None, "dtype": "u8/i32", "data": "synthetic",
             "config": {"workload": cfg.desc, "name": cfg.name, "shape": list(shape), "conn": conn, "NL": NL,
                        "sigma": cfg.sigma, "global_voxels": N, "parallelism": "z-slab x%d (NCCL halo + boundary "
-                       "union-find + per-level all_reduce)" % world,
+                       "union-find + per-level all_reduce)" % world, "transport": transport,
                        "l2": "inputs larger than L2 (slab grad %.0f MB, levels %.0f MB per GPU)" % (
                            grad_ext.numel() / 1e6, 4 * NL * own / 1e6)},
             "roofline": roofline, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
@@ -762,8 +773,23 @@ def run_ours(args):
     return 0
 
 
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: run the same command as N ranks,
+    one process per GPU (the contract's launch), and pass rank 0's line through."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        return relaunch_under_torchrun(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

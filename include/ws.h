@@ -44,7 +44,7 @@ typedef enum ws_status {
   WS_ERR_INVALID = 1,  /* bad dims / connectivity / NL / sigma / NULL pointer          */
   WS_ERR_OOM = 2,      /* workspace allocation failed                                   */
   WS_ERR_CUDA = 3,     /* a CUDA runtime error (message has the CUDA error string)      */
-  WS_ERR_NCCL = 4,     /* reserved for the sharded path                                 */
+  WS_ERR_NCCL = 4,     /* a transport (NCCL or caller callback) of the sharded path failed */
   WS_ERR_INTERNAL = 5, /* an internal consistency check failed                          */
   WS_ERR_LIMIT = 6     /* a documented size limit was exceeded (message says which)     */
 } ws_status;
@@ -313,6 +313,69 @@ ws_status ws_shard_wf_step(ws_ctx* ctx, const int64_t* best_in, int64_t* best_ou
 /* level maps + the NL level arrays of the owned voxels: levels_own i32[NL][(z1-z0)*n1*n2] */
 ws_status ws_shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const int32_t* dense_of, const int32_t* rep_of,
                           ws_dims dims_ext, int32_t connectivity, ws_slab slab, int32_t* levels_own, void* stream);
+
+/* ==================================================================================
+ * The sharded pipeline as ONE call per rank ("ctx created with
+ * ws_ctx_create_sharded(...); the same three calls then operate on the local slab").  The
+ * whole distributed control flow of DESIGN.md §9 runs inside the library on top of the
+ * ws_shard_* phases above: step II rounds with a halo-plane exchange after each until no rank
+ * has work (an all-reduce of the pending flags), the all-gather of the boundary tables and
+ * the replicated merge, rank-ordered dense ids (all-gather of the representative counts,
+ * all-reduce(max) of rep_of, all-gather of the boundary dense tables), the cut-plane label
+ * exchange, and per waterfall level an all-reduce(min) of the per-component minima.
+ * Rank r of K owns the planes [z0, z1) of slab (the ranks' slabs tile [0, D) in rank order);
+ * grad_ext is the u8 EXTENDED slab [e0, e1) (dims_ext.n0 = e1 - e0, the planes z0-1 and z1
+ * must be present when they exist: e0 <= z0-1, e1 >= z1+1); results are the owned planes
+ * with GLOBAL canonical labels, identical to the unsharded call (determinism).
+ *
+ * Collectives go through a ws_transport: three callbacks, each enqueued on / ordered with
+ * `stream` (device buffers; the callback returns 0 on success, anything else fails the call
+ * with WS_ERR_NCCL).  The library provides an NCCL transport (ws_transport_nccl_create:
+ * NCCL over NVLink / NVSwitch, the communicator owned by the library, libnccl.so.2 resolved at
+ * run time); callers may supply their own (e.g. torch.distributed / gloo for multi-process
+ * tests with several ranks on one GPU, threads for virtual ranks in one process).
+ * ================================================================================== */
+#define WS_NCCL_ID_BYTES 128
+typedef struct ws_transport {
+  void* user;        /* passed back to every callback                                      */
+  int32_t rank;      /* this rank                                                          */
+  int32_t nranks;    /* K                                                                  */
+  /* send_lo (this rank's first owned plane) to rank-1 and send_hi (last) to rank+1; receive
+   * rank-1's last plane into recv_below and rank+1's first into recv_above; `bytes` each;
+   * NULL where the neighbour does not exist */
+  int32_t (*exchange)(void* user, const void* send_lo, const void* send_hi, void* recv_below, void* recv_above,
+                      int64_t bytes, void* stream);
+  /* recv = the K ranks' `bytes`-byte send blocks in rank order */
+  int32_t (*allgather)(void* user, const void* send, void* recv, int64_t bytes, void* stream);
+  /* in place over `count` elements; dtype 0 = i32, 1 = i64; op 0 = min, 1 = max */
+  int32_t (*allreduce)(void* user, void* buf, int64_t count, int32_t dtype, int32_t op, void* stream);
+} ws_transport;
+
+/* NCCL transport: rank 0 makes the unique id (WS_NCCL_ID_BYTES bytes, HOST), the caller
+ * broadcasts it to the other ranks (e.g. over the torch.distributed store), every rank then
+ * creates its transport (collective: all ranks must call).  Errors: WS_ERR_NCCL (libnccl
+ * missing, NCCL failure), WS_ERR_INVALID. */
+ws_status ws_nccl_unique_id(void* out);
+ws_status ws_transport_nccl_create(const void* unique_id, int32_t rank, int32_t nranks, int32_t device,
+                                   ws_transport** out);
+ws_status ws_transport_nccl_destroy(ws_transport* tr);
+
+/* A context bound to a transport and a slab (the transport must outlive it): ws_watershed,
+ * ws_waterfall and ws_segment on it take the EXTENDED slab dims/grad and write the owned
+ * planes (labels i32[(z1-z0)*n1*n2], levels i32[NL][(z1-z0)*n1*n2]); counts / num_regions
+ * are global.  Volumes only, 6- or 26-connectivity. */
+ws_status ws_ctx_create_sharded(int32_t device, const ws_transport* transport, ws_slab slab, ws_ctx** out);
+
+/* the same with an explicit transport (any context); rounds (HOST, optional) = step II rounds */
+ws_status ws_watershed_sharded(ws_ctx* ctx, const ws_transport* transport, const uint8_t* grad_ext,
+                               ws_dims dims_ext, ws_slab slab, int32_t connectivity, int32_t* labels_own,
+                               int64_t* num_regions, int32_t* rounds, void* stream);
+ws_status ws_waterfall_sharded(ws_ctx* ctx, const ws_transport* transport, const int32_t* labels_own,
+                               const uint8_t* grad_ext, ws_dims dims_ext, ws_slab slab, int32_t connectivity,
+                               int32_t NL, int32_t* levels_own, int64_t* counts, void* stream);
+ws_status ws_segment_sharded(ws_ctx* ctx, const ws_transport* transport, const uint8_t* grad_ext, ws_dims dims_ext,
+                             ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own, int64_t* counts,
+                             int32_t* rounds, void* stream);
 
 #ifdef __cplusplus
 }

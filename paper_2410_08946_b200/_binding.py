@@ -22,7 +22,9 @@ EXPORTS = ("ws_ctx_create", "ws_ctx_destroy", "ws_last_error", "ws_version", "ws
            "ws_gradient", "ws_gradient_u16", "ws_watershed", "ws_watershed_u16", "ws_watershed_variant", "ws_waterfall", "ws_waterfall_u16", "ws_waterfall_reconstruct", "ws_segment", "ws_segment_host", "ws_plateau_debug",
            "ws_shard_table_bytes", "ws_shard_plateau", "ws_shard_halo", "ws_shard_local", "ws_shard_merge",
            "ws_shard_relabel", "ws_shard_wf_dense", "ws_shard_wf_btable", "ws_shard_wf_bfill", "ws_shard_wf_begin",
-           "ws_shard_wf_step", "ws_shard_wf_end")
+           "ws_shard_wf_step", "ws_shard_wf_end",
+           "ws_nccl_unique_id", "ws_transport_nccl_create", "ws_transport_nccl_destroy", "ws_ctx_create_sharded",
+           "ws_watershed_sharded", "ws_waterfall_sharded", "ws_segment_sharded")
 
 
 class WsDims(ctypes.Structure):
@@ -33,6 +35,20 @@ class WsDims(ctypes.Structure):
 class WsSlab(ctypes.Structure):
     _fields_ = [("D", ctypes.c_int64), ("z0", ctypes.c_int64), ("z1", ctypes.c_int64), ("e0", ctypes.c_int64),
                 ("e1", ctypes.c_int64)]
+
+
+# ws_transport (include/ws.h): the callbacks of the sharded pipeline
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                ctypes.c_void_p)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                ctypes.c_int32, ctypes.c_void_p)
+
+
+class WsTransport(ctypes.Structure):
+    _fields_ = [("user", ctypes.c_void_p), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("exchange", EXCHANGE_FN), ("allgather", ALLGATHER_FN), ("allreduce", ALLREDUCE_FN)]
 
 
 class WsStats(ctypes.Structure):
@@ -116,6 +132,14 @@ def load(path: str = SO_PATH):
         lib.ws_shard_wf_begin.argtypes = [vp, vp, vp, WsDims, i32, WsSlab, vp, i64, i32, vp, vp]
         lib.ws_shard_wf_step.argtypes = [vp, vp, vp, vp, pi32, vp]
         lib.ws_shard_wf_end.argtypes = [vp, vp, vp, vp, WsDims, i32, WsSlab, vp, vp]
+        ptr_t = ctypes.POINTER(WsTransport)
+        lib.ws_nccl_unique_id.argtypes = [vp]
+        lib.ws_transport_nccl_create.argtypes = [vp, i32, i32, i32, ctypes.POINTER(ptr_t)]
+        lib.ws_transport_nccl_destroy.argtypes = [ptr_t]
+        lib.ws_ctx_create_sharded.argtypes = [i32, ptr_t, WsSlab, ctypes.POINTER(vp)]
+        lib.ws_watershed_sharded.argtypes = [vp, ptr_t, vp, WsDims, WsSlab, i32, vp, ctypes.POINTER(i64), pi32, vp]
+        lib.ws_waterfall_sharded.argtypes = [vp, ptr_t, vp, vp, WsDims, WsSlab, i32, i32, vp, vp, vp]
+        lib.ws_segment_sharded.argtypes = [vp, ptr_t, vp, WsDims, WsSlab, i32, i32, vp, vp, pi32, vp]
         for name in EXPORTS:
             f = getattr(lib, name)
             if name not in ("ws_last_error", "ws_version", "ws_phase_name", "ws_shard_table_bytes"):

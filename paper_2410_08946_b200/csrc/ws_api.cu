@@ -233,9 +233,13 @@ ws_status ws_ctx_destroy(ws_ctx* ctx) {
   ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->tiles, &ctx->roots, &ctx->rootc, &ctx->blockcnt, &ctx->edges, &ctx->ebufA, &ctx->ebufB, &ctx->rootsA, &ctx->rootsB, &ctx->lvl,
                      &ctx->comp, &ctx->best, &ctx->rep_of, &ctx->levelmap, &ctx->lvcount,
                      &ctx->h_grad, &ctx->h_labels, &ctx->h_levels, &ctx->dimg, &ctx->sroots, &ctx->sblocks, &ctx->rank, &ctx->wimg, &ctx->vstate, &ctx->nmin, &ctx->tlist, &ctx->upairs, &ctx->exitmx,
-                     &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc, &ctx->best_lo, &ctx->repbits};
+                     &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc, &ctx->best_lo, &ctx->repbits,
+                     &ctx->sh_L, &ctx->sh_P, &ctx->sh_planes, &ctx->sh_tab, &ctx->sh_alltab, &ctx->sh_ec, &ctx->sh_lab,
+                     &ctx->sh_dense, &ctx->sh_rep, &ctx->sh_bt, &ctx->sh_allbt, &ctx->sh_lext, &ctx->sh_best,
+                     &ctx->sh_nxt, &ctx->sh_small};
   for (auto* b : bufs) b->release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->sh_small_h) cudaFreeHost(ctx->sh_small_h);
   for (int i = 0; i < ws_ctx::MAXEV; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   delete ctx;
@@ -310,6 +314,7 @@ ws_status ws_watershed(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t c
   if (!grad) return null_arg("grad");
   if (!labels) return null_arg("labels");
   begin_call(ctx, g);
+  if (ctx->sharded) return sharded_dispatch_watershed(ctx, grad, dims, connectivity, labels, num_regions, (cudaStream_t)stream);
   tbegin(ctx, (cudaStream_t)stream);
   ws_status s = run_watershed(ctx, grad, g, connectivity, labels, num_regions, (cudaStream_t)stream);
   tfinish(ctx);
@@ -348,6 +353,10 @@ ws_status ws_waterfall(ws_ctx* ctx, const int32_t* labels, const uint8_t* grad, 
   if (!labels) return null_arg("labels");
   if (!grad) return null_arg("grad");
   if (!levels) return null_arg("levels");
+  if (ctx->sharded) {
+    begin_call(ctx, g);
+    return sharded_dispatch_waterfall(ctx, labels, grad, dims, connectivity, NL, levels, counts, (cudaStream_t)stream);
+  }
   begin_call(ctx, g);
   tbegin(ctx, (cudaStream_t)stream);
   ws_status s = run_waterfall(ctx, labels, grad, g, connectivity, NL, levels, counts, (cudaStream_t)stream);
@@ -431,6 +440,7 @@ ws_status ws_segment(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t con
   if (!grad) return null_arg("grad");
   if (!levels) return null_arg("levels");
   begin_call(ctx, g);
+  if (ctx->sharded) return sharded_dispatch_segment(ctx, grad, dims, connectivity, NL, levels, counts, (cudaStream_t)stream);
   tbegin(ctx, (cudaStream_t)stream);
   ws_status s = run_segment(ctx, grad, g, connectivity, NL, levels, counts, (cudaStream_t)stream);
   tfinish(ctx);

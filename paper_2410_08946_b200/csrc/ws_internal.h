@@ -93,6 +93,15 @@ struct ws_ctx {
   ws::Buf lvcount;    // i64[NL]  device-side region counts
   ws::Buf pathc;      // u64[4]   code-path counters of the waterfall (look-back depth, k_edges chunks, RAG emits)
   ws::Buf h_grad, h_labels, h_levels;  // device copies used by ws_segment_host
+  // sharded pipeline (ws_sharded.cu): transport + slab of a ws_ctx_create_sharded context and
+  // the per-rank working buffers of ws_watershed_sharded / ws_segment_sharded
+  int sharded = 0;
+  ws_transport sh_tr{};
+  ws_slab sh_slab{};
+  ws::Buf sh_L, sh_P, sh_planes, sh_tab, sh_alltab, sh_ec, sh_lab, sh_dense, sh_rep, sh_bt, sh_allbt, sh_lext, sh_best,
+      sh_nxt, sh_small;
+  int64_t* sh_small_h = nullptr;
+  size_t sh_small_n = 0;
   int64_t* pinned = nullptr;           // small pinned host scratch (flags / counts)
   ws_stats stats{};
   // per-phase CUDA-event timing (ws_ctx_set_timing)
@@ -126,6 +135,13 @@ inline void launched(ws_ctx* ctx, int phase, int n = 1) {
 // CUDA error status and counts its launches into ctx->stats.kernel_launches.
 ws_status run_gradient(ws_ctx* ctx, const uint8_t* img, const Geo& g, int is3d, float sigma,
                        uint8_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st);
+// ws_watershed / ws_segment on a ws_ctx_create_sharded context (ws_sharded.cu)
+ws_status sharded_dispatch_watershed(ws_ctx* ctx, const uint8_t* grad_ext, const ws_dims& d, int conn, int32_t* labels,
+                                     int64_t* num_regions, cudaStream_t st);
+ws_status sharded_dispatch_segment(ws_ctx* ctx, const uint8_t* grad_ext, const ws_dims& d, int conn, int NL,
+                                   int32_t* levels, int64_t* counts, cudaStream_t st);
+ws_status sharded_dispatch_waterfall(ws_ctx* ctx, const int32_t* labels_own, const uint8_t* grad_ext, const ws_dims& d,
+                                     int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
 ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
                         int32_t* labels, int64_t* num_regions, cudaStream_t st, bool relabel = true);
 ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma,

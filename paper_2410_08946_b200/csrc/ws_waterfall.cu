@@ -163,9 +163,10 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
 // waterfall (RAG, level materialisation) reads D instead of labels, so no per-voxel or
 // per-edge dense_of gather remains on the hot path.  Each thread maps 4 consecutive voxels;
 // equal neighbours (the common case: regions are runs along x) reuse the previous gather.
+// vec == 0 (labels or D not 16-byte aligned): scalar accesses only.
 __global__ void __launch_bounds__(NTW) k_dimage(const int* __restrict__ labels, const int* __restrict__ dense_of,
-                                                 long long n, int* __restrict__ D) {
-  const long long n4 = n >> 2;
+                                                 long long n, int* __restrict__ D, int vec) {
+  const long long n4 = vec ? n >> 2 : 0;
   const int4* L4 = reinterpret_cast<const int4*>(labels);
   int4* D4 = reinterpret_cast<int4*>(D);
   for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n4; i += (long long)gridDim.x * NTW) {
@@ -188,8 +189,8 @@ __device__ __forceinline__ int rank_of(const uint2* __restrict__ rk, int l) {
 }
 
 __global__ void __launch_bounds__(NTW) k_dimage_rk(const int* __restrict__ labels, const uint2* __restrict__ rk,
-                                                    long long n, int* __restrict__ D) {
-  const long long n4 = n >> 2;
+                                                    long long n, int* __restrict__ D, int vec) {
+  const long long n4 = vec ? n >> 2 : 0;
   const int4* L4 = reinterpret_cast<const int4*>(labels);
   int4* D4 = reinterpret_cast<int4*>(D);
   for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n4; i += (long long)gridDim.x * NTW) {
@@ -974,11 +975,9 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const G
     const long long n = (long long)(z1 - g.zlo) * g.plane;
     const bool al = !(reinterpret_cast<uintptr_t>(labels + o) & 15) && !(reinterpret_cast<uintptr_t>(D + o) & 15);
     if (rk) {  // unsharded: the rank structure of k_dense
-      k_dimage_rk<<<grid_for(n / 4 + 1, ctx->num_sms), NTW, 0, st>>>(labels + o, rk, al ? n : 0, D + o);
-      if (!al) k_dimage_rk<<<grid_for(n, ctx->num_sms), NTW, 0, st>>>(labels + o, rk, n, D + o);
+      k_dimage_rk<<<grid_for(al ? n / 4 + 1 : n, ctx->num_sms), NTW, 0, st>>>(labels + o, rk, n, D + o, al ? 1 : 0);
     } else {
-      k_dimage<<<grid_for(n / 4 + 1, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, al ? n : 0, D + o);
-      if (!al) k_dimage<<<grid_for(n, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, n, D + o);
+      k_dimage<<<grid_for(al ? n / 4 + 1 : n, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, n, D + o, al ? 1 : 0);
     }
     launched(ctx, PH_WF_DENSE);
     ctx->wf.dofs = (long long)o;

@@ -329,3 +329,296 @@ def sharded_segment(tr, ctxs, slabs, grads_ext, NL: int, conn: int = 6):
     labels, R, rounds, nreps = sharded_watershed(tr, ctxs, slabs, grads_ext, conn, with_nreps=True)
     levels, counts = sharded_waterfall(tr, ctxs, slabs, grads_ext, labels, nreps, NL, conn)
     return labels, levels, counts, R, rounds
+
+
+# ============================================================================ library path
+# The sharded pipeline as ONE library call per rank (ws_segment_sharded / ws_watershed_sharded,
+# include/ws.h): the control flow above runs inside libws_b200; Python only supplies the
+# transport.  NcclLibTransport = the library's own NCCL communicator (production);
+# TorchCallbacks / ThreadCallbacks = caller callbacks (multi-process on one GPU with gloo,
+# K virtual ranks as threads in one process) for tests.
+
+class _DevBuf:
+    """A device pointer as a torch tensor (no copy) through __cuda_array_interface__."""
+
+    def __init__(self, p, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(p), False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+_TYPESTR = {torch.uint8: "|u1", torch.int32: "<i4", torch.int64: "<i8"}
+
+
+def _dev(p, n, dtype=torch.uint8):
+    return torch.as_tensor(_DevBuf(p, n, _TYPESTR[dtype]), device="cuda")
+
+
+def _torch_stream(ptr):
+    """the library's stream argument (NULL = the legacy default stream) as a torch stream"""
+    return torch.cuda.ExternalStream(ptr) if ptr else torch.cuda.default_stream()
+
+
+class _CallbackTransport:
+    """Wraps an object with exchange / allgather / allreduce methods on device tensors into a
+    ws_transport (ctypes callbacks; exceptions become a non-zero status)."""
+
+    def __init__(self, impl, rank: int, nranks: int):
+        self.impl = impl
+
+        def ex(user, slo, shi, rb, ra, nbytes, stream):
+            try:
+                self.impl.exchange(slo, shi, rb, ra, int(nbytes), stream)
+                return 0
+            except Exception as e:  # noqa: BLE001 - reported through the status
+                self.error = e
+                return -1
+
+        def ag(user, send, recv, nbytes, stream):
+            try:
+                self.impl.allgather(send, recv, int(nbytes), stream)
+                return 0
+            except Exception as e:  # noqa: BLE001
+                self.error = e
+                return -1
+
+        def ar(user, buf, count, dtype, op, stream):
+            try:
+                self.impl.allreduce(buf, int(count), int(dtype), int(op), stream)
+                return 0
+            except Exception as e:  # noqa: BLE001
+                self.error = e
+                return -1
+
+        self._fns = (_b.EXCHANGE_FN(ex), _b.ALLGATHER_FN(ag), _b.ALLREDUCE_FN(ar))  # keep alive
+        self.t = _b.WsTransport(None, int(rank), int(nranks), *self._fns)
+        self.error = None
+
+    def ptr(self):
+        return ctypes.pointer(self.t)
+
+
+class ThreadHub:
+    """Shared state of K virtual ranks running as threads of one process (one device)."""
+
+    def __init__(self, K: int):
+        import threading
+        self.K = K
+        self.bar = threading.Barrier(K)
+        self.slots = [None] * K
+
+
+class ThreadCallbacks:
+    """Collectives among the threads of a ThreadHub: device-to-device copies, ordered by
+    synchronising each rank's stream around a barrier."""
+
+    def __init__(self, hub: ThreadHub, rank: int):
+        self.hub, self.rank = hub, rank
+
+    def _sync(self, stream):
+        _torch_stream(stream).synchronize()
+
+    def exchange(self, slo, shi, rb, ra, n, stream):
+        h, r = self.hub, self.rank
+        self._sync(stream)
+        h.slots[r] = (slo, shi)
+        h.bar.wait()
+        if rb:
+            _dev(rb, n).copy_(_dev(h.slots[r - 1][1], n))
+        if ra:
+            _dev(ra, n).copy_(_dev(h.slots[r + 1][0], n))
+        torch.cuda.synchronize()
+        h.bar.wait()
+
+    def allgather(self, send, recv, n, stream):
+        h, r = self.hub, self.rank
+        self._sync(stream)
+        h.slots[r] = send
+        h.bar.wait()
+        out = _dev(recv, n * h.K)
+        for q in range(h.K):
+            out[q * n:(q + 1) * n].copy_(_dev(h.slots[q], n))
+        torch.cuda.synchronize()
+        h.bar.wait()
+
+    def allreduce(self, buf, count, dtype, op, stream):
+        h, r = self.hub, self.rank
+        dt = torch.int64 if dtype == 1 else torch.int32
+        self._sync(stream)
+        h.slots[r] = buf
+        h.bar.wait()
+        parts = torch.stack([_dev(h.slots[q], count, dt) for q in range(h.K)])
+        res = parts.amax(0) if op == 1 else parts.amin(0)
+        torch.cuda.synchronize()
+        h.bar.wait()  # every rank has read every buffer
+        _dev(buf, count, dt).copy_(res)
+        torch.cuda.synchronize()
+        h.bar.wait()
+
+
+class TorchCallbacks:
+    """Collectives over torch.distributed (one rank per process).  gloo: device buffers are
+    staged through host memory (several ranks may share one GPU); nccl: device buffers
+    directly (on the library's stream)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.K = dist.get_world_size(group)
+        self.host = dist.get_backend(group) == "gloo"
+
+    def _t(self, p, n, dtype=torch.uint8):
+        t = _dev(p, n, dtype)
+        return t.cpu() if self.host else t
+
+    def exchange(self, slo, shi, rb, ra, n, stream):
+        dist, r = self.dist, self.rank
+        es = _torch_stream(stream)
+        es.synchronize()
+        with torch.cuda.stream(es):
+            ops, outs = [], []
+            if rb:
+                b = self._t(rb, n)
+                ops += [dist.P2POp(dist.isend, self._t(slo, n), r - 1, self.group),
+                        dist.P2POp(dist.irecv, b, r - 1, self.group)]
+                outs.append((rb, b))
+            if ra:
+                a = self._t(ra, n)
+                ops += [dist.P2POp(dist.isend, self._t(shi, n), r + 1, self.group),
+                        dist.P2POp(dist.irecv, a, r + 1, self.group)]
+                outs.append((ra, a))
+            if ops:
+                for q in dist.batch_isend_irecv(ops):
+                    q.wait()
+            if self.host:
+                for p, t in outs:
+                    _dev(p, n).copy_(t)
+        es.synchronize()
+
+    def allgather(self, send, recv, n, stream):
+        es = _torch_stream(stream)
+        es.synchronize()
+        with torch.cuda.stream(es):
+            x = self._t(send, n)
+            if self.host:
+                parts = [torch.empty_like(x) for _ in range(self.K)]
+                self.dist.all_gather(parts, x, group=self.group)
+                _dev(recv, n * self.K).copy_(torch.cat(parts))
+            else:
+                self.dist.all_gather_into_tensor(_dev(recv, n * self.K), x, group=self.group)
+        es.synchronize()
+
+    def allreduce(self, buf, count, dtype, op, stream):
+        dt = torch.int64 if dtype == 1 else torch.int32
+        es = _torch_stream(stream)
+        es.synchronize()
+        with torch.cuda.stream(es):
+            x = self._t(buf, count, dt)
+            self.dist.all_reduce(x, op=self.dist.ReduceOp.MAX if op == 1 else self.dist.ReduceOp.MIN,
+                                 group=self.group)
+            if self.host:
+                _dev(buf, count, dt).copy_(x)
+        es.synchronize()
+
+
+class NcclLibTransport:
+    """The library's NCCL transport (ws_transport_nccl_create): rank 0 makes the unique id, it
+    travels to the other ranks over torch.distributed (a CPU object broadcast)."""
+
+    def __init__(self, device: int, group=None):
+        import torch.distributed as dist
+        lib = _b.load()
+        self.rank, self.K = dist.get_rank(group), dist.get_world_size(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _b.check(lib.ws_nccl_unique_id(uid))
+        obj = [bytes(uid.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = ctypes.create_string_buffer(obj[0], 128)
+        self._p = ctypes.POINTER(_b.WsTransport)()
+        _b.check(lib.ws_transport_nccl_create(uid, self.rank, self.K, int(device), ctypes.byref(self._p)))
+
+    def ptr(self):
+        return self._p
+
+    def close(self):
+        if getattr(self, "_p", None):
+            _b.load().ws_transport_nccl_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def segment_sharded(transport, ctx, slab: Slab, grad_ext, NL: int, conn: int = 6, out=None):
+    """ws_segment_sharded on this rank's extended slab grad_ext (u8 (e1-e0, n1, n2)).
+    Returns (levels_own [NL, z1-z0, n1, n2], counts (global), step II rounds)."""
+    lib = _b.load()
+    n1, n2 = grad_ext.shape[1], grad_ext.shape[2]
+    if out is None:
+        out = torch.empty((NL, slab.z1 - slab.z0, n1, n2), dtype=torch.int32, device=grad_ext.device)
+    counts = (ctypes.c_int64 * NL)()
+    rounds = ctypes.c_int32(0)
+    st = ctypes.c_void_p(torch.cuda.current_stream(grad_ext.device).cuda_stream)
+    s = lib.ws_segment_sharded(ctx.handle, transport.ptr(), _b.ptr(grad_ext), _dims(slab, n1, n2), slab.c(), conn, NL,
+                               _b.ptr(out), counts, ctypes.byref(rounds), st)
+    if s != _b.WS_OK and getattr(transport, "error", None) is not None:
+        raise RuntimeError("transport callback failed: %r" % (transport.error,))
+    _b.check(s)
+    return out, [int(c) for c in counts], rounds.value
+
+
+def watershed_sharded(transport, ctx, slab: Slab, grad_ext, conn: int = 6, out=None):
+    """ws_watershed_sharded: (labels_own [z1-z0, n1, n2], R (global), step II rounds)."""
+    lib = _b.load()
+    n1, n2 = grad_ext.shape[1], grad_ext.shape[2]
+    if out is None:
+        out = torch.empty((slab.z1 - slab.z0, n1, n2), dtype=torch.int32, device=grad_ext.device)
+    R = ctypes.c_int64(0)
+    rounds = ctypes.c_int32(0)
+    st = ctypes.c_void_p(torch.cuda.current_stream(grad_ext.device).cuda_stream)
+    _b.check(lib.ws_watershed_sharded(ctx.handle, transport.ptr(), _b.ptr(grad_ext), _dims(slab, n1, n2), slab.c(),
+                                      conn, _b.ptr(out), ctypes.byref(R), ctypes.byref(rounds), st))
+    return out, R.value, rounds.value
+
+
+def segment_threads(K: int, grad, NL: int, conn: int = 6):
+    """K virtual ranks as threads of this process, each running ws_segment_sharded on its
+    slab of the (D, n1, n2) volume grad with ThreadCallbacks.  Returns (levels [NL, D, n1, n2],
+    counts, rounds)."""
+    import threading
+    D, n1, n2 = grad.shape
+    slabs = make_slabs(D, K)
+    hub = ThreadHub(K)
+    res, errs = [None] * K, []
+    dev = grad.device
+
+    def run(r):
+        try:
+            torch.cuda.set_device(dev)
+            st = torch.cuda.Stream(dev)
+            with torch.cuda.stream(st):
+                s = slabs[r]
+                from . import _binding
+                ctx = _binding.Context(dev.index)
+                tr = _CallbackTransport(ThreadCallbacks(hub, r), r, K)
+                ge = grad[s.e0:s.e1].contiguous()
+                res[r] = segment_sharded(tr, ctx, s, ge, NL, conn)
+                st.synchronize()
+                ctx.close()
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+            hub.bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(K)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    levels = torch.cat([res[r][0] for r in range(K)], dim=1)
+    return levels, res[0][1], res[0][2]

@@ -72,3 +72,23 @@ def test_product_path_has_no_oracle_or_fallback():
                     src = f.read()
                 assert "import oracle" not in src and "from oracle" not in src, fn
                 assert "ws_oracle" not in src, fn
+
+
+def test_sharded_entry_points_validate_without_device():
+    """The sharded one-call path (ws_segment_sharded & co.) rejects bad transports / slabs
+    before any CUDA or NCCL call."""
+    lib, b = _lib()
+    dims = b.WsDims(3, 0, 6, 8, 8)
+    slab = b.WsSlab(8, 0, 4, 0, 6)
+    st = lib.ws_segment_sharded(None, None, None, dims, slab, 6, 6, None, None, None, None)
+    assert st == b.WS_ERR_INVALID
+    # a transport whose rank does not own the slab's end planes
+    fns = (b.EXCHANGE_FN(lambda *a: 0), b.ALLGATHER_FN(lambda *a: 0), b.ALLREDUCE_FN(lambda *a: 0))
+    tr = b.WsTransport(None, 1, 2, *fns)
+    h = ctypes.c_void_p()
+    st = lib.ws_ctx_create_sharded(0, ctypes.byref(tr), slab, ctypes.byref(h))
+    assert st == b.WS_ERR_INVALID and b"rank" in lib.ws_last_error()
+    p = ctypes.POINTER(b.WsTransport)()
+    st = lib.ws_transport_nccl_create(None, 0, 0, 0, ctypes.byref(p))
+    assert st == b.WS_ERR_INVALID
+    assert lib.ws_transport_nccl_destroy(None) == b.WS_OK
