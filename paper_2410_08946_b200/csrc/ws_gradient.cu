@@ -409,9 +409,223 @@ __global__ void __launch_bounds__(256) k_grad_stream(const Px* __restrict__ img,
   }
 }
 
+// ------------------------------------- 2.5-D streaming kernel, v2 (u8 volumes, r <= 3)
+// The same decomposition as k_grad_stream (C8-C10: x, then y, then z blur on x/255, central /
+// one-sided differences, quantisation), re-blocked so the instruction count per voxel is
+// small (the v1 kernel issues ~220 thread-instructions per voxel, IPC 3.5: issue-bound):
+//   - CTA = 64 x 16 output columns walking ZC2 planes; every index of a thread is fixed for
+//     the whole walk (no per-plane division);
+//   - input plane staged as u32 words (4 pixels; rows by-H .. by+TY+H-1, columns bx-4 ..);
+//   - x blur: a job = 8 consecutive outputs from two 8-byte shared loads; each byte is
+//     converted once (PRMT into the mantissa of 2^23, FADD) and the 7-tap sums run as
+//     packed fp32 pairs (__ffma2_rn, two outputs per instruction);
+//   - y blur + z blur by the same thread on its own 3 rows x 2 columns: the xy-blurred planes
+//     live in a 7-plane shared ring (own positions only, no barrier between the two), the z
+//     blur writes the fully blurred plane into a 3-plane ring;
+//   - gradient: lanes along x (conflict-free ring reads), 4 consecutive rows per thread.
+// Results are those of the v1 kernel up to fp32 rounding order (the same taps, the same
+// tap order per output), i.e. within the 1e-5 tolerance; parity tests cover both.
+constexpr int G2X = 64, G2Y = 16, G2Z = 64;
+template <int R> struct G2Smem {
+  static constexpr int H = R + 1, K = 2 * R + 1, SY = G2Y + 2 * H, YR = G2Y + 2, YP = G2X + 4;
+  static constexpr int bytes = 4 * (SY * 20 + SY * 72 + K * YR * YP + 3 * YR * YP);
+};
+
+__device__ __forceinline__ float u8f(unsigned w, int k) {  // byte k of w as an exact float
+  return __int_as_float((int)__byte_perm(w, 0x4B000000u, 0x7650u + k)) - 8388608.f;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256, 3) k_grad_s2(const uint8_t* __restrict__ img, Geo g, int ntx, int nty,
+                                                   uint8_t* __restrict__ q, float* __restrict__ blur_out,
+                                                   float* __restrict__ grad_out, const __grid_constant__ BlurW W) {
+  static_assert(R >= 1 && R <= 3, "x jobs read one 16-byte window: r <= 3");
+  constexpr int H = R + 1, K = 2 * R + 1;
+  constexpr int SY = G2Y + 2 * H;   // staged input rows by-H .. by+G2Y+H-1
+  constexpr int SXW = 20;           // staged words per row: columns bx-4 .. bx+75
+  constexpr int NJ = 9;             // x jobs per row: x' = bx-1+8j .. +7 (x' in [bx-1, bx+G2X] needed)
+  constexpr int XP = 8 * NJ;        // X row pitch (floats): index i = x' - (bx - 1)
+  constexpr int YR = G2Y + 2;       // xy-blurred rows by-1 .. by+G2Y
+  constexpr int YP = G2X + 2 + 2;   // ring row pitch (floats): columns i = 0 .. G2X+1 (+2 pad)
+  constexpr int NPAIR = (G2X + 2) / 2, NRG = YR / 3;  // y/z threads: 33 column pairs x 6 row groups
+  static_assert(YR % 3 == 0 && NPAIR * NRG <= 256, "y/z thread layout");
+  extern __shared__ __align__(16) unsigned char g2_smem[];  // G2Smem<R>::bytes
+  unsigned* sIn = reinterpret_cast<unsigned*>(g2_smem);     // SY * SXW words
+  float* X = reinterpret_cast<float*>(sIn + SY * SXW);        // SY * XP
+  float* XY = X + SY * XP;                                    // K * YR * YP
+  float* B = XY + K * YR * YP;                                // 3 * YR * YP
+  const int t0 = blockIdx.x;
+  const int bx = (t0 % ntx) * G2X, by = ((t0 / ntx) % nty) * G2Y, z0 = (t0 / (ntx * nty)) * G2Z;
+  const int z1 = min(z0 + G2Z, g.n0);
+  const int tid = threadIdx.x;
+  // ---- load jobs (fixed): word w of staged row; clamp-to-edge (C8) in y and x
+  const bool wide = bx >= 4 && bx + 4 * SXW - 4 <= g.n2 && (g.n2 & 3) == 0 &&
+                    (reinterpret_cast<uintptr_t>(img) & 3) == 0;
+  constexpr int NLD = (SY * SXW + 255) / 256;
+  int ldoff[NLD];  // in-plane offset of the word (wide) or of the row (not wide); -1: no job
+  int ldx[NLD];    // x of the word's first pixel (not wide)
+#pragma unroll
+  for (int u = 0; u < NLD; ++u) {
+    const int job = tid + 256 * u;
+    ldoff[u] = -1;
+    ldx[u] = 0;
+    if (job < SY * SXW) {
+      const int row = job / SXW, w = job % SXW;
+      const int gy = min(max(by + row - H, 0), g.n1 - 1);
+      ldx[u] = bx - 4 + 4 * w;
+      ldoff[u] = wide ? gy * g.n2 + ldx[u] : gy * g.n2;
+    }
+  }
+  unsigned pre[NLD];
+  auto load = [&](int zi) {
+    const int zc = min(max(zi, 0), g.n0 - 1);
+    const uint8_t* pl = img + (size_t)zc * g.plane;
+#pragma unroll
+    for (int u = 0; u < NLD; ++u) {
+      unsigned v = 0;
+      if (ldoff[u] >= 0) {
+        if (wide) {
+          v = __ldg(reinterpret_cast<const unsigned*>(pl + ldoff[u]));
+        } else {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) v |= (unsigned)__ldg(pl + ldoff[u] + min(max(ldx[u] + b, 0), g.n2 - 1)) << (8 * b);
+        }
+      }
+      pre[u] = v;
+    }
+  };
+  // ---- x jobs (fixed): row xr, job xj
+  const bool xjob = tid < SY * NJ;
+  const int xr = tid / NJ, xj = tid % NJ;
+  // ---- y/z positions (fixed): column pair yp, rows 3 yg .. 3 yg + 2 of the xy-blurred plane
+  const bool yz = tid < NPAIR * NRG;
+  const int yp = tid % NPAIR, yg = tid / NPAIR;
+  // ---- gradient outputs (fixed): column x, rows 4 gg .. 4 gg + 3
+  static_assert(G2X * G2Y == 4 * 256, "gradient thread layout");
+  const int gx = bx + tid % G2X, gg = tid / G2X, gy0 = by + 4 * gg;
+  const bool inner = bx > 0 && bx + G2X < g.n2 && by > 0 && by + G2Y < g.n1;
+  const int nin = (z1 - z0) + 2 * H;  // input planes z0 - H .. z1 + H - 1
+  load(z0 - H);
+#pragma unroll 1
+  for (int t = 0; t < nin; ++t) {
+    const int zi = z0 - H + t;
+#pragma unroll
+    for (int u = 0; u < NLD; ++u)
+      if (tid + 256 * u < SY * SXW) sIn[tid + 256 * u] = pre[u];
+    __syncthreads();  // (A) staged plane visible
+    if (t + 1 < nin) load(zi + 1);  // in flight during this plane's work
+    // x blur: outputs x' = bx - 1 + 8 xj + o, o = 0..7, from bytes 8 xj .. 8 xj + 15 of row xr
+    if (xjob) {
+      const uint2 wa = *reinterpret_cast<const uint2*>(sIn + xr * SXW + 2 * xj);  // 8-byte aligned
+      const uint2 wb = *reinterpret_cast<const uint2*>(sIn + xr * SXW + 2 * xj + 2);
+      float v[16];
+      const unsigned wd[4] = {wa.x, wa.y, wb.x, wb.y};
+#pragma unroll
+      for (int b = 0; b < 16; ++b) v[b] = (b >= 3 - R && b <= 10 + R) ? u8f(wd[b >> 2], b & 3) : 0.f;
+      float2 acc[4];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) acc[o] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const float2 wi = make_float2(W.wn[i], W.wn[i]);
+#pragma unroll
+        for (int o = 0; o < 4; ++o)  // outputs 2o, 2o+1 (x' index 3 + 2o + ... in the window)
+          acc[o] = __ffma2_rn(wi, make_float2(v[3 - R + 2 * o + i], v[4 - R + 2 * o + i]), acc[o]);
+      }
+      float4* dst = reinterpret_cast<float4*>(X + xr * XP + 8 * xj);
+      dst[0] = make_float4(acc[0].x, acc[0].y, acc[1].x, acc[1].y);
+      dst[1] = make_float4(acc[2].x, acc[2].y, acc[3].x, acc[3].y);
+    }
+    __syncthreads();  // (B) X plane visible
+    // y blur of rows 3 yg .. 3 yg + 2 at columns 2 yp, 2 yp + 1 -> XY ring slot t % K; once K
+    // planes are in, z blur of plane zi - R -> B ring slot tb % 3 (own positions only)
+    const int tb = t - 2 * R;
+    if (yz) {
+      float2 xv[3 + 2 * R];
+#pragma unroll
+      for (int i = 0; i < 3 + 2 * R; ++i) xv[i] = *reinterpret_cast<const float2*>(X + (3 * yg + i) * XP + 2 * yp);
+      float* ring = XY + (t % K) * YR * YP;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc = __ffma2_rn(make_float2(W.w[i], W.w[i]), xv[r + i], acc);
+        *reinterpret_cast<float2*>(ring + (3 * yg + r) * YP + 2 * yp) = acc;
+      }
+      if (tb >= 0) {
+        float* Bt = B + (tb % 3) * YR * YP;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const int off = (3 * yg + r) * YP + 2 * yp;
+          float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < K; ++i)  // plane zi - R - R + i sits in ring slot (t - 2R + i) % K
+            acc = __ffma2_rn(make_float2(W.w[i], W.w[i]),
+                             *reinterpret_cast<const float2*>(XY + ((tb + i) % K) * YR * YP + off), acc);
+          *reinterpret_cast<float2*>(Bt + off) = acc;
+        }
+      }
+    }
+    if (tb < 2) continue;  // (uniform) the next plane's barrier (A) orders the rings
+    __syncthreads();  // (C) B ring visible
+    // gradient of plane zo = zi - R - 1 (blurred planes zo - 1, zo, zo + 1 in the B ring):
+    // lanes along x (conflict-free ring reads), 4 consecutive rows per thread
+    const int zo = zi - R - 1;
+    if (zo < z0 || zo >= z1 || gx >= g.n2) continue;
+    const float* Bm = B + ((tb - 2) % 3) * YR * YP;
+    const float* Bc = B + ((tb - 1) % 3) * YR * YP;
+    const float* Bp = B + (tb % 3) * YR * YP;
+    const int ci = gx - bx + 1;  // ring column of x
+    const bool zin = zo > 0 && zo < g.n0 - 1;
+    float col[6];  // rows gy0 - 1 .. gy0 + 4 at x
+#pragma unroll
+    for (int j = 0; j < 6; ++j) col[j] = Bc[(4 * gg + j) * YP + ci];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int gy = gy0 + o;
+      if (gy >= g.n1) break;
+      const int c = (4 * gg + o + 1) * YP + ci;
+      const float v = col[o + 1];
+      const float xl = Bc[c - 1], xr = Bc[c + 1];
+      float dx, dy, dz;
+      if (inner) {
+        dx = 0.5f * (xr - xl);
+        dy = 0.5f * (col[o + 2] - col[o]);
+      } else {
+        dx = g.n2 < 2 ? 0.f : (gx == 0 ? xr - v : (gx == g.n2 - 1 ? v - xl : 0.5f * (xr - xl)));
+        dy = g.n1 < 2 ? 0.f : (gy == 0 ? col[o + 2] - v : (gy == g.n1 - 1 ? v - col[o] : 0.5f * (col[o + 2] - col[o])));
+      }
+      if (zin) dz = 0.5f * (Bp[c] - Bm[c]);
+      else dz = g.n0 < 2 ? 0.f : (zo == 0 ? Bp[c] - v : (zo == g.n0 - 1 ? v - Bm[c] : 0.5f * (Bp[c] - Bm[c])));
+      float ss = 0.f;
+      ss = fmaf(dx, dx, ss);
+      ss = fmaf(dy, dy, ss);
+      ss = fmaf(dz, dz, ss);
+      const float gm = sqrtf(ss);
+      const float qq = floorf(fmaf(255.f, gm, 0.5f));
+      const size_t p = (size_t)zo * g.plane + (size_t)gy * g.n2 + gx;
+      q[p] = (uint8_t)(qq > 255.f ? 255.f : qq);
+      if (blur_out) blur_out[p] = v;
+      if (grad_out) grad_out[p] = gm;
+    }
+  }
+}
+
 template <int R, class Px>
 static ws_status grad_stream_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, float* blur, float* grad,
                                const BlurW& W, cudaStream_t st) {
+  if constexpr (sizeof(Px) == 1 && R <= 3) {
+    const char* v1 = getenv("WS_GRAD_V1");  // A/B and parity of the v1 kernel
+    if (!(v1 && v1[0] == '1')) {
+      const int ntx = (g.n2 + G2X - 1) / G2X, nty = (g.n1 + G2Y - 1) / G2Y, ntz = (g.n0 + G2Z - 1) / G2Z;
+      WS_CUDA(cudaFuncSetAttribute(k_grad_s2<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, G2Smem<R>::bytes));
+      k_grad_s2<R><<<ntx * nty * ntz, 256, G2Smem<R>::bytes, st>>>(img, g, ntx, nty, q, blur, grad, W);
+      launched(ctx, PH_GRAD_MAG);
+      tmark(ctx, st, PH_GRAD_MAG);
+      WS_CUDA(cudaGetLastError());
+      return WS_OK;
+    }
+  }
   const int ntx = (g.n2 + GSX - 1) / GSX, nty = (g.n1 + GSY - 1) / GSY, ntz = (g.n0 + GZC - 1) / GZC;
   k_grad_stream<R, Px><<<ntx * nty * ntz, 256, 0, st>>>(img, g, ntx, nty, q, blur, grad, W);
   launched(ctx, PH_GRAD_MAG);
