@@ -113,6 +113,7 @@ static ws_status null_arg(const char* name) {
 }
 
 static void begin_call(ws_ctx* ctx, const Geo& g) {
+  ++ctx->calls;
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   ctx->stats.n_voxels = g.N;
 }
@@ -240,6 +241,8 @@ ws_status ws_ctx_destroy(ws_ctx* ctx) {
   for (auto* b : bufs) b->release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->sh_small_h) cudaFreeHost(ctx->sh_small_h);
+  if (ctx->sg.exec) cudaGraphExecDestroy(ctx->sg.exec);
+  if (ctx->cap_st) cudaStreamDestroy(ctx->cap_st);
   for (int i = 0; i < ws_ctx::MAXEV; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   delete ctx;

@@ -49,6 +49,9 @@ struct WSState {
   long long dofs = 0;  // offset of the owned planes in ctx->dimg
   long long sorted_n = 0;  // sharded: length of the exchanged minima (current roots, sorted)
   int NL = 1, stride = 4, lv = 0, k = 1, eflip = 0, rflip = -1;
+  // sync-free ws_segment (small inputs): R and E stay on the device (R, E above are bounds)
+  const unsigned long long* Rdev = nullptr;
+  const unsigned long long* Edev = nullptr;
 };
 
 struct ws_ctx {
@@ -103,6 +106,22 @@ struct ws_ctx {
   int64_t* sh_small_h = nullptr;
   size_t sh_small_n = 0;
   int64_t* pinned = nullptr;           // small pinned host scratch (flags / counts)
+  // ws_segment on small inputs: the sync-free call captured once as a CUDA graph and replayed
+  // while the arguments stay the same (ws_waterfall.cu run_segment)
+  struct SegGraph {
+    const void* I = nullptr;
+    void* levels = nullptr;
+    cudaStream_t st = nullptr;
+    int n0 = 0, n1 = 0, n2 = 0, conn = 0, NL = 0;
+    int seen = 0;             // calls with this key so far (the buffers are sized after one)
+    int failed = 0;           // capture unsupported: stay direct
+    int64_t launches = 0;     // kernels in the graph
+    int64_t last_call = -2;   // ctx->calls at its last use: any other call in between (it may
+                              // re-allocate a workspace buffer the graph refers to) drops it
+    cudaGraphExec_t exec = nullptr;
+  } sg;
+  cudaStream_t cap_st = nullptr;  // capture stream (the caller's may be the legacy stream)
+  int64_t calls = 0;          // API calls on this context (begin_call)
   ws_stats stats{};
   // per-phase CUDA-event timing (ws_ctx_set_timing)
   bool timing = false;
@@ -143,12 +162,13 @@ ws_status sharded_dispatch_segment(ws_ctx* ctx, const uint8_t* grad_ext, const w
 ws_status sharded_dispatch_waterfall(ws_ctx* ctx, const int32_t* labels_own, const uint8_t* grad_ext, const ws_dims& d,
                                      int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
 ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
-                        int32_t* labels, int64_t* num_regions, cudaStream_t st, bool relabel = true);
+                        int32_t* labels, int64_t* num_regions, cudaStream_t st, bool relabel = true,
+                        bool small = false);
 ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma,
                            uint16_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st);
 namespace px16 {  // ws_watershed16.cu: the same watershed on u16 pixels (unsharded)
 ws_status run_watershed(ws_ctx* ctx, const uint16_t* grad, const Geo& g, int conn, int32_t* labels,
-                        int64_t* num_regions, cudaStream_t st, bool relabel = true);
+                        int64_t* num_regions, cudaStream_t st, bool relabel = true, bool small = false);
 }
 ws_status run_plateau_debug(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
                             int32_t* dist, int32_t* parent, cudaStream_t st);

@@ -12,6 +12,8 @@
 //                (compaction), fold the survivors into best[] (per-component min-K edge)
 //   k_levelmap   per dense id: the chain comp^k(d) = its level-k root -> canonical label rows
 //   k_levels     levels[k][p] = map_k[dense(labels(p))]  (Alg. 5 l.12 output, one pass)
+#include <cstdio>
+
 #include "ws_internal.h"
 #include "ws_tile.cuh"
 
@@ -749,7 +751,9 @@ __global__ void __launch_bounds__(NTW) k_edges(const uint64_t* __restrict__ in_k
 // region's own canonical label).  x stays its own root below lvl[x]; from level lvl[x] on,
 // comp[x] is its root at that level.
 __global__ void k_levelmap(const int* __restrict__ comp, const uint8_t* __restrict__ lvl,
-                           const int* __restrict__ rep_of, int R, int NL, int stride, int* __restrict__ levelmap) {
+                           const int* __restrict__ rep_of, int R, int NL, int stride, int* __restrict__ levelmap,
+                           const unsigned long long* Rdev) {
+  if (Rdev) R = (int)*Rdev;
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < R; d += gridDim.x * blockDim.x) {
     int x = d;
     int* row = levelmap + (size_t)d * stride;
@@ -949,6 +953,7 @@ static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
   k_iota<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(ctx->comp.as<int>(), (int)R);
   launched(ctx, PH_WF_LEVELS);
   ctx->wf.R = R;
+  ctx->wf.Rdev = nullptr;
   ctx->wf.NL = NL;
   ctx->wf.stride = stride;
   return WS_OK;
@@ -961,7 +966,7 @@ static ws_status wf_alloc(ws_ctx* ctx, int64_t R, int NL, cudaStream_t st) {
 // best[] fold; the u16 level loop takes its minima in two passes).
 template <class Px = uint8_t>
 static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const Geo& g, int conn,
-                        const int* dense_of, cudaStream_t st, const uint2* rk = nullptr) {
+                        const int* dense_of, cudaStream_t st, const uint2* rk = nullptr, bool small = false) {
   constexpr size_t ESZ = sizeof(Px) == 1 ? sizeof(uint64_t) : sizeof(E16);
   unsigned long long* ecount = reinterpret_cast<unsigned long long*>(ctx->flags.as<char>() + 136);
   unsigned long long* pathc = ctx->pathc.as<unsigned long long>();
@@ -985,7 +990,8 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const G
   tmark(ctx, st, PH_WF_DENSE);
   const long long own = (long long)(g.zhi - g.zlo) * g.plane;
   long long cap = (long long)(ctx->edges.bytes / ESZ);
-  const long long want = own / 4 + 4096;
+  // small (sync-free ws_segment): every boundary record fits, the count stays on the device
+  const long long want = small ? own * (conn - conn / 2) + 4096 : own / 4 + 4096;
   if (cap < want) {
     WS_TRY(ctx->edges.ensure((size_t)want * ESZ, "edges"));
     cap = want;
@@ -1001,6 +1007,10 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const G
                    EdgeOut{ctx->edges.as<uint64_t>(), ecount, cap, ctx->best.as<uint64_t>(), pathc + 2,
                            sizeof(Px) == 1 ? nullptr : ctx->edges.as<E16>(), pathc + 3}, st));
     launched(ctx, PH_WF_RAG);
+    if (small) {
+      E = cap;  // a bound; k_edges reads the count from ecount
+      break;
+    }
     WS_TRY(read_i64(ctx, ecount, &E, st));
     if (E <= cap) break;
     if (attempt >= 4) {
@@ -1025,6 +1035,7 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const G
   ctx->wf.k = 1;
   ctx->wf.eflip = 0;
   ctx->wf.rflip = -1;  // level 1 hooks every region
+  ctx->wf.Edev = small ? ecount : nullptr;
   return WS_OK;
 }
 
@@ -1040,7 +1051,7 @@ static ws_status wf_level(ws_ctx* ctx, bool edges_next, cudaStream_t st) {
   int* rB = ctx->rootsB.as<int>();
   int* rin = w.rflip < 0 ? nullptr : (w.rflip == 0 ? rA : rB);
   int* rout = (w.rflip == 0) ? rB : rA;
-  const unsigned long long* nin = rin ? cnt + (k - 1) : nullptr;  // level 1: all R regions
+  const unsigned long long* nin = rin ? cnt + (k - 1) : w.Rdev;  // level 1: all R regions
   k_hook<<<grid_for(w.R, ctx->num_sms), 256, 0, st>>>(best, comp, rin, (int)w.R, nin);
   k_flatten<<<grid_for(w.R, ctx->num_sms, 8), NTW, 0, st>>>(comp, rin, (int)w.R, nin, rout, cnt + k,
                                                              ctx->lvl.as<uint8_t>(), k);
@@ -1060,7 +1071,7 @@ static ws_status wf_level(ws_ctx* ctx, bool edges_next, cudaStream_t st) {
     const long long chunks = (w.E + ECH - 1) / ECH;
     const int grid = (int)std::min<long long>(chunks, (long long)ctx->num_sms * std::max(1, occ));
     k_edges<<<grid, NTW, esmem, st>>>(k == 1 ? ctx->edges.as<uint64_t>() : nullptr, ein, w.E,
-                                      k == 1 ? nullptr : cnt + LVC + k, comp, best, eout, cnt + LVC + k + 1,
+                                      k == 1 ? w.Edev : cnt + LVC + k, comp, best, eout, cnt + LVC + k + 1,
                                       ctx->pathc.as<unsigned long long>() + 1);
     launched(ctx, PH_WF_LEVELS);
   }
@@ -1121,7 +1132,8 @@ static ws_status wf_finish(ws_ctx* ctx, const int32_t* D, const Geo& g, int conn
   ctx->stats.waterfall_levels = w.lv;
   int* levelmap = ctx->levelmap.as<int>();
   k_levelmap<<<grid_for(w.R, ctx->num_sms), 256, 0, st>>>(ctx->comp.as<int>(), ctx->lvl.as<uint8_t>(),
-                                                           ctx->rep_of.as<int>(), (int)w.R, NL, stride, levelmap);
+                                                           ctx->rep_of.as<int>(), (int)w.R, NL, stride, levelmap,
+                                                           w.Rdev);
   launched(ctx, PH_WF_LEVELS);
   tmark(ctx, st, PH_WF_LEVELS);
   const int N = g.N;
@@ -1276,19 +1288,33 @@ __global__ void __launch_bounds__(NTW) k_relabel_seg(const int* __restrict__ P, 
   }
 }
 
-ws_status run_segment(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int NL, int32_t* levels,
-                      int64_t* counts, cudaStream_t st) {
-  if (NL > LVC) {
-    set_error(WS_ERR_LIMIT, "ws_segment: NL must be <= %d", LVC);
-    return WS_ERR_LIMIT;
-  }
-  if ((reinterpret_cast<uintptr_t>(levels) & 15) != 0) {
-    set_error(WS_ERR_INVALID, "ws_segment: levels must be 16-byte aligned");
-    return WS_ERR_INVALID;
-  }
+__global__ void k_store_count(const int* __restrict__ src, unsigned long long* dst) { *dst = (unsigned long long)*src; }
+
+static void begin_call_stats(ws_ctx* ctx, const Geo& g) {
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+  ctx->stats.n_voxels = g.N;
+}
+
+// Inputs small enough that every list can be sized from N (the sync-free mode of ws_segment:
+// no host round trip until the final counts; a list that still overflowed is caught by the
+// final read, and the call then reruns on the regular path)
+static bool segment_small(const Geo& g, int conn) {
+  const char* e = getenv("WS_NO_SMALL");
+  if (e && e[0] == '1') return false;
+  const long long nf = conn - conn / 2;
+  return (long long)g.N * nf <= (1ll << 27);
+}
+
+static ws_status seg_small_finish(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int NL, int32_t* levels,
+                                  int64_t* counts, cudaStream_t st);
+
+// enqueue == true (small only): stop after enqueuing the final device-to-host copies (no
+// synchronisation: the sequence can be captured as a graph); seg_small_finish reads them
+static ws_status run_segment_impl(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int NL, int32_t* levels,
+                                  int64_t* counts, cudaStream_t st, bool small, bool enqueue = false) {
   // steps I-IV: every voxel points at a listed root, listed roots hold -1 - canonical label,
   // the representative bitmap is set
-  WS_TRY(run_watershed(ctx, I, g, conn, levels, nullptr, st, false));
+  WS_TRY(run_watershed(ctx, I, g, conn, levels, nullptr, st, false, small));
   const int* P = ctx->aux.as<int>();
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->pathc.ensure(4 * sizeof(unsigned long long), "path counters"));
@@ -1304,11 +1330,21 @@ ws_status run_segment(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int
   k_scan_counts<<<1, NTW, 0, st>>>(bsum, nb);
   k_rank_write<<<nb, NTW, 0, st>>>(bits, nw, bsum, rk);
   launched(ctx, PH_WF_DENSE, 3);
-  WS_CUDA(cudaMemcpyAsync(ctx->pinned, bsum + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
-  WS_CUDA(cudaStreamSynchronize(st));
-  const int64_t R = reinterpret_cast<const int*>(ctx->pinned)[0];
-  ctx->stats.n_regions = R;
-  WS_TRY(wf_alloc(ctx, R, NL, st));
+  int64_t R;
+  if (small) {
+    R = g.N;  // a bound: the level loop reads R from the device
+    WS_TRY(wf_alloc(ctx, R, NL, st));
+    unsigned long long* Rd = ctx->lvcount.as<unsigned long long>();  // slot 0 (levels use 1..)
+    k_store_count<<<1, 1, 0, st>>>(bsum + nb, Rd);
+    launched(ctx, PH_WF_DENSE);
+    ctx->wf.Rdev = Rd;
+  } else {
+    WS_CUDA(cudaMemcpyAsync(ctx->pinned, bsum + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+    WS_CUDA(cudaStreamSynchronize(st));
+    R = reinterpret_cast<const int*>(ctx->pinned)[0];
+    ctx->stats.n_regions = R;
+    WS_TRY(wf_alloc(ctx, R, NL, st));
+  }
   WS_TRY(ctx->rep_of.ensure((size_t)R * sizeof(int), "rep_of"));
   WS_TRY(ctx->dimg.ensure((size_t)g.N * sizeof(int), "dense-id image"));
   int* D = ctx->dimg.as<int>();
@@ -1316,15 +1352,139 @@ ws_status run_segment(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int
   k_relabel_seg<<<grid_for(g.N / 4 + 1, ctx->num_sms), NTW, 0, st>>>(P, rk, g.N, D, ctx->rep_of.as<int>());
   launched(ctx, PH_WS_RELABEL);
   tmark(ctx, st, PH_WS_RELABEL);
-  WS_TRY(wf_rag<uint8_t>(ctx, nullptr, I, g, conn, nullptr, st));
-  if (counts) counts[0] = R;
-  ctx->stats.level_counts[0] = R;
-  ctx->stats.level_edges[1] = ctx->wf.E;
+  const unsigned long long* Rdev = ctx->wf.Rdev;
+  WS_TRY(wf_rag<uint8_t>(ctx, nullptr, I, g, conn, nullptr, st, nullptr, small));
+  ctx->wf.Rdev = Rdev;
   for (int k = 1; k < NL; ++k) WS_TRY(wf_level(ctx, k + 1 < NL, st));
   WS_TRY(wf_finish(ctx, D, g, conn, levels, st));
-  if (NL > 1) WS_TRY(wf_read_counts(ctx, NL - 1, counts, st));
+  if (!small) {
+    if (counts) counts[0] = R;
+    ctx->stats.level_counts[0] = R;
+    ctx->stats.level_edges[1] = ctx->wf.E;
+    if (NL > 1) WS_TRY(wf_read_counts(ctx, NL - 1, counts, st));
+    ctx->stats.waterfall_levels = ctx->wf.lv;
+    return WS_OK;
+  }
+  // the one host read of the sync-free mode: flags (step II depth limit, pair count, rounds,
+  // edge count), R, the level counters and the code-path counters
+  char* hp = reinterpret_cast<char*>(ctx->pinned);
+  WS_CUDA(cudaMemcpyAsync(hp, ctx->flags.p, 256, cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaMemcpyAsync(hp + 256, ctx->lvcount.p, 2 * LVC * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  WS_CUDA(cudaMemcpyAsync(hp + 256 + 2 * LVC * 8, ctx->pathc.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          st));
+  if (enqueue) return WS_OK;
+  return seg_small_finish(ctx, I, g, conn, NL, levels, counts, st);
+}
+
+static ws_status seg_small_finish(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int NL, int32_t* levels,
+                                  int64_t* counts, cudaStream_t st) {
+  WS_CUDA(cudaStreamSynchronize(st));
+  const char* hp = reinterpret_cast<const char*>(ctx->pinned);
+  int64_t R;
+  const int* fi = reinterpret_cast<const int*>(hp);
+  const unsigned long long* lv = reinterpret_cast<const unsigned long long*>(hp + 256);
+  const unsigned long long* pc = reinterpret_cast<const unsigned long long*>(hp + 256 + 2 * LVC * 8);
+  if (fi[1]) {
+    set_error(WS_ERR_LIMIT, "a non-minimal plateau is deeper than 2^26-2 voxels");
+    return WS_ERR_LIMIT;
+  }
+  const long long npairs = fi[10], pcap = (long long)(ctx->upairs.bytes / sizeof(int2));
+  const unsigned long long E = *reinterpret_cast<const unsigned long long*>(hp + 136);
+  if (npairs > pcap || (long long)E > ctx->wf.E) return run_segment_impl(ctx, I, g, conn, NL, levels, counts, st, false);
+  R = (int64_t)lv[0];
+  ctx->stats.n_regions = R;
+  ctx->stats.n_edges = (int64_t)E;
+  if (ctx->stats.plateau_rounds < 0) ctx->stats.plateau_rounds = 1 + fi[24];  // the cooperative rounds
+  ctx->stats.level_counts[0] = R;
+  ctx->stats.level_edges[1] = (int64_t)E;
+  ctx->stats.edge_chunks_max = (int32_t)pc[1];
+  ctx->stats.rag_global_emits = (int64_t)pc[2];
+  ctx->stats.rag_records = (int64_t)pc[3];
+  if (counts) counts[0] = R;
+  long long prev = R;
+  ctx->wf.lv = 0;
+  for (int k = 1; k < NL && k < LVC; ++k) {
+    const long long c = (long long)lv[k];
+    if (c < prev) ctx->wf.lv = k;
+    prev = c;
+    if (counts) counts[k] = c;
+    if (k < 16) ctx->stats.level_counts[k] = c;
+    if (k >= 2 && k < 16) ctx->stats.level_edges[k] = (long long)lv[LVC + k];
+  }
+  ctx->wf.prev = prev;
   ctx->stats.waterfall_levels = ctx->wf.lv;
   return WS_OK;
+}
+
+ws_status run_segment(ws_ctx* ctx, const uint8_t* I, const Geo& g, int conn, int NL, int32_t* levels,
+                      int64_t* counts, cudaStream_t st) {
+  if (NL > LVC) {
+    set_error(WS_ERR_LIMIT, "ws_segment: NL must be <= %d", LVC);
+    return WS_ERR_LIMIT;
+  }
+  if ((reinterpret_cast<uintptr_t>(levels) & 15) != 0) {
+    set_error(WS_ERR_INVALID, "ws_segment: levels must be 16-byte aligned");
+    return WS_ERR_INVALID;
+  }
+  const bool small = segment_small(g, conn) && ctx->coop;
+  if (!small) return run_segment_impl(ctx, I, g, conn, NL, levels, counts, st, false);
+  // small: replay the captured call while the arguments stay the same; capture it on the
+  // second call with these arguments (the first one sized every workspace buffer, so the
+  // capture allocates nothing); per-phase timing keeps the direct path
+  ws_ctx::SegGraph& G = ctx->sg;
+  const bool same = G.I == I && G.levels == levels && G.st == st && G.n0 == g.n0 && G.n1 == g.n1 &&
+                    G.n2 == g.n2 && G.conn == conn && G.NL == NL && G.last_call == ctx->calls - 1;
+  const char* ng = getenv("WS_NO_GRAPH");
+  const bool graphs = !(ng && ng[0] == '1') && !ctx->timing && !G.failed;
+  if (!same) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    G = ws_ctx::SegGraph();
+    G.I = I;
+    G.levels = levels;
+    G.st = st;
+    G.n0 = g.n0;
+    G.n1 = g.n1;
+    G.n2 = g.n2;
+    G.conn = conn;
+    G.NL = NL;
+  }
+  G.last_call = ctx->calls;
+  if (graphs && G.exec) {
+    WS_CUDA(cudaGraphLaunch(G.exec, st));
+    ctx->stats.kernel_launches = G.launches;
+    ctx->stats.plateau_rounds = -1;
+    ctx->stats.union_order = 0;
+    ctx->total_launches += G.launches;
+    return seg_small_finish(ctx, I, g, conn, NL, levels, counts, st);
+  }
+  if (graphs && G.seen >= 1) {
+    cudaGraph_t graph = nullptr;
+    const int64_t l0 = ctx->stats.kernel_launches;
+    if (!ctx->cap_st) cudaStreamCreateWithFlags(&ctx->cap_st, cudaStreamNonBlocking);
+    const cudaError_t eb = ctx->cap_st ? cudaStreamBeginCapture(ctx->cap_st, cudaStreamCaptureModeRelaxed)
+                                       : cudaErrorInvalidResourceHandle;
+    if (eb == cudaSuccess) {
+      const ws_status s = run_segment_impl(ctx, I, g, conn, NL, levels, counts, ctx->cap_st, true, true);
+      const cudaError_t e = cudaStreamEndCapture(ctx->cap_st, &graph);
+      if (getenv("WS_DEBUG_GRAPH"))
+        fprintf(stderr, "ws_segment capture: status %d (%s) end %s\n", (int)s, ws_last_error(), cudaGetErrorString(e));
+      if (s == WS_OK && e == cudaSuccess && graph &&
+          cudaGraphInstantiate(&G.exec, graph, 0) == cudaSuccess) {
+        cudaGraphDestroy(graph);
+        G.launches = ctx->stats.kernel_launches - l0;
+        WS_CUDA(cudaGraphLaunch(G.exec, st));
+        return seg_small_finish(ctx, I, g, conn, NL, levels, counts, st);
+      }
+      if (graph) cudaGraphDestroy(graph);
+    }
+    if (getenv("WS_DEBUG_GRAPH")) fprintf(stderr, "ws_segment capture failed (begin %s)\n", cudaGetErrorString(eb));
+    (void)cudaGetLastError();  // capture unsupported here: stay on the direct path
+    G.exec = nullptr;
+    G.failed = 1;
+    begin_call_stats(ctx, g);
+  }
+  ++G.seen;
+  return run_segment_impl(ctx, I, g, conn, NL, levels, counts, st, true);
 }
 
 // ------------------------------------------------- 16-bit waterfall (ws_waterfall_u16)

@@ -892,7 +892,9 @@ __global__ void k_union(const Px* __restrict__ I, int* P, Geo g) {
 }
 
 // step IV Union on the cross-tile pairs k_resolve listed (the in-tile ones are merged there)
-__global__ void k_union_pairs(int* P, const int2* __restrict__ pairs, int n) {
+// nptr != nullptr: the count is k_resolve's device counter (clipped to the list capacity n)
+__global__ void k_union_pairs(int* P, const int2* __restrict__ pairs, int n, const int* nptr = nullptr) {
+  if (nptr) n = min(*nptr, n);
   for (int i = blockIdx.x * NT + threadIdx.x; i < n; i += gridDim.x * NT) {
     const int2 e = pairs[i];
     if (ld_cg(P + e.x) != ld_cg(P + e.y)) uf_unite(P, e.x, e.y);
@@ -998,14 +1000,16 @@ static int grid1d(long long n, int sms, int per_sm = 8) {
 
 template <int CONN>
 static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* L, const TileGrid& tg,
-                               const Maps& mp, cudaStream_t st) {
+                               const Maps& mp, cudaStream_t st, bool small = false) {
   WS_TRY(ctx->flags.ensure(256, "flags"));
   WS_TRY(ctx->tiles.ensure((size_t)tg.n * 3, "tile flags"));
   int* flags = ctx->flags.as<int>();
   uint8_t* cur = ctx->tiles.as<uint8_t>();
   uint8_t* next = cur + tg.n;
   uint8_t* hasplat = next + tg.n;
-  WS_TRY(ctx->tlist.ensure((size_t)tg.n * sizeof(int), "active tile list"));
+  // two lists (the cooperative loop ping-pongs); sized BEFORE k_tile_list writes the first:
+  // a later ensure() may re-allocate (no copy)
+  WS_TRY(ctx->tlist.ensure((size_t)tg.n * 2 * sizeof(int), "active tile lists"));
   int* list = ctx->tlist.as<int>();
   const int gl = std::max(1, std::min((tg.n + NT - 1) / NT, ctx->num_sms * 8));
   WS_CUDA(cudaMemsetAsync(flags, 0, 5 * sizeof(int), st));
@@ -1024,9 +1028,28 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
                     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relax_loop<CONN>, NT, 0) == cudaSuccess &&
                     occ > 0;
   const int wave = occ * ctx->num_sms;
-  if (coop) {
-    WS_TRY(ctx->tlist.ensure((size_t)tg.n * 2 * sizeof(int), "active tile lists"));
-    list = ctx->tlist.as<int>();
+  // small inputs (every tile list fits one wave): all rounds after the first in the
+  // cooperative kernel straight away, no host read (the depth-limit flag and the round
+  // count are read with the call's final counts)
+  if (small && coop && tg.n <= wave) {
+    int* list1 = list + tg.n;
+    int* ls = flags + 20;
+    WS_CUDA(cudaMemsetAsync(ls, 0, 5 * sizeof(int), st));
+    WS_CUDA(cudaMemcpyAsync(ls + 2, flags + 4, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    const int grid = std::max(1, std::min(tg.n, wave));
+    CUtensorMap mI = mp.mI, mL = mp.mL;
+    int tma = mp.tma, ntx = tg.ntx, nty = tg.nty, ntiles = tg.n, maxr = g.N + 2;
+    Geo gg = g;
+    int32_t* LL = L;
+    const Px* II = grad;
+    void* args[] = {&mI, &mL, &tma, &II, &LL, &gg, &ntx, &nty, &ntiles, &next, &hasplat, &flags, &ls, &list, &list1,
+                    &maxr};
+    WS_CUDA(cudaLaunchCooperativeKernel((const void*)k_relax_loop<CONN>, dim3(grid), dim3(NT), args, 0, st));
+    launched(ctx, PH_WS_RELAX);
+    ctx->stats.plateau_rounds = -1;  // filled from ls[4] by the final read
+    tmark(ctx, st, PH_WS_RELAX);
+    WS_CUDA(cudaGetLastError());
+    return WS_OK;
   }
   while (true) {
     WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 5 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1107,12 +1130,12 @@ static ws_status pair_out(ws_ctx* ctx, const Geo& g, PairOut& po, cudaStream_t s
 // ctx->repbits (N/32 + 1 words) has bit c set for every canonical label c.
 template <int CONN>
 static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t* L, int64_t* num_regions,
-                             cudaStream_t st, bool relabel = true) {
+                             cudaStream_t st, bool relabel = true, bool small = false) {
   const TileGrid tg = tiles_of<CONN>(g);
   Maps mp;
   make_maps<CONN>(grad, L, g, mp);
   ctx->stats.tma = mp.tma;
-  WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, mp, st));
+  WS_TRY(plateau_phase<CONN>(ctx, grad, g, L, tg, mp, st, small));
   WS_TRY(ctx->aux.ensure((size_t)g.N * sizeof(int), "aux"));
   int* P = ctx->aux.as<int>();
   PairOut po;
@@ -1125,7 +1148,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   // inside the tiles and left every minimal voxel pointing at its in-tile root), then step III
   // across tiles: the chase ends at the FINAL roots, whose minima k_jump folds directly
   size_t cap = ctx->roots.bytes / sizeof(int);
-  const size_t want = (size_t)g.N / 16 + 1024;
+  const size_t want = small ? (size_t)g.N + 1024 : (size_t)g.N / 16 + 1024;  // small: never overflows
   if (cap < want) {
     WS_TRY(ctx->roots.ensure(want * sizeof(int), "roots"));
     WS_TRY(ctx->rootc.ensure(want * sizeof(int), "root labels"));
@@ -1142,6 +1165,25 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   }
   WS_CUDA(cudaMemsetAsync(nr, 0, sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(nfinal, 0, sizeof(unsigned long long), st));
+  if (small) {
+    // sync-free (ws_segment on small inputs): unions first with the device pair count, the
+    // chase, the root labels; a pair-list overflow is detected by the call's final read
+    // (which then redoes the call on the regular path)
+    k_union_pairs<<<grid1d(std::min<long long>(po.cap, g.N / 8 + 1), ctx->num_sms), NT, 0, st>>>(
+        P, po.pairs, po.cap, po.npairs);
+    launched(ctx, PH_WS_UNION);
+    tmark(ctx, st, PH_WS_UNION);
+    k_jump<<<grid1d(g.N, ctx->num_sms), NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
+    launched(ctx, PH_WS_JUMP);
+    tmark(ctx, st, PH_WS_JUMP);
+    k_root_canon<<<grid1d((long long)g.N / 32, ctx->num_sms), NT, 0, st>>>(P, L, ctx->roots.as<int>(), nr, (int)cap,
+                                                                          bits);
+    launched(ctx, PH_WS_FIND);
+    tmark(ctx, st, PH_WS_FIND);
+    ctx->stats.union_order = 0;
+    WS_CUDA(cudaGetLastError());
+    return WS_OK;
+  }
   WS_CUDA(cudaMemcpyAsync(ctx->pinned, po.npairs, sizeof(int), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaStreamSynchronize(st));
   const int n_pairs = (int)reinterpret_cast<const int*>(ctx->pinned)[0];
@@ -1371,12 +1413,12 @@ ws_status resolve_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, con
 #endif  // !WS_PX16
 
 ws_status run_watershed(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* labels,
-                        int64_t* num_regions, cudaStream_t st, bool relabel) {
+                        int64_t* num_regions, cudaStream_t st, bool relabel, bool small) {
   switch (conn) {
-    case 4: return watershed_t<4>(ctx, grad, g, labels, num_regions, st, relabel);
-    case 8: return watershed_t<8>(ctx, grad, g, labels, num_regions, st, relabel);
-    case 6: return watershed_t<6>(ctx, grad, g, labels, num_regions, st, relabel);
-    case 26: return watershed_t<26>(ctx, grad, g, labels, num_regions, st, relabel);
+    case 4: return watershed_t<4>(ctx, grad, g, labels, num_regions, st, relabel, small);
+    case 8: return watershed_t<8>(ctx, grad, g, labels, num_regions, st, relabel, small);
+    case 6: return watershed_t<6>(ctx, grad, g, labels, num_regions, st, relabel, small);
+    case 26: return watershed_t<26>(ctx, grad, g, labels, num_regions, st, relabel, small);
   }
   set_error(WS_ERR_INVALID, "connectivity must be 4, 8, 6 or 26");
   return WS_ERR_INVALID;
