@@ -716,7 +716,11 @@ def run_ours(args):
         barrier(world)
         ems = max_over_ranks(a.elapsed_time(b) / args.e2e_steps, world)
         e2e = {"value": N * world / (ems / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": N,
-               "d2h_bytes_per_step": NL * N * 4, "ms_per_step": ems, "api": "ws_segment_host"}
+               "d2h_bytes_per_step": NL * N * 4, "ms_per_step": ems, "api": "ws_segment_host",
+               "pcie_GBps": (N + NL * N * 4) / (ems / 1e3) / 1e9,
+               "note": "host-to-device grad + device-to-host NL i32 level arrays per step: PCIe-bound "
+                       "(the levels are %.1f GB; the device step is %.1f ms of the %.1f ms)" % (
+                           NL * N * 4 / 1e9, ms, ems)}
         del gh, lh
 
     cpu = None

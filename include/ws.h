@@ -285,8 +285,12 @@ ws_status ws_shard_relabel(ws_ctx* ctx, const int32_t* P_ext, int32_t* L_ext, co
 
 /* z-slab sharded waterfall (same slabs; labels_own = ws_shard_relabel output).
  * Dense ids follow the rank order: doff = owned representatives (ws_shard_relabel nreps) of
- * all lower ranks; R = all ranks' total.  dense_of: i32[D*n1*n2] indexed by GLOBAL label
- * (device, sparse: only labels met by this rank are written).  rep_of: i32[R] (device); this
+ * all lower ranks; R = all ranks' total.  dense_of: the slab's WINDOW of dense ids, i32[(z1 -
+ * z0 + 1) * n1 * n2] (device): entry i = dense id of global label z0*n1*n2 + i (the owned
+ * planes and the plane above; sparse: only labels met by this rank are written).  Labels
+ * below the window (regions crossing the lower cut, at most two planes of them) are kept in
+ * a small map in the context (filled by ws_shard_wf_bfill), so no rank holds a global-size
+ * array.  rep_of: i32[R] (device); this
  * rank writes its segment [doff, doff + count), the caller reduces (max) it over ranks with
  * the other entries at -1.  btable: i32[4*n1*n2]: (label, dense id if owned here else -1) of
  * the first and last owned plane; ws_shard_wf_bfill gives every rank the dense ids of all
@@ -296,7 +300,7 @@ ws_status ws_shard_wf_dense(ws_ctx* ctx, const int32_t* labels_own, ws_dims dims
 ws_status ws_shard_wf_btable(ws_ctx* ctx, const int32_t* labels_own, const int32_t* dense_of, ws_dims dims_ext,
                              ws_slab slab, int32_t* btable, void* stream);
 ws_status ws_shard_wf_bfill(ws_ctx* ctx, const int32_t* btables_all, int32_t nranks, ws_dims dims_ext,
-                            int32_t* dense_of, void* stream);
+                            ws_slab slab, int32_t* dense_of, void* stream);
 /* RAG of the owned planes plus the cut pairs with the rank above (labels_ext: owned planes and
  * the plane above, extended layout); best_out: i64[R] this rank's level-1 minima */
 ws_status ws_shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* grad_ext, ws_dims dims_ext,

@@ -128,7 +128,7 @@ def load(path: str = SO_PATH):
         lib.ws_shard_relabel.argtypes = [vp, vp, vp, vp, WsDims, WsSlab, vp, vp, vp]
         lib.ws_shard_wf_dense.argtypes = [vp, vp, WsDims, WsSlab, i64, vp, vp, vp, vp]
         lib.ws_shard_wf_btable.argtypes = [vp, vp, vp, WsDims, WsSlab, vp, vp]
-        lib.ws_shard_wf_bfill.argtypes = [vp, vp, i32, WsDims, vp, vp]
+        lib.ws_shard_wf_bfill.argtypes = [vp, vp, i32, WsDims, WsSlab, vp, vp]
         lib.ws_shard_wf_begin.argtypes = [vp, vp, vp, WsDims, i32, WsSlab, vp, i64, i32, vp, vp]
         lib.ws_shard_wf_step.argtypes = [vp, vp, vp, vp, pi32, vp]
         lib.ws_shard_wf_end.argtypes = [vp, vp, vp, vp, WsDims, i32, WsSlab, vp, vp]

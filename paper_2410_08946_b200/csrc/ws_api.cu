@@ -237,7 +237,7 @@ ws_status ws_ctx_destroy(ws_ctx* ctx) {
                      &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc, &ctx->best_lo, &ctx->repbits,
                      &ctx->sh_L, &ctx->sh_P, &ctx->sh_planes, &ctx->sh_tab, &ctx->sh_alltab, &ctx->sh_ec, &ctx->sh_lab,
                      &ctx->sh_dense, &ctx->sh_rep, &ctx->sh_bt, &ctx->sh_allbt, &ctx->sh_lext, &ctx->sh_best,
-                     &ctx->sh_nxt, &ctx->sh_small};
+                     &ctx->sh_nxt, &ctx->sh_small, &ctx->fmap};
   for (auto* b : bufs) b->release();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->sh_small_h) cudaFreeHost(ctx->sh_small_h);
@@ -606,11 +606,14 @@ ws_status ws_shard_wf_btable(ws_ctx* ctx, const int32_t* labels_own, const int32
                          (cudaStream_t)stream);
 }
 
-ws_status ws_shard_wf_bfill(ws_ctx* ctx, const int32_t* btables_all, int32_t nranks, ws_dims dims, int32_t* dense_of,
-                            void* stream) {
+ws_status ws_shard_wf_bfill(ws_ctx* ctx, const int32_t* btables_all, int32_t nranks, ws_dims dims, ws_slab slab,
+                            int32_t* dense_of, void* stream) {
   WS_TRY(check_ctx(ctx));
+  Geo g;
+  WS_TRY(check_slab(dims, slab, 6, &g));
   if (!btables_all || !dense_of || nranks < 1) return null_arg("btables_all/dense_of");
-  return shard_wf_bfill(ctx, btables_all, nranks, (int)(dims.n1 * dims.n2), dense_of, (cudaStream_t)stream);
+  return shard_wf_bfill(ctx, btables_all, nranks, g.plane, (int)(slab.z0 * g.plane), (int)((slab.z1 + 1) * g.plane),
+                        dense_of, (cudaStream_t)stream);
 }
 
 ws_status ws_shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* grad_ext, ws_dims dims,

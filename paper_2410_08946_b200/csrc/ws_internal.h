@@ -52,6 +52,8 @@ struct WSState {
   // sync-free ws_segment (small inputs): R and E stay on the device (R, E above are bounds)
   const unsigned long long* Rdev = nullptr;
   const unsigned long long* Edev = nullptr;
+  // sharded dense ids: the slab's label window [dlo, dhi) and the foreign map (ctx->fmap)
+  int dlo = 0, dhi = 0, fbits = 4;
 };
 
 struct ws_ctx {
@@ -79,6 +81,7 @@ struct ws_ctx {
   int shard_nroots = 0;
   int seg_nroots = 0;     // ws_segment: listed roots left by the watershed (ctx->roots)
   ws::Buf repbits;        // u32[N/32+1] ws_segment: bit c set <=> c is a canonical label
+  ws::Buf fmap;           // u64 slots: foreign labels -> dense ids (sharded waterfall)
   int shard_conn = 6;     // connectivity of the last ws_shard_local (6 or 26)
   int shard_tiles = 0;    // tile count of the current sharded plateau phase
   int shard_flip = 0;     // which tile-flag buffer holds "next"
@@ -190,7 +193,8 @@ ws_status shard_wf_dense(ws_ctx* ctx, const int32_t* labels_own, int n, int pofs
                          int* rep_of_global, int64_t* count, cudaStream_t st);
 ws_status shard_wf_btable(ws_ctx* ctx, const int32_t* labels_own, int nplanes, int plane, int pofs, const int* dense_of,
                           int32_t* out, cudaStream_t st);
-ws_status shard_wf_bfill(ws_ctx* ctx, const int32_t* tabs, int K, int plane, int* dense_of, cudaStream_t st);
+ws_status shard_wf_bfill(ws_ctx* ctx, const int32_t* tabs, int K, int plane, int lo, int hi, int* dense_of,
+                         cudaStream_t st);
 ws_status shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* I_ext, const Geo& g, int conn,
                          const int* dense_of, int64_t R, int NL, uint64_t* best_out, cudaStream_t st);
 ws_status shard_wf_step(ws_ctx* ctx, const uint64_t* best_in, uint64_t* best_out, int64_t* count, int* more,

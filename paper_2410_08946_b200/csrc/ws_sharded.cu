@@ -238,7 +238,7 @@ ws_status sharded_waterfall(ws_ctx* ctx, const ws_transport* tr, const uint8_t* 
                             int conn, int NL, const int32_t* labels_own, int64_t nreps, int32_t* levels_own,
                             int64_t* counts, cudaStream_t st) {
   const int K = tr->nranks, r = tr->rank;
-  const int64_t plane = d.n1 * d.n2, next = d.n0 * plane, nglob = sl.D * plane;
+  const int64_t plane = d.n1 * d.n2, next = d.n0 * plane;
   const int zlo = (int)(sl.z0 - sl.e0), zhi = (int)(sl.z1 - sl.e0);
   Small s;
   WS_TRY(small_of(ctx, K, s));
@@ -250,7 +250,7 @@ ws_status sharded_waterfall(ws_ctx* ctx, const ws_transport* tr, const uint8_t* 
     R += cnt[q];
   }
   // dense ids in rank order; rep_of reduced (max) over the ranks (other entries -1)
-  WS_TRY(ctx->sh_dense.ensure((size_t)nglob * 4, "dense_of"));
+  WS_TRY(ctx->sh_dense.ensure((size_t)(sl.z1 - sl.z0 + 1) * plane * 4, "dense-id window"));
   WS_TRY(ctx->sh_rep.ensure((size_t)std::max<int64_t>(R, 1) * 4, "rep_of"));
   int32_t* dense_of = ctx->sh_dense.as<int32_t>();
   int32_t* rep_of = ctx->sh_rep.as<int32_t>();
@@ -263,7 +263,7 @@ ws_status sharded_waterfall(ws_ctx* ctx, const ws_transport* tr, const uint8_t* 
   WS_TRY(ctx->sh_allbt.ensure((size_t)plane * 4 * 4 * K, "gathered boundary dense tables"));
   WS_TRY(ws_shard_wf_btable(ctx, labels_own, dense_of, d, sl, ctx->sh_bt.as<int32_t>(), st));
   TR_TRY(tr->allgather(tr->user, ctx->sh_bt.p, ctx->sh_allbt.p, plane * 4 * 4, st), "allgather(dense tables)");
-  WS_TRY(ws_shard_wf_bfill(ctx, ctx->sh_allbt.as<int32_t>(), K, d, dense_of, st));
+  WS_TRY(ws_shard_wf_bfill(ctx, ctx->sh_allbt.as<int32_t>(), K, d, sl, dense_of, st));
   // labels of the owned planes + the first plane of the rank above (the cut pairs)
   WS_TRY(ctx->sh_lext.ensure((size_t)next * 4, "extended labels"));
   WS_TRY(ctx->sh_planes.ensure((size_t)plane * 4 * 2, "halo planes"));

@@ -59,7 +59,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int* smem, int& total) {
 // dense ids keep the canonical label order, C14), publishes its aggregate, then warp 0 looks
 // back over 32 predecessors at a time until an inclusive prefix is found.
 // pofs: label value of a representative at local index 0 (global index of local voxel 0);
-// doff: dense id of this call's first representative (z-slab sharding; 0 / 0 otherwise).
+// doff: dense id of this call's first representative (z-slab sharding; 0 / 0 otherwise);
+// dense_of (sharded) is the slab's window, indexed by label - pofs.
 // rk != nullptr (unsharded): instead of dense_of, the rank structure rk[w] = (dense id of the
 // first representative at or after voxel 32 w, bit mask of the representatives among voxels
 // 32 w .. 32 w + 31) is written: dense(l) = rk[l/32].x + popc(rk[l/32].y & ((1 << l%32) - 1)).
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
     while (m) {
       const int u = __ffs(m) - 1;
       m &= m - 1;
-      if (!rk) dense_of[p0 + u + pofs] = d + doff;
+      if (!rk) dense_of[p0 + u] = d + doff;  // sharded: the slab's window, index = label - pofs
       if (d < rep_cap) rep_of[d] = p0 + u + pofs;
       ++d;
     }
@@ -165,23 +166,46 @@ __global__ void __launch_bounds__(NTW) k_dense(const int* __restrict__ labels, i
 // waterfall (RAG, level materialisation) reads D instead of labels, so no per-voxel or
 // per-edge dense_of gather remains on the hot path.  Each thread maps 4 consecutive voxels;
 // equal neighbours (the common case: regions are runs along x) reuse the previous gather.
+// Sharded dense ids (z-slab waterfall): labels in the slab's window [lo, hi) (its own planes
+// and the plane above) index the window array; the few labels below it (regions that cross
+// the slab's lower cut, all listed in the gathered boundary tables) live in a small
+// open-addressing map of 64-bit slots (label << 32 | dense id), empty = ~0.
+struct DenseMap {
+  const int* win;                   // dense id of label lo + i
+  int lo, hi;
+  const unsigned long long* fmap;   // foreign labels
+  int fbits;                        // log2 of the map's slot count
+};
+
+__device__ __forceinline__ uint32_t fmap_hash(int l, int bits) { return ((uint32_t)l * 0x9E3779B1u) >> (32 - bits); }
+
+__device__ __forceinline__ int dense_lookup(const DenseMap& m, int l) {
+  if (l >= m.lo && l < m.hi) return __ldg(m.win + (l - m.lo));
+  const uint32_t mask = (1u << m.fbits) - 1;
+  for (uint32_t h = fmap_hash(l, m.fbits);; h = (h + 1) & mask) {
+    const unsigned long long v = __ldg(m.fmap + h);
+    if (v == ~0ull) return -1;  // not a label of this slab (never met on valid input)
+    if ((int)(v >> 32) == l) return (int)(unsigned)v;
+  }
+}
+
 // vec == 0 (labels or D not 16-byte aligned): scalar accesses only.
-__global__ void __launch_bounds__(NTW) k_dimage(const int* __restrict__ labels, const int* __restrict__ dense_of,
-                                                 long long n, int* __restrict__ D, int vec) {
+__global__ void __launch_bounds__(NTW) k_dimage(const int* __restrict__ labels, DenseMap m, long long n,
+                                                 int* __restrict__ D, int vec) {
   const long long n4 = vec ? n >> 2 : 0;
   const int4* L4 = reinterpret_cast<const int4*>(labels);
   int4* D4 = reinterpret_cast<int4*>(D);
   for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n4; i += (long long)gridDim.x * NTW) {
     const int4 v = __ldcs(L4 + i);
     int4 d;
-    d.x = __ldg(dense_of + v.x);
-    d.y = v.y == v.x ? d.x : __ldg(dense_of + v.y);
-    d.z = v.z == v.y ? d.y : __ldg(dense_of + v.z);
-    d.w = v.w == v.z ? d.z : __ldg(dense_of + v.w);
+    d.x = dense_lookup(m, v.x);
+    d.y = v.y == v.x ? d.x : dense_lookup(m, v.y);
+    d.z = v.z == v.y ? d.y : dense_lookup(m, v.z);
+    d.w = v.w == v.z ? d.z : dense_lookup(m, v.w);
     D4[i] = d;
   }
   for (long long p = (n4 << 2) + blockIdx.x * (long long)NTW + threadIdx.x; p < n; p += (long long)gridDim.x * NTW)
-    D[p] = __ldg(dense_of + labels[p]);
+    D[p] = dense_lookup(m, labels[p]);
 }
 
 // the same from the rank structure of k_dense (unsharded calls)
@@ -982,7 +1006,8 @@ static ws_status wf_rag(ws_ctx* ctx, const int32_t* labels, const Px* I, const G
     if (rk) {  // unsharded: the rank structure of k_dense
       k_dimage_rk<<<grid_for(al ? n / 4 + 1 : n, ctx->num_sms), NTW, 0, st>>>(labels + o, rk, n, D + o, al ? 1 : 0);
     } else {
-      k_dimage<<<grid_for(al ? n / 4 + 1 : n, ctx->num_sms), NTW, 0, st>>>(labels + o, dense_of, n, D + o, al ? 1 : 0);
+      const DenseMap m{dense_of, ctx->wf.dlo, ctx->wf.dhi, ctx->fmap.as<unsigned long long>(), ctx->wf.fbits};
+      k_dimage<<<grid_for(al ? n / 4 + 1 : n, ctx->num_sms), NTW, 0, st>>>(labels + o, m, n, D + o, al ? 1 : 0);
     }
     launched(ctx, PH_WF_DENSE);
     ctx->wf.dofs = (long long)o;
@@ -1616,17 +1641,31 @@ __global__ void k_wf_btable(const int* __restrict__ labels_own, int nplanes, int
     const int z = s == 0 ? 0 : nplanes - 1;
     const int l = labels_own[(size_t)z * plane + xy];
     out[i] = l;
-    out[2 * plane + i] = (l >= pofs_lo && l < pofs_hi) ? dense_of[l] : -1;
+    out[2 * plane + i] = (l >= pofs_lo && l < pofs_hi) ? dense_of[l - pofs_lo] : -1;
   }
 }
 
-__global__ void k_wf_bfill(const int* __restrict__ tabs, int K, int plane, int* dense_of) {
+// every gathered (label, dense id) with a dense id: into the slab's window, or into the
+// foreign map if below it (a label of a region crossing the lower cut); others are not met here
+__global__ void k_wf_bfill(const int* __restrict__ tabs, int K, int plane, int* win, int lo, int hi,
+                           unsigned long long* fmap, int fbits) {
   const long long n = (long long)K * 2 * plane;
+  const uint32_t mask = (1u << fbits) - 1;
   for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n; i += (long long)gridDim.x * NTW) {
     const long long r = i / (2 * plane), j = i % (2 * plane);
     const int* t = tabs + r * 4 * plane;
     const int d = t[2 * plane + j];
-    if (d >= 0) dense_of[t[j]] = d;
+    if (d < 0) continue;
+    const int l = t[j];
+    if (l >= lo && l < hi) {
+      win[l - lo] = d;
+    } else if (l < lo) {
+      const unsigned long long v = ((unsigned long long)(unsigned)l << 32) | (unsigned)d;
+      for (uint32_t h = fmap_hash(l, fbits);; h = (h + 1) & mask) {
+        const unsigned long long cur = atomicCAS(fmap + h, ~0ull, v);
+        if (cur == ~0ull || (int)(cur >> 32) == l) break;  // inserted / already there (same d)
+      }
+    }
   }
 }
 
@@ -1651,8 +1690,17 @@ ws_status shard_wf_btable(ws_ctx* ctx, const int32_t* labels_own, int nplanes, i
   return WS_OK;
 }
 
-ws_status shard_wf_bfill(ws_ctx* ctx, const int32_t* tabs, int K, int plane, int* dense_of, cudaStream_t st) {
-  k_wf_bfill<<<grid_for((long long)K * 2 * plane, ctx->num_sms), NTW, 0, st>>>(tabs, K, plane, dense_of);
+ws_status shard_wf_bfill(ws_ctx* ctx, const int32_t* tabs, int K, int plane, int lo, int hi, int* dense_of,
+                         cudaStream_t st) {
+  int bits = 4;
+  while ((1ll << bits) < 4ll * plane) ++bits;  // 2 planes of foreign labels at most, load <= 1/2
+  WS_TRY(ctx->fmap.ensure(((size_t)1 << bits) * sizeof(unsigned long long), "foreign dense-id map"));
+  WS_CUDA(cudaMemsetAsync(ctx->fmap.p, 0xFF, ((size_t)1 << bits) * sizeof(unsigned long long), st));
+  ctx->wf.dlo = lo;
+  ctx->wf.dhi = hi;
+  ctx->wf.fbits = bits;
+  k_wf_bfill<<<grid_for((long long)K * 2 * plane, ctx->num_sms), NTW, 0, st>>>(tabs, K, plane, dense_of, lo, hi,
+                                                                              ctx->fmap.as<unsigned long long>(), bits);
   launched(ctx, PH_WF_DENSE);
   WS_CUDA(cudaGetLastError());
   return WS_OK;

@@ -267,7 +267,7 @@ def sharded_waterfall(tr, ctxs, slabs, grads_ext, labels_own, nreps, NL: int, co
     dev = grads_ext[0].device
     cnt_all = tr.allgather_i64([nreps[i] for i in range(len(slabs))])
     R = int(sum(cnt_all[0]))
-    dense_of = [torch.empty(N, dtype=torch.int32, device=dev) for _ in slabs]
+    dense_of = [torch.empty((s.z1 - s.z0 + 1) * plane, dtype=torch.int32, device=dev) for s in slabs]  # window
     rep_of = [torch.full((R,), -1, dtype=torch.int32, device=dev) for _ in slabs]
     for i, s in enumerate(slabs):
         doff = int(sum(cnt_all[i][:s.rank]))
@@ -281,8 +281,8 @@ def sharded_waterfall(tr, ctxs, slabs, grads_ext, labels_own, nreps, NL: int, co
                                         s.c(), _b.ptr(bt[i]), _stream()))
     allbt = tr.allgather(bt)
     for i, s in enumerate(slabs):
-        _b.check(lib.ws_shard_wf_bfill(ctxs[i].handle, _b.ptr(allbt[i]), K, _dims(s, n1, n2), _b.ptr(dense_of[i]),
-                                       _stream()))
+        _b.check(lib.ws_shard_wf_bfill(ctxs[i].handle, _b.ptr(allbt[i]), K, _dims(s, n1, n2), s.c(),
+                                       _b.ptr(dense_of[i]), _stream()))
     # labels of the owned planes plus the first plane of the rank above (cut pairs)
     send_lo = [lo[0].contiguous() if s.rank > 0 else None for lo, s in zip(labels_own, slabs)]
     send_hi = [lo[-1].contiguous() if s.rank < K - 1 else None for lo, s in zip(labels_own, slabs)]
