@@ -5,9 +5,9 @@ for t in memcheck initcheck synccheck; do
   timeout 1500 compute-sanitizer --tool $t python tools/sanitize_run.py > gpurun_out/san_$t.log 2>&1
   echo "$t: $(grep 'ERROR SUMMARY' gpurun_out/san_$t.log | tail -1)" >> $O
 done
-timeout 2400 compute-sanitizer --tool racecheck --racecheck-report hazard python tools/sanitize_run.py > gpurun_out/san_racecheck.log 2>&1
-echo "racecheck (shared-memory hazards, grouped by source line):" >> $O
-grep -o "Race reported between [A-Za-z]* access at .* in [a-z_0-9]*\.cu[h]*:[0-9]*" gpurun_out/san_racecheck.log | sed 's/(.*)//' | sort | uniq -c | sort -rn | head -20 >> $O
+timeout 2400 compute-sanitizer --tool racecheck --racecheck-report analysis --print-limit 100000 python tools/sanitize_run.py > gpurun_out/san_racecheck.log 2>&1
+echo "racecheck (analysis mode: every reported race, grouped by kernel and the two source lines):" >> $O
+python tools/race_group.py gpurun_out/san_racecheck.log >> $O
 grep "RACECHECK SUMMARY" gpurun_out/san_racecheck.log | tail -1 >> $O
 grep -h " ok" gpurun_out/san_memcheck.log >> $O
 cat $O

@@ -32,6 +32,24 @@ for name, shape, conn, nd in (("C1", None, 4, 2), ("C4", (20, 48, 64), 6, 3)):
         assert np.array_equal(torch.cat(labs).cpu().numpy(), ref)
     print(name, "ok", R, c, c2)
 
+# ws_segment: the regular path, the sync-free small mode and its CUDA-graph replays; the
+# library's sharded pipeline with K = 3 thread ranks
+for name, shape, conn, nd in (("C1", None, 4, 2), ("C4", (20, 48, 64), 6, 3), ("C4", (12, 32, 40), 26, 3)):
+    raw = synth.make_config_image(name, device="cuda", shape=shape)
+    q = ws.gradient(raw, 1.0, ndim=nd)
+    qn = q.cpu().numpy()
+    ref = oracle.watershed(qn, conn, ndim=nd)
+    rlv = oracle.waterfall(ref, qn, conn, 6, ndim=nd)[0]
+    ctx = ws.Context()
+    out = torch.empty((6,) + tuple(q.shape), dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        lv, _ = ws.segment(q, conn, 6, ndim=nd, ctx=ctx, out=out)
+        assert np.array_equal(lv.cpu().numpy(), rlv)
+    if nd == 3:
+        lvs, _, _ = shard.segment_threads(3, q, 6, conn)
+        assert np.array_equal(lvs.cpu().numpy(), rlv)
+    print("segment", name, conn, "ok")
+
 # 16-bit images (NEXT f4): gradient (streaming kernel and generic path) + watershed
 rng = np.random.default_rng(7)
 for shape, conn, nd, sig in (((20, 48, 64), 6, 3, 1.0), ((18, 40, 36), 26, 3, 2.0), ((2, 70, 96), 8, 2, 1.0)):
