@@ -199,7 +199,10 @@ ws_status sharded_watershed(ws_ctx* ctx, const ws_transport* tr, const uint8_t* 
     if (has_hi) WS_TRY(ws_shard_halo(ctx, L, d, sl, 1, above, ch_hi, st));
     return WS_OK;
   };
-  // steps I + II: relaxation rounds until no rank has pending work or a changed halo
+  // steps I + II: relaxation rounds until no rank has pending work or a changed halo (the
+  // halo planes start defined: the first exchange compares against them)
+  if (has_lo) WS_CUDA(cudaMemsetAsync(L + (size_t)(zlo - 1) * plane, 0xFF, plane * 4, st));
+  if (has_hi) WS_CUDA(cudaMemsetAsync(L + (size_t)zhi * plane, 0xFF, plane * 4, st));
   int pend = 0, ch_lo = 0, ch_hi = 0;
   WS_TRY(ws_shard_plateau(ctx, grad_ext, d, conn, sl, L, 0, 0, 0, &pend, st));
   WS_TRY(halo(&ch_lo, &ch_hi));

@@ -1012,7 +1012,8 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   WS_TRY(ctx->tlist.ensure((size_t)tg.n * 2 * sizeof(int), "active tile lists"));
   int* list = ctx->tlist.as<int>();
   const int gl = std::max(1, std::min((tg.n + NT - 1) / NT, ctx->num_sms * 8));
-  WS_CUDA(cudaMemsetAsync(flags, 0, 5 * sizeof(int), st));
+  // the whole flag block (later host reads copy ranges of it; every field is defined)
+  WS_CUDA(cudaMemsetAsync(flags, 0, 256, st));
   WS_CUDA(cudaMemsetAsync(next, 0, 2 * (size_t)tg.n, st));  // next and hasplat
   k_relax_first<CONN><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, next, hasplat, flags);
   k_tile_list<<<gl, NT, 0, st>>>(next, hasplat, tg.n, list, flags + 4);
