@@ -380,6 +380,20 @@ ws_status ws_waterfall_sharded(ws_ctx* ctx, const ws_transport* transport, const
 ws_status ws_segment_sharded(ws_ctx* ctx, const ws_transport* transport, const uint8_t* grad_ext, ws_dims dims_ext,
                              ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own, int64_t* counts,
                              int32_t* rounds, void* stream);
+/* 16-bit images (NEXT f4): the same on u16 gradients -- the watershed of
+ * ws_watershed_u16 and the graph waterfall of ws_waterfall_u16 (K = (w:16, ~max, ~min); its
+ * per-component minima are reduced over the ranks in two steps per level, the 16-bit height
+ * and the larger label first, then the smaller label among those).  grad_ext 2-byte aligned;
+ * ws_watershed_u16 / ws_waterfall_u16 on a sharded context run these. */
+ws_status ws_watershed_sharded_u16(ws_ctx* ctx, const ws_transport* transport, const uint16_t* grad_ext,
+                                   ws_dims dims_ext, ws_slab slab, int32_t connectivity, int32_t* labels_own,
+                                   int64_t* num_regions, int32_t* rounds, void* stream);
+ws_status ws_waterfall_sharded_u16(ws_ctx* ctx, const ws_transport* transport, const int32_t* labels_own,
+                                   const uint16_t* grad_ext, ws_dims dims_ext, ws_slab slab, int32_t connectivity,
+                                   int32_t NL, int32_t* levels_own, int64_t* counts, void* stream);
+ws_status ws_segment_sharded_u16(ws_ctx* ctx, const ws_transport* transport, const uint16_t* grad_ext,
+                                 ws_dims dims_ext, ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own,
+                                 int64_t* counts, int32_t* rounds, void* stream);
 
 #ifdef __cplusplus
 }

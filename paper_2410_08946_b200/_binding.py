@@ -24,7 +24,8 @@ EXPORTS = ("ws_ctx_create", "ws_ctx_destroy", "ws_last_error", "ws_version", "ws
            "ws_shard_relabel", "ws_shard_wf_dense", "ws_shard_wf_btable", "ws_shard_wf_bfill", "ws_shard_wf_begin",
            "ws_shard_wf_step", "ws_shard_wf_end",
            "ws_nccl_unique_id", "ws_transport_nccl_create", "ws_transport_nccl_destroy", "ws_ctx_create_sharded",
-           "ws_watershed_sharded", "ws_waterfall_sharded", "ws_segment_sharded")
+           "ws_watershed_sharded", "ws_waterfall_sharded", "ws_segment_sharded", "ws_watershed_sharded_u16",
+           "ws_waterfall_sharded_u16", "ws_segment_sharded_u16")
 
 
 class WsDims(ctypes.Structure):
@@ -140,6 +141,9 @@ def load(path: str = SO_PATH):
         lib.ws_watershed_sharded.argtypes = [vp, ptr_t, vp, WsDims, WsSlab, i32, vp, ctypes.POINTER(i64), pi32, vp]
         lib.ws_waterfall_sharded.argtypes = [vp, ptr_t, vp, vp, WsDims, WsSlab, i32, i32, vp, vp, vp]
         lib.ws_segment_sharded.argtypes = [vp, ptr_t, vp, WsDims, WsSlab, i32, i32, vp, vp, pi32, vp]
+        lib.ws_watershed_sharded_u16.argtypes = lib.ws_watershed_sharded.argtypes
+        lib.ws_waterfall_sharded_u16.argtypes = lib.ws_waterfall_sharded.argtypes
+        lib.ws_segment_sharded_u16.argtypes = lib.ws_segment_sharded.argtypes
         for name in EXPORTS:
             f = getattr(lib, name)
             if name not in ("ws_last_error", "ws_version", "ws_phase_name", "ws_shard_table_bytes"):

@@ -337,6 +337,8 @@ ws_status ws_watershed_u16(ws_ctx* ctx, const uint16_t* grad, ws_dims dims, int3
     return WS_ERR_INVALID;
   }
   begin_call(ctx, g);
+  if (ctx->sharded)
+    return sharded_dispatch_watershed_u16(ctx, grad, dims, connectivity, labels, num_regions, (cudaStream_t)stream);
   tbegin(ctx, (cudaStream_t)stream);
   ws_status s = px16::run_watershed(ctx, grad, g, connectivity, labels, num_regions, (cudaStream_t)stream);
   tfinish(ctx);
@@ -385,6 +387,9 @@ ws_status ws_waterfall_u16(ws_ctx* ctx, const int32_t* labels, const uint16_t* g
     return WS_ERR_INVALID;
   }
   begin_call(ctx, g);
+  if (ctx->sharded)
+    return sharded_dispatch_waterfall_u16(ctx, labels, grad, dims, connectivity, NL, levels, counts,
+                                          (cudaStream_t)stream);
   tbegin(ctx, (cudaStream_t)stream);
   ws_status s = run_waterfall_u16(ctx, labels, grad, g, connectivity, NL, levels, counts, (cudaStream_t)stream);
   tfinish(ctx);

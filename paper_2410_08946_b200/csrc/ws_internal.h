@@ -164,14 +164,32 @@ ws_status sharded_dispatch_segment(ws_ctx* ctx, const uint8_t* grad_ext, const w
                                    int32_t* levels, int64_t* counts, cudaStream_t st);
 ws_status sharded_dispatch_waterfall(ws_ctx* ctx, const int32_t* labels_own, const uint8_t* grad_ext, const ws_dims& d,
                                      int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st);
+ws_status sharded_dispatch_watershed_u16(ws_ctx* ctx, const uint16_t* grad_ext, const ws_dims& d, int conn,
+                                         int32_t* labels, int64_t* num_regions, cudaStream_t st);
+ws_status sharded_dispatch_waterfall_u16(ws_ctx* ctx, const int32_t* labels_own, const uint16_t* grad_ext,
+                                         const ws_dims& d, int conn, int NL, int32_t* levels, int64_t* counts,
+                                         cudaStream_t st);
 ws_status run_watershed(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
                         int32_t* labels, int64_t* num_regions, cudaStream_t st, bool relabel = true,
                         bool small = false);
 ws_status run_gradient_u16(ws_ctx* ctx, const uint16_t* img, const Geo& g, int is3d, float sigma,
                            uint16_t* grad_q, float* blur_f32, float* grad_f32, cudaStream_t st);
-namespace px16 {  // ws_watershed16.cu: the same watershed on u16 pixels (unsharded)
+namespace px16 {  // ws_watershed16.cu / ws_shard16.cu: the same watershed on u16 pixels
 ws_status run_watershed(ws_ctx* ctx, const uint16_t* grad, const Geo& g, int conn, int32_t* labels,
                         int64_t* num_regions, cudaStream_t st, bool relabel = true, bool small = false);
+ws_status plateau_first_shard(ws_ctx* ctx, const uint16_t* grad, const Geo& g, int conn, int32_t* L, int* pending,
+                              cudaStream_t st);
+ws_status plateau_round_shard(ws_ctx* ctx, const uint16_t* grad, const Geo& g, int conn, int32_t* L, int act_lo,
+                              int act_hi, int* pending, cudaStream_t st);
+ws_status shard_halo(ws_ctx* ctx, int32_t* L, const Geo& g, int side, const int32_t* plane_in, int32_t* changed,
+                     cudaStream_t st);
+ws_status shard_local(ws_ctx* ctx, const uint16_t* grad, const Geo& g, int conn, int32_t* L, int32_t* P, void* table,
+                      cudaStream_t st);
+ws_status shard_merge(ws_ctx* ctx, const void* tables, const int64_t* z0s, const int64_t* z1s, int K, int rank,
+                      const Geo& g, int32_t* L, int32_t* exitcanon, cudaStream_t st);
+ws_status shard_relabel(ws_ctx* ctx, const int32_t* P, int32_t* L, const int32_t* exitcanon, const Geo& g,
+                        int32_t* labels_own, int64_t* nreps, cudaStream_t st);
+size_t shard_table_bytes(size_t plane);
 }
 ws_status run_plateau_debug(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn,
                             int32_t* dist, int32_t* parent, cudaStream_t st);
@@ -188,6 +206,7 @@ ws_status shard_merge(ws_ctx* ctx, const void* tables, const int64_t* z0s, const
                       const Geo& g, int32_t* L, int32_t* exitcanon, cudaStream_t st);
 ws_status shard_relabel(ws_ctx* ctx, const int32_t* P, int32_t* L, const int32_t* exitcanon, const Geo& g,
                         int32_t* labels_own, int64_t* nreps, cudaStream_t st);
+size_t shard_table_bytes(size_t plane);  // boundary table bytes of one rank (u8 pixels)
 
 ws_status shard_wf_dense(ws_ctx* ctx, const int32_t* labels_own, int n, int pofs, int doff, int* dense_of,
                          int* rep_of_global, int64_t* count, cudaStream_t st);
@@ -199,6 +218,9 @@ ws_status shard_wf_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint8_t* 
                          const int* dense_of, int64_t R, int NL, uint64_t* best_out, cudaStream_t st);
 ws_status shard_wf_step(ws_ctx* ctx, const uint64_t* best_in, uint64_t* best_out, int64_t* count, int* more,
                         cudaStream_t st);
+ws_status shard_wf16_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint16_t* I_ext, const Geo& g, int conn,
+                           const int* dense_of, int64_t R, int NL, cudaStream_t st);
+ws_status shard_wf16_level(ws_ctx* ctx, int step, int64_t* count, cudaStream_t st);
 ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, int conn, const int* dense_of,
                        const int* rep_of_global, int32_t* levels_own, cudaStream_t st);
 

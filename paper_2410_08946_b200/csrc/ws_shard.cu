@@ -26,6 +26,12 @@
 #include "ws_internal.h"
 
 namespace ws {
+#ifdef WS_PX16
+namespace px16 {  // ws_shard16.cu: the same phases on 16-bit pixels (NEXT f4)
+using Px = uint16_t;
+#else
+using Px = uint8_t;
+#endif
 
 constexpr int NTS = 256;
 
@@ -33,11 +39,12 @@ struct Table {  // views into one rank's boundary table
   int* term;
   int* rootmin;
   int* exitmin;
-  uint8_t* I;
-  uint8_t* rootI;
+  Px* I;
+  Px* rootI;
 };
 
-__host__ __device__ inline size_t table_bytes(size_t plane) { return plane * 28; }
+// 2 slots x (term, rootmin, exitmin: 12 B + I, rootI: 2 sizeof(Px)) per plane voxel
+__host__ __device__ inline size_t table_bytes(size_t plane) { return plane * (24 + 4 * sizeof(Px)); }
 
 __host__ __device__ inline Table table_view(void* base, size_t plane) {
   Table t;
@@ -45,8 +52,8 @@ __host__ __device__ inline Table table_view(void* base, size_t plane) {
   t.term = reinterpret_cast<int*>(b);
   t.rootmin = reinterpret_cast<int*>(b + plane * 8);
   t.exitmin = reinterpret_cast<int*>(b + plane * 16);
-  t.I = reinterpret_cast<uint8_t*>(b + plane * 24);
-  t.rootI = reinterpret_cast<uint8_t*>(b + plane * 26);
+  t.I = reinterpret_cast<Px*>(b + plane * 24);
+  t.rootI = reinterpret_cast<Px*>(b + plane * (24 + 2 * sizeof(Px)));
   return t;
 }
 
@@ -160,7 +167,7 @@ __global__ void k_union_pairs_shard(int* P, const int2* __restrict__ pairs, int 
 // whose terminal is an exit descends out of the slab and is never on a minimal plateau
 // (minimal-plateau pointers are kept inside the slab by k_resolve).
 template <int CONN>
-__global__ void k_union_shard(const uint8_t* __restrict__ I, int* P, Geo g) {
+__global__ void k_union_shard(const Px* __restrict__ I, int* P, Geo g) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= g.n2 || y >= g.n1) return;
@@ -200,7 +207,7 @@ __global__ void k_root_fold(const int* P, int* L, const int* __restrict__ roots,
 }
 
 // boundary table of the owned first/last planes (+ the exit minima)
-__global__ void k_table(const uint8_t* __restrict__ I, const int* P, const int* __restrict__ L,
+__global__ void k_table(const Px* __restrict__ I, const int* P, const int* __restrict__ L,
                         const int* __restrict__ exitmx, Geo g, Table t) {
   const int n = 2 * g.plane;
   for (int i = blockIdx.x * NTS + threadIdx.x; i < n; i += gridDim.x * NTS) {
@@ -209,7 +216,7 @@ __global__ void k_table(const uint8_t* __restrict__ I, const int* P, const int* 
     const int p = z * g.plane + xy;
     const int c = P[p];
     int term, rmin = INT_MAX;
-    uint8_t ri = 0;
+    Px ri = 0;
     if (c >= 0) {
       term = sfind_ro(P, g, c);
       rmin = INT_MAX - L[term - g.gofs];
@@ -399,16 +406,12 @@ __global__ void k_relabel_shard(const int* __restrict__ P, const int* __restrict
   }
 }
 
-}  // namespace ws
-
-// ================================================================== host side + C ABI
-namespace ws {
-
-ws_status plateau_first_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int* pending,
+// ================================================================== host side
+ws_status plateau_first_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* L, int* pending,
                               cudaStream_t st);
-ws_status plateau_round_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int act_lo,
+ws_status plateau_round_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* L, int act_lo,
                               int act_hi, int* pending, cudaStream_t st);
-ws_status resolve_shard(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, const int32_t* L, int32_t* P,
+ws_status resolve_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, const int32_t* L, int32_t* P,
                         cudaStream_t st);
 
 static int grid_s(long long n, int sms) {
@@ -417,7 +420,7 @@ static int grid_s(long long n, int sms) {
   return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
-ws_status shard_local(ws_ctx* ctx, const uint8_t* grad, const Geo& g, int conn, int32_t* L, int32_t* P, void* table,
+ws_status shard_local(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* L, int32_t* P, void* table,
                       cudaStream_t st) {
   WS_TRY(resolve_shard(ctx, grad, g, conn, L, P, st));
   const size_t own = (size_t)(g.zhi - g.zlo) * g.plane;
@@ -559,4 +562,9 @@ ws_status shard_halo(ws_ctx* ctx, int32_t* L, const Geo& g, int side, const int3
   return WS_OK;
 }
 
+size_t shard_table_bytes(size_t plane) { return table_bytes(plane); }
+
+#ifdef WS_PX16
+}  // namespace px16
+#endif
 }  // namespace ws

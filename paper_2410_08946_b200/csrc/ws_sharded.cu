@@ -170,12 +170,91 @@ ws_status check_transport(const ws_transport* tr, const ws_slab& sl) {
   return WS_OK;
 }
 
+// the phases of one pixel type (u8: ws_shard.cu; u16: ws_shard16.cu, NEXT f4)
+template <class Px> struct ShardOps;
+template <> struct ShardOps<uint8_t> {
+  static ws_status first(ws_ctx* c, const uint8_t* I, const Geo& g, int conn, int32_t* L, int* p, cudaStream_t st) {
+    return ws::plateau_first_shard(c, I, g, conn, L, p, st);
+  }
+  static ws_status round(ws_ctx* c, const uint8_t* I, const Geo& g, int conn, int32_t* L, int lo, int hi, int* p,
+                         cudaStream_t st) {
+    return ws::plateau_round_shard(c, I, g, conn, L, lo, hi, p, st);
+  }
+  static ws_status halo(ws_ctx* c, int32_t* L, const Geo& g, int side, const int32_t* in, int32_t* ch, cudaStream_t st) {
+    return ws::shard_halo(c, L, g, side, in, ch, st);
+  }
+  static ws_status local(ws_ctx* c, const uint8_t* I, const Geo& g, int conn, int32_t* L, int32_t* P, void* t,
+                         cudaStream_t st) {
+    return ws::shard_local(c, I, g, conn, L, P, t, st);
+  }
+  static ws_status merge(ws_ctx* c, const void* t, const int64_t* z0, const int64_t* z1, int K, int r, const Geo& g,
+                         int32_t* L, int32_t* ec, cudaStream_t st) {
+    return ws::shard_merge(c, t, z0, z1, K, r, g, L, ec, st);
+  }
+  static ws_status relabel(ws_ctx* c, const int32_t* P, int32_t* L, const int32_t* ec, const Geo& g, int32_t* out,
+                           int64_t* nreps, cudaStream_t st) {
+    return ws::shard_relabel(c, P, L, ec, g, out, nreps, st);
+  }
+  static size_t table_bytes(size_t plane) { return ws::shard_table_bytes(plane); }
+};
+template <> struct ShardOps<uint16_t> {
+  static ws_status first(ws_ctx* c, const uint16_t* I, const Geo& g, int conn, int32_t* L, int* p, cudaStream_t st) {
+    return ws::px16::plateau_first_shard(c, I, g, conn, L, p, st);
+  }
+  static ws_status round(ws_ctx* c, const uint16_t* I, const Geo& g, int conn, int32_t* L, int lo, int hi, int* p,
+                         cudaStream_t st) {
+    return ws::px16::plateau_round_shard(c, I, g, conn, L, lo, hi, p, st);
+  }
+  static ws_status halo(ws_ctx* c, int32_t* L, const Geo& g, int side, const int32_t* in, int32_t* ch, cudaStream_t st) {
+    return ws::px16::shard_halo(c, L, g, side, in, ch, st);
+  }
+  static ws_status local(ws_ctx* c, const uint16_t* I, const Geo& g, int conn, int32_t* L, int32_t* P, void* t,
+                         cudaStream_t st) {
+    return ws::px16::shard_local(c, I, g, conn, L, P, t, st);
+  }
+  static ws_status merge(ws_ctx* c, const void* t, const int64_t* z0, const int64_t* z1, int K, int r, const Geo& g,
+                         int32_t* L, int32_t* ec, cudaStream_t st) {
+    return ws::px16::shard_merge(c, t, z0, z1, K, r, g, L, ec, st);
+  }
+  static ws_status relabel(ws_ctx* c, const int32_t* P, int32_t* L, const int32_t* ec, const Geo& g, int32_t* out,
+                           int64_t* nreps, cudaStream_t st) {
+    return ws::px16::shard_relabel(c, P, L, ec, g, out, nreps, st);
+  }
+  static size_t table_bytes(size_t plane) { return ws::px16::shard_table_bytes(plane); }
+};
+
+// extended-slab geometry (owned planes [zlo, zhi), global offset) with the checks of ws_shard_*
+ws_status slab_geo(const ws_dims& d, const ws_slab& sl, Geo* g) {
+  const int64_t plane = d.n1 * d.n2;
+  if (d.ndim != 3 || d.n0 < 1 || d.n1 < 1 || d.n2 < 1 || !(0 <= sl.e0 && sl.e0 <= sl.z0 && sl.z0 < sl.z1 &&
+                                                            sl.z1 <= sl.e1 && sl.e1 <= sl.D) ||
+      d.n0 != sl.e1 - sl.e0 || (double)sl.D * (double)plane >= 2147483648.0 || (sl.z0 > 0 && sl.e0 > sl.z0 - 1) ||
+      (sl.z1 < sl.D && sl.e1 < sl.z1 + 1)) {
+    set_error(WS_ERR_INVALID, "inconsistent slab (D=%lld z=[%lld,%lld) e=[%lld,%lld) n0=%lld)", (long long)sl.D,
+              (long long)sl.z0, (long long)sl.z1, (long long)sl.e0, (long long)sl.e1, (long long)d.n0);
+    return WS_ERR_INVALID;
+  }
+  g->n0 = (int)d.n0;
+  g->n1 = (int)d.n1;
+  g->n2 = (int)d.n2;
+  g->plane = (int)plane;
+  g->N = (int)(d.n0 * plane);
+  g->zlo = (int)(sl.z0 - sl.e0);
+  g->zhi = (int)(sl.z1 - sl.e0);
+  g->gofs = (int)(sl.e0 * plane);
+  return WS_OK;
+}
+
 // ------------------------------------------------------------------ the pipeline
 // Watershed on the slab: labels_own (i32[(z1-z0) plane], global canonical labels), nreps
 // (owned representatives), R (all ranks), rounds (step II rounds).
-ws_status sharded_watershed(ws_ctx* ctx, const ws_transport* tr, const uint8_t* grad_ext, ws_dims d, ws_slab sl,
+template <class Px>
+ws_status sharded_watershed(ws_ctx* ctx, const ws_transport* tr, const Px* grad_ext, ws_dims d, ws_slab sl,
                             int conn, int32_t* labels_own, int64_t* nreps, int64_t* R, int32_t* rounds,
                             cudaStream_t st) {
+  using O = ShardOps<Px>;
+  Geo g;
+  WS_TRY(slab_geo(d, sl, &g));
   const int K = tr->nranks, r = tr->rank;
   const int64_t plane = d.n1 * d.n2, next = d.n0 * plane;
   const int zlo = (int)(sl.z0 - sl.e0), zhi = (int)(sl.z1 - sl.e0);
@@ -195,8 +274,8 @@ ws_status sharded_watershed(ws_ctx* ctx, const ws_transport* tr, const uint8_t* 
                         has_hi ? above : nullptr, plane * 4, st),
            "halo exchange");
     *ch_lo = *ch_hi = 0;
-    if (has_lo) WS_TRY(ws_shard_halo(ctx, L, d, sl, 0, below, ch_lo, st));
-    if (has_hi) WS_TRY(ws_shard_halo(ctx, L, d, sl, 1, above, ch_hi, st));
+    if (has_lo) WS_TRY(O::halo(ctx, L, g, 0, below, ch_lo, st));
+    if (has_hi) WS_TRY(O::halo(ctx, L, g, 1, above, ch_hi, st));
     return WS_OK;
   };
   // steps I + II: relaxation rounds until no rank has pending work or a changed halo (the
@@ -204,29 +283,34 @@ ws_status sharded_watershed(ws_ctx* ctx, const ws_transport* tr, const uint8_t* 
   if (has_lo) WS_CUDA(cudaMemsetAsync(L + (size_t)(zlo - 1) * plane, 0xFF, plane * 4, st));
   if (has_hi) WS_CUDA(cudaMemsetAsync(L + (size_t)zhi * plane, 0xFF, plane * 4, st));
   int pend = 0, ch_lo = 0, ch_hi = 0;
-  WS_TRY(ws_shard_plateau(ctx, grad_ext, d, conn, sl, L, 0, 0, 0, &pend, st));
+  WS_TRY(O::first(ctx, grad_ext, g, conn, L, &pend, st));
   WS_TRY(halo(&ch_lo, &ch_hi));
   int nround = 1;
   while (true) {
     bool more = false;
     WS_TRY(any_rank(tr, s, pend || ch_lo || ch_hi, &more, st));
     if (!more) break;
-    WS_TRY(ws_shard_plateau(ctx, grad_ext, d, conn, sl, L, 1, ch_lo, ch_hi, &pend, st));
+    WS_TRY(O::round(ctx, grad_ext, g, conn, L, ch_lo, ch_hi, &pend, st));
     WS_TRY(halo(&ch_lo, &ch_hi));
     ++nround;
   }
   // pointers, local steps III/IV, boundary tables; replicated merge over the gathered tables
-  const int64_t tb = ws_shard_table_bytes(d);
+  const int64_t tb = (int64_t)O::table_bytes((size_t)plane);
   WS_TRY(ctx->sh_tab.ensure((size_t)tb, "boundary table"));
   WS_TRY(ctx->sh_alltab.ensure((size_t)tb * K, "gathered boundary tables"));
-  WS_TRY(ws_shard_local(ctx, grad_ext, L, d, conn, sl, P, ctx->sh_tab.p, st));
+  WS_TRY(O::local(ctx, grad_ext, g, conn, L, P, ctx->sh_tab.p, st));
   TR_TRY(tr->allgather(tr->user, ctx->sh_tab.p, ctx->sh_alltab.p, tb, st), "allgather(tables)");
   std::vector<int64_t> z0s(K), z1s(K);
   WS_TRY(allgather_i64(tr, s, sl.z0, z0s.data(), st));
   WS_TRY(allgather_i64(tr, s, sl.z1, z1s.data(), st));
   WS_TRY(ctx->sh_ec.ensure((size_t)plane * 2 * 4, "exit labels"));
-  WS_TRY(ws_shard_merge(ctx, ctx->sh_alltab.p, K, z0s.data(), z1s.data(), d, sl, L, ctx->sh_ec.as<int32_t>(), st));
-  WS_TRY(ws_shard_relabel(ctx, P, L, ctx->sh_ec.as<int32_t>(), d, sl, labels_own, nreps, st));
+  for (int q = 0; q < K; ++q)
+    if ((q > 0 && z0s[q] != z1s[q - 1]) || z0s[0] != 0 || z1s[K - 1] != sl.D || (q == r && (z0s[q] != sl.z0 || z1s[q] != sl.z1))) {
+      set_error(WS_ERR_INVALID, "the ranks' slabs must tile [0, D) in rank order");
+      return WS_ERR_INVALID;
+    }
+  WS_TRY(O::merge(ctx, ctx->sh_alltab.p, z0s.data(), z1s.data(), K, r, g, L, ctx->sh_ec.as<int32_t>(), st));
+  WS_TRY(O::relabel(ctx, P, L, ctx->sh_ec.as<int32_t>(), g, labels_own, nreps, st));
   std::vector<int64_t> cnt(K);
   WS_TRY(allgather_i64(tr, s, *nreps, cnt.data(), st));
   int64_t tot = 0;
@@ -237,7 +321,8 @@ ws_status sharded_watershed(ws_ctx* ctx, const ws_transport* tr, const uint8_t* 
 }
 
 // Graph waterfall (C13) on the slab: levels_own (i32[NL][(z1-z0) plane]), counts (host i64[NL])
-ws_status sharded_waterfall(ws_ctx* ctx, const ws_transport* tr, const uint8_t* grad_ext, ws_dims d, ws_slab sl,
+template <class Px>
+ws_status sharded_waterfall(ws_ctx* ctx, const ws_transport* tr, const Px* grad_ext, ws_dims d, ws_slab sl,
                             int conn, int NL, const int32_t* labels_own, int64_t nreps, int32_t* levels_own,
                             int64_t* counts, cudaStream_t st) {
   const int K = tr->nranks, r = tr->rank;
@@ -289,24 +374,43 @@ ws_status sharded_waterfall(ws_ctx* ctx, const ws_transport* tr, const uint8_t* 
   WS_TRY(ctx->sh_nxt.ensure((size_t)std::max<int64_t>(R, 1) * 8, "next minima"));
   int64_t* best = ctx->sh_best.as<int64_t>();
   int64_t* nxt = ctx->sh_nxt.as<int64_t>();
-  WS_TRY(ws_shard_wf_begin(ctx, lext, grad_ext, d, conn, sl, dense_of, R, NL, best, st));
-  TR_TRY(tr->allreduce(tr->user, best, R, 1, 0, st), "allreduce(min) level 1");
-  if (counts) counts[0] = R;
-  int more = (NL > 1 && R > 1) ? 1 : 0;
-  int64_t cur = R;
-  for (int k = 1; k < NL; ++k) {
-    if (more) {
-      int64_t cc = 0;
-      int32_t m = 0;
-      WS_TRY(ws_shard_wf_step(ctx, best, nxt, &cc, &m, st));
-      cur = cc;
-      more = m;
+  if constexpr (sizeof(Px) == 1) {
+    WS_TRY(ws_shard_wf_begin(ctx, lext, grad_ext, d, conn, sl, dense_of, R, NL, best, st));
+    TR_TRY(tr->allreduce(tr->user, best, R, 1, 0, st), "allreduce(min) level 1");
+    if (counts) counts[0] = R;
+    int more = (NL > 1 && R > 1) ? 1 : 0;
+    int64_t cur = R;
+    for (int k = 1; k < NL; ++k) {
       if (more) {
-        TR_TRY(tr->allreduce(tr->user, nxt, cur, 1, 0, st), "allreduce(min) level");
-        std::swap(best, nxt);
+        int64_t cc = 0;
+        int32_t m = 0;
+        WS_TRY(ws_shard_wf_step(ctx, best, nxt, &cc, &m, st));
+        cur = cc;
+        more = m;
+        if (more) {
+          TR_TRY(tr->allreduce(tr->user, nxt, cur, 1, 0, st), "allreduce(min) level");
+          std::swap(best, nxt);
+        }
       }
+      if (counts) counts[k] = cur;
     }
-    if (counts) counts[k] = cur;
+  } else {
+    // 16-bit: K = (hi, lo) reduced in two steps per level (ws_waterfall.cu shard_wf16_level)
+    Geo g;
+    WS_TRY(slab_geo(d, sl, &g));
+    WS_TRY(shard_wf16_begin(ctx, lext, grad_ext, g, conn, dense_of, R, NL, st));
+    if (counts) counts[0] = R;
+    int64_t cur = R;
+    for (int k = 1; k < NL; ++k) {
+      if (cur > 1) {
+        WS_TRY(shard_wf16_level(ctx, 0, &cur, st));
+        TR_TRY(tr->allreduce(tr->user, ctx->best.p, R, 1, 0, st), "allreduce(min) hi");
+        WS_TRY(shard_wf16_level(ctx, 1, &cur, st));
+        TR_TRY(tr->allreduce(tr->user, ctx->best_lo.p, R, 0, 0, st), "allreduce(min) lo");
+        WS_TRY(shard_wf16_level(ctx, 2, &cur, st));
+      }
+      if (counts) counts[k] = cur;
+    }
   }
   WS_TRY(ws_shard_wf_end(ctx, labels_own, dense_of, rep_of, d, conn, sl, levels_own, st));
   return WS_OK;
@@ -322,7 +426,7 @@ __global__ void k_count_reps(const int32_t* __restrict__ lab, long long n, long 
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
 }
 
-ws_status check_sharded_args(ws_ctx* ctx, const ws_transport* tr, const uint8_t* grad_ext, const ws_dims& d,
+ws_status check_sharded_args(ws_ctx* ctx, const ws_transport* tr, const void* grad_ext, const ws_dims& d,
                              const ws_slab& sl, int conn, const void* out) {
   if (!ctx) {
     set_error(WS_ERR_INVALID, "ctx is NULL");
@@ -405,10 +509,15 @@ ws_status ws_ctx_create_sharded(int32_t device, const ws_transport* tr, ws_slab 
   return WS_OK;
 }
 
-ws_status ws_watershed_sharded(ws_ctx* ctx, const ws_transport* tr, const uint8_t* grad_ext, ws_dims dims_ext,
-                               ws_slab slab, int32_t connectivity, int32_t* labels_own, int64_t* num_regions,
-                               int32_t* rounds, void* stream) {
+}  // extern "C"
+
+namespace {
+template <class Px>
+ws_status watershed_sharded_t(ws_ctx* ctx, const ws_transport* tr, const Px* grad_ext, ws_dims dims_ext, ws_slab slab,
+                              int32_t connectivity, int32_t* labels_own, int64_t* num_regions, int32_t* rounds,
+                              void* stream) {
   WS_TRY(check_sharded_args(ctx, tr, grad_ext, dims_ext, slab, connectivity, labels_own));
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   cudaStream_t st = (cudaStream_t)stream;
   int64_t nreps = 0, R = 0;
   int32_t nr = 0;
@@ -420,14 +529,16 @@ ws_status ws_watershed_sharded(ws_ctx* ctx, const ws_transport* tr, const uint8_
   return WS_OK;
 }
 
-ws_status ws_segment_sharded(ws_ctx* ctx, const ws_transport* tr, const uint8_t* grad_ext, ws_dims dims_ext,
-                             ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own, int64_t* counts,
-                             int32_t* rounds, void* stream) {
+template <class Px>
+ws_status segment_sharded_t(ws_ctx* ctx, const ws_transport* tr, const Px* grad_ext, ws_dims dims_ext, ws_slab slab,
+                            int32_t connectivity, int32_t NL, int32_t* levels_own, int64_t* counts, int32_t* rounds,
+                            void* stream) {
   WS_TRY(check_sharded_args(ctx, tr, grad_ext, dims_ext, slab, connectivity, levels_own));
   if (NL < 1 || NL > 16) {
     set_error(WS_ERR_INVALID, "NL must be in [1, 16] (got %d)", NL);
     return WS_ERR_INVALID;
   }
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nown = (slab.z1 - slab.z0) * dims_ext.n1 * dims_ext.n2;
   WS_TRY(ctx->sh_lab.ensure((size_t)nown * 4, "slab labels"));
@@ -447,9 +558,10 @@ ws_status ws_segment_sharded(ws_ctx* ctx, const ws_transport* tr, const uint8_t*
   return WS_OK;
 }
 
-ws_status ws_waterfall_sharded(ws_ctx* ctx, const ws_transport* tr, const int32_t* labels_own, const uint8_t* grad_ext,
-                               ws_dims dims_ext, ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own,
-                               int64_t* counts, void* stream) {
+template <class Px>
+ws_status waterfall_sharded_t(ws_ctx* ctx, const ws_transport* tr, const int32_t* labels_own, const Px* grad_ext,
+                              ws_dims dims_ext, ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own,
+                              int64_t* counts, void* stream) {
   WS_TRY(check_sharded_args(ctx, tr, grad_ext, dims_ext, slab, connectivity, levels_own));
   if (!labels_own) {
     set_error(WS_ERR_INVALID, "labels_own is NULL");
@@ -459,6 +571,7 @@ ws_status ws_waterfall_sharded(ws_ctx* ctx, const ws_transport* tr, const int32_
     set_error(WS_ERR_INVALID, "NL must be in [1, 16] (got %d)", NL);
     return WS_ERR_INVALID;
   }
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t plane = dims_ext.n1 * dims_ext.n2, nown = (slab.z1 - slab.z0) * plane;
   Small s;
@@ -477,6 +590,42 @@ ws_status ws_waterfall_sharded(ws_ctx* ctx, const ws_transport* tr, const int32_
   for (int k = 0; k < NL; ++k) ctx->stats.level_counts[k] = cts[k];
   return WS_OK;
 }
+}  // namespace
+
+extern "C" {
+
+ws_status ws_watershed_sharded(ws_ctx* ctx, const ws_transport* tr, const uint8_t* grad_ext, ws_dims dims_ext,
+                               ws_slab slab, int32_t connectivity, int32_t* labels_own, int64_t* num_regions,
+                               int32_t* rounds, void* stream) {
+  return watershed_sharded_t(ctx, tr, grad_ext, dims_ext, slab, connectivity, labels_own, num_regions, rounds, stream);
+}
+ws_status ws_watershed_sharded_u16(ws_ctx* ctx, const ws_transport* tr, const uint16_t* grad_ext, ws_dims dims_ext,
+                                   ws_slab slab, int32_t connectivity, int32_t* labels_own, int64_t* num_regions,
+                                   int32_t* rounds, void* stream) {
+  return watershed_sharded_t(ctx, tr, grad_ext, dims_ext, slab, connectivity, labels_own, num_regions, rounds, stream);
+}
+ws_status ws_segment_sharded(ws_ctx* ctx, const ws_transport* tr, const uint8_t* grad_ext, ws_dims dims_ext,
+                             ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own, int64_t* counts,
+                             int32_t* rounds, void* stream) {
+  return segment_sharded_t(ctx, tr, grad_ext, dims_ext, slab, connectivity, NL, levels_own, counts, rounds, stream);
+}
+ws_status ws_segment_sharded_u16(ws_ctx* ctx, const ws_transport* tr, const uint16_t* grad_ext, ws_dims dims_ext,
+                                 ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own, int64_t* counts,
+                                 int32_t* rounds, void* stream) {
+  return segment_sharded_t(ctx, tr, grad_ext, dims_ext, slab, connectivity, NL, levels_own, counts, rounds, stream);
+}
+ws_status ws_waterfall_sharded(ws_ctx* ctx, const ws_transport* tr, const int32_t* labels_own, const uint8_t* grad_ext,
+                               ws_dims dims_ext, ws_slab slab, int32_t connectivity, int32_t NL, int32_t* levels_own,
+                               int64_t* counts, void* stream) {
+  return waterfall_sharded_t(ctx, tr, labels_own, grad_ext, dims_ext, slab, connectivity, NL, levels_own, counts,
+                             stream);
+}
+ws_status ws_waterfall_sharded_u16(ws_ctx* ctx, const ws_transport* tr, const int32_t* labels_own,
+                                   const uint16_t* grad_ext, ws_dims dims_ext, ws_slab slab, int32_t connectivity,
+                                   int32_t NL, int32_t* levels_own, int64_t* counts, void* stream) {
+  return waterfall_sharded_t(ctx, tr, labels_own, grad_ext, dims_ext, slab, connectivity, NL, levels_own, counts,
+                             stream);
+}
 
 }  // extern "C"
 
@@ -493,5 +642,15 @@ ws_status sharded_dispatch_segment(ws_ctx* ctx, const uint8_t* grad_ext, const w
 ws_status sharded_dispatch_waterfall(ws_ctx* ctx, const int32_t* labels_own, const uint8_t* grad_ext, const ws_dims& d,
                                      int conn, int NL, int32_t* levels, int64_t* counts, cudaStream_t st) {
   return ws_waterfall_sharded(ctx, &ctx->sh_tr, labels_own, grad_ext, d, ctx->sh_slab, conn, NL, levels, counts, st);
+}
+ws_status sharded_dispatch_watershed_u16(ws_ctx* ctx, const uint16_t* grad_ext, const ws_dims& d, int conn,
+                                         int32_t* labels, int64_t* num_regions, cudaStream_t st) {
+  return ws_watershed_sharded_u16(ctx, &ctx->sh_tr, grad_ext, d, ctx->sh_slab, conn, labels, num_regions, nullptr, st);
+}
+ws_status sharded_dispatch_waterfall_u16(ws_ctx* ctx, const int32_t* labels_own, const uint16_t* grad_ext,
+                                         const ws_dims& d, int conn, int NL, int32_t* levels, int64_t* counts,
+                                         cudaStream_t st) {
+  return ws_waterfall_sharded_u16(ctx, &ctx->sh_tr, labels_own, grad_ext, d, ctx->sh_slab, conn, NL, levels, counts,
+                                  st);
 }
 }  // namespace ws

@@ -1792,6 +1792,79 @@ ws_status shard_wf_step(ws_ctx* ctx, const uint64_t* best_in, uint64_t* best_out
   return WS_OK;
 }
 
+// ---------------------------------------- z-slab sharded 16-bit waterfall (u16 sharding)
+// The per-component minimum of K = (hi, lo) (make_e16) is reduced over the ranks in two
+// steps per level, as on one GPU: the minimum hi of every component (all ranks' live edges,
+// all_reduce MIN), then the minimum lo among the edges with that hi (all_reduce MIN); both
+// travel sign-flipped (x ^ top bit) so unsigned order is the transport's signed order.  The
+// union-find over dense ids is replicated (k_hook16 / k_flatten on every rank, same result).
+__global__ void k_flip32(unsigned* a, long long n) {
+  for (long long i = blockIdx.x * (long long)NTW + threadIdx.x; i < n; i += (long long)gridDim.x * NTW)
+    a[i] ^= 0x80000000u;
+}
+
+ws_status shard_wf16_begin(ws_ctx* ctx, const int32_t* labels_ext, const uint16_t* I_ext, const Geo& g, int conn,
+                           const int* dense_of, int64_t R, int NL, cudaStream_t st) {
+  if (NL > LVC) {
+    set_error(WS_ERR_LIMIT, "ws_waterfall_u16: NL must be <= %d", LVC);
+    return WS_ERR_LIMIT;
+  }
+  WS_TRY(ctx->flags.ensure(256, "flags"));
+  WS_TRY(ctx->pathc.ensure(4 * sizeof(unsigned long long), "path counters"));
+  WS_CUDA(cudaMemsetAsync(ctx->pathc.p, 0, 4 * sizeof(unsigned long long), st));
+  WS_TRY(wf_alloc(ctx, R, NL, st));
+  WS_TRY(ctx->best_lo.ensure((size_t)R * sizeof(unsigned), "best lo"));
+  WS_CUDA(cudaMemsetAsync(ctx->best_lo.p, 0xFF, (size_t)R * sizeof(unsigned), st));
+  WS_TRY(wf_rag<uint16_t>(ctx, labels_ext, I_ext, g, conn, dense_of, st));
+  ctx->stats.level_counts[0] = R;
+  ctx->stats.level_edges[1] = ctx->wf.E;
+  return WS_OK;
+}
+
+// level k = ctx->wf.k, step 0: live edges + local minimum hi, flipped for the reduction
+// (exchange buffer: ctx->best, R x i64); step 1: local minimum lo among the edges with the
+// reduced hi, flipped (ctx->best_lo, R x i32); step 2: hook + flatten, *count = components
+// after the level (host)
+ws_status shard_wf16_level(ws_ctx* ctx, int step, int64_t* count, cudaStream_t st) {
+  WSState& w = ctx->wf;
+  const int k = w.k;
+  const int64_t R = w.R;
+  unsigned long long* cnt = ctx->lvcount.as<unsigned long long>();
+  uint64_t* best_hi = ctx->best.as<uint64_t>();
+  unsigned* best_lo = ctx->best_lo.as<unsigned>();
+  E16* eout = (k & 1) ? ctx->ebufA.as<E16>() : ctx->ebufB.as<E16>();
+  const int ge = grid_for(std::max<int64_t>(w.E, 1), ctx->num_sms, 8);
+  if (step == 0) {
+    const E16* ein = k == 1 ? ctx->edges.as<E16>() : ((k & 1) ? ctx->ebufB.as<E16>() : ctx->ebufA.as<E16>());
+    k_e16_live<<<ge, NTW, 0, st>>>(ein, w.E, k == 1 ? nullptr : cnt + LVC + k - 1, ctx->comp.as<int>(), best_hi, eout,
+                                   cnt + LVC + k);
+    k_flip_copy<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(best_hi, best_hi, R);
+    launched(ctx, PH_WF_LEVELS, 2);
+  } else if (step == 1) {
+    k_flip_copy<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(best_hi, best_hi, R);
+    k_e16_lo<<<ge, NTW, 0, st>>>(eout, cnt + LVC + k, best_hi, best_lo);
+    k_flip32<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(best_lo, R);
+    launched(ctx, PH_WF_LEVELS, 3);
+  } else {
+    k_flip32<<<grid_for(R, ctx->num_sms), NTW, 0, st>>>(best_lo, R);
+    int* rA = ctx->rootsA.as<int>();
+    int* rB = ctx->rootsB.as<int>();
+    int* rin = k == 1 ? nullptr : ((k & 1) ? rB : rA);  // roots of level k-1 (level 1: all R)
+    int* rout = (k & 1) ? rA : rB;
+    const unsigned long long* nin = k == 1 ? nullptr : cnt + (k - 1);
+    k_hook16<<<grid_for(R, ctx->num_sms), 256, 0, st>>>(best_hi, best_lo, ctx->comp.as<int>(), rin, (int)R, nin);
+    k_flatten<<<grid_for(R, ctx->num_sms, 8), NTW, 0, st>>>(ctx->comp.as<int>(), rin, (int)R, nin, rout, cnt + k,
+                                                           ctx->lvl.as<uint8_t>(), k);
+    launched(ctx, PH_WF_LEVELS, 3);
+    int64_t c[LVC] = {};
+    WS_TRY(wf_read_counts(ctx, k, c, st));
+    *count = c[k];
+    w.k = k + 1;
+  }
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
 ws_status shard_wf_end(ws_ctx* ctx, const int32_t* labels_own, const Geo& gown, int conn, const int* dense_of,
                        const int* rep_of_global, int32_t* levels_own, cudaStream_t st) {
   (void)labels_own;

@@ -1302,8 +1302,8 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   return WS_OK;
 }
 
-#ifndef WS_PX16
 // ------------------------------------------------------------- z-slab sharded phases
+// (both pixel types: the 16-bit instantiation shards ws_watershed_u16, NEXT f4)
 __global__ void k_mark_layer(uint8_t* cur, int layer, int per_layer) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < per_layer; i += gridDim.x * blockDim.x)
     cur[layer * per_layer + i] = 1;
@@ -1410,8 +1410,6 @@ ws_status resolve_shard(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, con
   set_error(WS_ERR_INVALID, "the sharded path supports 6- and 26-connectivity");
   return WS_ERR_INVALID;
 }
-
-#endif  // !WS_PX16
 
 ws_status run_watershed(ws_ctx* ctx, const Px* grad, const Geo& g, int conn, int32_t* labels,
                         int64_t* num_regions, cudaStream_t st, bool relabel, bool small) {

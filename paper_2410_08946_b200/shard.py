@@ -563,7 +563,8 @@ def segment_sharded(transport, ctx, slab: Slab, grad_ext, NL: int, conn: int = 6
     counts = (ctypes.c_int64 * NL)()
     rounds = ctypes.c_int32(0)
     st = ctypes.c_void_p(torch.cuda.current_stream(grad_ext.device).cuda_stream)
-    s = lib.ws_segment_sharded(ctx.handle, transport.ptr(), _b.ptr(grad_ext), _dims(slab, n1, n2), slab.c(), conn, NL,
+    fn = lib.ws_segment_sharded_u16 if grad_ext.dtype == torch.uint16 else lib.ws_segment_sharded
+    s = fn(ctx.handle, transport.ptr(), _b.ptr(grad_ext), _dims(slab, n1, n2), slab.c(), conn, NL,
                                _b.ptr(out), counts, ctypes.byref(rounds), st)
     if s != _b.WS_OK and getattr(transport, "error", None) is not None:
         raise RuntimeError("transport callback failed: %r" % (transport.error,))
@@ -580,7 +581,8 @@ def watershed_sharded(transport, ctx, slab: Slab, grad_ext, conn: int = 6, out=N
     R = ctypes.c_int64(0)
     rounds = ctypes.c_int32(0)
     st = ctypes.c_void_p(torch.cuda.current_stream(grad_ext.device).cuda_stream)
-    _b.check(lib.ws_watershed_sharded(ctx.handle, transport.ptr(), _b.ptr(grad_ext), _dims(slab, n1, n2), slab.c(),
+    fn = lib.ws_watershed_sharded_u16 if grad_ext.dtype == torch.uint16 else lib.ws_watershed_sharded
+    _b.check(fn(ctx.handle, transport.ptr(), _b.ptr(grad_ext), _dims(slab, n1, n2), slab.c(),
                                       conn, _b.ptr(out), ctypes.byref(R), ctypes.byref(rounds), st))
     return out, R.value, rounds.value
 

@@ -6,7 +6,9 @@
   - 2 processes on the one GPU over torch.distributed gloo (TorchCallbacks: the multi-process
     control flow of the NCCL deployment, planes staged through host memory);
   - the library's own NCCL transport at world size 1 (communicator creation, the collectives
-    on one rank) and ws_ctx_create_sharded (the three plain calls on a sharded context).
+    on one rank) and ws_ctx_create_sharded (the three plain calls on a sharded context);
+  - 16-bit volumes (NEXT f4 u16 sharding: ws_segment_sharded_u16 vs ws_watershed_u16 +
+    ws_waterfall_u16), K = 1..3, 6- and 26-connectivity, plateaux across the cuts.
 """
 import os
 import socket
@@ -132,3 +134,41 @@ def test_lib_nccl_transport_world1_and_sharded_context():
         tr.close()
     finally:
         dist.destroy_process_group()
+
+
+def _ref16(grad, conn, NL):
+    import paper_2410_08946_b200 as ws
+    lab, R = ws.watershed(grad, conn, ndim=3)
+    lv, counts = ws.waterfall(lab, grad, conn, NL, ndim=3)
+    assert torch.equal(lv[0], lab)
+    return lv, list(counts)
+
+
+@pytest.mark.parametrize("conn", [6, 26])
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_lib_sharded_u16(K, conn):
+    """u16 sharding (NEXT f4): the sharded watershed + two-step-reduced 16-bit waterfall equal
+    ws_watershed_u16 + ws_waterfall_u16 on the whole volume"""
+    import paper_2410_08946_b200 as ws
+    from paper_2410_08946_b200 import shard
+    raw = synth.make_config_image("C4", shape=(24, 40, 56), device="cuda")
+    gen = torch.Generator(device="cuda").manual_seed(11 + K)
+    raw16 = (raw.to(torch.int32) * 256 + torch.randint(0, 256, tuple(raw.shape), generator=gen, device="cuda",
+                                                        dtype=torch.int32)).to(torch.uint16)
+    q16 = ws.gradient(raw16, 1.0, ndim=3)
+    assert q16.dtype == torch.uint16
+    ref, rc = _ref16(q16, conn, 5)
+    got, counts, _ = shard.segment_threads(K, q16, 5, conn)
+    assert torch.equal(got, ref)
+    assert counts == rc
+
+
+def test_lib_sharded_u16_plateaux():
+    """16-bit values with few levels spread over the range: plateaux (minimal and not) cross
+    the cuts; odd plane size"""
+    from paper_2410_08946_b200 import shard
+    g8 = synth.random_plateau_image((12, 33, 47), 4, seed=5).cuda()
+    q16 = (g8.to(torch.int32) * 16000 + 7).to(torch.uint16)
+    ref, rc = _ref16(q16, 6, 6)
+    got, counts, _ = shard.segment_threads(3, q16, 6, 6)
+    assert torch.equal(got, ref) and counts == rc
