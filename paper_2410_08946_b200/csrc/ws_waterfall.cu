@@ -1299,7 +1299,7 @@ __global__ void __launch_bounds__(NTW) k_relabel_seg(const int* __restrict__ P, 
     d.y = c.y == c.x ? d.x : rank_of(rk, c.y);
     d.z = c.z == c.y ? d.y : rank_of(rk, c.z);
     d.w = c.w == c.z ? d.z : rank_of(rk, c.w);
-    reinterpret_cast<int4*>(D)[i] = d;
+    __stcs(reinterpret_cast<int4*>(D) + i, d);  // evict-first: keep L2 for the root gathers of P
     if (c.x == p) rep_of[d.x] = p;
     if (c.y == p + 1) rep_of[d.y] = p + 1;
     if (c.z == p + 2) rep_of[d.z] = p + 2;
