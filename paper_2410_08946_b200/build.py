@@ -28,16 +28,36 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(SO)
         if all(os.path.getmtime(d) <= t for d in deps()):
             return SO
-    cmd = [NVCC, *FLAGS, "-shared", "-o", SO, *sources(), "-lcudart"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit, in parallel, then one link (same flags as a single
+    # whole-list nvcc call: every .cu is its own device compilation unit either way)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        jobs.append(([NVCC, *FLAGS, "-c", "-o", obj, src], obj))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda j: subprocess.run(j[0], capture_output=True, text=True), jobs))
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", SO,
+            *[o for _, o in jobs], "-lcudart"]
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
+        for (cmd, _), r in zip(jobs, results):
+            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        failed = [r for r in results if r.returncode != 0]
+        if not failed:
+            r = subprocess.run(link, capture_output=True, text=True)
+            f.write(" ".join(link) + "\n" + r.stdout + r.stderr)
+            if r.returncode != 0:
+                failed = [r]
+    if failed:
+        for r in failed:
+            sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed (see %s)" % log)
     if verbose:
-        sys.stderr.write(r.stderr)
+        for r in results:
+            sys.stderr.write(r.stderr)
     return SO
 
 

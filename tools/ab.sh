@@ -1,6 +1,6 @@
 # A/B of an env-gated variant: bench phases without and with "$1"
 for v in 0 1 0 1; do
-  if [ $v = 1 ]; then export $1=1; else unset $1; fi
+  if [ $v = 1 ]; then export $1=${2:-1}; else unset $1; fi
   timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-paper-protocol --no-other-configs > gpurun_out/ab_$v.log 2>&1
   python -c "
 import json
