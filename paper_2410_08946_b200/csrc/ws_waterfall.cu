@@ -291,9 +291,23 @@ template <int CONN, class Px = uint8_t> struct RL {
   static constexpr int SMEM = SIA + SLA + SLOT * HP + 2 * STG;
 };
 
+// global-space atomics spelled out: through a generic pointer the compiler may emit ATOM.E
+// with a shared-space check (and wait for it) instead of the fire-and-forget RED
+__device__ __forceinline__ void red_min_g(uint64_t* p, uint64_t v) {
+  asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_g(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long atom_add_g(unsigned long long* p, unsigned long long v) {
+  unsigned long long r;
+  asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(v) : "memory");
+  return r;
+}
+
 __device__ __forceinline__ void fold_best(uint64_t* best, uint64_t k) {
-  atomicMin((unsigned long long*)(best + key_lo(k)), (unsigned long long)k);
-  atomicMin((unsigned long long*)(best + key_hi(k)), (unsigned long long)k);
+  red_min_g(best + key_lo(k), k);
+  red_min_g(best + key_hi(k), k);
 }
 
 // where the RAG's unique tile edges go (level-1 key list + best[]); emits counts the records
@@ -331,7 +345,7 @@ __host__ __device__ __forceinline__ E16 make_e16(uint32_t w, uint32_t a, uint32_
 }
 
 __device__ __noinline__ void emit_global(uint32_t w, uint32_t a, uint32_t b, const EdgeOut& eo) {
-  const unsigned long long i = atomicAdd(eo.ecount, 1ull);
+  const unsigned long long i = atom_add_g(eo.ecount, 1ull);
   if (eo.e16) {
     if ((long long)i < eo.cap) eo.e16[i] = make_e16(w, a, b);
   } else {
@@ -339,7 +353,7 @@ __device__ __noinline__ void emit_global(uint32_t w, uint32_t a, uint32_t b, con
     if ((long long)i < eo.cap) eo.edges[i] = k;
     fold_best(eo.best, k);
   }
-  atomicAdd(eo.emits, 1ull);
+  red_add_g(eo.emits, 1ull);
 }
 
 // Box indices of a warp's voxels: voxel k of lane l is D-box index wb.x + k * wb.y + l and
@@ -448,7 +462,7 @@ __device__ __forceinline__ int rag_pairs(const Px* sI, const int* sD, unsigned l
       wcnt += __popc(b);
     }
     if (R::MIDFOLD && wcnt > R::WCAP - NF * 32) {
-      if (eo.recs && lane == 0) atomicAdd(eo.recs, (unsigned long long)wcnt);
+      if (eo.recs && lane == 0) red_add_g(eo.recs, (unsigned long long)wcnt);
       __syncwarp();
       fold_warp<CONN, Px>(wst, wcnt, wb, offs, sI, sD, pk, pw, eo);
       __syncwarp();
@@ -480,12 +494,15 @@ __device__ __forceinline__ void rag_load_plain(const int* __restrict__ D, const 
   }
 }
 
-// Persistent CTAs walk the tiles t = blockIdx.x, + gridDim.x, ...; with TMA the next tile's
-// boxes are requested as soon as the current ones are consumed, so the load overlaps the flush.
+// One CTA per tile t = blockIdx.x (a 1-D grid: CTAs running together hold neighbouring tiles in
+// linear order, so the edge list comes out in tile order -- the level loop's per-chunk dedup
+// and comp gathers depend on it -- and the best[] atomics of neighbouring CTAs share L2 lines;
+// a 3-D grid measured 9.1 -> 11.2 ms).  Thread 0 decodes the tile coordinates (integer
+// divisions once per CTA, not per thread) and shares them.
 template <int CONN, class Px>
 __global__ void __launch_bounds__(NT, 5) k_rag(const __grid_constant__ CUtensorMap mI, const __grid_constant__ CUtensorMap mD,
                                                int tma, const int* __restrict__ D, const Px* __restrict__ I, Geo g,
-                                               int ntx, int nty, int ntiles, EdgeOut eo) {
+                                               int ntx, int nty, EdgeOut eo) {
   using R = RL<CONN, Px>;
   extern __shared__ __align__(128) unsigned char rag_smem[];
   Px* sI = reinterpret_cast<Px*>(rag_smem);                                       // R::SI pixels
@@ -497,6 +514,17 @@ __global__ void __launch_bounds__(NT, 5) k_rag(const __grid_constant__ CUtensorM
   __shared__ unsigned long long gbase;
   __shared__ int sscan[32];
   __shared__ short offs[32];  // [f]: D-box offset, [16 + f]: I-box offset of forward direction f
+  __shared__ TileCoord sc;
+  if (threadIdx.x == 0) {
+    const TileCoord c0 = tile_coord<CONN>((int)blockIdx.x, ntx, nty, g);
+    sc = c0;
+    if (tma) {
+      mbar_init(&bar, 1);
+      mbar_expect_tx(&bar, R::SI * (int)sizeof(Px) + R::SL * 4);
+      tma_load_3d(sI, &mI, c0.bx - R::IXO, c0.by - R::YO, c0.bz, &bar);
+      tma_load_3d(sD, &mD, c0.bx - R::LXO, c0.by - R::YO, c0.bz, &bar);
+    }
+  }
   if (threadIdx.x < R::NF) {
     offs[threadIdx.x] = (short)R::oL(Conn<CONN>::nfwd + threadIdx.x);
     offs[16 + threadIdx.x] = (short)R::oI(Conn<CONN>::nfwd + threadIdx.x);
@@ -504,71 +532,50 @@ __global__ void __launch_bounds__(NT, 5) k_rag(const __grid_constant__ CUtensorM
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 wb = warp_boxes<CONN, Px>();
   uint16_t* wst = stg + warp * R::WCAP;
-  if (tma && threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    if ((int)blockIdx.x < ntiles) {
-      const TileCoord c0 = tile_coord<CONN>(blockIdx.x, ntx, nty, g);
-      mbar_expect_tx(&bar, R::SI * (int)sizeof(Px) + R::SL * 4);
-      tma_load_3d(sI, &mI, c0.bx - R::IXO, c0.by - R::YO, c0.bz, &bar);
-      tma_load_3d(sD, &mD, c0.bx - R::LXO, c0.by - R::YO, c0.bz, &bar);
-    }
+#pragma unroll
+  for (int i = threadIdx.x; i < R::HP; i += NT) {
+    pk[i] = KEY_NONE;
+    if constexpr (!R::PACK) pw[i] = 0xffffffffu;
   }
-  uint32_t phase = 0;
-#pragma unroll 1
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const TileCoord c = tile_coord<CONN>(t, ntx, nty, g);
-    for (int i = threadIdx.x; i < R::HP; i += NT) {
-      pk[i] = KEY_NONE;
-      if constexpr (!R::PACK) pw[i] = 0xffffffffu;
-    }
-    if (tma) {
-      __syncthreads();  // barrier init visible; hash reset done
-      mbar_wait(&bar, phase);
-      phase ^= 1u;
-    } else {
-      rag_load_plain<CONN, Px>(D, I, g, c, sI, sD);
-      __syncthreads();
-    }
-    // 1. detection into the per-warp lists
-    const int n = tile_interior<CONN>(c, g) ? rag_pairs<CONN, false, Px>(sI, sD, pk, pw, wst, wb, offs, g, c, eo)
-                                             : rag_pairs<CONN, true, Px>(sI, sD, pk, pw, wst, wb, offs, g, c, eo);
-    // 2. dedup: every warp folds its own list
-    __syncwarp();
-    fold_warp<CONN, Px>(wst, n, wb, offs, sI, sD, pk, pw, eo);
-    if (eo.recs && lane == 0) atomicAdd(eo.recs, (unsigned long long)n);
-    __syncthreads();  // boxes consumed, hash complete
-    const int tn = t + gridDim.x;
-    if (tma && threadIdx.x == 0 && tn < ntiles) {
-      const TileCoord cn = tile_coord<CONN>(tn, ntx, nty, g);
-      mbar_expect_tx(&bar, R::SI * (int)sizeof(Px) + R::SL * 4);
-      tma_load_3d(sI, &mI, cn.bx - R::IXO, cn.by - R::YO, cn.bz, &bar);
-      tma_load_3d(sD, &mD, cn.bx - R::LXO, cn.by - R::YO, cn.bz, &bar);
-    }
-    // 3. flush: block scan of the per-thread counts, one global atomic per tile
-    constexpr int M = R::HP / NT;  // thread t owns the slots t, t + NT, ... (consecutive lanes,
-                                   // consecutive slots: no bank conflicts)
-    int cnt = 0;
-#pragma unroll
-    for (int m = 0; m < M; ++m) cnt += pk[threadIdx.x + m * NT] != KEY_NONE;
-    int tot;
-    const int ex = block_excl_scan(cnt, sscan, tot);
-    if (threadIdx.x == 0) gbase = tot ? atomicAdd(eo.ecount, (unsigned long long)tot) : 0;
+  __syncthreads();  // tile coordinates and barrier init visible; hash reset done
+  const TileCoord c = sc;
+  if (tma) {
+    mbar_wait(&bar, 0);
+  } else {
+    rag_load_plain<CONN, Px>(D, I, g, c, sI, sD);
     __syncthreads();
-    long long i = (long long)gbase + ex;
+  }
+  // 1. detection into the per-warp lists
+  const int n = tile_interior<CONN>(c, g) ? rag_pairs<CONN, false, Px>(sI, sD, pk, pw, wst, wb, offs, g, c, eo)
+                                           : rag_pairs<CONN, true, Px>(sI, sD, pk, pw, wst, wb, offs, g, c, eo);
+  // 2. dedup: every warp folds its own list
+  __syncwarp();
+  fold_warp<CONN, Px>(wst, n, wb, offs, sI, sD, pk, pw, eo);
+  if (eo.recs && lane == 0) red_add_g(eo.recs, (unsigned long long)n);
+  __syncthreads();  // hash complete
+  // 3. flush: block scan of the per-thread counts, one global atomic per tile
+  constexpr int M = R::HP / NT;  // thread t owns the slots t, t + NT, ... (consecutive lanes,
+                                 // consecutive slots: no bank conflicts)
+  int cnt = 0;
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const unsigned long long key = pk[threadIdx.x + m * NT];
-      if (key == KEY_NONE) continue;
-      if constexpr (R::PACK) {
-        const uint64_t k = make_key((uint32_t)(key & 0xff), (uint32_t)(key >> 36), (uint32_t)(key >> 8) & IDMASK);
-        if (i < eo.cap) eo.edges[i] = k;
-        fold_best(eo.best, k);
-      } else {
-        if (i < eo.cap) eo.e16[i] = make_e16(pw[threadIdx.x + m * NT], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
-      }
-      ++i;
+  for (int m = 0; m < M; ++m) cnt += pk[threadIdx.x + m * NT] != KEY_NONE;
+  int tot;
+  const int ex = block_excl_scan(cnt, sscan, tot);
+  if (threadIdx.x == 0) gbase = tot ? atom_add_g(eo.ecount, (unsigned long long)tot) : 0;
+  __syncthreads();
+  long long i = (long long)gbase + ex;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const unsigned long long key = pk[threadIdx.x + m * NT];
+    if (key == KEY_NONE) continue;
+    if constexpr (R::PACK) {
+      const uint64_t k = make_key((uint32_t)(key & 0xff), (uint32_t)(key >> 36), (uint32_t)(key >> 8) & IDMASK);
+      if (i < eo.cap) eo.edges[i] = k;
+      fold_best(eo.best, k);
+    } else {
+      if (i < eo.cap) eo.e16[i] = make_e16(pw[threadIdx.x + m * NT], (uint32_t)(key >> 28), (uint32_t)(key & IDMASK));
     }
-    __syncthreads();  // flush done before the hash is reset
+    ++i;
   }
 }
 
@@ -879,13 +886,11 @@ static ws_status rag_t(const int* D, const Px* I, const Geo& g, const EdgeOut& e
   const bool a = !off && encode_tmap_3d(&mp.mI, (int)sizeof(Px), I, g, R::SXI, R::SY, R::SZ);
   const bool b = !off && encode_tmap_3d(&mp.mL, 4, D, g, R::SXL, R::SY, R::SZ);
   mp.tma = (a && b) ? 1 : 0;
+  // one tile per CTA (a persistent grid interleaves distant tiles in the edge list and
+  // measured slower overall)
+  const int grid = ntx * nty * ntz;
   WS_CUDA(cudaFuncSetAttribute(k_rag<CONN, Px>, cudaFuncAttributeMaxDynamicSharedMemorySize, R::SMEM));
-  // one tile per CTA: CTAs running together hold neighbouring tiles, so the edge list comes
-  // out in tile order (the level loop's per-chunk dedup and comp gathers depend on it; a
-  // persistent grid interleaves distant tiles and measured slower overall)
-  const int ntiles = ntx * nty * ntz;
-  const int grid = ntiles;
-  k_rag<CONN, Px><<<grid, NT, R::SMEM, st>>>(mp.mI, mp.mL, mp.tma, D, I, g, ntx, nty, ntiles, eo);
+  k_rag<CONN, Px><<<grid, NT, R::SMEM, st>>>(mp.mI, mp.mL, mp.tma, D, I, g, ntx, nty, eo);
   WS_CUDA(cudaGetLastError());
   return WS_OK;
 }
