@@ -572,6 +572,11 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
                                              int* __restrict__ P, int* __restrict__ dist, const PairOut& po) {
   using T = TL<CONN>;
   uint32_t minmask = 0;  // bit k: voxel k of this thread is on a minimal plateau (or a strict minimum)
+  // 2-D tiles: minimal-plateau voxels start at their smallest in-tile backward equal neighbour
+  // (parent initialisation) and only the other backward neighbours are united -- large flat
+  // minimal plateaux (C5, C2) then do not contend for one growing root.  3-D tiles keep every
+  // minimal voxel as its own root (C4: fewer instructions in this issue-bound kernel).
+  constexpr bool PINIT = !Conn<CONN>::is3d;
   uint32_t gmask = 0;    // bit k: gk[k] holds sG[j] (stored once sD is dead: sG aliases sD)
   int gk[T::VPT];
 #pragma unroll
@@ -625,7 +630,18 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
     if (minimal) {
       minmask |= 1u << k;
       sP[j] = -2;  // root (set after the in-tile union below)
-      gk[k] = j;   // union-find parent (local index)
+      int par = j;  // union-find parent (local index)
+      if constexpr (PINIT) {
+#pragma unroll
+        for (int i = Conn<CONN>::nfwd - 1; i >= 0; --i) {
+          int dz, dy, dx;
+          nb_delta(CONN, i, dz, dy, dx);
+          if ((eqm & (1u << i)) && (unsigned)(lx + dx) < (unsigned)T::TX && (unsigned)(ly + dy) < (unsigned)T::TY &&
+              (unsigned)(lz + dz) < (unsigned)T::TZ)
+            par = j + (dz * T::TY + dy) * T::TX + dx;
+        }
+      }
+      gk[k] = par;
       gmask |= 1u << k;
     } else {
       int dz, dy, dx;
@@ -657,6 +673,21 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
       const int si = T::iI(lz, ly, lx);
       const int v = sI[si];
       const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
+      if constexpr (PINIT) {  // in-tile backward equal neighbours other than the parent
+        bool first = true;
+#pragma unroll
+        for (int i = 0; i < Conn<CONN>::nfwd; ++i) {
+          int dz, dy, dx;
+          nb_delta(CONN, i, dz, dy, dx);
+          const int nx = lx + dx, ny = ly + dy, nz = lz + dz;
+          if (!((unsigned)nx < (unsigned)T::TX && (unsigned)ny < (unsigned)T::TY && (unsigned)nz < (unsigned)T::TZ))
+            continue;
+          if (BORDER && !(vm & (1u << i))) continue;
+          if (sI[si + T::oI(i)] != v) continue;
+          if (!first) s_unite(sG, j, j + (dz * T::TY + dy) * T::TX + dx);
+          first = false;
+        }
+      }
 #pragma unroll
       for (int i = Conn<CONN>::nfwd; i < CONN; ++i) {
         if (sI[si + T::oI(i)] != v) continue;
@@ -665,7 +696,7 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
         const int nx = lx + dx, ny = ly + dy, nz = lz + dz;
         if (BORDER && (!(vm & (1u << i)) || c.bz + nz >= g.zhi)) continue;  // cut plane: ws_shard_merge
         if ((unsigned)nx < (unsigned)T::TX && (unsigned)ny < (unsigned)T::TY && (unsigned)nz < (unsigned)T::TZ) {
-          s_unite(sG, j, j + (dz * T::TY + dy) * T::TX + dx);
+          if constexpr (!PINIT) s_unite(sG, j, j + (dz * T::TY + dy) * T::TX + dx);
         } else {
           const int p = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx) + g.gofs;
           const int2 e = make_int2(p, p + nb_off<CONN>(g, i));
