@@ -128,22 +128,27 @@ __device__ __forceinline__ void stage(const CUtensorMap* mI, const CUtensorMap* 
     }
     mbar_wait(bar, 0);
   } else {
-    for (int s = threadIdx.x; s < T::SI; s += NT) {
-      const int sx = s % T::SXI, sy = (s / T::SXI) % T::SYI, sz = s / (T::SXI * T::SYI);
-      const int gx = c.bx + sx - T::IXO, gy = c.by + sy - T::IYO, gz = c.bz + sz - T::IZO;
-      Px v = 0;
-      if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
-        v = __ldg(I + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
-      sI[s] = v;
+    // plain loader (layouts without a tensor map, e.g. rows not a multiple of 16 bytes): one
+    // warp per box row, lanes along x (no per-element index division), zero fill outside
+    const int lane = threadIdx.x & 31;
+    for (int r = threadIdx.x >> 5; r < T::SYI * T::SZI; r += NT / 32) {
+      const int gy = c.by + r % T::SYI - T::IYO, gz = c.bz + r / T::SYI - T::IZO;
+      const bool rok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
+      const Px* row = I + ((size_t)gz * g.plane + (size_t)gy * g.n2);
+      for (int sx = lane; sx < T::SXI; sx += 32) {
+        const int gx = c.bx + sx - T::IXO;
+        sI[r * T::SXI + sx] = (rok && (unsigned)gx < (unsigned)g.n2) ? __ldg(row + gx) : (Px)0;
+      }
     }
     if (sL) {
-      for (int s = threadIdx.x; s < T::SL; s += NT) {
-        const int sx = s % T::SXL, sy = (s / T::SXL) % T::SYL, sz = s / (T::SXL * T::SYL);
-        const int gx = c.bx + sx - T::LXO, gy = c.by + sy - T::LYO, gz = c.bz + sz - T::LZO;
-        int v = 0;
-        if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
-          v = L[(size_t)gz * g.plane + (size_t)gy * g.n2 + gx];
-        sL[s] = v;
+      for (int r = threadIdx.x >> 5; r < T::SYL * T::SZL; r += NT / 32) {
+        const int gy = c.by + r % T::SYL - T::LYO, gz = c.bz + r / T::SYL - T::LZO;
+        const bool rok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
+        const int* row = L + ((size_t)gz * g.plane + (size_t)gy * g.n2);
+        for (int sx = lane; sx < T::SXL; sx += 32) {
+          const int gx = c.bx + sx - T::LXO;
+          sL[r * T::SXL + sx] = (rok && (unsigned)gx < (unsigned)g.n2) ? row[gx] : 0;
+        }
       }
     }
     __syncthreads();

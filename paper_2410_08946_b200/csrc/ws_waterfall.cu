@@ -476,21 +476,20 @@ template <int CONN, class Px>
 __device__ __forceinline__ void rag_load_plain(const int* __restrict__ D, const Px* __restrict__ I, const Geo& g,
                                                const TileCoord& c, Px* sI, int* sD) {
   using R = RL<CONN, Px>;
-  for (int s = threadIdx.x; s < R::SI; s += NT) {
-    const int sx = s % R::SXI, sy = (s / R::SXI) % R::SY, sz = s / (R::SXI * R::SY);
-    const int gx = c.bx + sx - R::IXO, gy = c.by + sy - R::YO, gz = c.bz + sz;
-    Px v = 0;
-    if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
-      v = __ldg(I + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
-    sI[s] = v;
-  }
-  for (int s = threadIdx.x; s < R::SL; s += NT) {
-    const int sx = s % R::SXL, sy = (s / R::SXL) % R::SY, sz = s / (R::SXL * R::SY);
-    const int gx = c.bx + sx - R::LXO, gy = c.by + sy - R::YO, gz = c.bz + sz;
-    int v = 0;
-    if ((unsigned)gx < (unsigned)g.n2 && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0)
-      v = __ldg(D + (size_t)gz * g.plane + (size_t)gy * g.n2 + gx);
-    sD[s] = v;
+  // one warp per box row, lanes along x (no per-element index division), zero fill outside
+  const int lane = threadIdx.x & 31;
+  for (int r = threadIdx.x >> 5; r < R::SY * R::SZ; r += NT / 32) {
+    const int gy = c.by + r % R::SY - R::YO, gz = c.bz + r / R::SY;
+    const bool rok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
+    const size_t ro = (size_t)gz * g.plane + (size_t)gy * g.n2;
+    for (int sx = lane; sx < R::SXI; sx += 32) {
+      const int gx = c.bx + sx - R::IXO;
+      sI[r * R::SXI + sx] = (rok && (unsigned)gx < (unsigned)g.n2) ? __ldg(I + ro + gx) : (Px)0;
+    }
+    for (int sx = lane; sx < R::SXL; sx += 32) {
+      const int gx = c.bx + sx - R::LXO;
+      sD[r * R::SXL + sx] = (rok && (unsigned)gx < (unsigned)g.n2) ? __ldg(D + ro + gx) : 0;
+    }
   }
 }
 
