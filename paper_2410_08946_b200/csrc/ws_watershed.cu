@@ -577,6 +577,13 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
   // minimal plateaux (C5, C2) then do not contend for one growing root.  3-D tiles keep every
   // minimal voxel as its own root (C4: fewer instructions in this issue-bound kernel).
   constexpr bool PINIT = !Conn<CONN>::is3d;
+  // 4-connectivity: the parent comes from the row runs instead -- a warp holds 32 consecutive
+  // voxels of one tile row, a ballot of "equal to my left neighbour" gives every plateau voxel
+  // its run start (the run's smallest index) as parent, and vertical unions are needed only
+  // where one of the two vertically adjacent runs starts (the leftmost voxel of their overlap)
+  constexpr bool RUNS = (CONN == 4);
+  __shared__ unsigned sStart[RUNS ? T::V / 32 : 1];  // bit: the voxel starts its row run
+  uint32_t leqm = 0;     // RUNS: bit k: voxel k is minimal and equal to its in-tile left neighbour
   uint32_t gmask = 0;    // bit k: gk[k] holds sG[j] (stored once sD is dead: sG aliases sD)
   int gk[T::VPT];
 #pragma unroll
@@ -630,8 +637,10 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
     if (minimal) {
       minmask |= 1u << k;
       sP[j] = -2;  // root (set after the in-tile union below)
-      int par = j;  // union-find parent (local index)
-      if constexpr (PINIT) {
+      int par = j;  // union-find parent (local index; RUNS: set with the row ballot below)
+      if constexpr (RUNS) {
+        if (((eqm >> 1) & 1u) && lx > 0) leqm |= 1u << k;  // direction 1 = (0, 0, -1)
+      } else if constexpr (PINIT) {
 #pragma unroll
         for (int i = Conn<CONN>::nfwd - 1; i >= 0; --i) {
           int dz, dy, dx;
@@ -662,8 +671,20 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
   // flushed with one global atomic per tile.
   const bool anymin = __syncthreads_or(minmask != 0);  // sD is dead from here on
 #pragma unroll
-  for (int k = 0; k < T::VPT; ++k)
-    if (gmask & (1u << k)) sG[threadIdx.x + k * NT] = gk[k];
+  for (int k = 0; k < T::VPT; ++k) {
+    const int j = threadIdx.x + k * NT;
+    int val = gk[k];
+    if constexpr (RUNS) {
+      const int lane = threadIdx.x & 31;
+      const unsigned b = __ballot_sync(0xffffffffu, (leqm >> k) & 1u);
+      if (lane == 0) sStart[j >> 5] = ~b;
+      if ((leqm >> k) & 1u) {
+        const unsigned st = ~b & ((2u << lane) - 1u);  // run starts at or left of me in this warp
+        val = st ? j - (lane - (31 - __clz(st))) : (lane ? j - lane : j - 1);
+      }
+    }
+    if (gmask & (1u << k)) sG[j] = val;
+  }
   __syncthreads();
   if (anymin) {
     for (uint32_t mm = minmask; mm; mm &= mm - 1) {
@@ -673,7 +694,12 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
       const int si = T::iI(lz, ly, lx);
       const int v = sI[si];
       const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
-      if constexpr (PINIT) {  // in-tile backward equal neighbours other than the parent
+      if constexpr (RUNS) {  // vertical: where one of the two runs starts
+        if (ly > 0 && (!BORDER || (vm & 1u)) && sI[si + T::oI(0)] == v) {
+          const int u = j - T::TX;
+          if (((sStart[j >> 5] >> (j & 31)) & 1u) || ((sStart[u >> 5] >> (u & 31)) & 1u)) s_unite(sG, j, u);
+        }
+      } else if constexpr (PINIT) {  // in-tile backward equal neighbours other than the parent
         bool first = true;
 #pragma unroll
         for (int i = 0; i < Conn<CONN>::nfwd; ++i) {
