@@ -435,7 +435,9 @@ __device__ __forceinline__ float u8f(unsigned w, int k) {  // byte k of w as an 
   return __int_as_float((int)__byte_perm(w, 0x4B000000u, 0x7650u + k)) - 8388608.f;
 }
 
-template <int R>
+// F32: the optional fp32 outputs (blur / gradient magnitude) were requested (parity tests);
+// the quantised path has no per-voxel branch for them
+template <int R, bool F32>
 __global__ void __launch_bounds__(256, 3) k_grad_s2(const uint8_t* __restrict__ img, Geo g, int ntx, int nty,
                                                    uint8_t* __restrict__ q, float* __restrict__ blur_out,
                                                    float* __restrict__ grad_out, const __grid_constant__ BlurW W) {
@@ -505,6 +507,9 @@ __global__ void __launch_bounds__(256, 3) k_grad_s2(const uint8_t* __restrict__ 
   const int gx = bx + tid % G2X, gg = tid / G2X, gy0 = by + 4 * gg;
   const bool inner = bx > 0 && bx + G2X < g.n2 && by > 0 && by + G2Y < g.n1;
   const int nin = (z1 - z0) + 2 * H;  // input planes z0 - H .. z1 + H - 1
+  // ring slots without integer modulo: plane t goes to XY slot xs = t % K, its z blur (plane
+  // tb = t - 2R) reads slots (tb + i) % K = (xs + 1 + i) % K, the B ring advances mod 3
+  int xs = 0, bs = 0;
   load(z0 - H);
 #pragma unroll 1
   for (int t = 0; t < nin; ++t) {
@@ -544,7 +549,7 @@ __global__ void __launch_bounds__(256, 3) k_grad_s2(const uint8_t* __restrict__ 
       float2 xv[3 + 2 * R];
 #pragma unroll
       for (int i = 0; i < 3 + 2 * R; ++i) xv[i] = *reinterpret_cast<const float2*>(X + (3 * yg + i) * XP + 2 * yp);
-      float* ring = XY + (t % K) * YR * YP;
+      float* ring = XY + xs * YR * YP;
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
         float2 acc = make_float2(0.f, 0.f);
@@ -553,28 +558,33 @@ __global__ void __launch_bounds__(256, 3) k_grad_s2(const uint8_t* __restrict__ 
         *reinterpret_cast<float2*>(ring + (3 * yg + r) * YP + 2 * yp) = acc;
       }
       if (tb >= 0) {
-        float* Bt = B + (tb % 3) * YR * YP;
+        float* Bt = B + bs * YR * YP;
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
           const int off = (3 * yg + r) * YP + 2 * yp;
           float2 acc = make_float2(0.f, 0.f);
+          int sl = xs + 1 == K ? 0 : xs + 1;  // plane zi - R - R + i sits in ring slot (t - 2R + i) % K
 #pragma unroll
-          for (int i = 0; i < K; ++i)  // plane zi - R - R + i sits in ring slot (t - 2R + i) % K
-            acc = __ffma2_rn(make_float2(W.w[i], W.w[i]),
-                             *reinterpret_cast<const float2*>(XY + ((tb + i) % K) * YR * YP + off), acc);
+          for (int i = 0; i < K; ++i) {
+            acc = __ffma2_rn(make_float2(W.w[i], W.w[i]), *reinterpret_cast<const float2*>(XY + sl * YR * YP + off), acc);
+            sl = sl + 1 == K ? 0 : sl + 1;
+          }
           *reinterpret_cast<float2*>(Bt + off) = acc;
         }
       }
     }
+    const int bc = bs;  // B slot of plane tb (this plane's z blur)
+    xs = xs + 1 == K ? 0 : xs + 1;
+    if (tb >= 0) bs = bs == 2 ? 0 : bs + 1;
     if (tb < 2) continue;  // (uniform) the next plane's barrier (A) orders the rings
     __syncthreads();  // (C) B ring visible
     // gradient of plane zo = zi - R - 1 (blurred planes zo - 1, zo, zo + 1 in the B ring):
     // lanes along x (conflict-free ring reads), 4 consecutive rows per thread
     const int zo = zi - R - 1;
     if (zo < z0 || zo >= z1 || gx >= g.n2) continue;
-    const float* Bm = B + ((tb - 2) % 3) * YR * YP;
-    const float* Bc = B + ((tb - 1) % 3) * YR * YP;
-    const float* Bp = B + (tb % 3) * YR * YP;
+    const float* Bp = B + bc * YR * YP;                      // plane tb
+    const float* Bc = B + (bc == 0 ? 2 : bc - 1) * YR * YP;  // tb - 1
+    const float* Bm = B + (bc == 2 ? 0 : bc + 1) * YR * YP;  // tb - 2
     const int ci = gx - bx + 1;  // ring column of x
     const bool zin = zo > 0 && zo < g.n0 - 1;
     float col[6];  // rows gy0 - 1 .. gy0 + 4 at x
@@ -601,12 +611,16 @@ __global__ void __launch_bounds__(256, 3) k_grad_s2(const uint8_t* __restrict__ 
       ss = fmaf(dx, dx, ss);
       ss = fmaf(dy, dy, ss);
       ss = fmaf(dz, dz, ss);
-      const float gm = sqrtf(ss);
+      // sqrt.approx (MUFU, ~1 ulp): far inside the 1e-5 tolerance of C11
+      float gm;
+      asm("sqrt.approx.f32 %0, %1;" : "=f"(gm) : "f"(ss));
       const float qq = floorf(fmaf(255.f, gm, 0.5f));
       const size_t p = (size_t)zo * g.plane + (size_t)gy * g.n2 + gx;
       q[p] = (uint8_t)(qq > 255.f ? 255.f : qq);
-      if (blur_out) blur_out[p] = v;
-      if (grad_out) grad_out[p] = gm;
+      if constexpr (F32) {
+        if (blur_out) blur_out[p] = v;
+        if (grad_out) grad_out[p] = gm;
+      }
     }
   }
 }
@@ -618,8 +632,15 @@ static ws_status grad_stream_t(ws_ctx* ctx, const Px* img, const Geo& g, Px* q, 
     const char* v1 = getenv("WS_GRAD_V1");  // A/B and parity of the v1 kernel
     if (!(v1 && v1[0] == '1')) {
       const int ntx = (g.n2 + G2X - 1) / G2X, nty = (g.n1 + G2Y - 1) / G2Y, ntz = (g.n0 + G2Z - 1) / G2Z;
-      WS_CUDA(cudaFuncSetAttribute(k_grad_s2<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, G2Smem<R>::bytes));
-      k_grad_s2<R><<<ntx * nty * ntz, 256, G2Smem<R>::bytes, st>>>(img, g, ntx, nty, q, blur, grad, W);
+      if (blur || grad) {
+        WS_CUDA(cudaFuncSetAttribute(k_grad_s2<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     G2Smem<R>::bytes));
+        k_grad_s2<R, true><<<ntx * nty * ntz, 256, G2Smem<R>::bytes, st>>>(img, g, ntx, nty, q, blur, grad, W);
+      } else {
+        WS_CUDA(cudaFuncSetAttribute(k_grad_s2<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     G2Smem<R>::bytes));
+        k_grad_s2<R, false><<<ntx * nty * ntz, 256, G2Smem<R>::bytes, st>>>(img, g, ntx, nty, q, blur, grad, W);
+      }
       launched(ctx, PH_GRAD_MAG);
       tmark(ctx, st, PH_GRAD_MAG);
       WS_CUDA(cudaGetLastError());
