@@ -558,19 +558,20 @@ __global__ void __launch_bounds__(256, 3) k_grad_s2(const uint8_t* __restrict__ 
         *reinterpret_cast<float2*>(ring + (3 * yg + r) * YP + 2 * yp) = acc;
       }
       if (tb >= 0) {
-        float* Bt = B + bs * YR * YP;
+        const int off = 3 * yg * YP + 2 * yp;
+        float2 acc[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        int sl = xs + 1 == K ? 0 : xs + 1;  // plane zi - R - R + i sits in ring slot (t - 2R + i) % K
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
-          const int off = (3 * yg + r) * YP + 2 * yp;
-          float2 acc = make_float2(0.f, 0.f);
-          int sl = xs + 1 == K ? 0 : xs + 1;  // plane zi - R - R + i sits in ring slot (t - 2R + i) % K
+        for (int i = 0; i < K; ++i) {  // tap-major: one slot address per tap for the 3 rows
+          const float* src = XY + sl * YR * YP + off;
+          const float2 wi = make_float2(W.w[i], W.w[i]);
 #pragma unroll
-          for (int i = 0; i < K; ++i) {
-            acc = __ffma2_rn(make_float2(W.w[i], W.w[i]), *reinterpret_cast<const float2*>(XY + sl * YR * YP + off), acc);
-            sl = sl + 1 == K ? 0 : sl + 1;
-          }
-          *reinterpret_cast<float2*>(Bt + off) = acc;
+          for (int r = 0; r < 3; ++r) acc[r] = __ffma2_rn(wi, *reinterpret_cast<const float2*>(src + r * YP), acc[r]);
+          sl = sl + 1 == K ? 0 : sl + 1;
         }
+        float* Bt = B + bs * YR * YP + off;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) *reinterpret_cast<float2*>(Bt + r * YP) = acc[r];
       }
     }
     const int bc = bs;  // B slot of plane tb (this plane's z blur)
