@@ -876,6 +876,79 @@ __global__ void __launch_bounds__(NT) k_jump(int* P, int* __restrict__ L, int N,
   }
 }
 
+// The same with V voxels per thread (p, p + NT, ... of a V NT window): every chase's first
+// load and first hop is issued before any is consumed (V times the loads in flight of a
+// latency-bound kernel, 1/V of the loop iterations); the rare longer chases (tile exits) follow.
+__device__ __forceinline__ int chase_tail(int* P, int p, int t, int nt) {
+  // t = P[p] != p and nt = P[t] != t: follow to the root, compress p
+  do {
+    t = nt;
+    nt = P[t];
+  } while (nt != t);
+  P[p] = t;
+  return t;
+}
+
+template <int V>
+__global__ void __launch_bounds__(NT) k_jumpv(int* P, int* __restrict__ L, int N, int* roots, int cap, int* nroots) {
+  constexpr int SB = 2 * V * NT > RBUF ? 2 * V * NT : RBUF;  // staged roots (two iterations' worth)
+  __shared__ int sbuf[SB];
+  __shared__ int scount, sbase;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1;
+  if (threadIdx.x == 0) scount = 0;
+  __syncthreads();
+  const int stride = gridDim.x * V * NT;
+  int cnt = 0;
+  for (int p0 = blockIdx.x * V * NT; p0 < N; p0 += stride) {
+    int t[V], n[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int p = p0 + v * NT + threadIdx.x;
+      t[v] = p < N ? P[p] : p;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int p = p0 + v * NT + threadIdx.x;
+      n[v] = t[v] != p ? P[t[v]] : t[v];
+    }
+    int nr = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int p = p0 + v * NT + threadIdx.x;
+      const bool valid = p < N;
+      if (n[v] != t[v]) t[v] = chase_tail(P, p, t[v], n[v]);
+      if (!valid) t[v] = -1 - lane;  // unique per lane (never equals a neighbour's root)
+      const int pr = __shfl_up_sync(0xffffffffu, t[v], 1);
+      if (valid && (lane == 0 || pr != t[v])) atomicMax(L + t[v], INT_MAX - p);
+      const bool isr = valid && t[v] == p;
+      const unsigned rb = __ballot_sync(0xffffffffu, isr);
+      if (rb) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&scount, __popc(rb));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (isr) sbuf[base + __popc(rb & lt)] = p;
+      }
+      nr += isr;
+    }
+    // block-uniform count of the staged roots: every thread reads scount between two barriers
+    __syncthreads();
+    cnt = scount;
+    __syncthreads();
+    if (cnt > SB - V * NT || p0 + stride >= N) {  // flush the staged roots
+      if (cnt > 0) {
+        if (threadIdx.x == 0) sbase = atomicAdd(nroots, cnt);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += NT)
+          if (sbase + i < cap) roots[sbase + i] = sbuf[i];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) scount = 0;
+      __syncthreads();
+    }
+  }
+}
+
 // rebuild the root list (only if k_jump's list overflowed): roots are P[p] == p
 __global__ void k_collect_roots(const int* __restrict__ P, int N, int* roots, int* nroots) {
   for (int p0 = blockIdx.x * NT; p0 < N; p0 += gridDim.x * NT) {
@@ -1168,6 +1241,24 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   return WS_OK;
 }
 
+// step III across tiles: k_jumpv with V voxels per thread (WS_JUMP_V = 1, 2, 4, 8; default 4;
+// 1 = the one-voxel k_jump)
+static ws_status launch_jump(ws_ctx* ctx, int* P, int* L, int N, int cap, int* nr, cudaStream_t st) {
+  const char* e = getenv("WS_JUMP_V");
+  const int v = e ? atoi(e) : 4;
+  int* roots = ctx->roots.as<int>();
+  if (v == 1)
+    k_jump<<<grid1d(N, ctx->num_sms), NT, 0, st>>>(P, L, N, roots, cap, nr);
+  else if (v == 2)
+    k_jumpv<2><<<grid1d(N / 2 + 1, ctx->num_sms), NT, 0, st>>>(P, L, N, roots, cap, nr);
+  else if (v == 8)
+    k_jumpv<8><<<grid1d(N / 8 + 1, ctx->num_sms), NT, 0, st>>>(P, L, N, roots, cap, nr);
+  else
+    k_jumpv<4><<<grid1d(N / 4 + 1, ctx->num_sms), NT, 0, st>>>(P, L, N, roots, cap, nr);
+  WS_CUDA(cudaGetLastError());
+  return WS_OK;
+}
+
 // cross-tile step IV pair list of k_resolve: ctx->upairs, counter at flags int 10
 static ws_status pair_out(ws_ctx* ctx, const Geo& g, PairOut& po, cudaStream_t st) {
   const size_t own = (size_t)(g.zhi - g.zlo) * g.plane;
@@ -1231,7 +1322,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
         P, po.pairs, po.cap, po.npairs);
     launched(ctx, PH_WS_UNION);
     tmark(ctx, st, PH_WS_UNION);
-    k_jump<<<grid1d(g.N, ctx->num_sms), NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
+    WS_TRY(launch_jump(ctx, P, L, g.N, (int)cap, nr, st));
     launched(ctx, PH_WS_JUMP);
     tmark(ctx, st, PH_WS_JUMP);
     k_root_canon<<<grid1d((long long)g.N / 32, ctx->num_sms), NT, 0, st>>>(P, L, ctx->roots.as<int>(), nr, (int)cap,
@@ -1258,7 +1349,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
       launched(ctx, PH_WS_UNION);
     }
     tmark(ctx, st, PH_WS_UNION);
-    k_jump<<<gN, NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
+    WS_TRY(launch_jump(ctx, P, L, g.N, (int)cap, nr, st));
     launched(ctx, PH_WS_JUMP);
     tmark(ctx, st, PH_WS_JUMP);
     k_root_canon<<<grid1d((long long)g.N / 32, ctx->num_sms), NT, 0, st>>>(P, L, roots, nr, (int)cap, bits);
@@ -1307,7 +1398,7 @@ static ws_status watershed_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_t*
   // many cross-tile pairs: chase first (per-root minima on the tiles' roots), then the union
   // (the pair list, or the full q > p scan when it overflowed), then merge the minima into
   // the final roots
-  k_jump<<<gN, NT, 0, st>>>(P, L, g.N, ctx->roots.as<int>(), (int)cap, nr);
+  WS_TRY(launch_jump(ctx, P, L, g.N, (int)cap, nr, st));
   launched(ctx, PH_WS_JUMP);
   WS_CUDA(cudaMemcpyAsync(ctx->pinned, nr, sizeof(int), cudaMemcpyDeviceToHost, st));
   WS_CUDA(cudaStreamSynchronize(st));
