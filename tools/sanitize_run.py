@@ -50,6 +50,13 @@ for name, shape, conn, nd in (("C1", None, 4, 2), ("C4", (20, 48, 64), 6, 3), ("
         assert np.array_equal(lvs.cpu().numpy(), rlv)
     print("segment", name, conn, "ok")
 
+# large flat minimal plateaux on 2-D tiles (the row-run / parent-initialised in-tile union)
+for conn in (4, 8):
+    g2 = synth.random_plateau_image((2, 96, 130), 2, seed=conn).cuda()
+    lab2, _ = ws.watershed(g2, conn, ndim=2)
+    assert np.array_equal(lab2.cpu().numpy(), oracle.watershed(g2.cpu().numpy(), conn, ndim=2))
+    print("plateau2d", conn, "ok")
+
 # 16-bit images (NEXT f4): gradient (streaming kernel and generic path) + watershed
 rng = np.random.default_rng(7)
 for shape, conn, nd, sig in (((20, 48, 64), 6, 3, 1.0), ((18, 40, 36), 26, 3, 2.0), ((2, 70, 96), 8, 2, 1.0)):
