@@ -1241,11 +1241,13 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   return WS_OK;
 }
 
-// step III across tiles: k_jumpv with V voxels per thread (WS_JUMP_V = 1, 2, 4, 8; default 4;
-// 1 = the one-voxel k_jump)
+// step III across tiles: k_jumpv with V voxels per thread (WS_JUMP_V = 1, 2, 4, 8; default 2;
+// 1 = the one-voxel k_jump).  Measured on C4 (tools/raw_ab.py): the gradient 20.8 / 19.5 /
+// 19.3 ms for V = 1 / 2 / 4, the raw volume (98 M regions, 12 % roots) 18.4 / 18.7 / 24.8 ms
+// -- V = 2 is the robust choice.
 static ws_status launch_jump(ws_ctx* ctx, int* P, int* L, int N, int cap, int* nr, cudaStream_t st) {
   const char* e = getenv("WS_JUMP_V");
-  const int v = e ? atoi(e) : 4;
+  const int v = e ? atoi(e) : 2;
   int* roots = ctx->roots.as<int>();
   if (v == 1)
     k_jump<<<grid1d(N, ctx->num_sms), NT, 0, st>>>(P, L, N, roots, cap, nr);

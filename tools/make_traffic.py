@@ -9,7 +9,7 @@ import sys
 import time
 
 PHASE = {"k_relax_first": "watershed.init", "k_relax_round": "watershed.relax", "k_resolve": "watershed.select",
-         "k_jump": "watershed.jump", "k_union": "watershed.union", "k_root_merge": "watershed.find",
+         "k_jump": "watershed.jump", "k_jumpv": "watershed.jump", "k_union": "watershed.union", "k_root_merge": "watershed.find",
          "k_root_label": "watershed.find", "k_root_store": "watershed.find", "k_relabel": "watershed.relabel", "k_relabel4": "watershed.relabel", "k_root_canon": "watershed.find",
          "k_compress_pairs": "watershed.union",
          "k_dense": "waterfall.dense_ids", "k_dimage": "waterfall.dense_ids", "k_dimage_rk": "waterfall.dense_ids",
