@@ -60,6 +60,7 @@ struct ws_ctx {
   int device = 0;
   int num_sms = 148;
   int coop = 0;       // cooperative launches available (the device-side step II loop); WS_NO_COOP=1 disables
+  int edges_occ = 0;  // resident k_edges CTAs per SM (queried once per context)
   ws::Buf aux;        // i32[N]   union-find canonical minima / dense ids (indexed by label)
   ws::Buf tmpA, tmpB; // f32[N]   gradient pre-pass intermediates
   ws::Buf flags;      // small device counters / flags

@@ -1095,7 +1095,7 @@ static ws_status wf_level(ws_ctx* ctx, bool edges_next, cudaStream_t st) {
     const int esmem = EHC * 16;
     WS_CUDA(cudaFuncSetAttribute(k_edges, cudaFuncAttributeMaxDynamicSharedMemorySize, esmem));
     // one wave of resident CTAs walking the chunks (no partial last wave)
-    static int occ = 0;
+    int& occ = ctx->edges_occ;  // per context (per device), computed once
     if (!occ) WS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_edges, NTW, esmem));
     const long long chunks = (w.E + ECH - 1) / ECH;
     const int grid = (int)std::min<long long>(chunks, (long long)ctx->num_sms * std::max(1, occ));
