@@ -233,7 +233,7 @@ ws_status ws_ctx_destroy(ws_ctx* ctx) {
   cudaSetDevice(ctx->device);
   ws::Buf* bufs[] = {&ctx->aux, &ctx->tmpA, &ctx->tmpB, &ctx->flags, &ctx->tiles, &ctx->roots, &ctx->rootc, &ctx->blockcnt, &ctx->edges, &ctx->ebufA, &ctx->ebufB, &ctx->rootsA, &ctx->rootsB, &ctx->lvl,
                      &ctx->comp, &ctx->best, &ctx->rep_of, &ctx->levelmap, &ctx->lvcount,
-                     &ctx->h_grad, &ctx->h_labels, &ctx->h_levels, &ctx->dimg, &ctx->sroots, &ctx->sblocks, &ctx->rank, &ctx->wimg, &ctx->vstate, &ctx->nmin, &ctx->tlist, &ctx->upairs, &ctx->exitmx,
+                     &ctx->h_grad, &ctx->h_labels, &ctx->h_levels, &ctx->dimg, &ctx->sroots, &ctx->sblocks, &ctx->rank, &ctx->wimg, &ctx->vstate, &ctx->nmin, &ctx->tlist, &ctx->upairs, &ctx->eqc, &ctx->exitmx,
                      &ctx->mtables, &ctx->mslabs, &ctx->mr0, &ctx->mmap, &ctx->pathc, &ctx->best_lo, &ctx->repbits,
                      &ctx->sh_L, &ctx->sh_P, &ctx->sh_planes, &ctx->sh_tab, &ctx->sh_alltab, &ctx->sh_ec, &ctx->sh_lab,
                      &ctx->sh_dense, &ctx->sh_rep, &ctx->sh_bt, &ctx->sh_allbt, &ctx->sh_lext, &ctx->sh_best,

@@ -68,6 +68,7 @@ struct ws_ctx {
   ws::Buf tlist;      // i32[ntiles]  compacted active tiles of the next step II round
   ws::Buf roots;      // i32[cap]  step III roots (self-loops), compact list
   ws::Buf upairs;     // int2[cap] step IV pairs crossing a tile face (k_resolve -> k_union_pairs)
+  ws::Buf eqc;        // u8[ntiles * 2048] step II equal-neighbour masks (k_relax_first -> later rounds)
   ws::Buf rootc;      // i32[cap]  canonical label per listed root
   ws::Buf blockcnt;   // per-block look-back status words of the dense-id scan
   ws::Buf edges;      // u64[cap] RAG edge keys (level 1)

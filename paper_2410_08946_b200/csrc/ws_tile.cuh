@@ -110,7 +110,8 @@ __device__ __forceinline__ unsigned valid_mask(const Geo& g, int gz, int gy, int
   return m;
 }
 
-// Stage the I box (and optionally the L box, as raw L values) into shared memory: one
+// Stage the I box (sI may be null: L box only) and optionally the L box (raw L values) into
+// shared memory: one
 // cp.async.bulk.tensor per box (TMA zero-fills outside the volume), or a plain loader when
 // the layout has no tensor map.
 template <int CONN, class Px>
@@ -122,8 +123,8 @@ __device__ __forceinline__ void stage(const CUtensorMap* mI, const CUtensorMap* 
     if (threadIdx.x == 0) mbar_init(bar, 1);
     __syncthreads();
     if (threadIdx.x == 0) {
-      mbar_expect_tx(bar, T::SI * (int)sizeof(Px) + (sL ? T::SL * 4 : 0));
-      tma_load_3d(sI, mI, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, bar);
+      mbar_expect_tx(bar, (sI ? T::SI * (int)sizeof(Px) : 0) + (sL ? T::SL * 4 : 0));
+      if (sI) tma_load_3d(sI, mI, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, bar);
       if (sL) tma_load_3d(sL, mL, c.bx - T::LXO, c.by - T::LYO, c.bz - T::LZO, bar);
     }
     mbar_wait(bar, 0);
@@ -131,7 +132,7 @@ __device__ __forceinline__ void stage(const CUtensorMap* mI, const CUtensorMap* 
     // plain loader (layouts without a tensor map, e.g. rows not a multiple of 16 bytes): one
     // warp per box row, lanes along x (no per-element index division), zero fill outside
     const int lane = threadIdx.x & 31;
-    for (int r = threadIdx.x >> 5; r < T::SYI * T::SZI; r += NT / 32) {
+    for (int r = threadIdx.x >> 5; sI && r < T::SYI * T::SZI; r += NT / 32) {
       const int gy = c.by + r % T::SYI - T::IYO, gz = c.bz + r / T::SYI - T::IZO;
       const bool rok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
       const Px* row = I + ((size_t)gz * g.plane + (size_t)gy * g.n2);

@@ -318,7 +318,7 @@ __device__ __forceinline__ void classify_box(const Px* sI, int* sD, const Geo& g
 template <int CONN, bool BORDER>
 __device__ __forceinline__ void relax_first_body(const Px* sI, int* sD, int* __restrict__ L, const Geo& g,
                                                  const TileCoord& c, int t, int ntx, int nty, uint8_t* next,
-                                                 uint8_t* hasplat, int* flags, RQ& q) {
+                                                 uint8_t* hasplat, int* flags, RQ& q, uint8_t* eqc) {
   using T = TL<CONN>;
   classify_box<CONN, BORDER>(sI, sD, g, c);
   __syncthreads();
@@ -342,6 +342,19 @@ __device__ __forceinline__ void relax_first_body(const Px* sI, int* sD, int* __r
     }
     eqm[k] = m;
   }
+  if constexpr (CONN <= 8) {
+    // the equal-neighbour masks of this thread's 8 voxels (one byte each) for the later step II
+    // rounds, which then stage only the L box (tile-major, thread-major inside the tile)
+    if (eqc) {
+      uint2 w = make_uint2(0u, 0u);
+#pragma unroll
+      for (int k = 0; k < T::VPT; ++k) {
+        if (k < 4) w.x |= eqm[k] << (8 * k);
+        else w.y |= eqm[k] << (8 * (k - 4));
+      }
+      reinterpret_cast<uint2*>(eqc + (size_t)t * T::V)[threadIdx.x] = w;
+    }
+  }
   relax_tile_q<CONN, false>(sD, s0, eqm, flags + 1, q);
   // every voxel is written once: 0 (d = 0) or the plateau code
 #pragma unroll
@@ -362,7 +375,8 @@ __device__ __forceinline__ void relax_first_body(const Px* sI, int* sD, int* __r
 template <int CONN>
 __global__ void __launch_bounds__(NT) k_relax_first(const __grid_constant__ CUtensorMap mI, int tma,
                                                      const Px* __restrict__ I, int* __restrict__ L, Geo g,
-                                                     int ntx, int nty, uint8_t* next, uint8_t* hasplat, int* flags) {
+                                                     int ntx, int nty, uint8_t* next, uint8_t* hasplat, int* flags,
+                                                     uint8_t* eqc) {
   using T = TL<CONN>;
   __shared__ alignas(128) Px sI[T::SI];
   __shared__ alignas(16) int sD[T::SL];
@@ -373,19 +387,25 @@ __global__ void __launch_bounds__(NT) k_relax_first(const __grid_constant__ CUte
   rq_zero(q);
   stage<CONN>(&mI, nullptr, tma, I, nullptr, g, c, sI, nullptr, &bar);
   if (tile_interior<CONN>(c, g))
-    relax_first_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, hasplat, flags, q);
+    relax_first_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, hasplat, flags, q, eqc);
   else
-    relax_first_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, hasplat, flags, q);
+    relax_first_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, hasplat, flags, q, eqc);
 }
 
 // ------------------------------------------------ further step II rounds (active tiles)
-template <int CONN, bool BORDER>
+template <int CONN, bool BORDER, bool EQC = false>
 __device__ __forceinline__ void relax_round_body(const Px* sI, int* sD, int* __restrict__ L, const Geo& g,
                                                  const TileCoord& c, int t, int ntx, int nty, uint8_t* next,
-                                                 int* changed_flag, int* limit_flag, RQ& q) {
+                                                 int* changed_flag, int* limit_flag, RQ& q,
+                                                 const uint8_t* eqc = nullptr) {
   using T = TL<CONN>;
   const int s0 = Mine<CONN>::s0();
   unsigned eqm[T::VPT];
+  if constexpr (EQC) {  // the masks k_relax_first cached (plateau voxels; 0 elsewhere)
+    const uint2 w = reinterpret_cast<const uint2*>(eqc + (size_t)t * T::V)[threadIdx.x];
+#pragma unroll
+    for (int k = 0; k < T::VPT; ++k) eqm[k] = ((k < 4 ? w.x : w.y) >> (8 * (k & 3))) & 0xffu;
+  } else {
 #pragma unroll
   for (int k = 0; k < T::VPT; ++k) {
     int lx, ly, lz;
@@ -402,32 +422,36 @@ __device__ __forceinline__ void relax_round_body(const Px* sI, int* sD, int* __r
     }
     eqm[k] = m;
   }
+  }
   const unsigned changed = relax_tile_q<CONN, true>(sD, s0, eqm, limit_flag, q);
   const bool marked = write_back<CONN>(sD, s0, eqm, changed, L, g, c, t, ntx, nty, next);
   if (__any_sync(0xffffffffu, marked) && (threadIdx.x & 31) == 0) *changed_flag = 1;  // idempotent, no barrier
 }
 
-template <int CONN>
+// EQC: the equal-neighbour masks come from k_relax_first's cache, so only the L box is staged
+// (no I box: 9 KB less shared memory and 25 -> 16 KB of box traffic per active tile)
+template <int CONN, bool EQC = false>
 __global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUtensorMap mI,
                                                      const __grid_constant__ CUtensorMap mL, int tma,
                                                      const Px* __restrict__ I, int* __restrict__ L, Geo g,
                                                      int ntx, int nty, const uint8_t* cur, uint8_t* next,
-                                                     const uint8_t* hasplat, int* flags, const int* list) {
+                                                     const uint8_t* hasplat, int* flags, const int* list,
+                                                     const uint8_t* eqc = nullptr) {
   using T = TL<CONN>;
   const int t = list ? list[blockIdx.x] : blockIdx.x;  // list: the compacted active tiles
   if (!list && (!cur[t] || !hasplat[t])) return;
-  __shared__ alignas(128) Px sI[T::SI];
+  __shared__ alignas(128) Px sI[EQC ? 16 : T::SI];
   __shared__ alignas(128) int sD[T::SL];
   __shared__ uint64_t bar;
   __shared__ RQ q;
   const TileCoord c = tile_coord<CONN>(t, ntx, nty, g);
   rq_zero(q);
-  stage<CONN>(&mI, &mL, tma, I, L, g, c, sI, sD, &bar);
+  stage<CONN>(&mI, &mL, tma, I, L, g, c, EQC ? nullptr : sI, sD, &bar);
   decode_box<CONN>(sD);
   if (tile_interior<CONN>(c, g))
-    relax_round_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, flags, flags + 1, q);
+    relax_round_body<CONN, false, EQC>(sI, sD, L, g, c, t, ntx, nty, next, flags, flags + 1, q, eqc);
   else
-    relax_round_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, flags, flags + 1, q);
+    relax_round_body<CONN, true, EQC>(sI, sD, L, g, c, t, ntx, nty, next, flags, flags + 1, q, eqc);
 }
 
 // All further step II rounds in ONE cooperative launch (no host round trip per round, P:363
@@ -441,16 +465,17 @@ __global__ void __launch_bounds__(NT) k_relax_round(const __grid_constant__ CUte
 // flags[0] says the previous round changed nothing).  A
 // round's slots are reset in the compaction phase of the round before it uses them, when no
 // CTA reads or writes them.
-template <int CONN>
+template <int CONN, bool EQC = false>
 __global__ void __launch_bounds__(NT, 8) k_relax_loop(const __grid_constant__ CUtensorMap mI,
                                                     const __grid_constant__ CUtensorMap mL, int tma,
                                                     const Px* __restrict__ I, int* __restrict__ L, Geo g, int ntx,
                                                     int nty, int ntiles, uint8_t* next, const uint8_t* hasplat,
-                                                    int* flags, int* ls, int* list0, int* list1, int max_rounds) {
+                                                    int* flags, int* ls, int* list0, int* list1, int max_rounds,
+                                                    const uint8_t* eqc) {
   using T = TL<CONN>;
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ alignas(128) Px sI[T::SI];
+  __shared__ alignas(128) Px sI[EQC ? 16 : T::SI];
   __shared__ alignas(128) int sD[T::SL];
   __shared__ uint64_t bar;
   __shared__ RQ q;
@@ -470,20 +495,20 @@ __global__ void __launch_bounds__(NT, 8) k_relax_loop(const __grid_constant__ CU
       rq_zero(q);
       if (tma) {
         if (threadIdx.x == 0) {
-          mbar_expect_tx(&bar, T::SI * (int)sizeof(Px) + T::SL * 4);
-          tma_load_3d(sI, &mI, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, &bar);
+          mbar_expect_tx(&bar, (EQC ? 0 : T::SI * (int)sizeof(Px)) + T::SL * 4);
+          if (!EQC) tma_load_3d(sI, &mI, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, &bar);
           tma_load_3d(sD, &mL, c.bx - T::LXO, c.by - T::LYO, c.bz - T::LZO, &bar);
         }
         mbar_wait(&bar, phase);
         phase ^= 1u;
       } else {
-        stage<CONN>(&mI, &mL, false, I, L, g, c, sI, sD, &bar);
+        stage<CONN>(&mI, &mL, false, I, L, g, c, EQC ? nullptr : sI, sD, &bar);
       }
       decode_box<CONN>(sD);
       if (tile_interior<CONN>(c, g))
-        relax_round_body<CONN, false>(sI, sD, L, g, c, t, ntx, nty, next, ls + (r & 1), flags + 1, q);
+        relax_round_body<CONN, false, EQC>(sI, sD, L, g, c, t, ntx, nty, next, ls + (r & 1), flags + 1, q, eqc);
       else
-        relax_round_body<CONN, true>(sI, sD, L, g, c, t, ntx, nty, next, ls + (r & 1), flags + 1, q);
+        relax_round_body<CONN, true, EQC>(sI, sD, L, g, c, t, ntx, nty, next, ls + (r & 1), flags + 1, q, eqc);
       __syncthreads();  // the boxes and q are reused by the next tile
     }
     grid.sync();
@@ -1145,7 +1170,19 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   // the whole flag block (later host reads copy ranges of it; every field is defined)
   WS_CUDA(cudaMemsetAsync(flags, 0, 256, st));
   WS_CUDA(cudaMemsetAsync(next, 0, 2 * (size_t)tg.n, st));  // next and hasplat
-  k_relax_first<CONN><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, next, hasplat, flags);
+  // equal-neighbour mask cache (CONN <= 8: one byte per voxel) so the later rounds stage only
+  // the L box; WS_NO_EQC=1 restages the I box
+  constexpr bool EQ = CONN <= 8;
+  uint8_t* eqc = nullptr;
+  {
+    const char* ne = getenv("WS_NO_EQC");
+    if (EQ && !(ne && ne[0] == '1')) {
+      WS_TRY(ctx->eqc.ensure((size_t)tg.n * TL<CONN>::V, "equal-neighbour mask cache"));
+      eqc = ctx->eqc.as<uint8_t>();
+    }
+  }
+  k_relax_first<CONN><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, next, hasplat, flags,
+                                                                        eqc);
   k_tile_list<<<gl, NT, 0, st>>>(next, hasplat, tg.n, list, flags + 4);
   launched(ctx, PH_WS_INIT, 2);
   tmark(ctx, st, PH_WS_INIT);
@@ -1156,7 +1193,9 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   // walking a long list measured slower than the per-round launches (C4 first round).
   int occ = 0;
   const bool coop = ctx->coop &&
-                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relax_loop<CONN>, NT, 0) == cudaSuccess &&
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                        &occ, eqc ? (const void*)k_relax_loop<CONN, EQ> : (const void*)k_relax_loop<CONN, false>, NT,
+                        0) == cudaSuccess &&
                     occ > 0;
   const int wave = occ * ctx->num_sms;
   // small inputs (every tile list fits one wave): all rounds after the first in the
@@ -1173,9 +1212,12 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
     Geo gg = g;
     int32_t* LL = L;
     const Px* II = grad;
+    const uint8_t* ec = eqc;
     void* args[] = {&mI, &mL, &tma, &II, &LL, &gg, &ntx, &nty, &ntiles, &next, &hasplat, &flags, &ls, &list, &list1,
-                    &maxr};
-    WS_CUDA(cudaLaunchCooperativeKernel((const void*)k_relax_loop<CONN>, dim3(grid), dim3(NT), args, 0, st));
+                    &maxr, &ec};
+    WS_CUDA(cudaLaunchCooperativeKernel(
+        eqc ? (const void*)k_relax_loop<CONN, EQ> : (const void*)k_relax_loop<CONN, false>, dim3(grid), dim3(NT), args, 0,
+        st));
     launched(ctx, PH_WS_RELAX);
     ctx->stats.plateau_rounds = -1;  // filled from ls[4] by the final read
     tmark(ctx, st, PH_WS_RELAX);
@@ -1209,9 +1251,12 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
       Geo gg = g;
       int32_t* LL = L;
       const Px* II = grad;
+      const uint8_t* ec = eqc;
       void* args[] = {&mI, &mL, &tma, &II, &LL, &gg, &ntx, &nty, &ntiles, &next, &hasplat, &flags, &ls, &list, &list1,
-                      &maxr};
-      WS_CUDA(cudaLaunchCooperativeKernel((const void*)k_relax_loop<CONN>, dim3(grid), dim3(NT), args, 0, st));
+                      &maxr, &ec};
+      WS_CUDA(cudaLaunchCooperativeKernel(
+          eqc ? (const void*)k_relax_loop<CONN, EQ> : (const void*)k_relax_loop<CONN, false>, dim3(grid), dim3(NT), args,
+          0, st));
       launched(ctx, PH_WS_RELAX);
       WS_CUDA(cudaMemcpyAsync(ctx->pinned, flags, 25 * sizeof(int), cudaMemcpyDeviceToHost, st));
       WS_CUDA(cudaStreamSynchronize(st));
@@ -1229,8 +1274,12 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
     std::swap(cur, next);
     WS_CUDA(cudaMemsetAsync(next, 0, tg.n, st));
     WS_CUDA(cudaMemsetAsync(flags, 0, 5 * sizeof(int), st));
-    k_relax_round<CONN><<<nact, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat,
-                                             flags, list);
+    if (eqc)
+      k_relax_round<CONN, EQ><<<nact, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat,
+                                                   flags, list, eqc);
+    else
+      k_relax_round<CONN><<<nact, NT, 0, st>>>(mp.mI, mp.mL, mp.tma, grad, L, g, tg.ntx, tg.nty, cur, next, hasplat,
+                                               flags, list);
     k_tile_list<<<gl, NT, 0, st>>>(next, hasplat, tg.n, list, flags + 4);
     launched(ctx, PH_WS_RELAX, 2);
     ++rounds;
@@ -1473,7 +1522,8 @@ static ws_status shard_first_t(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   WS_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), st));
   WS_CUDA(cudaMemsetAsync(a, 0, tg.n, st));
   WS_CUDA(cudaMemsetAsync(hasplat, 0, tg.n, st));
-  k_relax_first<CONN><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, a, hasplat, flags);
+  k_relax_first<CONN><<<tile_grid(tg.ntx, tg.nty, tg.ntz), NT, 0, st>>>(mp.mI, mp.tma, grad, L, g, tg.ntx, tg.nty, a, hasplat, flags,
+                                                                        nullptr);
   launched(ctx, PH_WS_INIT);
   ctx->shard_tiles = tg.n;
   ctx->shard_flip = 0;  // "next" = buffer 0
