@@ -92,10 +92,26 @@ def load_traffic():
         cur = hashlib.sha256(open(lib, "rb").read()).hexdigest()
         prov = d.get("_provenance", {})
         prov["matches_build"] = prov.get("lib_sha256") == cur
+        # nvcc output is not byte-reproducible: the source tree the capture was built from is
+        # the stable identity (tools/make_traffic.py records the same hash)
+        prov["matches_source"] = prov.get("src_sha256") == source_sha256()
         d["_provenance"] = prov
     except Exception:
         pass
     return d
+
+
+def source_sha256():
+    """sha256 over the library sources (csrc/*, include/ws.h), in sorted path order."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2410_08946_b200", "csrc", "*"))) + \
+        [os.path.join(ROOT, "include", "ws.h")]
+    for fn in files:
+        h.update(os.path.basename(fn).encode())
+        h.update(open(fn, "rb").read())
+    return h.hexdigest()
 
 
 class Clocks:

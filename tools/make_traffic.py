@@ -61,7 +61,14 @@ def main(path, out, n_vox):
     res["_step"] = {"dram_bytes": step, "ms_ncu": step_ms, "voxels": n_vox,
                     "dram_bytes_per_voxel": step / n_vox if n_vox else None,
                     "amplification_vs_38B": step / n_vox / 38.0 if n_vox else None}
-    res["_provenance"] = {"lib_sha256": hashlib.sha256(open(lib, "rb").read()).hexdigest() if os.path.exists(lib) else None,
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    hs = hashlib.sha256()
+    for fn in sorted(__import__("glob").glob(os.path.join(root, "paper_2410_08946_b200", "csrc", "*"))) + \
+            [os.path.join(root, "include", "ws.h")]:
+        hs.update(os.path.basename(fn).encode())
+        hs.update(open(fn, "rb").read())
+    res["_provenance"] = {"src_sha256": hs.hexdigest(),
+                          "lib_sha256": hashlib.sha256(open(lib, "rb").read()).hexdigest() if os.path.exists(lib) else None,
                           "launch_list": os.path.basename(path), "captured": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
     json.dump(res, open(out, "w"), indent=1, sort_keys=True)
     print(json.dumps(res, indent=1, sort_keys=True)[:3000])
