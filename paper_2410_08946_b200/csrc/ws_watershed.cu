@@ -315,6 +315,8 @@ __device__ __forceinline__ void classify_box(const Px* sI, int* sD, const Geo& g
 }
 
 // ------------------------------------------- step I + first step II round (all tiles)
+constexpr int EQB = NT * 8;  // equal-mask cache bytes per tile: one 8-byte word per thread (VPT <= 8)
+
 template <int CONN, bool BORDER>
 __device__ __forceinline__ void relax_first_body(const Px* sI, int* sD, int* __restrict__ L, const Geo& g,
                                                  const TileCoord& c, int t, int ntx, int nty, uint8_t* next,
@@ -345,6 +347,7 @@ __device__ __forceinline__ void relax_first_body(const Px* sI, int* sD, int* __r
   if constexpr (CONN <= 8) {
     // the equal-neighbour masks of this thread's 8 voxels (one byte each) for the later step II
     // rounds, which then stage only the L box (tile-major, thread-major inside the tile)
+    static_assert(T::VPT <= 8, "one 8-byte cache word per thread");
     if (eqc) {
       uint2 w = make_uint2(0u, 0u);
 #pragma unroll
@@ -352,7 +355,7 @@ __device__ __forceinline__ void relax_first_body(const Px* sI, int* sD, int* __r
         if (k < 4) w.x |= eqm[k] << (8 * k);
         else w.y |= eqm[k] << (8 * (k - 4));
       }
-      reinterpret_cast<uint2*>(eqc + (size_t)t * T::V)[threadIdx.x] = w;
+      reinterpret_cast<uint2*>(eqc + (size_t)t * EQB)[threadIdx.x] = w;
     }
   }
   relax_tile_q<CONN, false>(sD, s0, eqm, flags + 1, q);
@@ -402,7 +405,7 @@ __device__ __forceinline__ void relax_round_body(const Px* sI, int* sD, int* __r
   const int s0 = Mine<CONN>::s0();
   unsigned eqm[T::VPT];
   if constexpr (EQC) {  // the masks k_relax_first cached (plateau voxels; 0 elsewhere)
-    const uint2 w = reinterpret_cast<const uint2*>(eqc + (size_t)t * T::V)[threadIdx.x];
+    const uint2 w = reinterpret_cast<const uint2*>(eqc + (size_t)t * EQB)[threadIdx.x];
 #pragma unroll
     for (int k = 0; k < T::VPT; ++k) eqm[k] = ((k < 4 ? w.x : w.y) >> (8 * (k & 3))) & 0xffu;
   } else {
@@ -1177,7 +1180,7 @@ static ws_status plateau_phase(ws_ctx* ctx, const Px* grad, const Geo& g, int32_
   {
     const char* ne = getenv("WS_NO_EQC");
     if (EQ && !(ne && ne[0] == '1')) {
-      WS_TRY(ctx->eqc.ensure((size_t)tg.n * TL<CONN>::V, "equal-neighbour mask cache"));
+      WS_TRY(ctx->eqc.ensure((size_t)tg.n * EQB, "equal-neighbour mask cache"));
       eqc = ctx->eqc.as<uint8_t>();
     }
   }
