@@ -604,12 +604,16 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
   // (parent initialisation) and only the other backward neighbours are united -- large flat
   // minimal plateaux (C5, C2) then do not contend for one growing root.  3-D tiles keep every
   // minimal voxel as its own root (C4: fewer instructions in this issue-bound kernel).
-  constexpr bool PINIT = !Conn<CONN>::is3d;
-  // 4-connectivity: the parent comes from the row runs instead -- a warp holds 32 consecutive
-  // voxels of one tile row, a ballot of "equal to my left neighbour" gives every plateau voxel
-  // its run start (the run's smallest index) as parent, and vertical unions are needed only
-  // where one of the two vertically adjacent runs starts (the leftmost voxel of their overlap)
-  constexpr bool RUNS = (CONN == 4);
+  constexpr bool PINIT = false;
+  // 2-D tiles use the row runs instead (RUNS; PINIT stays as the measured alternative): a warp
+  // holds 32 consecutive voxels of one tile row, a ballot of "equal to my left neighbour" gives
+  // every plateau voxel its run start (the run's smallest index) as parent (the first lane of a
+  // warp that continues a run links to its left neighbour), and vertical unions are needed only
+  // where a run starts: 4-conn, runs R1 (row y) and R2 (row y - 1) overlap => at the leftmost
+  // voxel of the overlap one of them starts; 8-conn, they touch => R1's start sees R2 up-left or
+  // up, or R2 starts above R1's start or one voxel right of a voxel of R1 (up or up-right)
+  constexpr bool RUNS = !Conn<CONN>::is3d;
+  constexpr int LEFT = CONN == 4 ? 1 : 3;  // direction (0, 0, -1)
   __shared__ unsigned sStart[RUNS ? T::V / 32 : 1];  // bit: the voxel starts its row run
   uint32_t leqm = 0;     // RUNS: bit k: voxel k is minimal and equal to its in-tile left neighbour
   uint32_t gmask = 0;    // bit k: gk[k] holds sG[j] (stored once sD is dead: sG aliases sD)
@@ -667,7 +671,7 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
       sP[j] = -2;  // root (set after the in-tile union below)
       int par = j;  // union-find parent (local index; RUNS: set with the row ballot below)
       if constexpr (RUNS) {
-        if (((eqm >> 1) & 1u) && lx > 0) leqm |= 1u << k;  // direction 1 = (0, 0, -1)
+        if (((eqm >> LEFT) & 1u) && lx > 0) leqm |= 1u << k;
       } else if constexpr (PINIT) {
 #pragma unroll
         for (int i = Conn<CONN>::nfwd - 1; i >= 0; --i) {
@@ -722,10 +726,22 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
       const int si = T::iI(lz, ly, lx);
       const int v = sI[si];
       const unsigned vm = BORDER ? valid_mask<CONN>(g, c.bz + lz, c.by + ly, c.bx + lx) : (1u << CONN) - 1;
-      if constexpr (RUNS) {  // vertical: where one of the two runs starts
-        if (ly > 0 && (!BORDER || (vm & 1u)) && sI[si + T::oI(0)] == v) {
-          const int u = j - T::TX;
-          if (((sStart[j >> 5] >> (j & 31)) & 1u) || ((sStart[u >> 5] >> (u & 31)) & 1u)) s_unite(sG, j, u);
+      if constexpr (RUNS) {  // vertical: where a run starts
+        const bool sj = (sStart[j >> 5] >> (j & 31)) & 1u;
+        if (ly > 0) {
+          constexpr int UP = CONN == 4 ? 0 : 1;  // direction (0, -1, 0)
+          if ((!BORDER || ((vm >> UP) & 1u)) && sI[si + T::oI(UP)] == v) {
+            const int u = j - T::TX;
+            if (sj || ((sStart[u >> 5] >> (u & 31)) & 1u)) s_unite(sG, j, u);
+          }
+          if constexpr (CONN == 8) {
+            if (sj && lx > 0 && (!BORDER || (vm & 1u)) && sI[si + T::oI(0)] == v)  // up-left
+              s_unite(sG, j, j - T::TX - 1);
+            if (lx + 1 < T::TX && (!BORDER || (vm & 4u)) && sI[si + T::oI(2)] == v) {  // up-right
+              const int u = j - T::TX + 1;
+              if ((sStart[u >> 5] >> (u & 31)) & 1u) s_unite(sG, j, u);
+            }
+          }
         }
       } else if constexpr (PINIT) {  // in-tile backward equal neighbours other than the parent
         bool first = true;
@@ -750,7 +766,7 @@ __device__ __forceinline__ void resolve_body(const Px* sI, const int* sD, short*
         const int nx = lx + dx, ny = ly + dy, nz = lz + dz;
         if (BORDER && (!(vm & (1u << i)) || c.bz + nz >= g.zhi)) continue;  // cut plane: ws_shard_merge
         if ((unsigned)nx < (unsigned)T::TX && (unsigned)ny < (unsigned)T::TY && (unsigned)nz < (unsigned)T::TZ) {
-          if constexpr (!PINIT) s_unite(sG, j, j + (dz * T::TY + dy) * T::TX + dx);
+          if constexpr (!PINIT && !RUNS) s_unite(sG, j, j + (dz * T::TY + dy) * T::TX + dx);
         } else {
           const int p = (int)((size_t)(c.bz + lz) * g.plane + (size_t)(c.by + ly) * g.n2 + c.bx + lx) + g.gofs;
           const int2 e = make_int2(p, p + nb_off<CONN>(g, i));
