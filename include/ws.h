@@ -227,6 +227,18 @@ ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims,
                           int32_t connectivity, int32_t NL, int32_t* levels_host,
                           int64_t* counts, void* stream);
 
+/* ws_segment_host_async — ws_segment_host without the final wait: it returns once the levels'
+ * device-to-host copy is ENQUEUED on `stream` (counts are complete at return: the call reads
+ * them back before enqueuing the copy).  levels_host is written when the stream reaches the copy
+ * and must stay valid until then; the caller synchronises `stream` before reading it.  Two
+ * contexts on two streams pipeline a sequence of volumes: the PCIe copy of one volume's levels
+ * overlaps the host-to-device copy and the compute of the next (PCIe is full duplex).  The
+ * context's workspace holds the levels until the copy is done: do not reuse the context before
+ * synchronising `stream`.  Errors: as ws_segment_host. */
+ws_status ws_segment_host_async(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims,
+                                int32_t connectivity, int32_t NL, int32_t* levels_host,
+                                int64_t* counts, void* stream);
+
 /* ws_plateau_debug — intermediate of step II for per-kernel parity tests (T2):
  *   dist[p] = 0 for voxels with a lower neighbour, the BFS distance on non-minimal plateaux,
  *             -1 on minimal plateaux (regional minima, incl. strict single-voxel minima);

@@ -156,8 +156,11 @@ def segment(grad: torch.Tensor, conn: int, NL: int, ndim: int = None, ctx: Conte
 
 
 def segment_host(grad_host: torch.Tensor, conn: int, NL: int, ndim: int = None, device: int = None,
-                 ctx: Context = None, out: torch.Tensor = None):
-    """ws_segment_host: HOST u8 gradient -> HOST int32 levels [NL, *shape] (copies inside)."""
+                 ctx: Context = None, out: torch.Tensor = None, stream: torch.cuda.Stream = None,
+                 wait: bool = True):
+    """ws_segment_host: HOST u8 gradient -> HOST int32 levels [NL, *shape] (copies inside).
+    wait=False calls ws_segment_host_async: the levels are ready once `stream` (default: the
+    current stream) is synchronised."""
     if grad_host.is_cuda or grad_host.dtype != torch.uint8 or not grad_host.is_contiguous():
         raise TypeError("grad_host must be a contiguous CPU uint8 tensor")
     ndim = _ndim_for(conn, ndim)
@@ -168,9 +171,10 @@ def segment_host(grad_host: torch.Tensor, conn: int, NL: int, ndim: int = None, 
     levels = out if out is not None else torch.empty((int(NL),) + tuple(grad_host.shape), dtype=torch.int32,
                                                       pin_memory=True)
     counts = (ctypes.c_int64 * max(int(NL), 1))()
-    st = ctypes.c_void_p(torch.cuda.current_stream(ctx.device).cuda_stream)
-    _b.check(_b.load().ws_segment_host(ctx.handle, _b.ptr(grad_host), _b.dims_of(grad_host.shape, ndim), int(conn),
-                                       int(NL), _b.ptr(levels), counts, st))
+    st = ctypes.c_void_p((stream or torch.cuda.current_stream(ctx.device)).cuda_stream)
+    fn = _b.load().ws_segment_host if wait else _b.load().ws_segment_host_async
+    _b.check(fn(ctx.handle, _b.ptr(grad_host), _b.dims_of(grad_host.shape, ndim), int(conn), int(NL), _b.ptr(levels),
+                counts, st))
     return levels, list(counts)
 
 

@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "WS_OK", 1: "WS_ERR_INVALID", 2: "WS_ERR_OOM", 3: "WS_ERR_CUD
 # every symbol include/ws.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ws_ctx_create", "ws_ctx_destroy", "ws_last_error", "ws_version", "ws_get_stats",
            "ws_ctx_set_timing", "ws_phase_name",
-           "ws_gradient", "ws_gradient_u16", "ws_watershed", "ws_watershed_u16", "ws_watershed_variant", "ws_waterfall", "ws_waterfall_u16", "ws_waterfall_reconstruct", "ws_segment", "ws_segment_host", "ws_plateau_debug",
+           "ws_gradient", "ws_gradient_u16", "ws_watershed", "ws_watershed_u16", "ws_watershed_variant", "ws_waterfall", "ws_waterfall_u16", "ws_waterfall_reconstruct", "ws_segment", "ws_segment_host", "ws_segment_host_async", "ws_plateau_debug",
            "ws_shard_table_bytes", "ws_shard_plateau", "ws_shard_halo", "ws_shard_local", "ws_shard_merge",
            "ws_shard_relabel", "ws_shard_wf_dense", "ws_shard_wf_btable", "ws_shard_wf_bfill", "ws_shard_wf_begin",
            "ws_shard_wf_step", "ws_shard_wf_end",
@@ -117,6 +117,7 @@ def load(path: str = SO_PATH):
         lib.ws_waterfall_u16.argtypes = [vp, vp, vp, WsDims, i32, i32, vp, vp, vp]
         lib.ws_watershed_variant.argtypes = [vp, vp, WsDims, i32, i32, vp, vp, vp]
         lib.ws_segment_host.argtypes = [vp, vp, WsDims, i32, i32, vp, vp, vp]
+        lib.ws_segment_host_async.argtypes = [vp, vp, WsDims, i32, i32, vp, vp, vp]
         lib.ws_segment.argtypes = [vp, vp, WsDims, i32, i32, vp, vp, vp]
         lib.ws_plateau_debug.argtypes = [vp, vp, WsDims, i32, vp, vp, vp]
         lib.ws_shard_table_bytes.argtypes = [WsDims]

@@ -455,8 +455,8 @@ ws_status ws_segment(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t con
   return s;
 }
 
-ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims, int32_t connectivity, int32_t NL,
-                          int32_t* levels_host, int64_t* counts, void* stream) {
+static ws_status segment_host_impl(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims, int32_t connectivity,
+                                   int32_t NL, int32_t* levels_host, int64_t* counts, void* stream, bool wait) {
   WS_TRY(check_ctx(ctx));
   Geo g;
   WS_TRY(check_dims(dims, &g));
@@ -478,9 +478,20 @@ ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims, i
   WS_TRY(run_segment(ctx, ctx->h_grad.as<uint8_t>(), g, connectivity, NL, ctx->h_levels.as<int32_t>(), counts, st));
   WS_CUDA(cudaMemcpyAsync(levels_host, ctx->h_levels.p, N * (size_t)NL * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   tmark(ctx, st, PH_COPY);
+  if (!wait) return WS_OK;  // the caller synchronises the stream (per-phase timing not collected)
   WS_CUDA(cudaStreamSynchronize(st));
   tfinish(ctx);
   return WS_OK;
+}
+
+ws_status ws_segment_host(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims, int32_t connectivity, int32_t NL,
+                          int32_t* levels_host, int64_t* counts, void* stream) {
+  return segment_host_impl(ctx, grad_host, dims, connectivity, NL, levels_host, counts, stream, true);
+}
+
+ws_status ws_segment_host_async(ws_ctx* ctx, const uint8_t* grad_host, ws_dims dims, int32_t connectivity,
+                                int32_t NL, int32_t* levels_host, int64_t* counts, void* stream) {
+  return segment_host_impl(ctx, grad_host, dims, connectivity, NL, levels_host, counts, stream, false);
 }
 
 ws_status ws_plateau_debug(ws_ctx* ctx, const uint8_t* grad, ws_dims dims, int32_t connectivity, int32_t* dist,

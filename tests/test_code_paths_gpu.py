@@ -76,3 +76,24 @@ def test_gradient_v1_v2_agree(monkeypatch):
         if diff.any():
             t = 255.0 * og[diff]
             assert np.all(np.abs(t - np.floor(t) - 0.5) <= 255 * 1e-5)
+
+
+def test_segment_host_async_pipeline():
+    """ws_segment_host_async on two contexts / streams (the pipelined e2e of bench.py) gives the
+    synchronous call's levels and counts for every volume of a sequence."""
+    ws = _ws()
+    vols = [synth.random_plateau_image((9, 40, 70), 4, seed=s) for s in range(4)]
+    ref = [ws.segment_host(v, 6, 6, ndim=3) for v in vols]
+    ctxs = (ws.Context(0), ws.Context(0))
+    sts = (torch.cuda.Stream(), torch.cuda.Stream())
+    outs = [torch.empty((6,) + tuple(v.shape), dtype=torch.int32, pin_memory=True) for v in vols]
+    got = []
+    for i, v in enumerate(vols):
+        k = i & 1
+        sts[k].synchronize()
+        _, counts = ws.segment_host(v, 6, 6, ndim=3, ctx=ctxs[k], out=outs[i], stream=sts[k], wait=False)
+        got.append(counts)
+    for st in sts:
+        st.synchronize()
+    for (rl, rc), out, c in zip(ref, outs, got):
+        assert torch.equal(rl, out) and list(rc) == list(c)
