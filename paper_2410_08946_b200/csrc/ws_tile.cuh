@@ -112,6 +112,37 @@ __device__ __forceinline__ unsigned valid_mask(const Geo& g, int gz, int gy, int
   return m;
 }
 
+// box rows [0, ROWS) of width SX starting at global (x0, y0, z0) into dst (row pitch SX),
+// zero outside the volume; row r = (z - z0) * SY + (y - y0)
+template <class V, int SX, int SY, int ROWS, int RB>
+__device__ __forceinline__ void plain_rows(const V* __restrict__ src, const Geo& g, int x0, int y0, int z0, V* dst) {
+  constexpr int CH = (SX + 31) / 32, NW = NT / 32;
+  const int lane = threadIdx.x & 31;
+  for (int r0 = threadIdx.x >> 5; r0 < ROWS; r0 += RB * NW) {
+    V v[RB][CH];
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int r = r0 + u * NW;
+      const int gy = y0 + r % SY, gz = z0 + r / SY;
+      const bool rok = r < ROWS && (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
+      const V* row = src + ((size_t)gz * g.plane + (size_t)gy * g.n2);
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) {
+        const int gx = x0 + lane + 32 * ch;
+        v[u][ch] = (rok && lane + 32 * ch < SX && (unsigned)gx < (unsigned)g.n2) ? row[gx] : (V)0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      const int r = r0 + u * NW;
+      if (r >= ROWS) break;
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch)
+        if (lane + 32 * ch < SX) dst[r * SX + lane + 32 * ch] = v[u][ch];
+    }
+  }
+}
+
 // Stage the I box (sI may be null: L box only) and optionally the L box (raw L values) into
 // shared memory: one
 // cp.async.bulk.tensor per box (TMA zero-fills outside the volume), or a plain loader when
@@ -132,25 +163,33 @@ __device__ __forceinline__ void stage(const CUtensorMap* mI, const CUtensorMap* 
     mbar_wait(bar, 0);
   } else {
     // plain loader (layouts without a tensor map, e.g. rows not a multiple of 16 bytes): one
-    // warp per box row, lanes along x (no per-element index division), zero fill outside
-    const int lane = threadIdx.x & 31;
-    for (int r = threadIdx.x >> 5; sI && r < T::SYI * T::SZI; r += NT / 32) {
-      const int gy = c.by + r % T::SYI - T::IYO, gz = c.bz + r / T::SYI - T::IZO;
-      const bool rok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
-      const Px* row = I + ((size_t)gz * g.plane + (size_t)gy * g.n2);
-      for (int sx = lane; sx < T::SXI; sx += 32) {
-        const int gx = c.bx + sx - T::IXO;
-        sI[r * T::SXI + sx] = (rok && (unsigned)gx < (unsigned)g.n2) ? __ldg(row + gx) : (Px)0;
-      }
-    }
-    if (sL) {
-      for (int r = threadIdx.x >> 5; r < T::SYL * T::SZL; r += NT / 32) {
-        const int gy = c.by + r % T::SYL - T::LYO, gz = c.bz + r / T::SYL - T::LZO;
+    // warp per box row, lanes along x (no per-element index division), zero fill outside;
+    // 2-D tiles: 4 rows per warp at a time with all their loads issued before the shared
+    // stores (small images such as C5's have no tensor map); 3-D tiles (tensor maps in
+    // practice) keep the register-lean row loop
+    if constexpr (!T::is3d) {
+      if (sI) plain_rows<Px, T::SXI, T::SYI, T::SYI * T::SZI, 4>(I, g, c.bx - T::IXO, c.by - T::IYO, c.bz - T::IZO, sI);
+      if (sL) plain_rows<int, T::SXL, T::SYL, T::SYL * T::SZL, 4>(L, g, c.bx - T::LXO, c.by - T::LYO, c.bz - T::LZO, sL);
+    } else {
+      const int lane = threadIdx.x & 31;
+      for (int r = threadIdx.x >> 5; sI && r < T::SYI * T::SZI; r += NT / 32) {
+        const int gy = c.by + r % T::SYI - T::IYO, gz = c.bz + r / T::SYI - T::IZO;
         const bool rok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
-        const int* row = L + ((size_t)gz * g.plane + (size_t)gy * g.n2);
-        for (int sx = lane; sx < T::SXL; sx += 32) {
-          const int gx = c.bx + sx - T::LXO;
-          sL[r * T::SXL + sx] = (rok && (unsigned)gx < (unsigned)g.n2) ? row[gx] : 0;
+        const Px* row = I + ((size_t)gz * g.plane + (size_t)gy * g.n2);
+        for (int sx = lane; sx < T::SXI; sx += 32) {
+          const int gx = c.bx + sx - T::IXO;
+          sI[r * T::SXI + sx] = (rok && (unsigned)gx < (unsigned)g.n2) ? __ldg(row + gx) : (Px)0;
+        }
+      }
+      if (sL) {
+        for (int r = threadIdx.x >> 5; r < T::SYL * T::SZL; r += NT / 32) {
+          const int gy = c.by + r % T::SYL - T::LYO, gz = c.bz + r / T::SYL - T::LZO;
+          const bool rok = (unsigned)gy < (unsigned)g.n1 && (unsigned)gz < (unsigned)g.n0;
+          const int* row = L + ((size_t)gz * g.plane + (size_t)gy * g.n2);
+          for (int sx = lane; sx < T::SXL; sx += 32) {
+            const int gx = c.bx + sx - T::LXO;
+            sL[r * T::SXL + sx] = (rok && (unsigned)gx < (unsigned)g.n2) ? row[gx] : 0;
+          }
         }
       }
     }
